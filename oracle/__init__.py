@@ -1,0 +1,300 @@
+"""Python face of the fp64 CPU oracle (oracle.c).
+
+TEST INFRASTRUCTURE ONLY: only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+``--impl reference`` legs may import this module.  It shares no code with the CUDA path
+(paper_2202_12567_b200/) and neither imports the other; both consume inputs from scenegen/.
+
+Functions return numpy arrays; every stage follows PAPER.md as cited in oracle.c.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "liboracle.so")
+_lock = threading.Lock()
+_lib = None
+
+CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC", "-shared", "-Wall"]
+
+FLAG_DIRECT, FLAG_DIVERGED, FLAG_ZERO = 1, 2, 4
+
+
+def build(force: bool = False) -> str:
+    src = os.path.join(_HERE, "oracle.c")
+    hdr = os.path.join(_HERE, "oracle.h")
+    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < max(os.path.getmtime(src), os.path.getmtime(hdr)):
+        tmp = _SO + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, src, "-lm"])
+        os.replace(tmp, _SO)
+    return _SO
+
+
+class _Inputs(C.Structure):
+    _fields_ = [
+        ("m", C.c_int64),
+        *[(k, C.c_void_p) for k in ("px", "py", "pz", "nx", "ny", "nz", "vx", "vy", "vz", "rr", "rg", "rb", "spec")],
+        ("expo", C.c_void_p),
+        ("nv", C.c_int64),
+        *[(k, C.c_void_p) for k in ("lx", "ly", "lz", "lnx", "lny", "lnz", "lir", "lig", "lib")],
+        ("nn", C.c_int64),
+        ("left", C.c_void_p), ("right", C.c_void_p), ("rep", C.c_void_p),
+        ("tir", C.c_void_p), ("tig", C.c_void_p), ("tib", C.c_void_p),
+        ("ncut", C.c_int64), ("cut", C.c_void_p),
+        ("nsph", C.c_int32), ("nbox", C.c_int32), ("nrect", C.c_int32),
+        ("sph", C.c_void_p), ("box", C.c_void_p), ("rect", C.c_void_p),
+        ("clamp_dist", C.c_double), ("shadow_eps", C.c_double), ("diag", C.c_double),
+        ("wn", C.c_double), ("target", C.c_int32), ("seed", C.c_uint64),
+        ("nmax", C.c_int32), ("nmin", C.c_int32), ("tau", C.c_double), ("rate", C.c_double),
+        ("q", C.c_int32), ("solver", C.c_int32), ("K", C.c_int32),
+        ("tol", C.c_double), ("alpha", C.c_double), ("beta", C.c_double), ("gamma", C.c_double), ("lam", C.c_double),
+        ("order_seed", C.c_uint64),
+    ]
+
+
+class _Result(C.Structure):
+    _fields_ = [
+        ("slice", C.c_int32), ("m", C.c_int32), ("n", C.c_int32),
+        ("rows", C.POINTER(C.c_int32)), ("cut_nodes", C.POINTER(C.c_int32)),
+        ("n_proc", C.c_int32),
+        ("proc_node", C.POINTER(C.c_int32)), ("proc_merged", C.POINTER(C.c_int32)), ("proc_zoff", C.POINTER(C.c_int32)),
+        ("proc_eps", C.POINTER(C.c_double)), ("proc_cost", C.POINTER(C.c_double)),
+        ("proc_zrows", C.POINTER(C.c_int32)),
+        ("proc_Va", C.POINTER(C.c_double)), ("proc_Vb", C.POINTER(C.c_double)),
+        ("n_evals_coarsen", C.c_int64),
+        ("nnz", C.c_int64), ("n_carried", C.c_int64), ("n_new", C.c_int64), ("n_forced", C.c_int64),
+        ("n_draws", C.c_int64), ("target_N", C.c_int64),
+        ("om_row", C.POINTER(C.c_int32)), ("om_col", C.POINTER(C.c_int32)),
+        ("om_val", C.POINTER(C.c_double)), ("om_carried", C.POINTER(C.c_int32)),
+        ("weights", C.POINTER(C.c_uint32)),
+        ("q", C.c_int32), ("iters", C.c_int32), ("flags", C.c_int32),
+        ("sigma", C.c_double), ("resid", C.c_double),
+        ("U", C.POINTER(C.c_double)), ("V", C.POINTER(C.c_double)),
+        ("obj", C.POINTER(C.c_double)), ("n_obj", C.c_int32),
+        ("full", C.POINTER(C.c_double)),
+        ("rgb", C.POINTER(C.c_double)),
+    ]
+
+
+def lib():
+    global _lib
+    with _lock:
+        if _lib is None:
+            L = C.CDLL(build())
+            P = C.c_void_p
+            L.orc_philox.argtypes = [P, P, P]
+            L.orc_floyd.argtypes = [C.c_int32, C.c_int32, C.c_uint32, C.c_int32, C.c_uint64, C.c_uint32, P]
+            L.orc_floyd.restype = C.c_int32
+            L.orc_entry_T.argtypes = [C.POINTER(_Inputs), C.c_int64, C.c_int64]
+            L.orc_entry_T.restype = C.c_double
+            L.orc_visible.argtypes = [C.POINTER(_Inputs), P, P]
+            L.orc_visible.restype = C.c_int32
+            L.orc_build_slices.argtypes = [C.POINTER(_Inputs), P, P, P]
+            L.orc_run_slice.argtypes = [C.POINTER(_Inputs), P, C.c_int32, C.c_int32, C.c_int32]
+            L.orc_run_slice.restype = C.POINTER(_Result)
+            L.orc_run_slices.argtypes = [C.POINTER(_Inputs), P, P, C.c_int32, P, C.c_int32, P]
+            L.orc_free_result.argtypes = [C.POINTER(_Result)]
+            L.orc_adm.argtypes = [C.c_int32, C.c_int32, C.c_int64, P, P, P, C.c_int32, C.c_int32, C.c_double,
+                                  C.c_double, C.c_double, C.c_double, C.c_uint64, C.c_int32, P, P, P, P, P]
+            L.orc_adm.restype = C.c_int32
+            L.orc_mals.argtypes = [C.c_int32, C.c_int32, C.c_int64, P, P, P, C.c_int32, C.c_int32, C.c_double,
+                                   C.c_uint64, C.c_int32, P, P, P, P]
+            L.orc_mals.restype = C.c_int32
+            L.orc_fullcut_slice.argtypes = [C.POINTER(_Inputs), P, C.c_int32, P, C.c_int32, P]
+            L.orc_bruteforce_rows.argtypes = [C.POINTER(_Inputs), P, C.c_int32, P]
+            _lib = L
+    return _lib
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+class Oracle:
+    """Binds one scenegen.Inputs (arrays kept alive here) to the C oracle."""
+
+    def __init__(self, x, **override):
+        self.x = x
+        prm = x.params()
+        prm.update(override)
+        self.prm = prm
+        g, v, t, pr = x.gbuf, x.vpls, x.tree, x.prims
+        keep = []
+
+        def arr(a, dt):
+            a = np.ascontiguousarray(a, dt)
+            keep.append(a)
+            return _p(a)
+
+        s = _Inputs()
+        s.m = g["px"].shape[0]
+        for k, src in (("px", "px"), ("py", "py"), ("pz", "pz"), ("nx", "nx"), ("ny", "ny"), ("nz", "nz"),
+                       ("vx", "vx"), ("vy", "vy"), ("vz", "vz"), ("rr", "rho_r"), ("rg", "rho_g"),
+                       ("rb", "rho_b"), ("spec", "spec")):
+            setattr(s, k, arr(g[src], np.float32))
+        s.expo = arr(g["exponent"], np.int32)
+        s.nv = v["px"].shape[0]
+        for k, src in (("lx", "px"), ("ly", "py"), ("lz", "pz"), ("lnx", "nx"), ("lny", "ny"), ("lnz", "nz"),
+                       ("lir", "ir"), ("lig", "ig"), ("lib", "ib")):
+            setattr(s, k, arr(v[src], np.float32))
+        s.nn = t["left"].shape[0]
+        s.left = arr(t["left"], np.int32)
+        s.right = arr(t["right"], np.int32)
+        s.rep = arr(t["rep"], np.int32)
+        s.tir = arr(t["ir"], np.float32)
+        s.tig = arr(t["ig"], np.float32)
+        s.tib = arr(t["ib"], np.float32)
+        s.ncut = t["global_cut"].shape[0]
+        s.cut = arr(t["global_cut"], np.int32)
+        s.nsph, s.nbox, s.nrect = pr["sph"].shape[0], pr["box"].shape[0], pr["rect"].shape[0]
+        s.sph = arr(pr["sph"], np.float32)
+        s.box = arr(pr["box"], np.float32)
+        s.rect = arr(pr["rect"], np.float32)
+        s.clamp_dist, s.shadow_eps, s.diag = x.clamp_dist, x.shadow_eps, x.diag
+        s.wn = prm["normal_weight"]
+        s.target = prm["slice_target"]
+        s.seed = prm["seed"]
+        s.nmax, s.nmin = prm["p1_nmax"], prm["p1_nmin"]
+        s.tau, s.rate = prm["tau"], prm["rate"]
+        s.q, s.solver, s.K = prm["rank_q"], prm["solver"], prm["max_iter"]
+        s.tol, s.alpha, s.beta, s.gamma, s.lam = prm["tol"], prm["alpha"], prm["beta"], prm["gamma"], prm["lam"]
+        s.order_seed = prm.get("order_seed", 0)
+        self._keep = keep
+        self.s = s
+        self._slices = None
+
+    # -- primitives -------------------------------------------------------------------------
+    def entry_T(self, row: int, vpl: int) -> float:
+        return lib().orc_entry_T(C.byref(self.s), int(row), int(vpl))
+
+    def visible(self, x, y) -> bool:
+        a = np.ascontiguousarray(x, np.float64)
+        b = np.ascontiguousarray(y, np.float64)
+        return bool(lib().orc_visible(C.byref(self.s), _p(a), _p(b)))
+
+    def slices(self):
+        if self._slices is None:
+            m = int(self.s.m)
+            off = np.zeros(m + 2, np.int32)
+            rows = np.zeros(max(m, 1), np.int32)
+            ns = np.zeros(1, np.int64)
+            lib().orc_build_slices(C.byref(self.s), _p(off), _p(rows), _p(ns))
+            n = int(ns[0])
+            self._slices = (off[: n + 1].copy(), rows[:m].copy())
+        return self._slices
+
+    def run_slices(self, slice_ids, stage: int = 4):
+        off, rows = self.slices()
+        ids = np.ascontiguousarray(slice_ids, np.int32)
+        out = (C.POINTER(_Result) * max(len(ids), 1))()
+        lib().orc_run_slices(C.byref(self.s), _p(off), _p(rows), len(ids), _p(ids), stage, C.cast(out, C.c_void_p))
+        res = []
+        for k in range(len(ids)):
+            res.append(_convert(out[k].contents, stage))
+            lib().orc_free_result(out[k])
+        return res
+
+    def fullcut_slice(self, rows, cut_nodes):
+        rows = np.ascontiguousarray(rows, np.int32)
+        cut = np.ascontiguousarray(cut_nodes, np.int32)
+        out = np.zeros((rows.size, 3))
+        lib().orc_fullcut_slice(C.byref(self.s), _p(rows), rows.size, _p(cut), cut.size, _p(out))
+        return out
+
+    def bruteforce_rows(self, rows):
+        rows = np.ascontiguousarray(rows, np.int32)
+        out = np.zeros((rows.size, 3))
+        lib().orc_bruteforce_rows(C.byref(self.s), _p(rows), rows.size, _p(out))
+        return out
+
+    def render(self, slice_ids=None, stage: int = 4):
+        """Full pipeline; returns (image H*W*3 float64, per-slice results)."""
+        off, rows = self.slices()
+        if slice_ids is None:
+            slice_ids = np.arange(off.size - 1)
+        res = self.run_slices(slice_ids, stage)
+        img = np.zeros((self.x.height * self.x.width, 3))
+        pix = self.x.gbuf["pixel"]
+        for r in res:
+            if r.get("rgb") is not None:
+                img[pix[r["rows"]]] = r["rgb"]
+        return img, res
+
+
+def _arr(ptr, n, dt):
+    if n <= 0 or not ptr:
+        return np.zeros(0, dt)
+    return np.ctypeslib.as_array(ptr, shape=(n,)).astype(dt, copy=True)
+
+
+def _convert(r: _Result, stage: int) -> dict:
+    m, n, q = r.m, r.n, r.q
+    d = dict(slice=r.slice, m=m, n=n, rows=_arr(r.rows, m, np.int32), cut_nodes=_arr(r.cut_nodes, n, np.int32))
+    npr = r.n_proc
+    zoff = _arr(r.proc_zoff, npr + 1, np.int32)
+    nz = int(zoff[-1]) if npr else 0
+    d.update(proc_node=_arr(r.proc_node, npr, np.int32), proc_merged=_arr(r.proc_merged, npr, np.int32),
+             proc_eps=_arr(r.proc_eps, npr, np.float64), proc_cost=_arr(r.proc_cost, npr, np.float64),
+             proc_zoff=zoff, proc_zrows=_arr(r.proc_zrows, nz, np.int32),
+             proc_Va=_arr(r.proc_Va, nz, np.float64), proc_Vb=_arr(r.proc_Vb, nz, np.float64),
+             n_evals_coarsen=r.n_evals_coarsen)
+    if stage >= 2:
+        k = r.nnz
+        d.update(nnz=k, n_carried=r.n_carried, n_new=r.n_new, n_forced=r.n_forced, n_draws=r.n_draws,
+                 target_N=r.target_N, om_row=_arr(r.om_row, k, np.int32), om_col=_arr(r.om_col, k, np.int32),
+                 om_val=_arr(r.om_val, k, np.float64), om_carried=_arr(r.om_carried, k, np.int32),
+                 weights=_arr(r.weights, n, np.uint32))
+    if stage >= 3:
+        d.update(q=q, iters=r.iters, flags=r.flags, sigma=r.sigma, resid=r.resid,
+                 U=_arr(r.U, m * q, np.float64).reshape(m, q), V=_arr(r.V, q * n, np.float64).reshape(q, n),
+                 obj=_arr(r.obj, r.n_obj, np.float64),
+                 full=_arr(r.full, m * n, np.float64).reshape(m, n) if r.full else None)
+    if stage >= 4:
+        d["rgb"] = _arr(r.rgb, m * 3, np.float64).reshape(m, 3)
+    return d
+
+
+def philox(ctr, key):
+    c = np.ascontiguousarray(ctr, np.uint32)
+    k = np.ascontiguousarray(key, np.uint32)
+    o = np.zeros(4, np.uint32)
+    lib().orc_philox(_p(c), _p(k), _p(o))
+    return o
+
+
+def floyd(m, n, a, slice_id, seed, tag=1):
+    out = np.zeros(max(min(n, m), 1), np.int32)
+    cnt = lib().orc_floyd(m, n, a, slice_id, seed, tag, _p(out))
+    return out[:cnt].copy()
+
+
+def adm(m, n, row, col, val, q, K=100, tol=0.0, alpha=1.0, beta=1.0, gamma=1.6, seed=12567, slice_id=0):
+    row = np.ascontiguousarray(row, np.int32)
+    col = np.ascontiguousarray(col, np.int32)
+    val = np.ascontiguousarray(val, np.float64)
+    U = np.zeros((m, q))
+    V = np.zeros((q, n))
+    it = np.zeros(1, np.int32)
+    res = np.zeros(1)
+    sg = np.zeros(1)
+    flags = lib().orc_adm(m, n, row.size, _p(row), _p(col), _p(val), q, K, tol, alpha, beta, gamma, seed,
+                          slice_id, _p(U), _p(V), _p(it), _p(res), _p(sg))
+    return dict(U=U, V=V, iters=int(it[0]), resid=float(res[0]), sigma=float(sg[0]), flags=flags)
+
+
+def mals(m, n, row, col, val, q, K=100, lam=1e-3, seed=12567, slice_id=0):
+    row = np.ascontiguousarray(row, np.int32)
+    col = np.ascontiguousarray(col, np.int32)
+    val = np.ascontiguousarray(val, np.float64)
+    X = np.zeros((m, q))
+    Y = np.zeros((q, n))
+    obj = np.zeros(2 * K)
+    sg = np.zeros(1)
+    flags = lib().orc_mals(m, n, row.size, _p(row), _p(col), _p(val), q, K, lam, seed, slice_id, _p(X), _p(Y),
+                           _p(obj), _p(sg))
+    return dict(X=X, Y=Y, obj=obj, sigma=float(sg[0]), flags=flags)

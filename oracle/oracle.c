@@ -1,0 +1,1093 @@
+/*
+ * oracle.c — plain, slow, fp64 CPU oracle of arXiv 2202.12567's hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY (see oracle.h).  Shares no code with the CUDA path.
+ * Compile: gcc -O2 -ffp-contract=off -fno-fast-math -fopenmp -fPIC -shared.
+ *
+ * Citations: P:<line> = /root/reference/PAPER.md line; R<k> = DESIGN.md reading k (where the
+ * paper is silent, ambiguous or garbled).  Each stage is written in the paper's order and
+ * notation; no blocking, fusion or reordering beyond the stated algorithm.
+ *
+ * parity pins: see tests/test_oracle_*.py; the whole-pipeline error vs. the paper's own scenes
+ * and the free constants (R2, R3, R6, R11, R14, R19, R20) are "parity unpinned".
+ */
+#include "oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define INV_PI 0.31830988618379067
+#define INV_2PI 0.15915494309189535
+
+enum { TAG_P1 = 1, TAG_P2 = 2, TAG_FORCE = 3, TAG_X0 = 4, TAG_Y0 = 5 };
+
+/* ------------------------------------------------------------------------------------------
+ * Philox4x32-10 (R7/O3): counter-based RNG, Salmon et al. SC'11 (Random123 constants).
+ * ---------------------------------------------------------------------------------------- */
+void orc_philox(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4])
+{
+    uint32_t c0 = ctr[0], c1 = ctr[1], c2 = ctr[2], c3 = ctr[3];
+    uint32_t k0 = key[0], k1 = key[1];
+    for (int r = 0; r < 10; ++r) {
+        uint64_t p0 = (uint64_t)0xD2511F53u * (uint64_t)c0;
+        uint64_t p1 = (uint64_t)0xCD9E8D57u * (uint64_t)c2;
+        uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+        uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+        uint32_t n0 = hi1 ^ c1 ^ k0;
+        uint32_t n2 = hi0 ^ c3 ^ k1;
+        c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+        if (r < 9) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
+    }
+    out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+static void philox_draw(uint64_t seed, uint32_t a, uint32_t b, uint32_t s, uint32_t tag, uint32_t out[4])
+{
+    uint32_t ctr[4] = {a, b, s, tag};
+    uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+    orc_philox(ctr, key, out);
+}
+
+/* uniform integer in [0, n): (u * n) >> 32 */
+static uint32_t randint(uint32_t u, uint32_t n) { return (uint32_t)(((uint64_t)u * (uint64_t)n) >> 32); }
+/* uniform real in [0,1): (u >> 8) * 2^-24, exact */
+static double unif(uint32_t u) { return (double)(u >> 8) * (1.0 / 16777216.0); }
+
+static int cmp_i32(const void *a, const void *b)
+{
+    int32_t x = *(const int32_t *)a, y = *(const int32_t *)b;
+    return (x > y) - (x < y);
+}
+
+/* Floyd's algorithm: n distinct uniformly random rows of [0,m) ("uniformly distributed
+ * inside the image block", R7 without replacement), keyed by (a, j, slice, tag). */
+int32_t orc_floyd(int32_t m, int32_t n, uint32_t a, int32_t slice, uint64_t seed, uint32_t tag, int32_t *out)
+{
+    if (n > m) n = m;
+    int32_t cnt = 0;
+    for (int32_t j = m - n; j < m; ++j) {
+        uint32_t u[4];
+        philox_draw(seed, a, (uint32_t)j, (uint32_t)slice, tag, u);
+        int32_t t = (int32_t)randint(u[0], (uint32_t)(j + 1));
+        int in = 0;
+        for (int32_t k = 0; k < cnt; ++k)
+            if (out[k] == t) { in = 1; break; }
+        out[cnt++] = in ? j : t;
+    }
+    qsort(out, (size_t)cnt, sizeof(int32_t), cmp_i32);
+    return cnt;
+}
+
+/* ------------------------------------------------------------------------------------------
+ * Entry A(i,j) ("illumination contribution from light j to surface point i"; never
+ * stated — reading R1): cosine-weighted VPL emitter (R32), d^2 clamp (R2),
+ * normalised-Phong BRDF (R1), visibility against the analytic occluders (R3).
+ * ---------------------------------------------------------------------------------------- */
+static double dot3(const double a[3], const double b[3]) { return (a[0] * b[0] + a[1] * b[1]) + a[2] * b[2]; }
+
+static double lum3(double r, double g, double b) { return (0.2126 * r + 0.7152 * g) + 0.0722 * b; }
+
+static int seg_hits_sphere(const float *s, const double x[3], const double l[3], double tmin, double tmax)
+{
+    double c[3] = {s[0], s[1], s[2]};
+    double r = s[3];
+    double oc[3] = {x[0] - c[0], x[1] - c[1], x[2] - c[2]};
+    double b = dot3(oc, l);
+    double cc = dot3(oc, oc) - r * r;
+    double disc = b * b - cc;
+    if (disc < 0.0) return 0;
+    double sq = sqrt(disc);
+    double t0 = -b - sq, t1 = -b + sq;
+    return (t0 > tmin && t0 < tmax) || (t1 > tmin && t1 < tmax);
+}
+
+static int seg_hits_box(const float *bx, const double x[3], const double l[3], double tmin, double tmax)
+{
+    double tn[3], tf[3];
+    for (int a = 0; a < 3; ++a) {
+        double inv = 1.0 / l[a];
+        double t1 = ((double)bx[a] - x[a]) * inv;
+        double t2 = ((double)bx[3 + a] - x[a]) * inv;
+        tn[a] = fmin(t1, t2);
+        tf[a] = fmax(t1, t2);
+    }
+    double tnear = fmax(fmax(tn[0], tn[1]), tn[2]);
+    double tfar = fmin(fmin(tf[0], tf[1]), tf[2]);
+    return tnear <= tfar && tfar > tmin && tnear < tmax;
+}
+
+static int seg_hits_rect(const float *rc, const double x[3], const double l[3], double tmin, double tmax)
+{
+    double p0[3] = {rc[0], rc[1], rc[2]};
+    double e1[3] = {rc[3], rc[4], rc[5]};
+    double e2[3] = {rc[6], rc[7], rc[8]};
+    double nr[3] = {rc[9], rc[10], rc[11]};
+    double den = dot3(nr, l);
+    if (den == 0.0) return 0;
+    double pd[3] = {p0[0] - x[0], p0[1] - x[1], p0[2] - x[2]};
+    double t = dot3(pd, nr) / den;
+    if (!(t > tmin && t < tmax)) return 0;
+    double h[3] = {x[0] + t * l[0], x[1] + t * l[1], x[2] + t * l[2]};
+    double hp[3] = {h[0] - p0[0], h[1] - p0[1], h[2] - p0[2]};
+    double a = dot3(hp, e1) / dot3(e1, e1);
+    double b = dot3(hp, e2) / dot3(e2, e2);
+    return a >= 0.0 && a <= 1.0 && b >= 0.0 && b <= 1.0;
+}
+
+/* V(x, y): 1 iff no occluder is hit with t in (eps, dist - eps) along the segment. */
+static int visible_dir(const orc_inputs *in, const double x[3], const double l[3], double dist)
+{
+    double tmin = in->shadow_eps, tmax = dist - in->shadow_eps;
+    for (int k = 0; k < in->nsph; ++k)
+        if (seg_hits_sphere(in->sph + 4 * k, x, l, tmin, tmax)) return 0;
+    for (int k = 0; k < in->nbox; ++k)
+        if (seg_hits_box(in->box + 6 * k, x, l, tmin, tmax)) return 0;
+    for (int k = 0; k < in->nrect; ++k)
+        if (seg_hits_rect(in->rect + 12 * k, x, l, tmin, tmax)) return 0;
+    return 1;
+}
+
+int32_t orc_visible(const orc_inputs *in, const double x[3], const double y[3])
+{
+    double d[3] = {y[0] - x[0], y[1] - x[1], y[2] - x[2]};
+    double d2 = dot3(d, d);
+    if (d2 == 0.0) return 1;
+    double dist = sqrt(d2);
+    double l[3] = {d[0] / dist, d[1] / dist, d[2] / dist};
+    return visible_dir(in, x, l, dist);
+}
+
+static double powi(double base, int32_t e)
+{
+    double r = 1.0;
+    while (e > 0) {
+        if (e & 1) r = r * base;
+        base = base * base;
+        e >>= 1;
+    }
+    return r;
+}
+
+double orc_entry_T(const orc_inputs *in, int64_t p, int64_t v)
+{
+    double x[3] = {in->px[p], in->py[p], in->pz[p]};
+    double np_[3] = {in->nx[p], in->ny[p], in->nz[p]};
+    double o[3] = {in->vx[p], in->vy[p], in->vz[p]};
+    double y[3] = {in->lx[v], in->ly[v], in->lz[v]};
+    double nv[3] = {in->lnx[v], in->lny[v], in->lnz[v]};
+    double d[3] = {y[0] - x[0], y[1] - x[1], y[2] - x[2]};
+    double d2 = dot3(d, d);
+    if (d2 == 0.0) return 0.0;
+    double dist = sqrt(d2);
+    double l[3] = {d[0] / dist, d[1] / dist, d[2] / dist};
+    double ci = dot3(np_, l);
+    double cj = -dot3(nv, l);
+    if (ci <= 0.0 || cj <= 0.0) return 0.0;
+    double dc2 = in->clamp_dist * in->clamp_dist;
+    double G = (ci * cj) / fmax(d2, dc2);
+    double s = in->spec[p];
+    double phi;
+    if (s == 0.0) {
+        phi = INV_PI;
+    } else {
+        int32_t e = in->expo[p];
+        double rv = (2.0 * ci) * dot3(np_, o) - dot3(l, o);
+        double lobe = rv > 0.0 ? powi(rv, e) : 0.0;
+        phi = (1.0 - s) * INV_PI + (s * (((double)(e + 2)) * INV_2PI)) * lobe;
+    }
+    if (!visible_dir(in, x, l, dist)) return 0.0;
+    return phi * G;
+}
+
+static double lum_rho(const orc_inputs *in, int64_t p) { return lum3(in->rr[p], in->rg[p], in->rb[p]); }
+static double lum_node(const orc_inputs *in, int32_t f) { return lum3(in->tir[f], in->tig[f], in->tib[f]); }
+
+/* ------------------------------------------------------------------------------------------
+ * Matrix slicing (R26): rows as 6D points (x/D, w_n n), recursive binary
+ * split on the dimension of largest extent, lower median by (key, row), left gets ceil(n/2).
+ * ---------------------------------------------------------------------------------------- */
+typedef struct { double k; int32_t r; } keyrow;
+
+static int cmp_keyrow(const void *a, const void *b)
+{
+    const keyrow *x = a, *y = b;
+    if (x->k < y->k) return -1;
+    if (x->k > y->k) return 1;
+    return (x->r > y->r) - (x->r < y->r);
+}
+
+static double slice_key(const orc_inputs *in, int32_t r, int d)
+{
+    switch (d) {
+    case 0: return (double)in->px[r] / in->diag;
+    case 1: return (double)in->py[r] / in->diag;
+    case 2: return (double)in->pz[r] / in->diag;
+    case 3: return in->wn * (double)in->nx[r];
+    case 4: return in->wn * (double)in->ny[r];
+    default: return in->wn * (double)in->nz[r];
+    }
+}
+
+static void slice_rec(const orc_inputs *in, int32_t *rows, int32_t n, int32_t *off, int32_t *rows_out,
+                      int64_t *ns, int32_t *pos)
+{
+    if (n <= in->target) {
+        memcpy(rows_out + *pos, rows, (size_t)n * sizeof(int32_t));
+        *pos += n;
+        off[++(*ns)] = *pos;
+        return;
+    }
+    int best = 0;
+    double bext = -1.0;
+    for (int d = 0; d < 6; ++d) {
+        double lo = slice_key(in, rows[0], d), hi = lo;
+        for (int32_t i = 1; i < n; ++i) {
+            double k = slice_key(in, rows[i], d);
+            lo = fmin(lo, k);
+            hi = fmax(hi, k);
+        }
+        double ext = hi - lo;
+        if (ext > bext) { bext = ext; best = d; }
+    }
+    keyrow *kr = malloc((size_t)n * sizeof(keyrow));
+    for (int32_t i = 0; i < n; ++i) { kr[i].k = slice_key(in, rows[i], best); kr[i].r = rows[i]; }
+    qsort(kr, (size_t)n, sizeof(keyrow), cmp_keyrow);
+    for (int32_t i = 0; i < n; ++i) rows[i] = kr[i].r;
+    free(kr);
+    int32_t nl = (n + 1) / 2;
+    qsort(rows, (size_t)nl, sizeof(int32_t), cmp_i32);
+    qsort(rows + nl, (size_t)(n - nl), sizeof(int32_t), cmp_i32);
+    slice_rec(in, rows, nl, off, rows_out, ns, pos);
+    slice_rec(in, rows + nl, n - nl, off, rows_out, ns, pos);
+}
+
+int32_t orc_build_slices(const orc_inputs *in, int32_t *off, int32_t *rows, int64_t *nslices)
+{
+    int32_t m = (int32_t)in->m;
+    int32_t *work = malloc((size_t)(m > 0 ? m : 1) * sizeof(int32_t));
+    for (int32_t i = 0; i < m; ++i) work[i] = i;
+    int64_t ns = 0;
+    int32_t pos = 0;
+    off[0] = 0;
+    if (m > 0) slice_rec(in, work, m, off, rows, &ns, &pos);
+    free(work);
+    *nslices = ns;
+    return 0;
+}
+
+/* ------------------------------------------------------------------------------------------
+ * Small containers (hash map u64 -> double, dynamic arrays)
+ * ---------------------------------------------------------------------------------------- */
+typedef struct { uint64_t *key; double *val; int64_t cap, cnt; } hmap;
+
+static void hm_init(hmap *h, int64_t cap)
+{
+    int64_t c = 64;
+    while (c < 2 * cap) c <<= 1;
+    h->cap = c;
+    h->cnt = 0;
+    h->key = malloc((size_t)c * sizeof(uint64_t));
+    h->val = malloc((size_t)c * sizeof(double));
+    for (int64_t i = 0; i < c; ++i) h->key[i] = UINT64_MAX;
+}
+static void hm_free(hmap *h) { free(h->key); free(h->val); }
+static uint64_t hm_hash(uint64_t k) { k ^= k >> 33; k *= 0xff51afd7ed558ccdULL; k ^= k >> 33; return k; }
+static int hm_get(const hmap *h, uint64_t k, double *v)
+{
+    uint64_t i = hm_hash(k) & (uint64_t)(h->cap - 1);
+    while (h->key[i] != UINT64_MAX) {
+        if (h->key[i] == k) { *v = h->val[i]; return 1; }
+        i = (i + 1) & (uint64_t)(h->cap - 1);
+    }
+    return 0;
+}
+static void hm_put(hmap *h, uint64_t k, double v);
+static void hm_grow(hmap *h)
+{
+    hmap n;
+    hm_init(&n, h->cap);
+    for (int64_t i = 0; i < h->cap; ++i)
+        if (h->key[i] != UINT64_MAX) hm_put(&n, h->key[i], h->val[i]);
+    hm_free(h);
+    *h = n;
+}
+static void hm_put(hmap *h, uint64_t k, double v)
+{
+    if (2 * (h->cnt + 1) > h->cap) hm_grow(h);
+    uint64_t i = hm_hash(k) & (uint64_t)(h->cap - 1);
+    while (h->key[i] != UINT64_MAX) {
+        if (h->key[i] == k) { h->val[i] = v; return; }
+        i = (i + 1) & (uint64_t)(h->cap - 1);
+    }
+    h->key[i] = k;
+    h->val[i] = v;
+    h->cnt++;
+}
+
+typedef struct { int32_t *a; int64_t n, cap; } ivec;
+static void iv_push(ivec *v, int32_t x)
+{
+    if (v->n == v->cap) { v->cap = v->cap ? 2 * v->cap : 64; v->a = realloc(v->a, (size_t)v->cap * sizeof(int32_t)); }
+    v->a[v->n++] = x;
+}
+typedef struct { double *a; int64_t n, cap; } dvec;
+static void dv_push(dvec *v, double x)
+{
+    if (v->n == v->cap) { v->cap = v->cap ? 2 * v->cap : 64; v->a = realloc(v->a, (size_t)v->cap * sizeof(double)); }
+    v->a[v->n++] = x;
+}
+
+/* ------------------------------------------------------------------------------------------
+ * Per-slice state
+ * ---------------------------------------------------------------------------------------- */
+typedef struct {
+    const orc_inputs *in;
+    const int32_t *rows;
+    int32_t m, s;
+    hmap Tcache;                /* key (vpl << 16 | local row) -> T */
+    int64_t evals;
+} slice_ctx;
+
+static double T_cached(slice_ctx *c, int32_t i, int32_t vpl)
+{
+    uint64_t k = ((uint64_t)(uint32_t)vpl << 16) | (uint64_t)(uint32_t)i;
+    double v;
+    if (hm_get(&c->Tcache, k, &v)) return v;
+    v = orc_entry_T(c->in, c->rows[i], vpl);
+    hm_put(&c->Tcache, k, v);
+    c->evals++;
+    return v;
+}
+
+/* Pass-1 count n_f, linearly proportional to lum(I_f) (reading R6) */
+static int32_t n_of(const orc_inputs *in, int32_t m, double lum, double lmax)
+{
+    int32_t n;
+    if (lmax > 0.0) {
+        double x = ceil(((double)in->nmax * lum) / lmax);
+        n = x > (double)in->nmin ? (int32_t)x : in->nmin;
+    } else {
+        n = in->nmin;
+    }
+    return n < m ? n : m;
+}
+
+static uint64_t splitmix(uint64_t *s)
+{
+    uint64_t z = (*s += 0x9E3779B97F4A7C15ULL);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+/* ------------------------------------------------------------------------------------------
+ * Light coarsening (Eq. (1); readings R5, R8-R11).
+ * ---------------------------------------------------------------------------------------- */
+static void coarsen(slice_ctx *c, orc_slice_result *res, const int32_t *parent)
+{
+    const orc_inputs *in = c->in;
+    int64_t nn = in->nn;
+    uint8_t *in_cut = calloc((size_t)nn, 1);
+    uint8_t *merged = calloc((size_t)nn, 1);
+    double *cost = calloc((size_t)nn, sizeof(double));
+    int32_t *zidx = malloc((size_t)nn * sizeof(int32_t)); /* processed-record index of merged nodes */
+    for (int64_t k = 0; k < in->ncut; ++k) in_cut[in->cut[k]] = 1; /* cost = 0 on g */
+
+    /* base pairs B = parents with both children in g; l_max over B (global, R6) */
+    ivec work = {0};
+    double lmax = 0.0;
+    for (int64_t k = 0; k < in->ncut; ++k) {
+        int32_t g = in->cut[k];
+        int32_t f = parent[g];
+        if (f < 0 || in->left[f] != g) continue; /* visit each parent once, via its left child */
+        if (in_cut[in->right[f]]) {
+            iv_push(&work, f);
+            double lf = lum_node(in, f);
+            if (lf > lmax) lmax = lf;
+        }
+    }
+    qsort(work.a, (size_t)work.n, sizeof(int32_t), cmp_i32);
+
+    ivec pnode = {0}, pmerged = {0}, zoff = {0}, zrows = {0};
+    dvec peps = {0}, pcost = {0}, pva = {0}, pvb = {0};
+    iv_push(&zoff, 0);
+    int32_t *buf = malloc((size_t)(2 * c->m + 2) * sizeof(int32_t));
+    int32_t *fresh = malloc((size_t)(c->m + 1) * sizeof(int32_t));
+    uint64_t rs = in->order_seed;
+    int64_t head = 0;
+    while (head < work.n) {
+        int32_t f;
+        if (in->order_seed) { /* order-independence pin: process a random pending candidate */
+            int64_t pick = head + (int64_t)(splitmix(&rs) % (uint64_t)(work.n - head));
+            f = work.a[pick];
+            work.a[pick] = work.a[head];
+            work.a[head] = f;
+        } else {
+            f = work.a[head];
+        }
+        head++;
+        int32_t l = in->left[f], r = in->right[f];
+        /* "L_f is the same as L_a except intensity": a shares rep(f) (R5) */
+        int32_t a = (in->rep[l] == in->rep[f]) ? l : r;
+        int32_t b = (a == l) ? r : l;
+        /* zeta_f (R10) */
+        int32_t nz = 0;
+        if (!merged[l] && !merged[r]) {
+            nz = orc_floyd(c->m, n_of(in, c->m, lum_node(in, f), lmax), (uint32_t)f, c->s, in->seed, TAG_P1, buf);
+        } else {
+            const int32_t *A, *Bv;
+            int32_t na, nb;
+            if (merged[l] && merged[r]) {
+                A = zrows.a + zoff.a[zidx[l]]; na = zoff.a[zidx[l] + 1] - zoff.a[zidx[l]];
+                Bv = zrows.a + zoff.a[zidx[r]]; nb = zoff.a[zidx[r] + 1] - zoff.a[zidx[r]];
+            } else {
+                int32_t h = merged[l] ? l : r, o = merged[l] ? r : l;
+                A = zrows.a + zoff.a[zidx[h]]; na = zoff.a[zidx[h] + 1] - zoff.a[zidx[h]];
+                nb = orc_floyd(c->m, n_of(in, c->m, lum_node(in, o), lmax), (uint32_t)f, c->s, in->seed, TAG_P1, fresh);
+                Bv = fresh;
+            }
+            /* sorted set union */
+            int32_t i = 0, j = 0;
+            while (i < na || j < nb) {
+                if (j >= nb || (i < na && A[i] < Bv[j])) buf[nz++] = A[i++];
+                else if (i >= na || Bv[j] < A[i]) buf[nz++] = Bv[j++];
+                else { buf[nz++] = A[i++]; j++; }
+            }
+        }
+        /* V_a, V_b on zeta_f and the merge error (R8) */
+        double la = lum_node(in, a), lb = lum_node(in, b);
+        double eps = 0.0;
+        double ratio = la > 0.0 ? lb / la : 0.0;
+        for (int32_t k = 0; k < nz; ++k) {
+            int32_t i = buf[k];
+            double Ta = T_cached(c, i, in->rep[a]);
+            double Tb = T_cached(c, i, in->rep[b]);
+            double lr = lum_rho(in, c->rows[i]);
+            double Va = (lr * la) * Ta;
+            double Vb = (lr * lb) * Tb;
+            double e = la > 0.0 ? fabs(Vb - Va * ratio) : fabs(Vb);
+            if (e > eps) eps = e;
+            iv_push(&zrows, i);
+            dv_push(&pva, Ta);
+            dv_push(&pvb, Tb);
+        }
+        /* Eq. (1): cost(L_f) = eps(L_f) + cost(L_b) (R9) */
+        double cf = eps + cost[b];
+        int do_merge = cf < in->tau; /* P:116 "less than a prespecified error bound" (R11) */
+        zidx[f] = (int32_t)pnode.n;
+        iv_push(&pnode, f);
+        iv_push(&pmerged, do_merge);
+        dv_push(&peps, eps);
+        dv_push(&pcost, cf);
+        iv_push(&zoff, (int32_t)zrows.n);
+        if (do_merge) {
+            in_cut[l] = 0;
+            in_cut[r] = 0;
+            in_cut[f] = 1;
+            merged[f] = 1;
+            cost[f] = cf;
+            int32_t p = parent[f];
+            if (p >= 0) {
+                int32_t sib = in->left[p] == f ? in->right[p] : in->left[p];
+                if (in_cut[sib]) iv_push(&work, p);
+            }
+        }
+    }
+    /* final cut, sorted by node id = column order (R29) */
+    int32_t n = 0;
+    ivec cutv = {0};
+    for (int64_t k = 0; k < in->ncut; ++k) {
+        /* walk up from every g node to its topmost cut ancestor-or-self */
+        int32_t g = in->cut[k];
+        int32_t t = g;
+        while (!in_cut[t]) t = parent[t];
+        iv_push(&cutv, t);
+    }
+    qsort(cutv.a, (size_t)cutv.n, sizeof(int32_t), cmp_i32);
+    for (int64_t k = 0; k < cutv.n; ++k)
+        if (k == 0 || cutv.a[k] != cutv.a[k - 1]) cutv.a[n++] = cutv.a[k];
+    res->n = n;
+    res->cut_nodes = malloc((size_t)(n > 0 ? n : 1) * sizeof(int32_t));
+    memcpy(res->cut_nodes, cutv.a, (size_t)n * sizeof(int32_t));
+    res->n_proc = (int32_t)pnode.n;
+    res->proc_node = pnode.a;
+    res->proc_merged = pmerged.a;
+    res->proc_eps = peps.a;
+    res->proc_cost = pcost.a;
+    res->proc_zoff = zoff.a;
+    res->proc_zrows = zrows.a;
+    res->proc_Va = pva.a;
+    res->proc_Vb = pvb.a;
+    free(cutv.a);
+    free(work.a);
+    free(buf);
+    free(fresh);
+    free(in_cut);
+    free(merged);
+    free(cost);
+    free(zidx);
+}
+
+/* ------------------------------------------------------------------------------------------
+ * Sampling pass 2 (Eq. (2); readings R13-R17, R27).
+ * ---------------------------------------------------------------------------------------- */
+static void pass2(slice_ctx *c, orc_slice_result *res)
+{
+    const orc_inputs *in = c->in;
+    int32_t m = c->m, n = res->n;
+    uint8_t *obs = calloc((size_t)m * (size_t)(n > 0 ? n : 1), 1);
+    uint8_t *carried = calloc((size_t)m * (size_t)(n > 0 ? n : 1), 1);
+    double *val = calloc((size_t)m * (size_t)(n > 0 ? n : 1), sizeof(double));
+    int32_t *colcnt = calloc((size_t)(n > 0 ? n : 1), sizeof(int32_t));
+    /* carried observations ("we have actually sparsely sampled the lighting matrices", R13) */
+    int64_t n_obs = 0;
+    for (int32_t cc = 0; cc < n; ++cc) {
+        int32_t node = res->cut_nodes[cc];
+        int32_t v = in->rep[node];
+        double lI = lum_node(in, node);
+        for (int32_t i = 0; i < m; ++i) {
+            double T;
+            uint64_t k = ((uint64_t)(uint32_t)v << 16) | (uint64_t)(uint32_t)i;
+            if (hm_get(&c->Tcache, k, &T)) {
+                size_t at = (size_t)i * (size_t)n + (size_t)cc;
+                obs[at] = 1;
+                carried[at] = 1;
+                val[at] = (lum_rho(in, c->rows[i]) * lI) * T;
+                colcnt[cc]++;
+                n_obs++;
+            }
+        }
+    }
+    res->n_carried = n_obs;
+    /* light importance g(j) = max(C_j) - min(C_j) over observed entries (R14) */
+    uint32_t *w = malloc((size_t)(n > 0 ? n : 1) * sizeof(uint32_t));
+    double *g = calloc((size_t)(n > 0 ? n : 1), sizeof(double));
+    double G = 0.0;
+    for (int32_t cc = 0; cc < n; ++cc) {
+        if (!colcnt[cc]) continue;
+        double lo = INFINITY, hi = -INFINITY;
+        for (int32_t i = 0; i < m; ++i) {
+            size_t at = (size_t)i * (size_t)n + (size_t)cc;
+            if (obs[at]) { lo = fmin(lo, val[at]); hi = fmax(hi, val[at]); }
+        }
+        g[cc] = hi - lo;
+        if (g[cc] > G) G = g[cc];
+    }
+    /* pixel importance f(i) = 1; pdf(i,j) ∝ f(i) g(j) (Eq. 2) as integer weights (R14) */
+    if (G > 0.0) {
+        uint64_t sumw = 0;
+        int32_t nobsc = 0;
+        for (int32_t cc = 0; cc < n; ++cc) {
+            if (!colcnt[cc]) continue;
+            double x = floor(1048575.0 * (g[cc] / G));
+            uint32_t wc = 1u + (uint32_t)x;
+            w[cc] = wc > 65536u ? wc : 65536u;
+            sumw += w[cc];
+            nobsc++;
+        }
+        uint32_t wu = nobsc ? (uint32_t)(sumw / (uint64_t)nobsc) : 524288u;
+        for (int32_t cc = 0; cc < n; ++cc)
+            if (!colcnt[cc]) w[cc] = wu;
+    } else {
+        for (int32_t cc = 0; cc < n; ++cc) w[cc] = 1u;
+    }
+    uint64_t *cdf = malloc((size_t)(n > 0 ? n : 1) * sizeof(uint64_t));
+    uint64_t W = 0;
+    for (int32_t cc = 0; cc < n; ++cc) { W += w[cc]; cdf[cc] = W; }
+    /* draw: column by g, then row uniformly; skip already-sampled entries (R15, R16) */
+    int64_t N = (int64_t)ceil(((double)((int64_t)m * (int64_t)n)) * in->rate);
+    res->target_N = N;
+    int64_t n_new = 0, t = 0;
+    for (t = 0; t < 64 * N && n_obs < N; ++t) {
+        uint32_t u[4];
+        philox_draw(in->seed, (uint32_t)t, 0u, (uint32_t)c->s, TAG_P2, u);
+        uint64_t x = ((uint64_t)u[0] * W) >> 32;
+        int32_t lo = 0, hi = n - 1; /* smallest c with CDF_c > x */
+        while (lo < hi) {
+            int32_t mid = (lo + hi) / 2;
+            if (cdf[mid] > x) hi = mid; else lo = mid + 1;
+        }
+        int32_t cc = lo;
+        int32_t i = (int32_t)randint(u[1], (uint32_t)m);
+        size_t at = (size_t)i * (size_t)n + (size_t)cc;
+        if (!obs[at]) {
+            obs[at] = 1;
+            double T = T_cached(c, i, in->rep[res->cut_nodes[cc]]);
+            val[at] = (lum_rho(in, c->rows[i]) * lum_node(in, res->cut_nodes[cc])) * T;
+            colcnt[cc]++;
+            n_obs++;
+            n_new++;
+        }
+    }
+    res->n_draws = t;
+    res->n_new = n_new;
+    /* forced sample for every still-empty column (R17) */
+    int64_t n_forced = 0;
+    for (int32_t cc = 0; cc < n; ++cc) {
+        if (colcnt[cc]) continue;
+        uint32_t u[4];
+        philox_draw(in->seed, (uint32_t)cc, 0u, (uint32_t)c->s, TAG_FORCE, u);
+        int32_t i = (int32_t)randint(u[0], (uint32_t)m);
+        size_t at = (size_t)i * (size_t)n + (size_t)cc;
+        obs[at] = 1;
+        double T = T_cached(c, i, in->rep[res->cut_nodes[cc]]);
+        val[at] = (lum_rho(in, c->rows[i]) * lum_node(in, res->cut_nodes[cc])) * T;
+        colcnt[cc]++;
+        n_obs++;
+        n_forced++;
+    }
+    res->n_forced = n_forced;
+    /* Omega in CSR order */
+    res->nnz = n_obs;
+    res->om_row = malloc((size_t)(n_obs > 0 ? n_obs : 1) * sizeof(int32_t));
+    res->om_col = malloc((size_t)(n_obs > 0 ? n_obs : 1) * sizeof(int32_t));
+    res->om_val = malloc((size_t)(n_obs > 0 ? n_obs : 1) * sizeof(double));
+    res->om_carried = malloc((size_t)(n_obs > 0 ? n_obs : 1) * sizeof(int32_t));
+    int64_t k = 0;
+    for (int32_t i = 0; i < m; ++i)
+        for (int32_t cc = 0; cc < n; ++cc) {
+            size_t at = (size_t)i * (size_t)n + (size_t)cc;
+            if (!obs[at]) continue;
+            res->om_row[k] = i;
+            res->om_col[k] = cc;
+            res->om_val[k] = val[at];
+            res->om_carried[k] = carried[at];
+            k++;
+        }
+    res->weights = w;
+    free(cdf);
+    free(g);
+    free(obs);
+    free(carried);
+    free(val);
+    free(colcnt);
+}
+
+/* ------------------------------------------------------------------------------------------
+ * Dense helpers for the completion (fp64, plain loops)
+ * ---------------------------------------------------------------------------------------- */
+/* unpivoted Cholesky A = L L^T in place (lower), A is q x q SPD; returns 0 on failure */
+static int chol(double *A, int q)
+{
+    for (int j = 0; j < q; ++j) {
+        double d = A[j * q + j];
+        for (int k = 0; k < j; ++k) d -= A[j * q + k] * A[j * q + k];
+        if (!(d > 0.0)) return 0;
+        d = sqrt(d);
+        A[j * q + j] = d;
+        for (int i = j + 1; i < q; ++i) {
+            double s = A[i * q + j];
+            for (int k = 0; k < j; ++k) s -= A[i * q + k] * A[j * q + k];
+            A[i * q + j] = s / d;
+        }
+    }
+    return 1;
+}
+/* solve L L^T x = b in place */
+static void chol_solve(const double *L, int q, double *b)
+{
+    for (int i = 0; i < q; ++i) {
+        double s = b[i];
+        for (int k = 0; k < i; ++k) s -= L[i * q + k] * b[k];
+        b[i] = s / L[i * q + i];
+    }
+    for (int i = q - 1; i >= 0; --i) {
+        double s = b[i];
+        for (int k = i + 1; k < q; ++k) s -= L[k * q + i] * b[k];
+        b[i] = s / L[i * q + i];
+    }
+}
+
+static double max_omega(int64_t nnz, const double *val)
+{
+    double s = 0.0;
+    for (int64_t k = 0; k < nnz; ++k) s = fmax(s, val[k]);
+    return s;
+}
+
+/* R20: X_0, Y_0 Philox-uniform scaled so that E[X_0 Y_0] = mean_Omega(M^) */
+static void init_factors(int32_t m, int32_t n, int32_t q, double c0, uint64_t seed, int32_t s, double *X, double *Y)
+{
+    for (int32_t i = 0; i < m; ++i)
+        for (int32_t l = 0; l < q; ++l) {
+            uint32_t u[4];
+            philox_draw(seed, (uint32_t)i, (uint32_t)l, (uint32_t)s, TAG_X0, u);
+            X[(size_t)i * q + l] = c0 * unif(u[0]);
+        }
+    for (int32_t l = 0; l < q; ++l)
+        for (int32_t j = 0; j < n; ++j) {
+            uint32_t u[4];
+            philox_draw(seed, (uint32_t)l, (uint32_t)j, (uint32_t)s, TAG_Y0, u);
+            Y[(size_t)l * n + j] = c0 * unif(u[0]);
+        }
+}
+
+/* ------------------------------------------------------------------------------------------
+ * ADM nonnegative factorisation (Appendix A; typo readings R18).
+ * Literal: Z is kept dense (m x n), every product is formed as written.
+ * ---------------------------------------------------------------------------------------- */
+int32_t orc_adm(int32_t m, int32_t n, int64_t nnz, const int32_t *row, const int32_t *col, const double *val,
+                int32_t q, int32_t K, double tol, double alpha, double beta, double gamma, uint64_t seed,
+                int32_t slice, double *U, double *V, int32_t *iters, double *resid, double *sigma)
+{
+    size_t mq = (size_t)m * q, qn = (size_t)q * n, mn = (size_t)m * n;
+    double sg = max_omega(nnz, val); /* R23 */
+    *sigma = sg;
+    *iters = 0;
+    *resid = 0.0;
+    if (sg == 0.0) {
+        memset(U, 0, mq * sizeof(double));
+        memset(V, 0, qn * sizeof(double));
+        return ORC_FLAG_ZERO;
+    }
+    double *Mh = malloc((size_t)nnz * sizeof(double));
+    double mu = 0.0, nrmM = 0.0;
+    for (int64_t k = 0; k < nnz; ++k) { Mh[k] = val[k] / sg; mu += Mh[k]; nrmM += Mh[k] * Mh[k]; }
+    mu = mu / (double)nnz;
+    nrmM = sqrt(nrmM);
+    double c0 = 2.0 * sqrt(mu / (double)q);
+    double *X = malloc(mq * sizeof(double)), *Y = malloc(qn * sizeof(double));
+    double *Lam = calloc(mq, sizeof(double)), *Pi = calloc(qn, sizeof(double));
+    double *Z = calloc(mn, sizeof(double)), *W = malloc(mn * sizeof(double));
+    double *A = malloc((size_t)q * q * sizeof(double));
+    double *rhs = malloc((size_t)(q > 0 ? q : 1) * sizeof(double));
+    init_factors(m, n, q, c0, seed, slice, X, Y);
+    memcpy(U, X, mq * sizeof(double));
+    memcpy(V, Y, qn * sizeof(double));
+    for (int64_t k = 0; k < nnz; ++k) Z[(size_t)row[k] * n + col[k]] = Mh[k]; /* Z_0 = P_Omega(M) */
+    int32_t flags = 0;
+    int32_t it;
+    for (it = 0; it < K; ++it) {
+        /* X_{k+1} = (Z_k Y_k^T + alpha U_k - Lambda_k)(Y_k Y_k^T + alpha I)^{-1} */
+        for (int a = 0; a < q; ++a)
+            for (int b = 0; b < q; ++b) {
+                double s = 0.0;
+                for (int32_t j = 0; j < n; ++j) s += Y[(size_t)a * n + j] * Y[(size_t)b * n + j];
+                A[a * q + b] = s + (a == b ? alpha : 0.0);
+            }
+        if (!chol(A, q)) { flags |= ORC_FLAG_DIVERGED; break; }
+        for (int32_t i = 0; i < m; ++i) {
+            for (int a = 0; a < q; ++a) {
+                double s = 0.0;
+                for (int32_t j = 0; j < n; ++j) s += Z[(size_t)i * n + j] * Y[(size_t)a * n + j];
+                rhs[a] = s + alpha * U[(size_t)i * q + a] - Lam[(size_t)i * q + a];
+            }
+            chol_solve(A, q, rhs); /* (G + aI) symmetric: x (G + aI) = r  <=>  (G + aI) x^T = r^T */
+            for (int a = 0; a < q; ++a) X[(size_t)i * q + a] = rhs[a];
+        }
+        /* Y_{k+1} = (X_{k+1}^T X_{k+1} + beta I)^{-1}(X_{k+1}^T Z_k + beta V_k - Pi_k)   (R18: X^T Z) */
+        for (int a = 0; a < q; ++a)
+            for (int b = 0; b < q; ++b) {
+                double s = 0.0;
+                for (int32_t i = 0; i < m; ++i) s += X[(size_t)i * q + a] * X[(size_t)i * q + b];
+                A[a * q + b] = s + (a == b ? beta : 0.0);
+            }
+        if (!chol(A, q)) { flags |= ORC_FLAG_DIVERGED; break; }
+        for (int32_t j = 0; j < n; ++j) {
+            for (int a = 0; a < q; ++a) {
+                double s = 0.0;
+                for (int32_t i = 0; i < m; ++i) s += X[(size_t)i * q + a] * Z[(size_t)i * n + j];
+                rhs[a] = s + beta * V[(size_t)a * n + j] - Pi[(size_t)a * n + j];
+            }
+            chol_solve(A, q, rhs);
+            for (int a = 0; a < q; ++a) Y[(size_t)a * n + j] = rhs[a];
+        }
+        /* Z_{k+1} = X_{k+1} Y_{k+1} + P_Omega(M - X_{k+1} Y_{k+1})   (R18: P_Omega keeps Omega) */
+        for (int32_t i = 0; i < m; ++i)
+            for (int32_t j = 0; j < n; ++j) {
+                double s = 0.0;
+                for (int a = 0; a < q; ++a) s += X[(size_t)i * q + a] * Y[(size_t)a * n + j];
+                W[(size_t)i * n + j] = s;
+            }
+        memcpy(Z, W, mn * sizeof(double));
+        double r2 = 0.0;
+        for (int64_t k = 0; k < nnz; ++k) {
+            size_t at = (size_t)row[k] * n + col[k];
+            double d = Mh[k] - W[at];
+            r2 += d * d;
+            Z[at] = Mh[k];
+        }
+        /* U_{k+1} = P_+(X_{k+1} + Lambda_k/alpha);  V_{k+1} = P_+(Y_{k+1} + Pi_k/beta) */
+        for (size_t e = 0; e < mq; ++e) U[e] = fmax(0.0, X[e] + Lam[e] / alpha);
+        for (size_t e = 0; e < qn; ++e) V[e] = fmax(0.0, Y[e] + Pi[e] / beta);
+        /* Lambda_{k+1} = Lambda_k + gamma alpha (X_{k+1} - U_{k+1})   (R18: Lambda_k on the right) */
+        for (size_t e = 0; e < mq; ++e) Lam[e] = Lam[e] + gamma * alpha * (X[e] - U[e]);
+        for (size_t e = 0; e < qn; ++e) Pi[e] = Pi[e] + gamma * beta * (Y[e] - V[e]);
+        double r = sqrt(r2) / nrmM;
+        *resid = r;
+        if (!isfinite(r)) { flags |= ORC_FLAG_DIVERGED; it++; break; }
+        if (r < tol) { it++; break; } /* P:149 "stop ... when the error is below a tolerance" (R21) */
+    }
+    *iters = it;
+    for (size_t e = 0; e < qn; ++e) V[e] = sg * V[e]; /* R22: output (U, sigma V) */
+    free(Mh); free(X); free(Y); free(Lam); free(Pi); free(Z); free(W); free(A); free(rhs);
+    return flags;
+}
+
+/* ------------------------------------------------------------------------------------------
+ * Masked ALS (BASELINE north_star): per-row / per-column ridge normal equations over Omega.
+ * ---------------------------------------------------------------------------------------- */
+static double mals_objective(int32_t m, int32_t n, int32_t q, int64_t nnz, const int32_t *row, const int32_t *col,
+                             const double *Mh, const double *X, const double *Y, double lam)
+{
+    double f = 0.0;
+    for (int64_t k = 0; k < nnz; ++k) {
+        double s = 0.0;
+        for (int a = 0; a < q; ++a) s += X[(size_t)row[k] * q + a] * Y[(size_t)a * n + col[k]];
+        double d = s - Mh[k];
+        f += d * d;
+    }
+    double rx = 0.0, ry = 0.0;
+    for (size_t e = 0; e < (size_t)m * q; ++e) rx += X[e] * X[e];
+    for (size_t e = 0; e < (size_t)q * n; ++e) ry += Y[e] * Y[e];
+    return f + lam * (rx + ry);
+}
+
+int32_t orc_mals(int32_t m, int32_t n, int64_t nnz, const int32_t *row, const int32_t *col, const double *val,
+                 int32_t q, int32_t K, double lam, uint64_t seed, int32_t slice, double *X, double *Y,
+                 double *obj, double *sigma)
+{
+    size_t mq = (size_t)m * q, qn = (size_t)q * n;
+    double sg = max_omega(nnz, val);
+    *sigma = sg;
+    if (sg == 0.0) {
+        memset(X, 0, mq * sizeof(double));
+        memset(Y, 0, qn * sizeof(double));
+        return ORC_FLAG_ZERO;
+    }
+    double *Mh = malloc((size_t)nnz * sizeof(double));
+    double mu = 0.0;
+    for (int64_t k = 0; k < nnz; ++k) { Mh[k] = val[k] / sg; mu += Mh[k]; }
+    mu = mu / (double)nnz;
+    double c0 = 2.0 * sqrt(mu / (double)q);
+    init_factors(m, n, q, c0, seed, slice, X, Y);
+    /* CSC order: column-major listing of Omega (ascending row within a column) */
+    int64_t *cptr = calloc((size_t)n + 1, sizeof(int64_t));
+    int64_t *cidx = malloc((size_t)(nnz > 0 ? nnz : 1) * sizeof(int64_t));
+    for (int64_t k = 0; k < nnz; ++k) cptr[col[k] + 1]++;
+    for (int32_t j = 0; j < n; ++j) cptr[j + 1] += cptr[j];
+    int64_t *fill = malloc((size_t)(n > 0 ? n : 1) * sizeof(int64_t));
+    for (int32_t j = 0; j < n; ++j) fill[j] = cptr[j];
+    for (int64_t k = 0; k < nnz; ++k) cidx[fill[col[k]]++] = k;
+    int64_t *rptr = calloc((size_t)m + 1, sizeof(int64_t));
+    for (int64_t k = 0; k < nnz; ++k) rptr[row[k] + 1]++;
+    for (int32_t i = 0; i < m; ++i) rptr[i + 1] += rptr[i];
+    double *A = malloc((size_t)q * q * sizeof(double)), *b = malloc((size_t)q * sizeof(double));
+    int32_t flags = 0;
+    for (int32_t it = 0; it < K; ++it) {
+        /* X half: x_i = (sum_{j in Omega_i} y_j y_j^T + lam I)^{-1} sum_j M_ij y_j */
+        for (int32_t i = 0; i < m; ++i) {
+            for (int e = 0; e < q * q; ++e) A[e] = 0.0;
+            for (int a = 0; a < q; ++a) b[a] = 0.0;
+            for (int64_t k = rptr[i]; k < rptr[i + 1]; ++k) {
+                int32_t j = col[k];
+                for (int a = 0; a < q; ++a) {
+                    for (int c = 0; c < q; ++c) A[a * q + c] += Y[(size_t)a * n + j] * Y[(size_t)c * n + j];
+                    b[a] += Mh[k] * Y[(size_t)a * n + j];
+                }
+            }
+            for (int a = 0; a < q; ++a) A[a * q + a] += lam;
+            if (!chol(A, q)) { flags |= ORC_FLAG_DIVERGED; goto done; }
+            chol_solve(A, q, b);
+            for (int a = 0; a < q; ++a) X[(size_t)i * q + a] = b[a];
+        }
+        if (obj) obj[2 * it] = mals_objective(m, n, q, nnz, row, col, Mh, X, Y, lam);
+        /* Y half: y_j = (sum_{i in Omega^j} x_i x_i^T + lam I)^{-1} sum_i M_ij x_i */
+        for (int32_t j = 0; j < n; ++j) {
+            for (int e = 0; e < q * q; ++e) A[e] = 0.0;
+            for (int a = 0; a < q; ++a) b[a] = 0.0;
+            for (int64_t t = cptr[j]; t < cptr[j + 1]; ++t) {
+                int64_t k = cidx[t];
+                int32_t i = row[k];
+                for (int a = 0; a < q; ++a) {
+                    for (int c = 0; c < q; ++c) A[a * q + c] += X[(size_t)i * q + a] * X[(size_t)i * q + c];
+                    b[a] += Mh[k] * X[(size_t)i * q + a];
+                }
+            }
+            for (int a = 0; a < q; ++a) A[a * q + a] += lam;
+            if (!chol(A, q)) { flags |= ORC_FLAG_DIVERGED; goto done; }
+            chol_solve(A, q, b);
+            for (int a = 0; a < q; ++a) Y[(size_t)a * n + j] = b[a];
+        }
+        if (obj) obj[2 * it + 1] = mals_objective(m, n, q, nnz, row, col, Mh, X, Y, lam);
+    }
+    for (size_t e = 0; e < qn; ++e)
+        if (!isfinite(Y[e])) flags |= ORC_FLAG_DIVERGED;
+done:
+    for (size_t e = 0; e < qn; ++e) Y[e] = sg * Y[e];
+    free(Mh); free(cptr); free(cidx); free(fill); free(rptr); free(A); free(b);
+    return flags;
+}
+
+/* ------------------------------------------------------------------------------------------
+ * Image rendering of a slice: I(s) = X (Y e) with RGB weights (R4, O9).
+ * ---------------------------------------------------------------------------------------- */
+static void resolve(const orc_inputs *in, orc_slice_result *res)
+{
+    int32_t m = res->m, n = res->n, q = res->q;
+    res->rgb = calloc((size_t)m * 3, sizeof(double));
+    double *w = malloc((size_t)3 * (size_t)(n > 0 ? n : 1) * sizeof(double));
+    for (int32_t c = 0; c < n; ++c) {
+        int32_t f = res->cut_nodes[c];
+        double lI = lum_node(in, f);
+        w[0 * n + c] = lI != 0.0 ? (double)in->tir[f] / lI : 0.0;
+        w[1 * n + c] = lI != 0.0 ? (double)in->tig[f] / lI : 0.0;
+        w[2 * n + c] = lI != 0.0 ? (double)in->tib[f] / lI : 0.0;
+    }
+    if (res->flags & ORC_FLAG_ZERO) { free(w); return; }
+    for (int32_t i = 0; i < m; ++i) {
+        int32_t p = res->rows[i];
+        double lr = lum_rho(in, p);
+        double tint[3] = {lr != 0.0 ? (double)in->rr[p] / lr : 0.0, lr != 0.0 ? (double)in->rg[p] / lr : 0.0,
+                          lr != 0.0 ? (double)in->rb[p] / lr : 0.0};
+        for (int k = 0; k < 3; ++k) {
+            double s = 0.0;
+            if (res->flags & ORC_FLAG_DIRECT) {
+                for (int32_t c = 0; c < n; ++c) s += res->full[(size_t)i * n + c] * w[k * n + c];
+            } else {
+                for (int a = 0; a < q; ++a) {
+                    double t = 0.0; /* t^k = V w^k */
+                    for (int32_t c = 0; c < n; ++c) t += res->V[(size_t)a * n + c] * w[k * n + c];
+                    s += res->U[(size_t)i * q + a] * t;
+                }
+            }
+            res->rgb[(size_t)i * 3 + k] = tint[k] * s;
+        }
+    }
+    free(w);
+}
+
+static void direct_full(slice_ctx *c, orc_slice_result *res)
+{
+    const orc_inputs *in = c->in;
+    int32_t m = res->m, n = res->n;
+    res->full = malloc((size_t)m * (size_t)(n > 0 ? n : 1) * sizeof(double));
+    for (int32_t i = 0; i < m; ++i)
+        for (int32_t cc = 0; cc < n; ++cc) {
+            int32_t f = res->cut_nodes[cc];
+            double T = T_cached(c, i, in->rep[f]);
+            res->full[(size_t)i * n + cc] = (lum_rho(in, c->rows[i]) * lum_node(in, f)) * T;
+        }
+}
+
+static int32_t *make_parent(const orc_inputs *in)
+{
+    int32_t *parent = malloc((size_t)in->nn * sizeof(int32_t));
+    for (int64_t f = 0; f < in->nn; ++f) parent[f] = -1;
+    for (int64_t f = 0; f < in->nn; ++f)
+        if (in->left[f] >= 0) { parent[in->left[f]] = (int32_t)f; parent[in->right[f]] = (int32_t)f; }
+    return parent;
+}
+
+static orc_slice_result *run_slice(const orc_inputs *in, const int32_t *parent, const int32_t *rows, int32_t m,
+                                   int32_t s, int32_t stage)
+{
+    orc_slice_result *res = calloc(1, sizeof(orc_slice_result));
+    res->slice = s;
+    res->m = m;
+    res->q = in->q;
+    res->rows = malloc((size_t)(m > 0 ? m : 1) * sizeof(int32_t));
+    memcpy(res->rows, rows, (size_t)m * sizeof(int32_t));
+    slice_ctx c;
+    c.in = in;
+    c.rows = rows;
+    c.m = m;
+    c.s = s;
+    c.evals = 0;
+    hm_init(&c.Tcache, 4096);
+    coarsen(&c, res, parent);
+    res->n_evals_coarsen = c.evals;
+    if (stage >= 2) pass2(&c, res);
+    if (stage >= 3) {
+        int32_t q = in->q, n = res->n;
+        res->U = calloc((size_t)m * q + 1, sizeof(double));
+        res->V = calloc((size_t)q * n + 1, sizeof(double));
+        if (m <= q || n <= q) { /* R25: rank not below the slice dimensions -> direct */
+            res->flags = ORC_FLAG_DIRECT;
+        } else if (in->solver == 0) {
+            res->flags = orc_adm(m, n, res->nnz, res->om_row, res->om_col, res->om_val, q, in->K, in->tol,
+                                 in->alpha, in->beta, in->gamma, in->seed, s, res->U, res->V, &res->iters,
+                                 &res->resid, &res->sigma);
+        } else {
+            res->obj = malloc((size_t)2 * (size_t)(in->K > 0 ? in->K : 1) * sizeof(double));
+            res->n_obj = 2 * in->K;
+            res->flags = orc_mals(m, n, res->nnz, res->om_row, res->om_col, res->om_val, q, in->K, in->lam,
+                                  in->seed, s, res->U, res->V, res->obj, &res->sigma);
+            res->iters = in->K;
+        }
+        if (res->flags & ORC_FLAG_DIVERGED) res->flags |= ORC_FLAG_DIRECT; /* S:396 fallback */
+        if (res->flags & ORC_FLAG_DIRECT) direct_full(&c, res);
+    }
+    if (stage >= 4) resolve(in, res);
+    hm_free(&c.Tcache);
+    return res;
+}
+
+orc_slice_result *orc_run_slice(const orc_inputs *in, const int32_t *rows, int32_t m, int32_t slice, int32_t stage)
+{
+    int32_t *parent = make_parent(in);
+    orc_slice_result *r = run_slice(in, parent, rows, m, slice, stage);
+    free(parent);
+    return r;
+}
+
+void orc_run_slices(const orc_inputs *in, const int32_t *off, const int32_t *rows, int32_t nsel,
+                    const int32_t *slice_ids, int32_t stage, orc_slice_result **out)
+{
+    int32_t *parent = make_parent(in);
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int32_t k = 0; k < nsel; ++k) {
+        int32_t s = slice_ids[k];
+        out[k] = run_slice(in, parent, rows + off[s], off[s + 1] - off[s], s, stage);
+    }
+    free(parent);
+}
+
+void orc_free_result(orc_slice_result *r)
+{
+    if (!r) return;
+    free(r->rows); free(r->cut_nodes);
+    free(r->proc_node); free(r->proc_merged); free(r->proc_zoff); free(r->proc_eps); free(r->proc_cost);
+    free(r->proc_zrows); free(r->proc_Va); free(r->proc_Vb);
+    free(r->om_row); free(r->om_col); free(r->om_val); free(r->om_carried); free(r->weights);
+    free(r->U); free(r->V); free(r->obj); free(r->full); free(r->rgb);
+    free(r);
+}
+
+void orc_fullcut_slice(const orc_inputs *in, const int32_t *rows, int32_t m, const int32_t *cut_nodes,
+                       int32_t n, double *out)
+{
+    for (int32_t i = 0; i < m; ++i) {
+        int32_t p = rows[i];
+        double acc[3] = {0.0, 0.0, 0.0};
+        for (int32_t c = 0; c < n; ++c) {
+            int32_t f = cut_nodes[c];
+            double T = orc_entry_T(in, p, in->rep[f]);
+            acc[0] += ((double)in->rr[p] * (double)in->tir[f]) * T;
+            acc[1] += ((double)in->rg[p] * (double)in->tig[f]) * T;
+            acc[2] += ((double)in->rb[p] * (double)in->tib[f]) * T;
+        }
+        out[3 * i + 0] = acc[0];
+        out[3 * i + 1] = acc[1];
+        out[3 * i + 2] = acc[2];
+    }
+}
+
+void orc_bruteforce_rows(const orc_inputs *in, const int32_t *rows, int32_t nrows, double *out)
+{
+#pragma omp parallel for schedule(dynamic, 16)
+    for (int32_t i = 0; i < nrows; ++i) {
+        int32_t p = rows[i];
+        double acc[3] = {0.0, 0.0, 0.0};
+        for (int64_t v = 0; v < in->nv; ++v) {
+            double T = orc_entry_T(in, p, v);
+            acc[0] += ((double)in->rr[p] * (double)in->lir[v]) * T;
+            acc[1] += ((double)in->rg[p] * (double)in->lig[v]) * T;
+            acc[2] += ((double)in->rb[p] * (double)in->lib[v]) * T;
+        }
+        out[3 * i + 0] = acc[0];
+        out[3 * i + 1] = acc[1];
+        out[3 * i + 2] = acc[2];
+    }
+}

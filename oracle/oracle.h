@@ -1,0 +1,114 @@
+/*
+ * oracle.h — plain, slow, fp64 CPU oracle of the hot path of arXiv 2202.12567
+ * ("many-light rendering by sparse sampling and low-rank completion of the lighting matrix").
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load it.  It shares no code, header, table or
+ * helper with the CUDA path (paper_2202_12567_b200/), and neither includes the other.
+ *
+ * Every function follows a passage of /root/reference/PAPER.md ("P:<line>") read as in
+ * DESIGN.md §"Readings"; where the paper is silent the reading number (R<k>) is cited.
+ * Arithmetic: IEEE binary64, round-to-nearest, compiled with -ffp-contract=off (no FMA),
+ * products/sums in the written order.
+ */
+#ifndef LMC_ORACLE_H
+#define LMC_ORACLE_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct {
+    /* G-buffer rows (valid pixels), float32 promoted exactly to double */
+    int64_t m;
+    const float *px, *py, *pz, *nx, *ny, *nz, *vx, *vy, *vz, *rr, *rg, *rb, *spec;
+    const int32_t *expo;
+    /* VPLs */
+    int64_t nv;
+    const float *lx, *ly, *lz, *lnx, *lny, *lnz, *lir, *lig, *lib;
+    /* light tree + global cut */
+    int64_t nn;
+    const int32_t *left, *right, *rep;
+    const float *tir, *tig, *tib;
+    int64_t ncut;
+    const int32_t *cut;
+    /* analytic occluders */
+    int32_t nsph, nbox, nrect;
+    const float *sph, *box, *rect;
+    double clamp_dist, shadow_eps, diag;
+    /* method parameters */
+    double wn;
+    int32_t target;
+    uint64_t seed;
+    int32_t nmax, nmin;
+    double tau, rate;
+    int32_t q, solver, K;
+    double tol, alpha, beta, gamma, lam;
+    uint64_t order_seed; /* 0: FIFO candidate order; else a seeded shuffle (order-independence pin) */
+} orc_inputs;
+
+enum { ORC_FLAG_DIRECT = 1, ORC_FLAG_DIVERGED = 2, ORC_FLAG_ZERO = 4 };
+
+typedef struct {
+    int32_t slice, m, n;          /* rows, final columns */
+    int32_t *rows;                /* m G-buffer rows (ascending) */
+    int32_t *cut_nodes;           /* n, ascending node id = column order */
+    /* coarsening record, one entry per processed candidate, in processing order */
+    int32_t n_proc;
+    int32_t *proc_node, *proc_merged, *proc_zoff; /* zoff: n_proc+1 */
+    double *proc_eps, *proc_cost;
+    int32_t *proc_zrows;          /* concatenated zeta_f (sorted local rows) */
+    double *proc_Va, *proc_Vb;    /* T values (not scaled) on zeta_f: T(i,rep a), T(i,rep b) */
+    int64_t n_evals_coarsen;      /* unique (row, vpl) entry evaluations in pass 1 + coarsening */
+    /* pass 2 */
+    int64_t nnz, n_carried, n_new, n_forced, n_draws, target_N;
+    int32_t *om_row, *om_col;     /* CSR order */
+    double *om_val;               /* M~(i,c) */
+    int32_t *om_carried;
+    uint32_t *weights;            /* n */
+    /* completion */
+    int32_t q, iters, flags;
+    double sigma, resid;
+    double *U, *V;                /* m*q row-major, q*n row-major (V already times sigma) */
+    double *obj;                  /* MALS: objective after each half step (2K) */
+    int32_t n_obj;
+    double *full;                 /* m*n full M~ for direct slices, else NULL */
+    /* resolve */
+    double *rgb;                  /* m*3 */
+} orc_slice_result;
+
+/* P:? — Philox4x32-10 (Salmon et al. SC'11), R-readings O3 */
+void orc_philox(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
+/* Floyd sampling of n distinct rows of [0,m) keyed by (a, slice); writes sorted rows, returns count */
+int32_t orc_floyd(int32_t m, int32_t n, uint32_t a, int32_t slice, uint64_t seed, uint32_t tag, int32_t *out);
+/* Lighting-matrix entry T(p, v) (geometry x BRDF x visibility), P:61 with readings R1-R3 */
+double orc_entry_T(const orc_inputs *in, int64_t row, int64_t vpl);
+/* visibility only (1 visible, 0 occluded) of segment x -> y */
+int32_t orc_visible(const orc_inputs *in, const double x[3], const double y[3]);
+/* Matrix slicing, P:71-73 / P:172 with reading R26 */
+int32_t orc_build_slices(const orc_inputs *in, int32_t *off, int32_t *rows, int64_t *nslices);
+/* Per-slice pipeline: coarsening, sampling, completion (App. A),
+ * resolve.  stage: 1 = coarsen, 2 = + pass 2, 3 = + completion, 4 = + resolve */
+orc_slice_result *orc_run_slice(const orc_inputs *in, const int32_t *rows, int32_t m, int32_t slice, int32_t stage);
+void orc_run_slices(const orc_inputs *in, const int32_t *off, const int32_t *rows, int32_t nsel,
+                    const int32_t *slice_ids, int32_t stage, orc_slice_result **out);
+void orc_free_result(orc_slice_result *r);
+/* ADM (App. A) on an explicit sample set; literal dense Z.  vals are M~ (unnormalised). */
+int32_t orc_adm(int32_t m, int32_t n, int64_t nnz, const int32_t *row, const int32_t *col, const double *val,
+                int32_t q, int32_t K, double tol, double alpha, double beta, double gamma, uint64_t seed,
+                int32_t slice, double *U, double *V, int32_t *iters, double *resid, double *sigma);
+/* Masked ALS (BASELINE north_star) on an explicit sample set. obj: 2K objective values (may be NULL). */
+int32_t orc_mals(int32_t m, int32_t n, int64_t nnz, const int32_t *row, const int32_t *col, const double *val,
+                 int32_t q, int32_t K, double lam, uint64_t seed, int32_t slice, double *X, double *Y,
+                 double *obj, double *sigma);
+/* full-cut rendering of a slice (every entry of M~, exact column sums), out m*3 */
+void orc_fullcut_slice(const orc_inputs *in, const int32_t *rows, int32_t m, const int32_t *cut_nodes,
+                       int32_t n, double *out);
+/* brute force over all VPLs for the given rows, out nrows*3 */
+void orc_bruteforce_rows(const orc_inputs *in, const int32_t *rows, int32_t nrows, double *out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

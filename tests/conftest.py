@@ -1,0 +1,27 @@
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a B200 (runs the CUDA path through the C-ABI)")
+    config.addinivalue_line("markers", "slow: long-running (full-size configs)")
+
+
+@pytest.fixture(scope="session")
+def inputs_cache():
+    import scenegen
+    cache = {}
+
+    def get(name, **over):
+        key = (name, tuple(sorted(over.items())))
+        if key not in cache:
+            cfg = scenegen.preset(name, **over)
+            cache[key] = scenegen.make_inputs(cfg)
+        return cache[key]
+    return get
