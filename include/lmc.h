@@ -1,0 +1,204 @@
+/*
+ * lmc.h — C ABI of the B200-native lighting-matrix completion library (liblmc.so).
+ *
+ * Hot path of arXiv 2202.12567 ("many-light rendering by sparse sampling and low-rank
+ * completion"): per matrix slice, pass-1 uniform sampling + light-cut coarsening
+ * (PAPER.md:96-122), pass-2 pdf sampling, nonnegative low-rank completion by
+ * ADM (App. A) or masked ALS (BASELINE north_star), and the image as
+ * I(s) = X (Y e).  All per-slice work runs in hand-written sm_100a CUDA kernels.
+ *
+ * Conventions for every call:
+ *   - Return value: lmc_status; no exceptions cross the ABI; out-params are untouched on
+ *     failure.  lmc_last_error(ctx) gives a message valid until the next call on ctx.
+ *   - Streams: every stage call enqueues on cfg->stream (a cudaStream_t, NULL = legacy
+ *     default stream) and returns without synchronising.  Getters synchronise.
+ *   - Order: create -> build_slices -> sample_pass1 -> coarsen_cut -> sample_pass2 ->
+ *     complete -> resolve_image.  Calling a stage before its predecessor returns
+ *     LMC_ESTATE; re-running from any earlier stage is allowed (a new frame on the same
+ *     inputs re-runs from build_slices).
+ *   - Errors: LMC_EINVAL null pointers / sizes / invariants (rep(f) in {rep(l), rep(r)}, the
+ *     global cut is an antichain cover, rate in (0,1], gamma in (0,1.618), 1 <= q <= 32,
+ *     slice_target <= 1024, |global cut| <= 1024, p1_nmax <= 32);  LMC_ENOMEM device
+ *     allocation failed;  LMC_ECUDA a CUDA error (sticky: the ctx must be destroyed);
+ *     LMC_EOVERFLOW a per-slice capacity was exceeded (reported by the stage that detects it).
+ *   - Thread safety: a ctx is not thread-safe; distinct ctxs are independent.  One ctx per
+ *     GPU / rank.
+ */
+#ifndef LMC_H
+#define LMC_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    LMC_OK = 0,
+    LMC_EINVAL = 1,
+    LMC_ESTATE = 2,
+    LMC_ENOMEM = 3,
+    LMC_ECUDA = 4,
+    LMC_EOVERFLOW = 5
+} lmc_status;
+
+typedef enum { LMC_SOLVER_ADM = 0, LMC_SOLVER_MALS = 1 } lmc_solver;
+typedef enum { LMC_MEM_DEVICE = 0, LMC_MEM_HOST = 1 } lmc_memory;
+typedef enum { LMC_SLICE_DIRECT = 1, LMC_SLICE_DIVERGED = 2, LMC_SLICE_ZERO = 4 } lmc_slice_flags;
+
+/* G-buffer: one row per valid (hit) pixel = one surface point = one matrix row.
+ * SoA float32 arrays of length count; pixel[r] = image index (y*width + x) of row r;
+ * (vx,vy,vz) = unit direction from the point to the camera; rho = diffuse/glossy albedo;
+ * spec in [0,1] = glossy weight s; exponent = Phong exponent e (>= 0).
+ * Memory: device or host per lmc_config.input_memory; read only during lmc_create. */
+typedef struct {
+    int32_t width, height;
+    int64_t count;
+    const int32_t *pixel;
+    const float *px, *py, *pz, *nx, *ny, *nz, *vx, *vy, *vz, *rho_r, *rho_g, *rho_b, *spec;
+    const int32_t *exponent;
+} lmc_gbuffer;
+
+/* VPLs: position, unit normal, RGB intensity I_j; SoA float32, length count. */
+typedef struct {
+    int64_t count;
+    const float *px, *py, *pz, *nx, *ny, *nz, *ir, *ig, *ib;
+} lmc_vpls;
+
+/* Light tree: binary; left/right = -1 for leaves; rep[f] = representative
+ * VPL id (leaves: their VPL; internal: rep of one child); I_f = (ir, ig, ib)[f].
+ * global_cut: node ids of the conservative global cut g, an antichain covering every
+ * leaf.  int32/float32 arrays; memory per lmc_config.input_memory. */
+typedef struct {
+    int64_t num_nodes;
+    int32_t root;
+    const int32_t *left, *right, *rep;
+    const float *ir, *ig, *ib;
+    int64_t cut_size;
+    const int32_t *global_cut;
+} lmc_light_tree;
+
+/* Analytic occluders for the shadow-ray visibility test (BASELINE north_star "procedural
+ * analytic scene").  HOST pointers, float32: sph[4*k] = (cx,cy,cz,r); box[6*k] = (lo3, hi3);
+ * rect[12*k] = (p0, e1, e2, nrm = e1 x e2).  At most 64 of each.  clamp_dist = d_c of the
+ * d^2 clamp (DESIGN R2); shadow_eps = segment shrink at both ends (R3); diag = scene
+ * diagonal D used by the slicing keys (R26). */
+typedef struct {
+    int32_t n_sph, n_box, n_rect;
+    const float *sph, *box, *rect;
+    double clamp_dist, shadow_eps, diag;
+} lmc_scene;
+
+typedef struct {
+    int32_t slice_target;   /* max rows per slice ("about 800 pixels"), <= 1024 */
+    double normal_weight;   /* w_n of the 6D slicing key (R26) */
+    uint64_t seed;          /* Philox key for every random draw (R7) */
+    int32_t p1_nmax, p1_nmin; /* pass-1 rows per pair: min(m, max(nmin, ceil(nmax lum I_f / l_max))) (R6) */
+    double coarsen_tau;     /* coarsening bound: merge iff cost(L_f) < tau (R11) */
+    double rate;            /* sampling rate of the coarsened slice matrix (R27) */
+    int32_t rank_q;         /* q */
+    int32_t solver;         /* lmc_solver */
+    int32_t max_iter;       /* K (100) */
+    double tol;             /* stop when ||P_Omega(M - XY)|| / ||P_Omega M|| < tol (0 = run K) */
+    double alpha, beta, gamma; /* ADM penalties / step (R19) */
+    double lambda;          /* MALS ridge */
+    int32_t rank, world;    /* this process' share: slices [S*rank/world, S*(rank+1)/world) */
+    int32_t input_memory;   /* lmc_memory of the gbuffer / vpls / tree arrays */
+    void *stream;           /* cudaStream_t */
+} lmc_config;
+
+typedef struct {
+    int64_t n_slices;          /* S, whole frame */
+    int64_t slice_begin, slice_end; /* this rank's slices */
+    int64_t rows;              /* rows of this rank's slices */
+    int64_t sum_cols;          /* sum_s n_s (coarsened columns) */
+    int64_t sum_samples;       /* sum_s |Omega_s| */
+    int64_t sum_completed;     /* sum_s m_s * n_s: entries of the completed matrices */
+    int64_t evals_pass1, evals_coarsen, evals_pass2; /* entry evaluations (shadow rays) */
+    int64_t n_direct, n_zero, n_diverged;
+    int64_t pool_used_max, pool_cap; /* coarsening sample pool per slice (entries) */
+    float ms_slices, ms_pass1, ms_coarsen, ms_pass2, ms_complete, ms_resolve; /* last frame, if timed */
+} lmc_stats;
+
+typedef struct lmc_ctx lmc_ctx;
+
+/* Creates a context on the current CUDA device: validates and copies all inputs into a
+ * ctx-owned device arena (host->device when input_memory == LMC_MEM_HOST), builds the
+ * upper light tree (global cut + ancestors) and allocates every per-frame buffer, so the
+ * stage calls never allocate.  Synchronises cfg->stream before returning. */
+lmc_status lmc_create(const lmc_gbuffer *g, const lmc_vpls *v, const lmc_light_tree *t, const lmc_scene *sc,
+                      const lmc_config *cfg, lmc_ctx **out);
+
+/* Re-upload the per-frame inputs (G-buffer, VPLs) of an existing context: same counts and
+ * memory kind as at lmc_create; the light tree and global cut are those given at creation.
+ * Synchronises cfg->stream.  Resets the stage state to "created". */
+lmc_status lmc_upload_inputs(lmc_ctx *ctx, const lmc_gbuffer *g, const lmc_vpls *v, const lmc_light_tree *t);
+
+/* Matrix slicing: recursive binary split of the rows as 6D points
+ * (x/D, w_n n) on the dimension of largest extent at the lower median of (key, row), the
+ * left child taking ceil(n/2), until <= slice_target rows; slice ids in left-first DFS order,
+ * rows ascending within a slice. */
+lmc_status lmc_build_slices(lmc_ctx *ctx);
+
+/* Pass 1: for every slice of this rank and every base pair f (both children in g),
+ * n_f distinct rows drawn uniformly (Floyd + Philox keyed by (f, slice)) and the entries
+ * T(i, rep a), T(i, rep b) evaluated in fp64 (decision precision, DESIGN R30). */
+lmc_status lmc_sample_pass1(lmc_ctx *ctx);
+
+/* Light coarsening (Eq. (1)): per slice, bottom-up merge of sibling cut nodes
+ * while cost(L_f) = eps(L_f) + cost(L_b) < tau, reusing sample sets by union. */
+lmc_status lmc_coarsen_cut(lmc_ctx *ctx);
+
+/* Pass 2: carried observations, light importance g(j) = max C_j - min C_j,
+ * integer pdf weights and CDF, column-then-row draws skipping observed entries until
+ * ceil(rate m n) entries, one forced entry per empty column; CSR + CSC of Omega. */
+lmc_status lmc_sample_pass2(lmc_ctx *ctx);
+
+/* Completion (App. A): per slice M ~= U V with U, V >= 0 (ADM) or masked ALS;
+ * slices with min(m, n) <= q, or a non-finite residual, are rendered directly (flagged). */
+lmc_status lmc_complete(lmc_ctx *ctx);
+
+/* Image: per slice out^k = tint^k * U (V w^k), written into image_rgb
+ * (float32, height*width*3, row-major pixels, RGB interleaved) at this rank's pixels only;
+ * other pixels are untouched.  image_memory: LMC_MEM_DEVICE or LMC_MEM_HOST (then the
+ * rank's pixels are copied device->host and the call synchronises). */
+lmc_status lmc_resolve_image(lmc_ctx *ctx, float *image_rgb, int32_t image_memory);
+
+/* This rank's pixels as a packed tile in slice-row order (rows_rgb: float32 rows*3, device)
+ * for a cross-rank gather; lmc_scatter_rows() writes a gathered, slice-ordered array of all
+ * rows (every rank's tile concatenated in rank order) into a device image. */
+lmc_status lmc_resolve_rows(lmc_ctx *ctx, float *rows_rgb);
+lmc_status lmc_scatter_rows(lmc_ctx *ctx, const float *all_rows_rgb, float *image_rgb);
+
+void lmc_destroy(lmc_ctx *ctx);
+const char *lmc_last_error(const lmc_ctx *ctx);
+const char *lmc_status_str(lmc_status s);
+
+/* ---- introspection (synchronous; HOST buffers; NULL buffers -> sizes only) ------------------ */
+lmc_status lmc_get_slices(lmc_ctx *ctx, int32_t *off /* S+1 */, int32_t *rows /* count */, int64_t *n_slices);
+/* pass-1 record of a slice: for base pair k (ascending node id): node[k], count[k], rows
+ * (nmax per pair, local rows), Ta/Tb (fp64 T values, nmax per pair). */
+lmc_status lmc_get_pass1(lmc_ctx *ctx, int32_t slice, int32_t *node, int32_t *count, int32_t *rows, double *Ta,
+                         double *Tb, int32_t *n_pairs, int32_t *nmax);
+/* per upper-tree node (ascending node id) of a slice: processed / merged flags, eps, cost */
+lmc_status lmc_get_coarsen(lmc_ctx *ctx, int32_t slice, int32_t *node, int32_t *processed, int32_t *merged,
+                           double *eps, double *cost, int32_t *n_nodes);
+lmc_status lmc_get_cut(lmc_ctx *ctx, int32_t slice, int32_t *nodes, int32_t *n);
+/* Omega of a slice in CSR order: local row, column, value M~ (float32 of the fp64 entry),
+ * carried flag (1 = observed during pass 1 / coarsening) */
+lmc_status lmc_get_samples(lmc_ctx *ctx, int32_t slice, int32_t *row, int32_t *col, float *val, int32_t *carried,
+                           int64_t *n, int64_t *target_n);
+/* factors of a slice: U (m*q row-major), V (q*n row-major, already times sigma) */
+lmc_status lmc_get_factors(lmc_ctx *ctx, int32_t slice, float *U, float *V, int32_t *m, int32_t *n, int32_t *q,
+                           int32_t *flags, int32_t *iters, float *resid);
+lmc_status lmc_get_stats(lmc_ctx *ctx, lmc_stats *st);
+/* enable CUDA-event stage timing (stats.ms_*); adds event records on the stream */
+lmc_status lmc_set_timing(lmc_ctx *ctx, int32_t enabled);
+
+/* Test hook: evaluate T(row, vpl) with the fp64 decision-precision entry kernel for n
+ * arbitrary pairs (host arrays in, host array out).  Same device code as the stages. */
+lmc_status lmc_eval_entries(lmc_ctx *ctx, int64_t n, const int32_t *rows, const int32_t *vpls, double *out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

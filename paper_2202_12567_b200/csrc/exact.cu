@@ -1,0 +1,1090 @@
+// exact.cu — decision-precision kernels of the lighting-matrix hot path (sm_100a).
+//
+// Everything that takes a discrete decision (slice splits, pass-1 rows, merge decisions,
+// pass-2 weights/draws) or produces an entry value runs here in IEEE binary64 with NO
+// contraction (this translation unit is compiled with -fmad=false), in the operation order
+// fixed by DESIGN.md §"Entry formula" (readings R1-R3, R30) — so index sets and cuts are
+// bit-identical to an fp64 reference by construction.
+//
+//   slicing      PAPER.md:71-73, P:172   (R26)
+//   pass 1       P:104                   (R6, R7)
+//   coarsening   P:96-122, Eq. (1)       (R5, R8-R11)
+//   pass 2       P:129-147, Eq. (2)      (R13-R17, R27)
+//   entry A(i,j) P:61, P:48, P:50        (R1-R3, R32)
+#include <cub/cub.cuh>
+
+#include "lmc_internal.h"
+#include "philox.cuh"
+
+namespace lmc {
+
+__constant__ SceneConst c_scene;
+
+#define LMC_INV_PI 0.31830988618379067
+#define LMC_INV_2PI 0.15915494309189535
+#define FULL_MASK 0xffffffffu
+
+// ------------------------------------------------------------------------------------------
+// Entry T(p, v): cosine VPL emitter x clamped geometry x normalised Phong x visibility.
+// Packed row (4 x float4): (px,py,pz,nx) (ny,nz,vx,vy) (vz,spec,rr,rg) (rb,expo,0,0)
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ double dot3d(double a0, double a1, double a2, double b0, double b1, double b2)
+{
+    return (a0 * b0 + a1 * b1) + a2 * b2;
+}
+
+__device__ __forceinline__ double powi_d(double base, int e)
+{
+    double r = 1.0;
+    while (e > 0) {
+        if (e & 1) r = r * base;
+        base = base * base;
+        e >>= 1;
+    }
+    return r;
+}
+
+// 1 iff the open segment x + t l, t in (eps, dist - eps), misses every occluder
+__device__ bool visible_d(double x0, double x1, double x2, double l0, double l1, double l2, double dist)
+{
+    const double tmin = c_scene.eps, tmax = dist - c_scene.eps;
+    for (int k = 0; k < c_scene.nsph; ++k) {
+        const float *s = c_scene.sph + 4 * k;
+        double o0 = x0 - (double)s[0], o1 = x1 - (double)s[1], o2 = x2 - (double)s[2];
+        double r = s[3];
+        double b = dot3d(o0, o1, o2, l0, l1, l2);
+        double cc = dot3d(o0, o1, o2, o0, o1, o2) - r * r;
+        double disc = b * b - cc;
+        if (disc < 0.0) continue;
+        double sq = sqrt(disc);
+        double t0 = -b - sq, t1 = -b + sq;
+        if ((t0 > tmin && t0 < tmax) || (t1 > tmin && t1 < tmax)) return false;
+    }
+    if (c_scene.nbox > 0) {
+        const double i0 = 1.0 / l0, i1 = 1.0 / l1, i2 = 1.0 / l2;
+        for (int k = 0; k < c_scene.nbox; ++k) {
+            const float *bx = c_scene.box + 6 * k;
+            double a1 = ((double)bx[0] - x0) * i0, a2 = ((double)bx[3] - x0) * i0;
+            double b1 = ((double)bx[1] - x1) * i1, b2 = ((double)bx[4] - x1) * i1;
+            double e1 = ((double)bx[2] - x2) * i2, e2 = ((double)bx[5] - x2) * i2;
+            double tnear = fmax(fmax(fmin(a1, a2), fmin(b1, b2)), fmin(e1, e2));
+            double tfar = fmin(fmin(fmax(a1, a2), fmax(b1, b2)), fmax(e1, e2));
+            if (tnear <= tfar && tfar > tmin && tnear < tmax) return false;
+        }
+    }
+    for (int k = 0; k < c_scene.nrect; ++k) {
+        const float *rc = c_scene.rect + 12 * k;
+        double p0 = rc[0], p1 = rc[1], p2 = rc[2];
+        double e10 = rc[3], e11 = rc[4], e12 = rc[5];
+        double e20 = rc[6], e21 = rc[7], e22 = rc[8];
+        double n0 = rc[9], n1 = rc[10], n2 = rc[11];
+        double den = dot3d(n0, n1, n2, l0, l1, l2);
+        if (den == 0.0) continue;
+        double t = dot3d(p0 - x0, p1 - x1, p2 - x2, n0, n1, n2) / den;
+        if (!(t > tmin && t < tmax)) continue;
+        double h0 = x0 + t * l0, h1 = x1 + t * l1, h2 = x2 + t * l2;
+        double q0 = h0 - p0, q1 = h1 - p1, q2 = h2 - p2;
+        double a = dot3d(q0, q1, q2, e10, e11, e12) / dot3d(e10, e11, e12, e10, e11, e12);
+        double b = dot3d(q0, q1, q2, e20, e21, e22) / dot3d(e20, e21, e22, e20, e21, e22);
+        if (a >= 0.0 && a <= 1.0 && b >= 0.0 && b <= 1.0) return false;
+    }
+    return true;
+}
+
+__device__ double entry_T(const float4 *__restrict__ prow, int64_t li, const float4 *__restrict__ vpl, int32_t v)
+{
+    const float4 A = prow[4 * li], B = prow[4 * li + 1], C = prow[4 * li + 2], D = prow[4 * li + 3];
+    const float4 P = vpl[2 * (int64_t)v], Q = vpl[2 * (int64_t)v + 1];
+    double x0 = A.x, x1 = A.y, x2 = A.z;
+    double n0 = A.w, n1 = B.x, n2 = B.y;
+    double d0 = (double)P.x - x0, d1 = (double)P.y - x1, d2 = (double)P.z - x2;
+    double dd = dot3d(d0, d1, d2, d0, d1, d2);
+    if (dd == 0.0) return 0.0;
+    double dist = sqrt(dd);
+    double l0 = d0 / dist, l1 = d1 / dist, l2 = d2 / dist;
+    double ci = dot3d(n0, n1, n2, l0, l1, l2);
+    double cj = -dot3d((double)P.w, (double)Q.x, (double)Q.y, l0, l1, l2);
+    if (ci <= 0.0 || cj <= 0.0) return 0.0;
+    double G = (ci * cj) / fmax(dd, c_scene.dc2);
+    double s = C.y;
+    double phi;
+    if (s == 0.0) {
+        phi = LMC_INV_PI;
+    } else {
+        int e = __float_as_int(D.y);
+        double o0 = B.z, o1 = B.w, o2 = C.x;
+        double rv = (2.0 * ci) * dot3d(n0, n1, n2, o0, o1, o2) - dot3d(l0, l1, l2, o0, o1, o2);
+        double lobe = rv > 0.0 ? powi_d(rv, e) : 0.0;
+        phi = (1.0 - s) * LMC_INV_PI + (s * (((double)(e + 2)) * LMC_INV_2PI)) * lobe;
+    }
+    if (!visible_d(x0, x1, x2, l0, l1, l2, dist)) return 0.0;
+    return phi * G;
+}
+
+__device__ __forceinline__ double lum_rho_d(const float4 *__restrict__ prow, int64_t li)
+{
+    const float4 C = prow[4 * li + 2], D = prow[4 * li + 3];
+    return (0.2126 * (double)C.z + 0.7152 * (double)C.w) + 0.0722 * (double)D.x;
+}
+
+// ------------------------------------------------------------------------------------------
+// Slicing (R26)
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long enc_key(double k)
+{
+    k = __dadd_rn(k, 0.0);   // canonical +0 (the reference compares -0 == +0)
+    unsigned long long u = (unsigned long long)__double_as_longlong(k);
+    return (u & 0x8000000000000000ull) ? ~u : (u | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double dec_key(unsigned long long u)
+{
+    u = (u & 0x8000000000000000ull) ? (u & 0x7fffffffffffffffull) : ~u;
+    return __longlong_as_double((long long)u);
+}
+
+struct GView {
+    const float *px, *py, *pz, *nx, *ny, *nz;
+};
+
+__device__ __forceinline__ double slice_key(const GView &g, int32_t r, int d, double diag, double wn)
+{
+    switch (d) {
+    case 0: return (double)g.px[r] / diag;
+    case 1: return (double)g.py[r] / diag;
+    case 2: return (double)g.pz[r] / diag;
+    case 3: return wn * (double)g.nx[r];
+    case 4: return wn * (double)g.ny[r];
+    default: return wn * (double)g.nz[r];
+    }
+}
+
+__global__ void k_ext_init(unsigned long long *ext, int n)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n * 12) ext[i] = (i % 12) < 6 ? 0ull : ~0ull;   // [0,6) max slots, [6,12) min slots
+}
+
+// one CTA per work item (slot, start, len): extents of the 6 key dimensions of a chunk
+__global__ void __launch_bounds__(256) k_slice_extent(const int32_t *__restrict__ rows, const int32_t *__restrict__ work,
+                                                      unsigned long long *ext, GView g, double diag, double wn)
+{
+    int slot = work[3 * blockIdx.x], start = work[3 * blockIdx.x + 1], len = work[3 * blockIdx.x + 2];
+    unsigned long long mx[6], mn[6];
+#pragma unroll
+    for (int d = 0; d < 6; ++d) { mx[d] = 0ull; mn[d] = ~0ull; }
+    for (int k = threadIdx.x; k < len; k += blockDim.x) {
+        int r = rows[start + k];
+#pragma unroll
+        for (int d = 0; d < 6; ++d) {
+            unsigned long long e = enc_key(slice_key(g, r, d, diag, wn));
+            mx[d] = e > mx[d] ? e : mx[d];
+            mn[d] = e < mn[d] ? e : mn[d];
+        }
+    }
+    __shared__ unsigned long long red[8][12];
+    int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int d = 0; d < 6; ++d) {
+        for (int o = 16; o > 0; o >>= 1) {
+            unsigned long long a = __shfl_xor_sync(FULL_MASK, mx[d], o);
+            unsigned long long b = __shfl_xor_sync(FULL_MASK, mn[d], o);
+            mx[d] = a > mx[d] ? a : mx[d];
+            mn[d] = b < mn[d] ? b : mn[d];
+        }
+        if (lane == 0) { red[w][d] = mx[d]; red[w][6 + d] = mn[d]; }
+    }
+    __syncthreads();
+    if (threadIdx.x < 12) {
+        int d = threadIdx.x;
+        unsigned long long v = red[0][d];
+        for (int k = 1; k < (int)(blockDim.x >> 5); ++k) {
+            unsigned long long o = red[k][d];
+            v = d < 6 ? (o > v ? o : v) : (o < v ? o : v);
+        }
+        if (d < 6) atomicMax(&ext[slot * 12 + d], v);
+        else atomicMin(&ext[slot * 12 + d], v);
+    }
+}
+
+// sort key of every element: encoded key of the split dimension, 0 for tiles that do not split
+__global__ void k_slice_keys(const int32_t *__restrict__ rows, int64_t M, const int32_t *__restrict__ tbeg,
+                             const int32_t *__restrict__ tslot, int ntiles, const unsigned long long *__restrict__ ext,
+                             unsigned long long *keys, GView g, double diag, double wn)
+{
+    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= M) return;
+    int lo = 0, hi = ntiles - 1;   // last tile with begin <= k
+    while (lo < hi) {
+        int mid = (lo + hi + 1) >> 1;
+        if (tbeg[mid] <= k) lo = mid; else hi = mid - 1;
+    }
+    int slot = tslot[lo];
+    if (slot < 0) { keys[k] = 0ull; return; }
+    int best = 0;
+    double bext = -1.0;
+#pragma unroll
+    for (int d = 0; d < 6; ++d) {
+        double e = dec_key(ext[slot * 12 + d]) - dec_key(ext[slot * 12 + 6 + d]);
+        if (e > bext) { bext = e; best = d; }
+    }
+    keys[k] = enc_key(slice_key(g, rows[k], best, diag, wn));
+}
+
+__global__ void k_pack_rows(const int32_t *__restrict__ rows, int64_t row0, int64_t ML, GView g,
+                            const float *__restrict__ vx, const float *__restrict__ vy, const float *__restrict__ vz,
+                            const float *__restrict__ rr, const float *__restrict__ rg, const float *__restrict__ rb,
+                            const float *__restrict__ spec, const int32_t *__restrict__ expo, float4 *prow)
+{
+    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= ML) return;
+    int r = rows[row0 + k];
+    prow[4 * k + 0] = make_float4(g.px[r], g.py[r], g.pz[r], g.nx[r]);
+    prow[4 * k + 1] = make_float4(g.ny[r], g.nz[r], vx[r], vy[r]);
+    prow[4 * k + 2] = make_float4(vz[r], spec[r], rr[r], rg[r]);
+    prow[4 * k + 3] = make_float4(rb[r], __int_as_float(expo[r]), 0.f, 0.f);
+}
+
+__global__ void k_pack_vpls(const float *__restrict__ soa, int64_t nv, float4 *vpl)
+{
+    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= nv) return;
+    vpl[2 * k] = make_float4(soa[k], soa[nv + k], soa[2 * nv + k], soa[3 * nv + k]);
+    vpl[2 * k + 1] = make_float4(soa[4 * nv + k], soa[5 * nv + k], 0.f, 0.f);
+}
+
+cudaError_t run_pack_vpls(lmc_ctx *c)
+{
+    if (c->NV == 0) return cudaSuccess;
+    k_pack_vpls<<<(unsigned)((c->NV + 255) / 256), 256, 0, c->stream>>>(c->d.vpl_soa, c->NV, c->d.vpl);
+    return cudaGetLastError();
+}
+
+cudaError_t upload_scene(const SceneConst &sc) { return cudaMemcpyToSymbol(c_scene, &sc, sizeof(SceneConst)); }
+
+cudaError_t slicing_tmp_bytes(int64_t M, int32_t max_tiles, size_t *bytes)
+{
+    size_t a = 0, b = 0;
+    cudaError_t e = cub::DeviceSegmentedSort::StableSortPairs<unsigned long long, int32_t>(
+        nullptr, a, (const unsigned long long *)nullptr, (unsigned long long *)nullptr, (const int32_t *)nullptr,
+        (int32_t *)nullptr, (int)M, max_tiles, (const int32_t *)nullptr, (const int32_t *)nullptr, 0);
+    if (e != cudaSuccess) return e;
+    e = cub::DeviceSegmentedSort::SortKeys<int32_t>(nullptr, b, (const int32_t *)nullptr, (int32_t *)nullptr, (int)M,
+                                                     max_tiles, (const int32_t *)nullptr, (const int32_t *)nullptr, 0);
+    *bytes = a > b ? a : b;
+    return e;
+}
+
+static GView gview(lmc_ctx *c)
+{
+    GView g;
+    g.px = c->d.g[0]; g.py = c->d.g[1]; g.pz = c->d.g[2];
+    g.nx = c->d.g[3]; g.ny = c->d.g[4]; g.nz = c->d.g[5];
+    return g;
+}
+
+__global__ void k_iota(int32_t *a, int64_t n)
+{
+    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < n) a[k] = (int32_t)k;
+}
+
+cudaError_t run_slicing(lmc_ctx *c)
+{
+    cudaStream_t st = c->stream;
+    const int64_t M = c->M;
+    GView g = gview(c);
+    const double diag = c->diag, wn = c->cfg.normal_weight;
+    if (M == 0) return cudaSuccess;
+    k_iota<<<(unsigned)((M + 255) / 256), 256, 0, st>>>(c->d.rows, M);
+    for (const auto &L : c->levels) {
+        const int32_t *tbeg = c->d.lvl_begin + L.tile_off;
+        const int32_t *tend = c->d.lvl_end + L.tile_off;
+        const int32_t *tslot = c->d.lvl_slot + L.tile_off;
+        int nslots = L.nslots;
+        k_ext_init<<<(nslots * 12 + 255) / 256, 256, 0, st>>>(c->d.ext, nslots);
+        k_slice_extent<<<L.work_n, 256, 0, st>>>(c->d.rows, c->d.lvl_work + 3 * L.work_off, c->d.ext, g, diag, wn);
+        k_slice_keys<<<(unsigned)((M + 255) / 256), 256, 0, st>>>(c->d.rows, M, tbeg, tslot, L.tile_n, c->d.ext,
+                                                                   c->d.keys, g, diag, wn);
+        size_t bytes = c->d.cub_tmp_bytes;
+        cudaError_t e = cub::DeviceSegmentedSort::StableSortPairs(c->d.cub_tmp, bytes, c->d.keys, c->d.keys_alt,
+                                                                  c->d.rows, c->d.rows_alt, (int)M, L.tile_n, tbeg,
+                                                                  tend, st);
+        if (e != cudaSuccess) return e;
+        bytes = c->d.cub_tmp_bytes;
+        e = cub::DeviceSegmentedSort::SortKeys(c->d.cub_tmp, bytes, c->d.rows_alt, c->d.rows, (int)M, L.next_tile_n,
+                                               c->d.lvl_begin + L.next_tile_off, c->d.lvl_end + L.next_tile_off, st);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t run_pack_rows(lmc_ctx *c)
+{
+    if (c->ML == 0) return cudaSuccess;
+    GView g = gview(c);
+    k_pack_rows<<<(unsigned)((c->ML + 255) / 256), 256, 0, c->stream>>>(
+        c->d.rows, c->row0, c->ML, g, c->d.g[6], c->d.g[7], c->d.g[8], c->d.g[9], c->d.g[10], c->d.g[11], c->d.g[12],
+        c->d.expo, c->d.prow);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------------
+// Pass 1: Floyd sampling of n_f distinct rows per base pair, one warp per (slice, pair)
+// ------------------------------------------------------------------------------------------
+// lane k < n returns the k-th smallest of Floyd(m, n) keyed by (a, j, slice, tag)
+__device__ int warp_floyd(int m, int n, uint32_t a, int s, uint64_t seed, int lane)
+{
+    int j = m - n + lane;
+    int t = -1;
+    if (lane < n) {
+        uint4 u = philox4(a, (uint32_t)j, (uint32_t)s, TAG_P1, seed);
+        t = (int)randint_u(u.x, (uint32_t)(j + 1));
+    }
+    int elem = -1;
+    for (int k = 0; k < n; ++k) {
+        int tk = __shfl_sync(FULL_MASK, t, k);
+        bool mem = __ballot_sync(FULL_MASK, lane < k && elem == tk) != 0u;
+        if (lane == k) elem = mem ? (m - n + k) : tk;
+    }
+    int rank = 0;
+    for (int k = 0; k < n; ++k) {
+        int ek = __shfl_sync(FULL_MASK, elem, k);
+        rank += (lane < n && ek < elem) ? 1 : 0;
+    }
+    int out = -1;
+    for (int k = 0; k < n; ++k) {
+        int ek = __shfl_sync(FULL_MASK, elem, k);
+        int rk = __shfl_sync(FULL_MASK, rank, k);
+        if (rk == lane) out = ek;
+    }
+    return out;
+}
+
+__global__ void __launch_bounds__(256) k_pass1(Upper up, const int32_t *__restrict__ slice_off, int32_t s0, int32_t SL,
+                                               int32_t lbase, const float4 *__restrict__ prow,
+                                               const float4 *__restrict__ vpl, uint64_t seed, int nmax,
+                                               uint16_t *p1_rows, double *p1_Ta, double *p1_Tb, int32_t *p1_cnt,
+                                               unsigned long long *counters)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (gw >= (int64_t)SL * up.nB) return;
+    const int ls = (int)(gw / up.nB), b = (int)(gw % up.nB);
+    const int s = s0 + ls;
+    const int m = slice_off[s + 1] - slice_off[s];
+    const int64_t lrow0 = slice_off[s] - lbase;
+    const int f = up.base_list[b];
+    const int l = up.left[f], r = up.right[f];
+    const int a = (up.rep[l] == up.rep[f]) ? l : r;
+    const int bb = (a == l) ? r : l;
+    int n = up.nunc[f] < m ? up.nunc[f] : m;
+    int row = warp_floyd(m, n, (uint32_t)up.node[f], s, seed, lane);
+    const int64_t o = gw * nmax;
+    if (lane < n) {
+        double Ta = entry_T(prow, lrow0 + row, vpl, up.rep[a]);
+        double Tb = entry_T(prow, lrow0 + row, vpl, up.rep[bb]);
+        p1_rows[o + lane] = (uint16_t)row;
+        p1_Ta[o + lane] = Ta;
+        p1_Tb[o + lane] = Tb;
+    }
+    if (lane == 0) {
+        p1_cnt[gw] = n;
+        atomicAdd(&counters[0], (unsigned long long)(2 * n));
+    }
+}
+
+cudaError_t run_pass1(lmc_ctx *c)
+{
+    if (c->SL == 0 || c->up.nB == 0) return cudaSuccess;
+    int64_t warps = (int64_t)c->SL * c->up.nB;
+    unsigned blocks = (unsigned)((warps * 32 + 255) / 256);
+    k_pass1<<<blocks, 256, 0, c->stream>>>(c->up, c->d.slice_off, c->s0, c->SL, c->h_slice_off[c->s0], c->d.prow,
+                                           c->d.vpl, c->cfg.seed, c->nmax, c->d.p1_rows, c->d.p1_Ta, c->d.p1_Tb,
+                                           c->d.p1_cnt, c->d.counters);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------------
+// Coarsening: one CTA per slice, level-synchronous over node heights.  A node's
+// outcome depends only on its own subtree (fresh rows keyed by node id), so any order over
+// candidates of one height gives the reference's cut.
+// ------------------------------------------------------------------------------------------
+enum { F_INCUT = 1, F_MERGED = 2, F_PROC = 4 };
+constexpr int CO_THREADS = 256;
+constexpr int CO_WARPS = CO_THREADS / 32;
+
+__device__ __forceinline__ double warp_max_d(double v)
+{
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(FULL_MASK, v, o));
+    return v;
+}
+
+__global__ void __launch_bounds__(CO_THREADS) k_coarsen(
+    Upper up, const int32_t *__restrict__ slice_off, int32_t s0, int32_t lbase, const float4 *__restrict__ prow,
+    const float4 *__restrict__ vpl, uint64_t seed, int nmax, double tau, const uint16_t *__restrict__ p1_rows,
+    const double *__restrict__ p1_Ta, const double *__restrict__ p1_Tb, const int32_t *__restrict__ p1_cnt,
+    uint16_t *pool_rows, double *pool_Ta, double *pool_Tb, int32_t *pool_used, int64_t pool_cap, uint8_t *cs_flags,
+    double *cs_eps, double *cs_cost, int32_t *cs_zoff, int32_t *cs_zlen, int32_t *cut_n, int32_t *cut_cols,
+    int32_t *src_off, int32_t *src_len, int32_t *src_side, int G, unsigned long long *counters)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int U = up.U;
+    double *sh_cost = (double *)smem;
+    double *sh_eps = sh_cost + U;
+    int32_t *sh_zoff = (int32_t *)(sh_eps + U);
+    int32_t *sh_zlen = sh_zoff + U;
+    uint32_t *sh_bm = (uint32_t *)(sh_zlen + U);           // CO_WARPS x 32 words
+    uint8_t *sh_flag = (uint8_t *)(sh_bm + CO_WARPS * 32);
+    __shared__ int sh_pool;
+    __shared__ int sh_scan[CO_THREADS];
+
+    const int ls = blockIdx.x, s = s0 + ls;
+    const int m = slice_off[s + 1] - slice_off[s];
+    const int64_t lrow0 = slice_off[s] - lbase;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t pbase = (int64_t)ls * pool_cap;
+    for (int u = threadIdx.x; u < U; u += CO_THREADS) {
+        sh_flag[u] = up.left[u] < 0 ? F_INCUT : 0;
+        sh_cost[u] = 0.0;
+        sh_eps[u] = 0.0;
+        sh_zoff[u] = 0;
+        sh_zlen[u] = 0;
+    }
+    if (threadIdx.x == 0) sh_pool = 0;
+    __syncthreads();
+    unsigned long long evals = 0;
+    bool overflow = false;
+    uint32_t *bm = sh_bm + w * 32;
+    for (int h = 1; h <= up.H; ++h) {
+        for (int idx = up.hoff[h] + w; idx < up.hoff[h + 1]; idx += CO_WARPS) {
+            const int f = up.hlist[idx];
+            const int l = up.left[f], r = up.right[f];
+            if (!((sh_flag[l] & F_INCUT) && (sh_flag[r] & F_INCUT))) continue;   // not a candidate
+            const int a = (up.rep[l] == up.rep[f]) ? l : r;
+            const int b = (a == l) ? r : l;
+            const int va = up.rep[a], vb = up.rep[b];
+            const double la = up.lum[a], lb = up.lum[b];
+            const double ratio = la > 0.0 ? lb / la : 0.0;
+            const bool ml = (sh_flag[l] & F_MERGED) != 0, mr = (sh_flag[r] & F_MERGED) != 0;
+            int total, off = 0;
+            double eps = 0.0;
+            if (!ml && !mr) {
+                // base pair: rows and entries from pass 1
+                const int bi = up.base_of[f];
+                const int64_t pi = ((int64_t)ls * up.nB + bi);
+                total = p1_cnt[pi];
+                if (lane == 0) off = atomicAdd(&sh_pool, total);
+                off = __shfl_sync(FULL_MASK, off, 0);
+                if (off + total > pool_cap) { overflow = true; continue; }
+                if (lane < total) {
+                    int i = p1_rows[pi * nmax + lane];
+                    double Ta = p1_Ta[pi * nmax + lane], Tb = p1_Tb[pi * nmax + lane];
+                    pool_rows[pbase + off + lane] = (uint16_t)i;
+                    pool_Ta[pbase + off + lane] = Ta;
+                    pool_Tb[pbase + off + lane] = Tb;
+                    double lr = lum_rho_d(prow, lrow0 + i);
+                    double Va = (lr * la) * Ta, Vb = (lr * lb) * Tb;
+                    eps = la > 0.0 ? fabs(Vb - Va * ratio) : fabs(Vb);
+                }
+            } else {
+                // zeta_f = zeta_a U zeta_b (both merged) or zeta_h U Floyd(n(o)) (mixed), R10
+                bm[lane] = 0u;
+                __syncwarp();
+                const int h1 = ml ? l : r;
+                {
+                    int o1 = sh_zoff[h1], n1 = sh_zlen[h1];
+                    for (int k = lane; k < n1; k += 32) {
+                        int i = pool_rows[pbase + o1 + k];
+                        atomicOr(&bm[i >> 5], 1u << (i & 31));
+                    }
+                }
+                if (ml && mr) {
+                    int o2 = sh_zoff[r], n2 = sh_zlen[r];
+                    for (int k = lane; k < n2; k += 32) {
+                        int i = pool_rows[pbase + o2 + k];
+                        atomicOr(&bm[i >> 5], 1u << (i & 31));
+                    }
+                } else {
+                    const int o = ml ? r : l;
+                    int n = up.nunc[o] < m ? up.nunc[o] : m;
+                    int i = warp_floyd(m, n, (uint32_t)up.node[f], s, seed, lane);
+                    if (lane < n) atomicOr(&bm[i >> 5], 1u << (i & 31));
+                }
+                __syncwarp();
+                uint32_t word = bm[lane];
+                int cnt = __popc(word), incl = cnt;
+                for (int o = 1; o < 32; o <<= 1) {
+                    int t = __shfl_up_sync(FULL_MASK, incl, o);
+                    if (lane >= o) incl += t;
+                }
+                total = __shfl_sync(FULL_MASK, incl, 31);
+                if (lane == 0) off = atomicAdd(&sh_pool, total);
+                off = __shfl_sync(FULL_MASK, off, 0);
+                if (off + total > pool_cap) { overflow = true; continue; }
+                int pos = off + incl - cnt;
+                while (word) {
+                    int bit = __ffs(word) - 1;
+                    word &= word - 1;
+                    pool_rows[pbase + pos++] = (uint16_t)(lane * 32 + bit);
+                }
+                __syncwarp();
+                for (int k = lane; k < total; k += 32) {
+                    int i = pool_rows[pbase + off + k];
+                    double Ta = entry_T(prow, lrow0 + i, vpl, va);
+                    double Tb = entry_T(prow, lrow0 + i, vpl, vb);
+                    pool_Ta[pbase + off + k] = Ta;
+                    pool_Tb[pbase + off + k] = Tb;
+                    double lr = lum_rho_d(prow, lrow0 + i);
+                    double Va = (lr * la) * Ta, Vb = (lr * lb) * Tb;
+                    double e = la > 0.0 ? fabs(Vb - Va * ratio) : fabs(Vb);
+                    eps = fmax(eps, e);
+                }
+                evals += (lane == 0) ? 2ull * total : 0ull;
+            }
+            eps = warp_max_d(eps);
+            // Eq. (1): cost(L_f) = eps(L_f) + cost(L_b); merge iff below the bound
+            const double cf = eps + sh_cost[b];
+            if (lane == 0) {
+                sh_eps[f] = eps;
+                sh_cost[f] = cf;
+                sh_zoff[f] = off;
+                sh_zlen[f] = total;
+                uint8_t fl = F_PROC;
+                if (cf < tau) {
+                    fl |= F_INCUT | F_MERGED;
+                    sh_flag[l] &= (uint8_t)~F_INCUT;
+                    sh_flag[r] &= (uint8_t)~F_INCUT;
+                }
+                sh_flag[f] = fl;
+            }
+            __syncwarp();
+        }
+        __syncthreads();
+    }
+    if (lane == 0 && evals) atomicAdd(&counters[1], evals);
+    if (overflow) atomicOr(&counters[3], 1ull);
+    // write the per-node record
+    const int64_t nb = (int64_t)ls * U;
+    for (int u = threadIdx.x; u < U; u += CO_THREADS) {
+        cs_flags[nb + u] = sh_flag[u];
+        cs_eps[nb + u] = sh_eps[u];
+        cs_cost[nb + u] = sh_cost[u];
+        cs_zoff[nb + u] = sh_zoff[u];
+        cs_zlen[nb + u] = sh_zlen[u];
+    }
+    // final cut in ascending node id (= local id) order, with each column's carried-sample source
+    const int per = (U + CO_THREADS - 1) / CO_THREADS;
+    const int u0 = threadIdx.x * per;
+    int mine = 0;
+    for (int u = u0; u < u0 + per && u < U; ++u) mine += (sh_flag[u] & F_INCUT) ? 1 : 0;
+    sh_scan[threadIdx.x] = mine;
+    __syncthreads();
+    for (int o = 1; o < CO_THREADS; o <<= 1) {
+        int t = threadIdx.x >= o ? sh_scan[threadIdx.x - o] : 0;
+        __syncthreads();
+        sh_scan[threadIdx.x] += t;
+        __syncthreads();
+    }
+    int col = sh_scan[threadIdx.x] - mine;
+    if (threadIdx.x == CO_THREADS - 1) cut_n[ls] = sh_scan[threadIdx.x];
+    const int64_t cb = (int64_t)ls * G;
+    for (int u = u0; u < u0 + per && u < U; ++u) {
+        if (!(sh_flag[u] & F_INCUT)) continue;
+        cut_cols[cb + col] = u;
+        int p = up.parent[u];
+        int so = 0, sl = 0, sd = 0;
+        if (p >= 0 && (sh_flag[p] & F_PROC)) {
+            int ap = (up.rep[up.left[p]] == up.rep[p]) ? up.left[p] : up.right[p];
+            so = sh_zoff[p];
+            sl = sh_zlen[p];
+            sd = (u == ap) ? 0 : 1;
+        } else if (sh_flag[u] & F_MERGED) {
+            so = sh_zoff[u];
+            sl = sh_zlen[u];
+            sd = 0;
+        }
+        src_off[cb + col] = so;
+        src_len[cb + col] = sl;
+        src_side[cb + col] = sd;
+        ++col;
+    }
+    if (threadIdx.x == 0) {
+        pool_used[ls] = sh_pool;
+        atomicMax(&counters[4], (unsigned long long)sh_pool);
+    }
+}
+
+static size_t coarsen_smem(int U) { return (size_t)U * (8 + 8 + 4 + 4) + CO_WARPS * 32 * 4 + (size_t)U + 16; }
+
+cudaError_t run_coarsen(lmc_ctx *c)
+{
+    if (c->SL == 0) return cudaSuccess;
+    size_t sm = coarsen_smem(c->up.U);
+    cudaError_t e = cudaFuncSetAttribute(k_coarsen, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    k_coarsen<<<c->SL, CO_THREADS, sm, c->stream>>>(
+        c->up, c->d.slice_off, c->s0, c->h_slice_off[c->s0], c->d.prow, c->d.vpl, c->cfg.seed, c->nmax,
+        c->cfg.coarsen_tau, c->d.p1_rows, c->d.p1_Ta, c->d.p1_Tb, c->d.p1_cnt, c->d.pool_rows, c->d.pool_Ta,
+        c->d.pool_Tb, c->d.pool_used, c->pool_cap, c->d.cs_flags, c->d.cs_eps, c->d.cs_cost, c->d.cs_zoff,
+        c->d.cs_zlen, c->d.cut_n, c->d.cut_cols, c->d.src_off, c->d.src_len, c->d.src_side, c->G, c->d.counters);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------------
+// Pass 2: one CTA (1024 threads) per slice; the observed-cell bitmap lives in
+// shared memory (m x n <= 2^20 bits).
+// ------------------------------------------------------------------------------------------
+constexpr int P2_THREADS = 1024;
+constexpr unsigned P2_INVALID = 0x1FFFFFu;   // 21-bit sort key sentinel (cells < 2^20)
+
+struct P2Args {
+    Upper up;
+    const int32_t *slice_off;
+    int32_t s0, lbase, G;
+    const float4 *prow;
+    uint64_t seed;
+    double rate;
+    const int32_t *cut_n, *cut_cols, *src_off, *src_len, *src_side;
+    const uint16_t *pool_rows;
+    const double *pool_Ta, *pool_Tb;
+    int64_t pool_cap, ncap;
+    int mmax;
+    int32_t *rowptr;
+    uint16_t *col;
+    float *val;
+    uint8_t *carried;
+    int32_t *colptr;
+    uint16_t *csc_row;
+    int32_t *csc_src;
+    int32_t *nnz, *target_n, *n_new;
+    uint32_t *newcells;
+    int32_t *newpos;
+    unsigned long long *counters;
+};
+
+__device__ __forceinline__ int csr_pos(const uint32_t *bm, const uint16_t *P, const int32_t *rp, int W, int i, int c)
+{
+    const int wi = c >> 5;
+    return rp[i] + P[i * (W + 1) + wi] + __popc(bm[i * W + wi] & ((1u << (c & 31)) - 1u));
+}
+
+__global__ void __launch_bounds__(P2_THREADS, 1) k_pass2(P2Args A)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    typedef cub::BlockRadixSort<uint32_t, P2_THREADS, 1, int32_t> Sort;
+    typedef cub::BlockScan<int32_t, P2_THREADS> ScanI;
+    typedef cub::BlockScan<unsigned long long, P2_THREADS> ScanU;
+    const int ls = blockIdx.x, s = A.s0 + ls, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int m = A.slice_off[s + 1] - A.slice_off[s];
+    const int n = A.cut_n[ls];
+    const int64_t lrow0 = A.slice_off[s] - A.lbase;
+    const int W = (n + 31) >> 5;
+    const int64_t cb = (int64_t)ls * A.G, pb = (int64_t)ls * A.pool_cap, ob = (int64_t)ls * A.ncap;
+    // shared memory carve-up
+    uint32_t *bm = (uint32_t *)smem;                                    // m*W
+    int32_t *colcnt = (int32_t *)(bm + (size_t)A.mmax * 32);            // G
+    unsigned char *phase = (unsigned char *)(colcnt + A.G);
+    // phase A
+    unsigned long long *cdf = (unsigned long long *)phase;              // G (also holds g as double)
+    int32_t *firstf = (int32_t *)(cdf + A.G);                           // P2_THREADS
+    uint32_t *skeys = (uint32_t *)(firstf + P2_THREADS);                // P2_THREADS
+    unsigned char *tmp = (unsigned char *)(skeys + P2_THREADS);
+    typename Sort::TempStorage &sort_tmp = *reinterpret_cast<typename Sort::TempStorage *>(tmp);
+    __shared__ typename ScanI::TempStorage scani_tmp;
+    __shared__ typename ScanU::TempStorage scanu_tmp;
+    // phase B
+    uint16_t *P = (uint16_t *)phase;                                    // m*(W+1)
+    int32_t *rp = (int32_t *)(P + (((size_t)A.mmax * 33 + 7) & ~(size_t)7));  // m+1
+    __shared__ double sh_dred[32];
+    __shared__ unsigned long long sh_ured[32];
+    __shared__ int sh_ired[32];
+    __shared__ int sh_count, sh_obs, sh_nnew, sh_draws;
+
+    for (int k = tid; k < m * W; k += P2_THREADS) bm[k] = 0u;
+    for (int c = tid; c < n; c += P2_THREADS) colcnt[c] = 0;
+    __syncthreads();
+    // carried observations (R13) and light importance g(c) = max C_c - min C_c
+    double *gcol = (double *)cdf;
+    int obs_local = 0;
+    for (int c = w; c < n; c += 32) {
+        const int so = A.src_off[cb + c], sl = A.src_len[cb + c], sd = A.src_side[cb + c];
+        const int u = A.cut_cols[cb + c];
+        const double lI = A.up.lum[u];
+        const double *Tv = sd ? A.pool_Tb : A.pool_Ta;
+        double lo = INFINITY, hi = -INFINITY;
+        for (int k = lane; k < sl; k += 32) {
+            int i = A.pool_rows[pb + so + k];
+            double v = (lum_rho_d(A.prow, lrow0 + i) * lI) * Tv[pb + so + k];
+            lo = fmin(lo, v);
+            hi = fmax(hi, v);
+            atomicOr(&bm[i * W + (c >> 5)], 1u << (c & 31));
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            lo = fmin(lo, __shfl_xor_sync(FULL_MASK, lo, o));
+            hi = fmax(hi, __shfl_xor_sync(FULL_MASK, hi, o));
+        }
+        if (lane == 0) {
+            colcnt[c] = sl;
+            gcol[c] = sl > 0 ? hi - lo : -1.0;
+            obs_local += sl;
+        }
+    }
+    __syncthreads();
+    // G = max g; integer weights (R14)
+    double gmax = 0.0;
+    for (int c = tid; c < n; c += P2_THREADS) gmax = fmax(gmax, gcol[c]);
+    gmax = warp_max_d(gmax);
+    if (lane == 0) sh_dred[w] = gmax;
+    int obs_w = obs_local;
+    for (int o = 16; o > 0; o >>= 1) obs_w += __shfl_xor_sync(FULL_MASK, obs_w, o);
+    if (lane == 0) sh_ired[w] = obs_w;
+    __syncthreads();
+    if (tid == 0) {
+        double gm = 0.0;
+        int ob = 0;
+        for (int k = 0; k < 32; ++k) { gm = fmax(gm, sh_dred[k]); ob += sh_ired[k]; }
+        sh_dred[0] = gm;
+        sh_obs = ob;
+    }
+    __syncthreads();
+    const double Gm = sh_dred[0];
+    unsigned long long wc = 0ull;
+    int observed = 0;
+    if (tid < n) {
+        double gc = gcol[tid];
+        observed = gc >= 0.0;
+        if (Gm > 0.0) {
+            if (observed) {
+                double x = floor(1048575.0 * (gc / Gm));
+                uint32_t ww = 1u + (uint32_t)x;
+                wc = ww > 65536u ? ww : 65536u;
+            }
+        } else {
+            wc = 1ull;
+        }
+    }
+    __syncthreads();   // gcol (aliases cdf) fully read
+    unsigned long long sumw = observed ? wc : 0ull;
+    for (int o = 16; o > 0; o >>= 1) sumw += __shfl_xor_sync(FULL_MASK, sumw, o);
+    int nobs = observed;
+    for (int o = 16; o > 0; o >>= 1) nobs += __shfl_xor_sync(FULL_MASK, nobs, o);
+    if (lane == 0) { sh_ured[w] = sumw; sh_ired[w] = nobs; }
+    __syncthreads();
+    if (tid < n && Gm > 0.0 && !observed) {
+        unsigned long long sw = 0ull;
+        int no = 0;
+        for (int k = 0; k < 32; ++k) { sw += sh_ured[k]; no += sh_ired[k]; }
+        wc = no ? (unsigned long long)(uint32_t)(sw / (unsigned long long)no) : 524288ull;
+    }
+    unsigned long long incl;
+    ScanU(scanu_tmp).InclusiveSum(wc, incl);
+    __syncthreads();
+    if (tid < n) cdf[tid] = incl;
+    __syncthreads();
+    const unsigned long long Wsum = n > 0 ? cdf[n - 1] : 0ull;
+    const int64_t N = (int64_t)ceil(((double)((int64_t)m * (int64_t)n)) * A.rate);
+    const int64_t cap = 64 * N;
+    if (tid == 0) { sh_count = sh_obs; sh_nnew = 0; sh_draws = 0; }
+    __syncthreads();
+    // draws: column by the CDF, row uniformly; skip observed entries (R15, R16)
+    for (int64_t t0 = 0; t0 < cap; t0 += P2_THREADS) {
+        const int count = sh_count;
+        if (count >= N) break;
+        const int64_t t = t0 + tid;
+        uint32_t key = P2_INVALID;
+        int cell = 0, cc = 0;
+        if (t < cap && n > 0) {
+            uint4 u = philox4((uint32_t)t, 0u, (uint32_t)s, TAG_P2, A.seed);
+            unsigned long long x = ((unsigned long long)u.x * Wsum) >> 32;
+            int lo = 0, hi = n - 1;
+            while (lo < hi) {
+                int mid = (lo + hi) >> 1;
+                if (cdf[mid] > x) hi = mid; else lo = mid + 1;
+            }
+            cc = lo;
+            int i = (int)randint_u(u.y, (uint32_t)m);
+            cell = i * n + cc;
+            if (!(bm[i * W + (cc >> 5)] & (1u << (cc & 31)))) key = (uint32_t)cell;
+        }
+        uint32_t k1[1] = {key};
+        int32_t v1[1] = {tid};
+        Sort(sort_tmp).Sort(k1, v1, 0, 21);
+        skeys[tid] = k1[0];
+        __syncthreads();
+        bool first = k1[0] != P2_INVALID && (tid == 0 || skeys[tid - 1] != k1[0]);
+        firstf[v1[0]] = first ? 1 : 0;
+        __syncthreads();
+        int acc = firstf[tid], pre, tot;
+        ScanI(scani_tmp).ExclusiveSum(acc, pre, tot);
+        const int64_t remaining = N - count;
+        const bool accept = acc && pre < remaining;
+        if (accept) {
+            atomicOr(&bm[(cell / n) * W + (cc >> 5)], 1u << (cc & 31));
+            atomicAdd(&colcnt[cc], 1);
+            A.newcells[ob + (count - sh_obs) + pre] = (uint32_t)cell;
+            if (pre == remaining - 1) sh_draws = (int)(t + 1);
+        }
+        __syncthreads();
+        if (tid == 0) sh_count = count + (int)(tot < remaining ? tot : remaining);
+        __syncthreads();
+    }
+    // one forced entry per still-empty column (R17)
+    int nd = sh_count - sh_obs;
+    {
+        int need = 0, cell = 0;
+        if (tid < n && colcnt[tid] == 0) {
+            uint4 u = philox4((uint32_t)tid, 0u, (uint32_t)s, TAG_FORCE, A.seed);
+            int i = (int)randint_u(u.x, (uint32_t)m);
+            cell = i * n + tid;
+            need = 1;
+        }
+        int pre, tot;
+        ScanI(scani_tmp).ExclusiveSum(need, pre, tot);
+        if (need) {
+            int c = cell % n;
+            atomicOr(&bm[(cell / n) * W + (c >> 5)], 1u << (c & 31));
+            colcnt[c] = 1;
+            A.newcells[ob + nd + pre] = (uint32_t)cell;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            sh_nnew = nd + tot;
+            if (sh_draws == 0) sh_draws = (int)(sh_count >= N ? 0 : cap);
+        }
+        __syncthreads();
+    }
+    const int nnew = sh_nnew;
+    const int nnz = sh_obs + nnew;
+    // phase B: CSR row pointers from per-row word prefix counts
+    int rowtot = 0;
+    if (tid < m) {
+        uint16_t run = 0;
+        for (int wi = 0; wi < W; ++wi) {
+            P[tid * (W + 1) + wi] = run;
+            run = (uint16_t)(run + __popc(bm[tid * W + wi]));
+        }
+        P[tid * (W + 1) + W] = run;
+        rowtot = run;
+    }
+    __syncthreads();
+    int rpre, rtot;
+    ScanI(scani_tmp).ExclusiveSum(rowtot, rpre, rtot);
+    if (tid < m) rp[tid] = rpre;
+    if (tid == 0) rp[m] = rtot;
+    __syncthreads();
+    int32_t *grp = A.rowptr + (int64_t)ls * (A.mmax + 1);
+    for (int i = tid; i <= m; i += P2_THREADS) grp[i] = rp[i];
+    if (tid < m) {   // column indices, ascending within the row
+        int pos = rp[tid];
+        for (int wi = 0; wi < W; ++wi) {
+            uint32_t word = bm[tid * W + wi];
+            while (word) {
+                int bit = __ffs(word) - 1;
+                word &= word - 1;
+                A.col[ob + pos++] = (uint16_t)(wi * 32 + bit);
+            }
+        }
+    }
+    // CSC: column pointers, rows ascending within a column, CSR index of each entry
+    int cpre, ctot;
+    int cc0 = tid < n ? colcnt[tid] : 0;
+    ScanI(scani_tmp).ExclusiveSum(cc0, cpre, ctot);
+    int32_t *gcp = A.colptr + (int64_t)ls * (A.G + 1);
+    if (tid < n) gcp[tid] = cpre;
+    if (tid == 0) gcp[n] = ctot;
+    if (tid < n) {
+        int k = cpre;
+        const int wi = tid >> 5;
+        const uint32_t bit = 1u << (tid & 31);
+        for (int i = 0; i < m; ++i) {
+            if (bm[i * W + wi] & bit) {
+                A.csc_row[ob + k] = (uint16_t)i;
+                A.csc_src[ob + k] = csr_pos(bm, P, rp, W, i, tid);
+                ++k;
+            }
+        }
+    }
+    // carried values at their CSR positions
+    for (int c = w; c < n; c += 32) {
+        const int so = A.src_off[cb + c], sl = A.src_len[cb + c], sd = A.src_side[cb + c];
+        const double lI = A.up.lum[A.cut_cols[cb + c]];
+        const double *Tv = sd ? A.pool_Tb : A.pool_Ta;
+        for (int k = lane; k < sl; k += 32) {
+            int i = A.pool_rows[pb + so + k];
+            double v = (lum_rho_d(A.prow, lrow0 + i) * lI) * Tv[pb + so + k];
+            int pos = csr_pos(bm, P, rp, W, i, c);
+            A.val[ob + pos] = (float)v;
+            A.carried[ob + pos] = 1;
+        }
+    }
+    // new entries: CSR positions (values are evaluated by k_eval_new)
+    for (int k = tid; k < nnew; k += P2_THREADS) {
+        uint32_t cell = A.newcells[ob + k];
+        int i = (int)(cell / (uint32_t)n), c = (int)(cell % (uint32_t)n);
+        int pos = csr_pos(bm, P, rp, W, i, c);
+        A.newpos[ob + k] = pos;
+        A.carried[ob + pos] = 0;
+    }
+    if (tid == 0) {
+        A.nnz[ls] = nnz;
+        A.target_n[ls] = (int32_t)N;
+        A.n_new[ls] = nnew;
+        if (nnz > A.ncap) atomicOr(&A.counters[3], 2ull);
+    }
+}
+
+__global__ void __launch_bounds__(256) k_eval_new(Upper up, const int32_t *__restrict__ slice_off, int32_t s0,
+                                                  int32_t lbase, int G, const float4 *__restrict__ prow,
+                                                  const float4 *__restrict__ vpl, const int32_t *__restrict__ cut_n,
+                                                  const int32_t *__restrict__ cut_cols, const uint32_t *__restrict__ newcells,
+                                                  const int32_t *__restrict__ newpos, const int32_t *__restrict__ n_new,
+                                                  float *val, int64_t ncap, unsigned long long *counters)
+{
+    const int ls = blockIdx.y, s = s0 + ls;
+    const int n = cut_n[ls], nn = n_new[ls];
+    const int64_t lrow0 = slice_off[s] - lbase;
+    const int64_t ob = (int64_t)ls * ncap, cb = (int64_t)ls * G;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nn; k += gridDim.x * blockDim.x) {
+        uint32_t cell = newcells[ob + k];
+        int i = (int)(cell / (uint32_t)n), c = (int)(cell % (uint32_t)n);
+        int u = cut_cols[cb + c];
+        double T = entry_T(prow, lrow0 + i, vpl, up.rep[u]);
+        val[ob + newpos[ob + k]] = (float)((lum_rho_d(prow, lrow0 + i) * up.lum[u]) * T);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&counters[2], (unsigned long long)nn);
+}
+
+static size_t pass2_smem(int mmax, int G)
+{
+    typedef cub::BlockRadixSort<uint32_t, P2_THREADS, 1, int32_t> Sort;
+    size_t tmp = sizeof(typename Sort::TempStorage);
+    size_t phaseA = (size_t)G * 8 + P2_THREADS * 4 * 2 + tmp;
+    size_t phaseB = ((((size_t)mmax * 33 + 7) & ~(size_t)7) * 2) + ((size_t)mmax + 1) * 4;
+    size_t base = (size_t)mmax * 32 * 4 + (size_t)G * 4;
+    return base + (phaseA > phaseB ? phaseA : phaseB) + 64;
+}
+
+cudaError_t run_pass2(lmc_ctx *c)
+{
+    if (c->SL == 0) return cudaSuccess;
+    P2Args A;
+    A.up = c->up;
+    A.slice_off = c->d.slice_off;
+    A.s0 = c->s0;
+    A.lbase = c->h_slice_off[c->s0];
+    A.G = c->G;
+    A.prow = c->d.prow;
+    A.seed = c->cfg.seed;
+    A.rate = c->cfg.rate;
+    A.cut_n = c->d.cut_n;
+    A.cut_cols = c->d.cut_cols;
+    A.src_off = c->d.src_off;
+    A.src_len = c->d.src_len;
+    A.src_side = c->d.src_side;
+    A.pool_rows = c->d.pool_rows;
+    A.pool_Ta = c->d.pool_Ta;
+    A.pool_Tb = c->d.pool_Tb;
+    A.pool_cap = c->pool_cap;
+    A.ncap = c->ncap;
+    A.mmax = c->mmax;
+    A.rowptr = c->d.rowptr;
+    A.col = c->d.col;
+    A.val = c->d.val;
+    A.carried = c->d.carried;
+    A.colptr = c->d.colptr;
+    A.csc_row = c->d.csc_row;
+    A.csc_src = c->d.csc_src;
+    A.nnz = c->d.nnz;
+    A.target_n = c->d.target_n;
+    A.n_new = c->d.n_new;
+    A.newcells = c->d.newcells;
+    A.newpos = c->d.newpos;
+    A.counters = c->d.counters;
+    size_t sm = pass2_smem(c->mmax, c->G);
+    cudaError_t e = cudaFuncSetAttribute(k_pass2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    k_pass2<<<c->SL, P2_THREADS, sm, c->stream>>>(A);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    dim3 grid(16, c->SL);
+    k_eval_new<<<grid, 256, 0, c->stream>>>(c->up, c->d.slice_off, c->s0, A.lbase, c->G, c->d.prow, c->d.vpl,
+                                             c->d.cut_n, c->d.cut_cols, c->d.newcells, c->d.newpos, c->d.n_new,
+                                             c->d.val, c->ncap, c->d.counters);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------------
+// Direct rendering of flagged slices (R25 / non-finite fallback): every entry, fp64 sums
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_direct(Upper up, const int32_t *__restrict__ slice_off, int32_t s0,
+                                                int32_t lbase, int G, const float4 *__restrict__ prow,
+                                                const float4 *__restrict__ vpl, const int32_t *__restrict__ cut_n,
+                                                const int32_t *__restrict__ cut_cols, const int32_t *__restrict__ flags,
+                                                float *direct_rgb)
+{
+    const int ls = blockIdx.x, s = s0 + ls;
+    if (!(flags[ls] & LMC_SLICE_DIRECT)) return;
+    const int m = slice_off[s + 1] - slice_off[s], n = cut_n[ls];
+    const int64_t lrow0 = slice_off[s] - lbase, cb = (int64_t)ls * G;
+    for (int i = threadIdx.x; i < m; i += blockDim.x) {
+        double lr = lum_rho_d(prow, lrow0 + i);
+        double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
+        for (int c = 0; c < n; ++c) {
+            int u = cut_cols[cb + c];
+            double lI = up.lum[u];
+            double T = entry_T(prow, lrow0 + i, vpl, up.rep[u]);
+            double v = (lr * lI) * T;
+            double w0 = lI != 0.0 ? (double)up.I[3 * u + 0] / lI : 0.0;
+            double w1 = lI != 0.0 ? (double)up.I[3 * u + 1] / lI : 0.0;
+            double w2 = lI != 0.0 ? (double)up.I[3 * u + 2] / lI : 0.0;
+            acc0 += v * w0;
+            acc1 += v * w1;
+            acc2 += v * w2;
+        }
+        const float4 C = prow[4 * (lrow0 + i) + 2], D = prow[4 * (lrow0 + i) + 3];
+        double t0 = lr != 0.0 ? (double)C.z / lr : 0.0;
+        double t1 = lr != 0.0 ? (double)C.w / lr : 0.0;
+        double t2 = lr != 0.0 ? (double)D.x / lr : 0.0;
+        direct_rgb[3 * (lrow0 + i) + 0] = (float)(t0 * acc0);
+        direct_rgb[3 * (lrow0 + i) + 1] = (float)(t1 * acc1);
+        direct_rgb[3 * (lrow0 + i) + 2] = (float)(t2 * acc2);
+    }
+}
+
+cudaError_t run_direct(lmc_ctx *c)
+{
+    if (c->SL == 0) return cudaSuccess;
+    k_direct<<<c->SL, 256, 0, c->stream>>>(c->up, c->d.slice_off, c->s0, c->h_slice_off[c->s0], c->G, c->d.prow,
+                                            c->d.vpl, c->d.cut_n, c->d.cut_cols, c->d.flags, c->d.direct_rgb);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------------
+// Test hook: T on arbitrary (row, vpl) pairs through the same entry function
+// ------------------------------------------------------------------------------------------
+__global__ void k_eval_pairs(int64_t n, const int32_t *rows, const int32_t *vpls, GView g, const float *vx,
+                             const float *vy, const float *vz, const float *rr, const float *rg, const float *rb,
+                             const float *spec, const int32_t *expo, float4 *tmp, const float4 *vpl, double *out)
+{
+    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    int r = rows[k];
+    tmp[4 * k + 0] = make_float4(g.px[r], g.py[r], g.pz[r], g.nx[r]);
+    tmp[4 * k + 1] = make_float4(g.ny[r], g.nz[r], vx[r], vy[r]);
+    tmp[4 * k + 2] = make_float4(vz[r], spec[r], rr[r], rg[r]);
+    tmp[4 * k + 3] = make_float4(rb[r], __int_as_float(expo[r]), 0.f, 0.f);
+    out[k] = entry_T(tmp, k, vpl, vpls[k]);
+}
+
+cudaError_t run_eval_entries(lmc_ctx *c, int64_t n, const int32_t *d_rows, const int32_t *d_vpls, double *d_out,
+                             float4 *d_tmp_rows)
+{
+    if (n == 0) return cudaSuccess;
+    GView g = gview(c);
+    k_eval_pairs<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(
+        n, d_rows, d_vpls, g, c->d.g[6], c->d.g[7], c->d.g[8], c->d.g[9], c->d.g[10], c->d.g[11], c->d.g[12],
+        c->d.expo, d_tmp_rows, c->d.vpl, d_out);
+    return cudaGetLastError();
+}
+
+}  // namespace lmc

@@ -1,0 +1,935 @@
+// lmc_api.cu — host side of liblmc: context, validation, upper light tree, capacities, stage
+// state machine and getters.  No per-slice arithmetic runs here; every stage of the path is a
+// kernel in exact.cu / complete.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <new>
+#include <vector>
+
+#include "lmc_internal.h"
+
+using namespace lmc;
+
+namespace {
+
+lmc_status fail(lmc_ctx *c, lmc_status s, const char *fmt, ...)
+{
+    if (c) {
+        char buf[512];
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(buf, sizeof buf, fmt, ap);
+        va_end(ap);
+        c->err = buf;
+        if (s == LMC_ECUDA) c->sticky = LMC_ECUDA;
+    }
+    return s;
+}
+
+lmc_status cuda_fail(lmc_ctx *c, cudaError_t e, const char *where)
+{
+    if (e == cudaErrorMemoryAllocation) return fail(c, LMC_ENOMEM, "%s: %s", where, cudaGetErrorString(e));
+    return fail(c, LMC_ECUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+#define CK(expr, where)                                   \
+    do {                                                  \
+        cudaError_t e_ = (expr);                          \
+        if (e_ != cudaSuccess) return cuda_fail(c, e_, where); \
+    } while (0)
+
+double lum3(double r, double g, double b) { return (0.2126 * r + 0.7152 * g) + 0.0722 * b; }
+
+template <typename T>
+cudaError_t dalloc(T **p, size_t n)
+{
+    *p = nullptr;
+    if (n == 0) n = 1;
+    return cudaMalloc((void **)p, n * sizeof(T));
+}
+
+// copy n elements of an input array (device or host) into device memory
+template <typename T>
+cudaError_t dcopy_in(T *dst, const T *src, size_t n, int memory, cudaStream_t st)
+{
+    if (n == 0) return cudaSuccess;
+    return cudaMemcpyAsync(dst, src, n * sizeof(T), memory == LMC_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
+                           st);
+}
+
+template <typename T>
+cudaError_t hcopy_in(std::vector<T> &dst, const T *src, size_t n, int memory, cudaStream_t st)
+{
+    dst.resize(n);
+    if (n == 0) return cudaSuccess;
+    if (memory == LMC_MEM_HOST) {
+        memcpy(dst.data(), src, n * sizeof(T));
+        return cudaSuccess;
+    }
+    cudaError_t e = cudaMemcpyAsync(dst.data(), src, n * sizeof(T), cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) return e;
+    return cudaStreamSynchronize(st);
+}
+
+void free_all(lmc_ctx *c)
+{
+    Dev &d = c->d;
+    void *ptrs[] = {d.pixel, d.g[0], d.g[1], d.g[2], d.g[3], d.g[4], d.g[5], d.g[6], d.g[7], d.g[8], d.g[9], d.g[10],
+                    d.g[11], d.g[12], d.expo, d.vpl, d.ut_i32, d.ut_lum, d.ut_I, d.rows, d.rows_alt, d.keys,
+                    d.keys_alt, d.lvl_begin, d.lvl_end, d.lvl_slot, d.lvl_work, d.ext, d.slice_off, d.cub_tmp, d.prow,
+                    d.p1_rows, d.p1_Ta, d.p1_Tb, d.p1_cnt, d.pool_rows, d.pool_Ta, d.pool_Tb, d.pool_used, d.cs_flags,
+                    d.cs_eps, d.cs_cost, d.cs_zoff, d.cs_zlen, d.cut_n, d.cut_cols, d.src_off, d.src_len, d.src_side,
+                    d.rowptr, d.col, d.val, d.carried, d.colptr, d.csc_row, d.csc_src, d.nnz, d.target_n, d.n_new,
+                    d.newcells, d.newpos, d.U, d.V, d.Lam, d.Pi, d.Xold, d.S, d.flags, d.iters, d.resid,
+                    d.direct_rgb, d.counters, d.img, d.rows_rgb, d.vpl_soa};
+    for (void *p : ptrs)
+        if (p) cudaFree(p);
+    if (c->h_stage) cudaFreeHost(c->h_stage);
+    memset(&c->d, 0, sizeof(c->d));
+    c->h_stage = nullptr;
+    if (c->ev_ok)
+        for (auto &e : c->ev) cudaEventDestroy(e);
+    c->ev_ok = false;
+}
+
+// ------------------------------------------------------------------------------------------
+// upper light tree (global cut + ancestors) on the host
+// ------------------------------------------------------------------------------------------
+struct HostTree {
+    std::vector<int32_t> left, right, rep, cut;
+    std::vector<float> ir, ig, ib;
+};
+
+lmc_status build_upper(lmc_ctx *c, const HostTree &t)
+{
+    const int64_t NN = c->NN;
+    std::vector<int32_t> parent(NN, -1);
+    for (int64_t f = 0; f < NN; ++f) {
+        int32_t l = t.left[f], r = t.right[f];
+        if ((l < 0) != (r < 0)) return fail(c, LMC_EINVAL, "node %lld has exactly one child", (long long)f);
+        if (l >= 0) {
+            if (l >= NN || r >= NN) return fail(c, LMC_EINVAL, "child index out of range at node %lld", (long long)f);
+            if (parent[l] >= 0 || parent[r] >= 0) return fail(c, LMC_EINVAL, "node with two parents under %lld", (long long)f);
+            parent[l] = (int32_t)f;
+            parent[r] = (int32_t)f;
+            if (!(t.rep[f] == t.rep[l] || t.rep[f] == t.rep[r]))
+                return fail(c, LMC_EINVAL, "rep(%lld) is not the rep of a child (R5)", (long long)f);
+        } else if (t.rep[f] < 0 || t.rep[f] >= c->NV) {
+            return fail(c, LMC_EINVAL, "leaf %lld has an invalid VPL id", (long long)f);
+        }
+    }
+    // antichain cover: every leaf has exactly one ancestor-or-self in the cut
+    std::vector<uint8_t> in_cut(NN, 0);
+    for (int32_t g : t.cut) {
+        if (g < 0 || g >= NN) return fail(c, LMC_EINVAL, "global cut node out of range");
+        if (in_cut[g]) return fail(c, LMC_EINVAL, "duplicate node in the global cut");
+        in_cut[g] = 1;
+    }
+    std::vector<uint8_t> upper(NN, 0);
+    for (int32_t g : t.cut) {
+        for (int32_t a = parent[g]; a >= 0; a = parent[a]) {
+            if (in_cut[a]) return fail(c, LMC_EINVAL, "global cut is not an antichain");
+            if (upper[a]) break;
+            upper[a] = 1;
+        }
+    }
+    // leaf coverage by counting leaves under cut nodes
+    {
+        int64_t leaves = 0, covered = 0;
+        for (int64_t f = 0; f < NN; ++f) leaves += t.left[f] < 0;
+        std::vector<int32_t> st;
+        for (int32_t g : t.cut) {
+            st.push_back(g);
+            while (!st.empty()) {
+                int32_t f = st.back();
+                st.pop_back();
+                if (t.left[f] < 0) ++covered;
+                else { st.push_back(t.left[f]); st.push_back(t.right[f]); }
+            }
+        }
+        if (covered != leaves) return fail(c, LMC_EINVAL, "global cut does not cover every leaf exactly once");
+    }
+    std::vector<int32_t> nodes;
+    for (int64_t f = 0; f < NN; ++f)
+        if (upper[f] || in_cut[f]) nodes.push_back((int32_t)f);
+    const int U = (int)nodes.size();
+    std::vector<int32_t> loc(NN, -1);
+    for (int u = 0; u < U; ++u) loc[nodes[u]] = u;
+    std::vector<int32_t> L(U), R(U), P(U), rep(U), height(U, 0), nunc(U), base_of(U, -1);
+    std::vector<double> lum(U);
+    std::vector<float> I(3 * (size_t)U);
+    for (int u = 0; u < U; ++u) {
+        int32_t f = nodes[u];
+        L[u] = in_cut[f] ? -1 : loc[t.left[f]];
+        R[u] = in_cut[f] ? -1 : loc[t.right[f]];
+        P[u] = parent[f] >= 0 ? loc[parent[f]] : -1;
+        rep[u] = t.rep[f];
+        lum[u] = lum3(t.ir[f], t.ig[f], t.ib[f]);
+        I[3 * u] = t.ir[f];
+        I[3 * u + 1] = t.ig[f];
+        I[3 * u + 2] = t.ib[f];
+    }
+    // heights (children before parents: iterate until stable over reverse local order)
+    std::function<int(int)> hgt = [&](int u) -> int {
+        if (L[u] < 0) return 0;
+        if (height[u] > 0) return height[u];
+        int h = 1 + std::max(hgt(L[u]), hgt(R[u]));
+        height[u] = h;
+        return h;
+    };
+    int H = 0;
+    for (int u = 0; u < U; ++u) H = std::max(H, hgt(u));
+    std::vector<int32_t> hlist, hoff(H + 2, 0), base_list;
+    for (int h = 1; h <= H; ++h) {
+        hoff[h] = (int32_t)hlist.size();
+        for (int u = 0; u < U; ++u)
+            if (L[u] >= 0 && height[u] == h) hlist.push_back(u);
+    }
+    hoff[H + 1] = (int32_t)hlist.size();
+    if (H == 0) hoff[1] = 0;
+    double lmax = 0.0;
+    for (int u = 0; u < U; ++u)
+        if (L[u] >= 0 && L[L[u]] < 0 && L[R[u]] < 0) {
+            base_of[u] = (int32_t)base_list.size();
+            base_list.push_back(u);
+            lmax = std::max(lmax, lum[u]);
+        }
+    for (int u = 0; u < U; ++u) {
+        // P:104 n_f proportional to I_f (R6): max(nmin, ceil(nmax lum / l_max)), clamped by m in-kernel
+        if (lmax > 0.0) {
+            double x = ceil(((double)c->cfg.p1_nmax * lum[u]) / lmax);
+            if (x > 1073741824.0) x = 1073741824.0;
+            nunc[u] = x > (double)c->cfg.p1_nmin ? (int32_t)x : c->cfg.p1_nmin;
+        } else {
+            nunc[u] = c->cfg.p1_nmin;
+        }
+    }
+    // capacity of the per-slice sample pool: sum over internal nodes of a bound on |zeta_f|
+    {
+        const int64_t m = c->mmax;
+        std::vector<int64_t> zb(U, 0);
+        std::function<int64_t(int)> zbound = [&](int u) -> int64_t {
+            if (L[u] < 0) return std::min<int64_t>(m, nunc[u]);
+            if (zb[u] > 0) return zb[u];
+            int64_t v;
+            if (base_of[u] >= 0) v = std::min<int64_t>(m, nunc[u]);
+            else v = std::min<int64_t>(m, zbound(L[u]) + zbound(R[u]));
+            zb[u] = v;
+            return v;
+        };
+        int64_t tot = 0;
+        for (int u = 0; u < U; ++u)
+            if (L[u] >= 0) tot += zbound(u);
+        c->pool_cap = std::max<int64_t>(tot, 32);
+    }
+    // upload: int32 block [node L R P rep nunc hlist hoff base_list base_of]
+    std::vector<int32_t> blk;
+    auto put = [&](const std::vector<int32_t> &v) { size_t o = blk.size(); blk.insert(blk.end(), v.begin(), v.end()); return o; };
+    size_t o_node = put(nodes), o_L = put(L), o_R = put(R), o_P = put(P), o_rep = put(rep), o_n = put(nunc),
+           o_hl = put(hlist), o_ho = put(hoff), o_bl = put(base_list), o_bo = put(base_of);
+    Dev &d = c->d;
+    CK(dalloc(&d.ut_i32, blk.size()), "alloc upper tree");
+    CK(dalloc(&d.ut_lum, (size_t)U), "alloc upper tree");
+    CK(dalloc(&d.ut_I, 3 * (size_t)U), "alloc upper tree");
+    CK(cudaMemcpy(d.ut_i32, blk.data(), blk.size() * 4, cudaMemcpyHostToDevice), "upload upper tree");
+    CK(cudaMemcpy(d.ut_lum, lum.data(), (size_t)U * 8, cudaMemcpyHostToDevice), "upload upper tree");
+    CK(cudaMemcpy(d.ut_I, I.data(), (size_t)U * 12, cudaMemcpyHostToDevice), "upload upper tree");
+    Upper &up = c->up;
+    up.U = U;
+    up.H = H;
+    up.nB = (int32_t)base_list.size();
+    up.node = d.ut_i32 + o_node;
+    up.left = d.ut_i32 + o_L;
+    up.right = d.ut_i32 + o_R;
+    up.parent = d.ut_i32 + o_P;
+    up.rep = d.ut_i32 + o_rep;
+    up.nunc = d.ut_i32 + o_n;
+    up.hlist = d.ut_i32 + o_hl;
+    up.hoff = d.ut_i32 + o_ho;
+    up.base_list = d.ut_i32 + o_bl;
+    up.base_of = d.ut_i32 + o_bo;
+    up.lum = d.ut_lum;
+    up.I = d.ut_I;
+    c->h_up_node = nodes;
+    return LMC_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// slicing structure: sizes depend only on (M, target): left child takes ceil(n/2)
+// ------------------------------------------------------------------------------------------
+lmc_status build_levels(lmc_ctx *c)
+{
+    struct Node { int32_t start, len, depth; bool leaf; };
+    std::vector<Node> all;
+    std::function<void(int32_t, int32_t, int32_t)> rec = [&](int32_t start, int32_t len, int32_t depth) {
+        bool leaf = len <= c->cfg.slice_target;
+        all.push_back({start, len, depth, leaf});
+        if (leaf) return;
+        int32_t nl = (len + 1) / 2;
+        rec(start, nl, depth + 1);
+        rec(start + nl, len - nl, depth + 1);
+    };
+    c->h_slice_off.assign(1, 0);
+    c->levels.clear();
+    if (c->M > 0) rec(0, (int32_t)c->M, 0);
+    int32_t maxd = 0;
+    for (auto &n : all) maxd = std::max(maxd, n.depth);
+    std::vector<Node> leaves;
+    for (auto &n : all)
+        if (n.leaf) leaves.push_back(n);
+    std::sort(leaves.begin(), leaves.end(), [](const Node &a, const Node &b) { return a.start < b.start; });
+    for (auto &n : leaves) c->h_slice_off.push_back(n.start + n.len);
+    c->S = (int32_t)leaves.size();
+    // tilings per depth: nodes at depth d + leaves at depth < d
+    std::vector<int32_t> beg, end, slot, work;
+    auto tiling = [&](int d, std::vector<Node> &out) {
+        out.clear();
+        for (auto &n : all)
+            if (n.depth == d || (n.leaf && n.depth < d)) out.push_back(n);
+        std::sort(out.begin(), out.end(), [](const Node &a, const Node &b) { return a.start < b.start; });
+    };
+    int max_tiles = 1;
+    std::vector<Node> cur, nxt;
+    for (int d = 0; d < maxd; ++d) {
+        tiling(d, cur);
+        tiling(d + 1, nxt);
+        lmc_ctx::Level L;
+        L.tile_off = (int32_t)beg.size();
+        L.tile_n = (int32_t)cur.size();
+        int ns = 0;
+        L.work_off = (int32_t)(work.size() / 3);
+        for (auto &n : cur) {
+            beg.push_back(n.start);
+            end.push_back(n.start + n.len);
+            if (n.depth == d && !n.leaf) {
+                slot.push_back(ns);
+                for (int32_t o = 0; o < n.len; o += 4096) {
+                    work.push_back(ns);
+                    work.push_back(n.start + o);
+                    work.push_back(std::min<int32_t>(4096, n.len - o));
+                }
+                ++ns;
+            } else {
+                slot.push_back(-1);
+            }
+        }
+        L.work_n = (int32_t)(work.size() / 3) - L.work_off;
+        L.nslots = ns;
+        L.next_tile_off = (int32_t)beg.size();
+        L.next_tile_n = (int32_t)nxt.size();
+        for (auto &n : nxt) {
+            beg.push_back(n.start);
+            end.push_back(n.start + n.len);
+            slot.push_back(-1);
+        }
+        max_tiles = std::max(max_tiles, (int)std::max(cur.size(), nxt.size()));
+        c->levels.push_back(L);
+    }
+    c->max_tiles = max_tiles;
+    Dev &d = c->d;
+    CK(dalloc(&d.lvl_begin, beg.size()), "alloc slicing");
+    CK(dalloc(&d.lvl_end, end.size()), "alloc slicing");
+    CK(dalloc(&d.lvl_slot, slot.size()), "alloc slicing");
+    CK(dalloc(&d.lvl_work, work.size()), "alloc slicing");
+    CK(dalloc(&d.ext, (size_t)max_tiles * 12), "alloc slicing");
+    if (!beg.empty()) {
+        CK(cudaMemcpy(d.lvl_begin, beg.data(), beg.size() * 4, cudaMemcpyHostToDevice), "upload slicing");
+        CK(cudaMemcpy(d.lvl_end, end.data(), end.size() * 4, cudaMemcpyHostToDevice), "upload slicing");
+        CK(cudaMemcpy(d.lvl_slot, slot.data(), slot.size() * 4, cudaMemcpyHostToDevice), "upload slicing");
+    }
+    if (!work.empty()) CK(cudaMemcpy(d.lvl_work, work.data(), work.size() * 4, cudaMemcpyHostToDevice), "upload slicing");
+    CK(dalloc(&d.slice_off, c->h_slice_off.size()), "alloc slicing");
+    CK(cudaMemcpy(d.slice_off, c->h_slice_off.data(), c->h_slice_off.size() * 4, cudaMemcpyHostToDevice), "upload slicing");
+    return LMC_OK;
+}
+
+lmc_status check_stage(lmc_ctx *c, int need)
+{
+    if (!c) return LMC_EINVAL;
+    if (c->sticky != LMC_OK) return c->sticky;
+    if (c->state < need) return fail(c, LMC_ESTATE, "stage called out of order (state %d, needs %d)", c->state, need);
+    return LMC_OK;
+}
+
+lmc_status check_overflow(lmc_ctx *c)
+{
+    unsigned long long cnt[5];
+    CK(cudaMemcpyAsync(cnt, c->d.counters, sizeof cnt, cudaMemcpyDeviceToHost, c->stream), "read counters");
+    CK(cudaStreamSynchronize(c->stream), "sync");
+    if (cnt[3] & 1ull) return fail(c, LMC_EOVERFLOW, "coarsening sample pool overflow (cap %lld)", (long long)c->pool_cap);
+    if (cnt[3] & 2ull) return fail(c, LMC_EOVERFLOW, "pass-2 sample capacity overflow (cap %lld)", (long long)c->ncap);
+    return LMC_OK;
+}
+
+template <typename T>
+cudaError_t d2h(T *dst, const T *src, size_t n)
+{
+    if (!dst || n == 0) return cudaSuccess;
+    return cudaMemcpy(dst, src, n * sizeof(T), cudaMemcpyDeviceToHost);
+}
+
+void ev_rec(lmc_ctx *c, int k)
+{
+    if (c->timing && c->ev_ok) cudaEventRecord(c->ev[k], c->stream);
+}
+
+}  // namespace
+
+// ==========================================================================================
+extern "C" {
+
+const char *lmc_status_str(lmc_status s)
+{
+    switch (s) {
+    case LMC_OK: return "LMC_OK";
+    case LMC_EINVAL: return "LMC_EINVAL";
+    case LMC_ESTATE: return "LMC_ESTATE";
+    case LMC_ENOMEM: return "LMC_ENOMEM";
+    case LMC_ECUDA: return "LMC_ECUDA";
+    case LMC_EOVERFLOW: return "LMC_EOVERFLOW";
+    }
+    return "LMC_UNKNOWN";
+}
+
+const char *lmc_last_error(const lmc_ctx *c) { return c ? c->err.c_str() : "null context"; }
+
+void lmc_destroy(lmc_ctx *c)
+{
+    if (!c) return;
+    free_all(c);
+    delete c;
+}
+
+static lmc_status create_impl(lmc_ctx *c, const lmc_gbuffer *g, const lmc_vpls *v, const lmc_light_tree *t,
+                              const lmc_scene *sc)
+{
+    const lmc_config &cfg = c->cfg;
+    c->stream = (cudaStream_t)cfg.stream;
+    if (cfg.slice_target < 1 || cfg.slice_target > MAX_SLICE) return fail(c, LMC_EINVAL, "slice_target must be in [1, %d]", MAX_SLICE);
+    if (!(cfg.rate > 0.0 && cfg.rate <= 1.0)) return fail(c, LMC_EINVAL, "rate must be in (0, 1]");
+    if (!(cfg.gamma > 0.0 && cfg.gamma < 1.618)) return fail(c, LMC_EINVAL, "gamma must be in (0, 1.618)");
+    if (!(cfg.alpha > 0.0 && cfg.beta > 0.0)) return fail(c, LMC_EINVAL, "alpha, beta must be > 0");
+    if (!(cfg.rank_q == 4 || cfg.rank_q == 8 || cfg.rank_q == 16 || cfg.rank_q == 32))
+        return fail(c, LMC_EINVAL, "rank_q must be one of 4, 8, 16, 32");
+    if (cfg.solver == LMC_SOLVER_MALS && cfg.rank_q > 16) return fail(c, LMC_EINVAL, "MALS supports rank_q <= 16");
+    if (cfg.solver != LMC_SOLVER_ADM && cfg.solver != LMC_SOLVER_MALS) return fail(c, LMC_EINVAL, "unknown solver");
+    if (cfg.p1_nmax < 1 || cfg.p1_nmax > MAX_NMAX || cfg.p1_nmin < 1) return fail(c, LMC_EINVAL, "p1_nmax must be in [1, 32], p1_nmin >= 1");
+    if (cfg.max_iter < 0) return fail(c, LMC_EINVAL, "max_iter must be >= 0");
+    if (cfg.world < 1 || cfg.rank < 0 || cfg.rank >= cfg.world) return fail(c, LMC_EINVAL, "bad rank/world");
+    if (cfg.input_memory != LMC_MEM_DEVICE && cfg.input_memory != LMC_MEM_HOST) return fail(c, LMC_EINVAL, "bad input_memory");
+    if (!g || !v || !t || !sc) return fail(c, LMC_EINVAL, "null input struct");
+    if (g->count < 0 || g->count > (1ll << 31) - 1) return fail(c, LMC_EINVAL, "bad gbuffer count");
+    if (g->count > 0 && (!g->pixel || !g->px || !g->py || !g->pz || !g->nx || !g->ny || !g->nz || !g->vx || !g->vy ||
+                         !g->vz || !g->rho_r || !g->rho_g || !g->rho_b || !g->spec || !g->exponent))
+        return fail(c, LMC_EINVAL, "null gbuffer array");
+    if (v->count < 1 || !v->px || !v->py || !v->pz || !v->nx || !v->ny || !v->nz) return fail(c, LMC_EINVAL, "bad VPL set");
+    if (t->num_nodes < 1 || !t->left || !t->right || !t->rep || !t->ir || !t->ig || !t->ib || !t->global_cut)
+        return fail(c, LMC_EINVAL, "bad light tree");
+    if (t->cut_size < 1 || t->cut_size > MAX_CUT) return fail(c, LMC_EINVAL, "global cut size must be in [1, %d]", MAX_CUT);
+    if (sc->n_sph < 0 || sc->n_sph > MAX_PRIMS || sc->n_box < 0 || sc->n_box > MAX_PRIMS || sc->n_rect < 0 ||
+        sc->n_rect > MAX_PRIMS)
+        return fail(c, LMC_EINVAL, "at most %d occluders of each kind", MAX_PRIMS);
+    if ((sc->n_sph && !sc->sph) || (sc->n_box && !sc->box) || (sc->n_rect && !sc->rect)) return fail(c, LMC_EINVAL, "null occluder array");
+    if (!(sc->diag > 0.0)) return fail(c, LMC_EINVAL, "scene diagonal must be > 0");
+    c->M = g->count;
+    c->W = g->width;
+    c->H = g->height;
+    c->NV = v->count;
+    c->NN = t->num_nodes;
+    c->G = (int32_t)t->cut_size;
+    c->diag = sc->diag;
+    c->q = cfg.rank_q;
+    c->nmax = cfg.p1_nmax;
+    // scene constants
+    memset(&c->scene, 0, sizeof c->scene);
+    c->scene.nsph = sc->n_sph;
+    c->scene.nbox = sc->n_box;
+    c->scene.nrect = sc->n_rect;
+    c->scene.dc2 = sc->clamp_dist * sc->clamp_dist;
+    c->scene.eps = sc->shadow_eps;
+    if (sc->n_sph) memcpy(c->scene.sph, sc->sph, sizeof(float) * 4 * sc->n_sph);
+    if (sc->n_box) memcpy(c->scene.box, sc->box, sizeof(float) * 6 * sc->n_box);
+    if (sc->n_rect) memcpy(c->scene.rect, sc->rect, sizeof(float) * 12 * sc->n_rect);
+    CK(upload_scene(c->scene), "upload scene");
+    // slicing structure and this rank's share
+    lmc_status st = build_levels(c);
+    if (st != LMC_OK) return st;
+    c->s0 = (int32_t)((int64_t)c->S * cfg.rank / cfg.world);
+    c->s1 = (int32_t)((int64_t)c->S * (cfg.rank + 1) / cfg.world);
+    c->SL = c->s1 - c->s0;
+    c->row0 = c->h_slice_off[c->s0];
+    c->ML = c->h_slice_off[c->s1] - c->row0;
+    c->mmax = 1;
+    for (int s = 0; s < c->S; ++s) c->mmax = std::max(c->mmax, c->h_slice_off[s + 1] - c->h_slice_off[s]);
+    // light tree on the host for the upper-tree construction
+    HostTree ht;
+    CK(hcopy_in(ht.left, t->left, (size_t)c->NN, cfg.input_memory, c->stream), "read tree");
+    CK(hcopy_in(ht.right, t->right, (size_t)c->NN, cfg.input_memory, c->stream), "read tree");
+    CK(hcopy_in(ht.rep, t->rep, (size_t)c->NN, cfg.input_memory, c->stream), "read tree");
+    CK(hcopy_in(ht.ir, t->ir, (size_t)c->NN, cfg.input_memory, c->stream), "read tree");
+    CK(hcopy_in(ht.ig, t->ig, (size_t)c->NN, cfg.input_memory, c->stream), "read tree");
+    CK(hcopy_in(ht.ib, t->ib, (size_t)c->NN, cfg.input_memory, c->stream), "read tree");
+    CK(hcopy_in(ht.cut, t->global_cut, (size_t)c->G, cfg.input_memory, c->stream), "read tree");
+    st = build_upper(c, ht);
+    if (st != LMC_OK) return st;
+    const int64_t G = c->G, SL = c->SL, ML = c->ML, M = c->M;
+    {
+        int64_t nt = (int64_t)std::ceil((double)(c->mmax * G) * cfg.rate);
+        c->ncap = std::min<int64_t>((int64_t)c->mmax * G, std::max<int64_t>(nt, 2 * c->pool_cap) + G);
+    }
+    // device arena
+    Dev &d = c->d;
+    CK(dalloc(&d.pixel, M), "alloc gbuffer");
+    for (int k = 0; k < 13; ++k) CK(dalloc(&d.g[k], M), "alloc gbuffer");
+    CK(dalloc(&d.expo, M), "alloc gbuffer");
+    CK(dalloc(&d.vpl, 2 * (size_t)c->NV), "alloc vpls");
+    CK(dalloc(&d.vpl_soa, 6 * (size_t)c->NV), "alloc vpls");
+    CK(dalloc(&d.rows, M), "alloc slicing");
+    CK(dalloc(&d.rows_alt, M), "alloc slicing");
+    CK(dalloc(&d.keys, M), "alloc slicing");
+    CK(dalloc(&d.keys_alt, M), "alloc slicing");
+    CK(slicing_tmp_bytes(std::max<int64_t>(M, 1), c->max_tiles, &d.cub_tmp_bytes), "cub sizing");
+    CK(cudaMalloc(&d.cub_tmp, std::max<size_t>(d.cub_tmp_bytes, 16)), "alloc cub");
+    CK(dalloc(&d.prow, 4 * (size_t)ML), "alloc rows");
+    const int64_t nB = c->up.nB, U = c->up.U;
+    CK(dalloc(&d.p1_rows, SL * nB * c->nmax), "alloc pass1");
+    CK(dalloc(&d.p1_Ta, SL * nB * c->nmax), "alloc pass1");
+    CK(dalloc(&d.p1_Tb, SL * nB * c->nmax), "alloc pass1");
+    CK(dalloc(&d.p1_cnt, SL * nB), "alloc pass1");
+    CK(dalloc(&d.pool_rows, SL * c->pool_cap), "alloc pool");
+    CK(dalloc(&d.pool_Ta, SL * c->pool_cap), "alloc pool");
+    CK(dalloc(&d.pool_Tb, SL * c->pool_cap), "alloc pool");
+    CK(dalloc(&d.pool_used, SL), "alloc pool");
+    CK(dalloc(&d.cs_flags, SL * U), "alloc coarsen");
+    CK(dalloc(&d.cs_eps, SL * U), "alloc coarsen");
+    CK(dalloc(&d.cs_cost, SL * U), "alloc coarsen");
+    CK(dalloc(&d.cs_zoff, SL * U), "alloc coarsen");
+    CK(dalloc(&d.cs_zlen, SL * U), "alloc coarsen");
+    CK(dalloc(&d.cut_n, SL), "alloc cut");
+    CK(dalloc(&d.cut_cols, SL * G), "alloc cut");
+    CK(dalloc(&d.src_off, SL * G), "alloc cut");
+    CK(dalloc(&d.src_len, SL * G), "alloc cut");
+    CK(dalloc(&d.src_side, SL * G), "alloc cut");
+    CK(dalloc(&d.rowptr, SL * (c->mmax + 1)), "alloc pass2");
+    CK(dalloc(&d.col, SL * c->ncap), "alloc pass2");
+    CK(dalloc(&d.val, SL * c->ncap), "alloc pass2");
+    CK(dalloc(&d.carried, SL * c->ncap), "alloc pass2");
+    CK(dalloc(&d.colptr, SL * (G + 1)), "alloc pass2");
+    CK(dalloc(&d.csc_row, SL * c->ncap), "alloc pass2");
+    CK(dalloc(&d.csc_src, SL * c->ncap), "alloc pass2");
+    CK(dalloc(&d.nnz, SL), "alloc pass2");
+    CK(dalloc(&d.target_n, SL), "alloc pass2");
+    CK(dalloc(&d.n_new, SL), "alloc pass2");
+    CK(dalloc(&d.newcells, SL * c->ncap), "alloc pass2");
+    CK(dalloc(&d.newpos, SL * c->ncap), "alloc pass2");
+    CK(dalloc(&d.U, ML * c->q), "alloc factors");
+    CK(dalloc(&d.Lam, ML * c->q), "alloc factors");
+    CK(dalloc(&d.Xold, ML * c->q), "alloc factors");
+    CK(dalloc(&d.V, SL * G * c->q), "alloc factors");
+    CK(dalloc(&d.Pi, SL * G * c->q), "alloc factors");
+    CK(dalloc(&d.S, SL * c->ncap), "alloc factors");
+    CK(dalloc(&d.flags, SL), "alloc factors");
+    CK(dalloc(&d.iters, SL), "alloc factors");
+    CK(dalloc(&d.resid, SL), "alloc factors");
+    CK(dalloc(&d.direct_rgb, 3 * ML), "alloc resolve");
+    CK(dalloc(&d.rows_rgb, 3 * ML), "alloc resolve");
+    CK(dalloc(&d.img, 3 * (size_t)std::max<int64_t>((int64_t)c->W * c->H, 1)), "alloc resolve");
+    CK(cudaMallocHost(&c->h_stage, 3 * sizeof(float) * (size_t)std::max<int64_t>((int64_t)c->W * c->H, 1)), "alloc staging");
+    CK(dalloc(&d.counters, 8), "alloc counters");
+    CK(cudaMemsetAsync(d.counters, 0, 8 * sizeof(unsigned long long), c->stream), "memset");
+    CK(cudaMemsetAsync(d.flags, 0, SL * sizeof(int32_t), c->stream), "memset");
+    CK(cudaMemsetAsync(d.img, 0, 3 * sizeof(float) * (size_t)std::max<int64_t>((int64_t)c->W * c->H, 1), c->stream), "memset");
+    size_t need = complete_smem_bytes(c->q, c->mmax, (int)G, cfg.solver);
+    int maxsm = 0, dev = 0;
+    CK(cudaGetDevice(&dev), "device");
+    CK(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev), "device attr");
+    if (need > (size_t)maxsm)
+        return fail(c, LMC_EINVAL, "rank %d with slices of %d rows and a %lld-node cut needs %zu B of shared memory (max %d)",
+                    c->q, c->mmax, (long long)G, need, maxsm);
+    for (auto &e : c->ev) CK(cudaEventCreate(&e), "events");
+    c->ev_ok = true;
+    return lmc_upload_inputs(c, g, v, t);
+}
+
+lmc_status lmc_create(const lmc_gbuffer *g, const lmc_vpls *v, const lmc_light_tree *t, const lmc_scene *sc,
+                      const lmc_config *cfg, lmc_ctx **out)
+{
+    if (!cfg || !out) return LMC_EINVAL;
+    lmc_ctx *c = new (std::nothrow) lmc_ctx();
+    if (!c) return LMC_ENOMEM;
+    memset(&c->d, 0, sizeof(c->d));
+    c->cfg = *cfg;
+    lmc_status st = create_impl(c, g, v, t, sc);
+    if (st != LMC_OK) {
+        static thread_local std::string last;
+        last = c->err;
+        fprintf(stderr, "lmc_create: %s: %s\n", lmc_status_str(st), c->err.c_str());
+        lmc_destroy(c);
+        return st;
+    }
+    *out = c;
+    return LMC_OK;
+}
+
+lmc_status lmc_upload_inputs(lmc_ctx *c, const lmc_gbuffer *g, const lmc_vpls *v, const lmc_light_tree *t)
+{
+    if (!c || !g || !v) return LMC_EINVAL;
+    if (c->sticky != LMC_OK) return c->sticky;
+    (void)t;
+    if (g->count != c->M || v->count != c->NV) return fail(c, LMC_EINVAL, "upload: sizes differ from lmc_create");
+    const int mem = c->cfg.input_memory;
+    cudaStream_t st = c->stream;
+    Dev &d = c->d;
+    const float *src[13] = {g->px, g->py, g->pz, g->nx, g->ny, g->nz, g->vx, g->vy, g->vz, g->rho_r, g->rho_g, g->rho_b, g->spec};
+    CK(dcopy_in(d.pixel, g->pixel, (size_t)c->M, mem, st), "copy gbuffer");
+    for (int k = 0; k < 13; ++k) CK(dcopy_in(d.g[k], src[k], (size_t)c->M, mem, st), "copy gbuffer");
+    CK(dcopy_in(d.expo, g->exponent, (size_t)c->M, mem, st), "copy gbuffer");
+    // VPLs packed as (px,py,pz,nx)(ny,nz,0,0) by a kernel from a SoA staging copy
+    {
+        const size_t nv = (size_t)c->NV;
+        const float *vs[6] = {v->px, v->py, v->pz, v->nx, v->ny, v->nz};
+        for (int k = 0; k < 6; ++k) CK(dcopy_in(d.vpl_soa + k * nv, vs[k], nv, mem, st), "copy vpls");
+        CK(run_pack_vpls(c), "pack vpls");
+    }
+    CK(cudaStreamSynchronize(st), "sync");
+    c->state = 0;
+    return LMC_OK;
+}
+
+lmc_status lmc_set_timing(lmc_ctx *c, int32_t enabled)
+{
+    if (!c) return LMC_EINVAL;
+    c->timing = enabled;
+    return LMC_OK;
+}
+
+lmc_status lmc_build_slices(lmc_ctx *c)
+{
+    lmc_status s = check_stage(c, 0);
+    if (s != LMC_OK) return s;
+    ev_rec(c, 0);
+    CK(cudaMemsetAsync(c->d.counters, 0, 8 * sizeof(unsigned long long), c->stream), "memset counters");
+    CK(run_slicing(c), "slicing");
+    CK(run_pack_rows(c), "pack rows");
+    ev_rec(c, 1);
+    c->state = 1;
+    return LMC_OK;
+}
+
+lmc_status lmc_sample_pass1(lmc_ctx *c)
+{
+    lmc_status s = check_stage(c, 1);
+    if (s != LMC_OK) return s;
+    CK(run_pass1(c), "pass 1");
+    ev_rec(c, 2);
+    c->state = 2;
+    return LMC_OK;
+}
+
+lmc_status lmc_coarsen_cut(lmc_ctx *c)
+{
+    lmc_status s = check_stage(c, 2);
+    if (s != LMC_OK) return s;
+    CK(run_coarsen(c), "coarsening");
+    ev_rec(c, 3);
+    c->state = 3;
+    return LMC_OK;
+}
+
+lmc_status lmc_sample_pass2(lmc_ctx *c)
+{
+    lmc_status s = check_stage(c, 3);
+    if (s != LMC_OK) return s;
+    CK(run_pass2(c), "pass 2");
+    ev_rec(c, 4);
+    c->state = 4;
+    return LMC_OK;
+}
+
+lmc_status lmc_complete(lmc_ctx *c)
+{
+    lmc_status s = check_stage(c, 4);
+    if (s != LMC_OK) return s;
+    CK(run_complete(c), "completion");
+    CK(run_direct(c), "direct slices");
+    ev_rec(c, 5);
+    c->state = 5;
+    return LMC_OK;
+}
+
+lmc_status lmc_resolve_image(lmc_ctx *c, float *image, int32_t image_memory)
+{
+    lmc_status s = check_stage(c, 5);
+    if (s != LMC_OK) return s;
+    if (!image) return fail(c, LMC_EINVAL, "null image");
+    if (image_memory == LMC_MEM_DEVICE) {
+        CK(run_resolve(c, image, nullptr), "resolve");
+        ev_rec(c, 6);
+        return LMC_OK;
+    }
+    if (image_memory != LMC_MEM_HOST) return fail(c, LMC_EINVAL, "bad image_memory");
+    CK(run_resolve(c, c->d.img, nullptr), "resolve");
+    ev_rec(c, 6);
+    const size_t bytes = 3 * sizeof(float) * (size_t)c->W * c->H;
+    CK(cudaMemcpyAsync(image, c->d.img, bytes, cudaMemcpyDeviceToHost, c->stream), "image download");
+    CK(cudaStreamSynchronize(c->stream), "sync");
+    return LMC_OK;
+}
+
+lmc_status lmc_resolve_rows(lmc_ctx *c, float *rows_rgb)
+{
+    lmc_status s = check_stage(c, 5);
+    if (s != LMC_OK) return s;
+    if (!rows_rgb) return fail(c, LMC_EINVAL, "null rows_rgb");
+    CK(run_resolve(c, nullptr, rows_rgb), "resolve");
+    ev_rec(c, 6);
+    return LMC_OK;
+}
+
+lmc_status lmc_scatter_rows(lmc_ctx *c, const float *all_rows, float *image)
+{
+    lmc_status s = check_stage(c, 1);
+    if (s != LMC_OK) return s;
+    if (!all_rows || !image) return fail(c, LMC_EINVAL, "null buffer");
+    CK(run_scatter(c, all_rows, image), "scatter");
+    return LMC_OK;
+}
+
+// ---- introspection -------------------------------------------------------------------------
+static lmc_status sync_check(lmc_ctx *c, int need)
+{
+    lmc_status s = check_stage(c, need);
+    if (s != LMC_OK) return s;
+    CK(cudaStreamSynchronize(c->stream), "sync");
+    return check_overflow(c);
+}
+
+static lmc_status local_slice(lmc_ctx *c, int32_t slice, int *ls)
+{
+    if (slice < c->s0 || slice >= c->s1) return fail(c, LMC_EINVAL, "slice %d is not on this rank [%d, %d)", slice, c->s0, c->s1);
+    *ls = slice - c->s0;
+    return LMC_OK;
+}
+
+lmc_status lmc_get_slices(lmc_ctx *c, int32_t *off, int32_t *rows, int64_t *n_slices)
+{
+    lmc_status s = sync_check(c, 1);
+    if (s != LMC_OK) return s;
+    if (n_slices) *n_slices = c->S;
+    if (off) memcpy(off, c->h_slice_off.data(), c->h_slice_off.size() * 4);
+    CK(d2h(rows, c->d.rows, (size_t)c->M), "get slices");
+    return LMC_OK;
+}
+
+lmc_status lmc_get_pass1(lmc_ctx *c, int32_t slice, int32_t *node, int32_t *count, int32_t *rows, double *Ta, double *Tb,
+                         int32_t *n_pairs, int32_t *nmax)
+{
+    lmc_status s = sync_check(c, 2);
+    if (s != LMC_OK) return s;
+    int ls;
+    if ((s = local_slice(c, slice, &ls)) != LMC_OK) return s;
+    const int nB = c->up.nB, nm = c->nmax;
+    if (n_pairs) *n_pairs = nB;
+    if (nmax) *nmax = nm;
+    if (node) {
+        std::vector<int32_t> bl(nB);
+        CK(d2h(bl.data(), c->up.base_list, (size_t)nB), "get pass1");
+        for (int k = 0; k < nB; ++k) node[k] = c->h_up_node[bl[k]];
+    }
+    const size_t o = (size_t)ls * nB * nm;
+    CK(d2h(count, c->d.p1_cnt + (size_t)ls * nB, (size_t)nB), "get pass1");
+    if (rows) {
+        std::vector<uint16_t> r((size_t)nB * nm);
+        CK(d2h(r.data(), c->d.p1_rows + o, r.size()), "get pass1");
+        for (size_t k = 0; k < r.size(); ++k) rows[k] = r[k];
+    }
+    CK(d2h(Ta, c->d.p1_Ta + o, (size_t)nB * nm), "get pass1");
+    CK(d2h(Tb, c->d.p1_Tb + o, (size_t)nB * nm), "get pass1");
+    return LMC_OK;
+}
+
+lmc_status lmc_get_coarsen(lmc_ctx *c, int32_t slice, int32_t *node, int32_t *processed, int32_t *merged, double *eps,
+                           double *cost, int32_t *n_nodes)
+{
+    lmc_status s = sync_check(c, 3);
+    if (s != LMC_OK) return s;
+    int ls;
+    if ((s = local_slice(c, slice, &ls)) != LMC_OK) return s;
+    const int U = c->up.U;
+    if (n_nodes) *n_nodes = U;
+    if (node) memcpy(node, c->h_up_node.data(), (size_t)U * 4);
+    std::vector<uint8_t> fl(U);
+    CK(d2h(fl.data(), c->d.cs_flags + (size_t)ls * U, (size_t)U), "get coarsen");
+    for (int u = 0; u < U; ++u) {
+        if (processed) processed[u] = (fl[u] & 4) ? 1 : 0;
+        if (merged) merged[u] = (fl[u] & 2) ? 1 : 0;
+    }
+    CK(d2h(eps, c->d.cs_eps + (size_t)ls * U, (size_t)U), "get coarsen");
+    CK(d2h(cost, c->d.cs_cost + (size_t)ls * U, (size_t)U), "get coarsen");
+    return LMC_OK;
+}
+
+lmc_status lmc_get_cut(lmc_ctx *c, int32_t slice, int32_t *nodes, int32_t *n)
+{
+    lmc_status s = sync_check(c, 3);
+    if (s != LMC_OK) return s;
+    int ls;
+    if ((s = local_slice(c, slice, &ls)) != LMC_OK) return s;
+    int32_t cnt = 0;
+    CK(d2h(&cnt, c->d.cut_n + ls, 1), "get cut");
+    if (n) *n = cnt;
+    if (nodes) {
+        std::vector<int32_t> u(cnt);
+        CK(d2h(u.data(), c->d.cut_cols + (size_t)ls * c->G, (size_t)cnt), "get cut");
+        for (int k = 0; k < cnt; ++k) nodes[k] = c->h_up_node[u[k]];
+    }
+    return LMC_OK;
+}
+
+lmc_status lmc_get_samples(lmc_ctx *c, int32_t slice, int32_t *row, int32_t *col, float *val, int32_t *carried,
+                           int64_t *n, int64_t *target_n)
+{
+    lmc_status s = sync_check(c, 4);
+    if (s != LMC_OK) return s;
+    int ls;
+    if ((s = local_slice(c, slice, &ls)) != LMC_OK) return s;
+    int32_t nnz = 0, tn = 0;
+    CK(d2h(&nnz, c->d.nnz + ls, 1), "get samples");
+    CK(d2h(&tn, c->d.target_n + ls, 1), "get samples");
+    if (n) *n = nnz;
+    if (target_n) *target_n = tn;
+    const int m = c->h_slice_off[slice + 1] - c->h_slice_off[slice];
+    const size_t ob = (size_t)ls * c->ncap;
+    if (row) {
+        std::vector<int32_t> rp(m + 1);
+        CK(d2h(rp.data(), c->d.rowptr + (size_t)ls * (c->mmax + 1), (size_t)m + 1), "get samples");
+        for (int i = 0; i < m; ++i)
+            for (int k = rp[i]; k < rp[i + 1]; ++k) row[k] = i;
+    }
+    if (col) {
+        std::vector<uint16_t> cc(nnz);
+        CK(d2h(cc.data(), c->d.col + ob, (size_t)nnz), "get samples");
+        for (int k = 0; k < nnz; ++k) col[k] = cc[k];
+    }
+    CK(d2h(val, c->d.val + ob, (size_t)nnz), "get samples");
+    if (carried) {
+        std::vector<uint8_t> cr(nnz);
+        CK(d2h(cr.data(), c->d.carried + ob, (size_t)nnz), "get samples");
+        for (int k = 0; k < nnz; ++k) carried[k] = cr[k];
+    }
+    return LMC_OK;
+}
+
+lmc_status lmc_get_factors(lmc_ctx *c, int32_t slice, float *U, float *V, int32_t *m, int32_t *n, int32_t *q,
+                           int32_t *flags, int32_t *iters, float *resid)
+{
+    lmc_status s = sync_check(c, 5);
+    if (s != LMC_OK) return s;
+    int ls;
+    if ((s = local_slice(c, slice, &ls)) != LMC_OK) return s;
+    const int mm = c->h_slice_off[slice + 1] - c->h_slice_off[slice];
+    int32_t nn = 0;
+    CK(d2h(&nn, c->d.cut_n + ls, 1), "get factors");
+    if (m) *m = mm;
+    if (n) *n = nn;
+    if (q) *q = c->q;
+    CK(d2h(flags, c->d.flags + ls, 1), "get factors");
+    CK(d2h(iters, c->d.iters + ls, 1), "get factors");
+    CK(d2h(resid, c->d.resid + ls, 1), "get factors");
+    const int64_t lrow0 = c->h_slice_off[slice] - c->row0;
+    CK(d2h(U, c->d.U + lrow0 * c->q, (size_t)mm * c->q), "get factors");
+    if (V) {   // device layout: column j contiguous (n x q); returned q x n row-major
+        std::vector<float> vt((size_t)nn * c->q);
+        CK(d2h(vt.data(), c->d.V + (size_t)ls * c->G * c->q, vt.size()), "get factors");
+        for (int j = 0; j < nn; ++j)
+            for (int a = 0; a < c->q; ++a) V[(size_t)a * nn + j] = vt[(size_t)j * c->q + a];
+    }
+    return LMC_OK;
+}
+
+lmc_status lmc_get_stats(lmc_ctx *c, lmc_stats *st)
+{
+    if (!c || !st) return LMC_EINVAL;
+    lmc_status s = sync_check(c, 0);
+    if (s != LMC_OK) return s;
+    memset(st, 0, sizeof *st);
+    st->n_slices = c->S;
+    st->slice_begin = c->s0;
+    st->slice_end = c->s1;
+    st->rows = c->ML;
+    st->pool_cap = c->pool_cap;
+    unsigned long long cnt[5];
+    CK(d2h(cnt, c->d.counters, 5), "stats");
+    st->evals_pass1 = (int64_t)cnt[0];
+    st->evals_coarsen = (int64_t)cnt[1];
+    st->evals_pass2 = (int64_t)cnt[2];
+    st->pool_used_max = (int64_t)cnt[4];
+    if (c->state >= 3) {
+        std::vector<int32_t> cn(c->SL);
+        CK(d2h(cn.data(), c->d.cut_n, (size_t)c->SL), "stats");
+        for (int ls = 0; ls < c->SL; ++ls) {
+            int64_t m = c->h_slice_off[c->s0 + ls + 1] - c->h_slice_off[c->s0 + ls];
+            st->sum_cols += cn[ls];
+            st->sum_completed += m * cn[ls];
+        }
+    }
+    if (c->state >= 4) {
+        std::vector<int32_t> nz(c->SL);
+        CK(d2h(nz.data(), c->d.nnz, (size_t)c->SL), "stats");
+        for (int v : nz) st->sum_samples += v;
+    }
+    if (c->state >= 5) {
+        std::vector<int32_t> fl(c->SL);
+        CK(d2h(fl.data(), c->d.flags, (size_t)c->SL), "stats");
+        for (int f : fl) {
+            st->n_direct += (f & LMC_SLICE_DIRECT) ? 1 : 0;
+            st->n_zero += (f & LMC_SLICE_ZERO) ? 1 : 0;
+            st->n_diverged += (f & LMC_SLICE_DIVERGED) ? 1 : 0;
+        }
+    }
+    if (c->timing && c->ev_ok && c->state >= 5) {
+        float *ms[6] = {&st->ms_slices, &st->ms_pass1, &st->ms_coarsen, &st->ms_pass2, &st->ms_complete, &st->ms_resolve};
+        for (int k = 0; k < 6; ++k) {
+            float v = 0.f;
+            if (cudaEventElapsedTime(&v, c->ev[k], c->ev[k + 1]) == cudaSuccess) *ms[k] = v;
+        }
+        cudaGetLastError();
+    }
+    return LMC_OK;
+}
+
+lmc_status lmc_eval_entries(lmc_ctx *c, int64_t n, const int32_t *rows, const int32_t *vpls, double *out)
+{
+    if (!c || n < 0 || (n > 0 && (!rows || !vpls || !out))) return LMC_EINVAL;
+    if (c->sticky != LMC_OK) return c->sticky;
+    for (int64_t k = 0; k < n; ++k)
+        if (rows[k] < 0 || rows[k] >= c->M || vpls[k] < 0 || vpls[k] >= c->NV) return fail(c, LMC_EINVAL, "pair %lld out of range", (long long)k);
+    int32_t *dr = nullptr, *dv = nullptr;
+    double *dout = nullptr;
+    float4 *tmp = nullptr;
+    lmc_status st = LMC_OK;
+    cudaError_t e;
+    if ((e = dalloc(&dr, (size_t)n)) != cudaSuccess || (e = dalloc(&dv, (size_t)n)) != cudaSuccess ||
+        (e = dalloc(&dout, (size_t)n)) != cudaSuccess || (e = dalloc(&tmp, 4 * (size_t)n)) != cudaSuccess) {
+        st = cuda_fail(c, e, "eval alloc");
+    } else if ((e = cudaMemcpy(dr, rows, n * 4, cudaMemcpyHostToDevice)) != cudaSuccess ||
+               (e = cudaMemcpy(dv, vpls, n * 4, cudaMemcpyHostToDevice)) != cudaSuccess ||
+               (e = run_eval_entries(c, n, dr, dv, dout, tmp)) != cudaSuccess ||
+               (e = cudaStreamSynchronize(c->stream)) != cudaSuccess ||
+               (e = cudaMemcpy(out, dout, n * 8, cudaMemcpyDeviceToHost)) != cudaSuccess) {
+        st = cuda_fail(c, e, "eval entries");
+    }
+    cudaFree(dr);
+    cudaFree(dv);
+    cudaFree(dout);
+    cudaFree(tmp);
+    return st;
+}
+
+}  // extern "C"

@@ -1,0 +1,163 @@
+// lmc_internal.h — device views and launcher declarations shared by the liblmc translation units.
+// (Internal to the CUDA path; the oracle never sees this file.)
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "lmc.h"
+
+namespace lmc {
+
+constexpr int TAG_P1 = 1, TAG_P2 = 2, TAG_FORCE = 3, TAG_X0 = 4, TAG_Y0 = 5;
+constexpr int MAX_PRIMS = 64;
+constexpr int MAX_Q = 32;
+constexpr int MAX_SLICE = 1024;   // rows per slice (bitmap words per row set = 32)
+constexpr int MAX_CUT = 1024;     // |global cut| (columns per slice)
+constexpr int MAX_NMAX = 32;      // pass-1 rows per pair (one warp)
+
+// Analytic occluders + entry constants (host-filled, uploaded to __constant__ of the exact TU)
+struct SceneConst {
+    int32_t nsph, nbox, nrect, pad;
+    double dc2;        // clamp_dist * clamp_dist
+    double eps;        // shadow_eps
+    float sph[MAX_PRIMS * 4];
+    float box[MAX_PRIMS * 6];
+    float rect[MAX_PRIMS * 12];
+};
+
+// Upper light tree: the global cut g and all its ancestors, local ids in ascending node id.
+struct Upper {
+    int32_t U;                // nodes
+    int32_t H;                // max height (g nodes have height 0)
+    int32_t nB;               // base pairs (both children in g)
+    const int32_t *node;      // global node id
+    const int32_t *left, *right, *parent;   // local ids, -1 if none
+    const int32_t *rep;       // representative VPL
+    const int32_t *nunc;      // max(nmin, ceil(nmax lum / l_max)) (unclamped by m)
+    const int32_t *hlist;     // internal nodes ordered by (height, id)
+    const int32_t *hoff;      // H+2 offsets into hlist by height (height 1..H)
+    const int32_t *base_list; // local ids of base pairs (ascending)
+    const int32_t *base_of;   // local id -> base index or -1
+    const double *lum;        // lum(I_f), fp64 from the float32 intensities
+    const float *I;           // 3 per node
+};
+
+// Per-frame device state (all allocated in lmc_create)
+struct Dev {
+    // inputs
+    int32_t *pixel;
+    float *g[13];             // px py pz nx ny nz vx vy vz rho_r rho_g rho_b spec
+    int32_t *expo;
+    float4 *vpl;              // 2 per VPL: (px,py,pz,nx) (ny,nz,0,0)
+    // upper tree arrays (backing store of Upper)
+    int32_t *ut_i32;
+    double *ut_lum;
+    float *ut_I;
+    // slicing
+    int32_t *rows, *rows_alt;          // M
+    unsigned long long *keys, *keys_alt; // M
+    int32_t *lvl_begin, *lvl_end;      // concatenated level tilings
+    int32_t *lvl_slot;                 // per tile: extent slot of a splitting tile, -1 otherwise
+    int32_t *lvl_work;                 // concatenated extent work items (seg, start, len) triples
+    unsigned long long *ext;           // max-segments * 12
+    int32_t *slice_off;                // S+1
+    void *cub_tmp;
+    size_t cub_tmp_bytes;
+    float4 *prow;                      // 4 per local row (slice order)
+    // pass 1: [SL][nB][nmax]
+    uint16_t *p1_rows;
+    double *p1_Ta, *p1_Tb;
+    int32_t *p1_cnt;                   // [SL][nB]
+    // coarsening
+    uint16_t *pool_rows;               // [SL][pool_cap]
+    double *pool_Ta, *pool_Tb;
+    int32_t *pool_used;                // [SL]
+    uint8_t *cs_flags;                 // [SL][U]  bit0 in_cut, bit1 merged, bit2 processed
+    double *cs_eps, *cs_cost;          // [SL][U]
+    int32_t *cs_zoff, *cs_zlen;        // [SL][U]
+    int32_t *cut_n;                    // [SL]
+    int32_t *cut_cols;                 // [SL][G] local upper ids
+    int32_t *src_off, *src_len, *src_side; // [SL][G] carried-observation source per column
+    // pass 2: per slice capacity ncap
+    int32_t *rowptr;                   // [SL][mmax+1]
+    uint16_t *col;                     // [SL][ncap]
+    float *val;                        // [SL][ncap]
+    uint8_t *carried;                  // [SL][ncap]
+    int32_t *colptr;                   // [SL][G+1]
+    uint16_t *csc_row;                 // [SL][ncap]
+    int32_t *csc_src;                  // [SL][ncap]
+    int32_t *nnz, *target_n, *n_new;   // [SL]
+    uint32_t *newcells;                // [SL][ncap] (cell = i*n + c)
+    int32_t *newpos;                   // [SL][ncap] CSR position of new cell
+    // completion
+    float *U, *V, *Lam, *Pi, *Xold, *S; // U/Lam/Xold [ML][q], V/Pi [SL][G][q], S [SL][ncap]
+    int32_t *flags, *iters;            // [SL]
+    float *resid;                      // [SL]
+    float *direct_rgb;                 // [ML][3]
+    float *rows_rgb;                   // [ML][3]
+    float *img;                        // [H*W][3] staging image for host output
+    float *vpl_soa;                    // 6 * NV staging for the VPL packing kernel
+    // counters: 0 evals_pass1, 1 evals_coarsen, 2 evals_pass2, 3 overflow flags, 4 pool_used_max
+    unsigned long long *counters;
+};
+
+}  // namespace lmc
+
+struct lmc_ctx {
+    lmc_config cfg;
+    cudaStream_t stream = nullptr;
+    int state = 0;                 // 0 created, 1 sliced, 2 pass1, 3 coarsened, 4 pass2, 5 completed
+    lmc_status sticky = LMC_OK;
+    std::string err;
+    // sizes
+    int64_t M = 0;                 // valid rows
+    int32_t W = 0, H = 0;
+    int64_t NV = 0, NN = 0;
+    double diag = 1.0;
+    int32_t G = 0;                 // |global cut|
+    int32_t S = 0;                 // slices (whole frame)
+    std::vector<int32_t> h_slice_off;
+    int32_t s0 = 0, s1 = 0, SL = 0;
+    int64_t row0 = 0, ML = 0;
+    int32_t mmax = 0;
+    int32_t q = 0, nmax = 0;
+    int64_t pool_cap = 0, ncap = 0;
+    // slicing level structure
+    struct Level { int32_t tile_off, tile_n, work_off, work_n, next_tile_off, next_tile_n, nslots; };
+    std::vector<Level> levels;
+    int32_t max_tiles = 0;
+    // scene + upper tree
+    lmc::SceneConst scene;
+    lmc::Upper up;
+    std::vector<int32_t> h_up_node;   // for getters
+    lmc::Dev d;
+    // timing
+    int timing = 0;
+    cudaEvent_t ev[8];
+    float ms[6] = {0, 0, 0, 0, 0, 0};
+    bool ev_ok = false;
+    float *h_stage = nullptr;
+};
+
+namespace lmc {
+// exact.cu (fp64 decision precision, compiled with -fmad=false)
+cudaError_t upload_scene(const SceneConst &sc);
+cudaError_t run_slicing(lmc_ctx *c);
+cudaError_t run_pack_rows(lmc_ctx *c);
+cudaError_t run_pass1(lmc_ctx *c);
+cudaError_t run_coarsen(lmc_ctx *c);
+cudaError_t run_pass2(lmc_ctx *c);
+cudaError_t run_direct(lmc_ctx *c);
+cudaError_t run_eval_entries(lmc_ctx *c, int64_t n, const int32_t *d_rows, const int32_t *d_vpls, double *d_out,
+                             float4 *d_tmp_rows);
+cudaError_t slicing_tmp_bytes(int64_t M, int32_t max_tiles, size_t *bytes);
+cudaError_t run_pack_vpls(lmc_ctx *c);
+// complete.cu (fp32 completion + resolve)
+cudaError_t run_complete(lmc_ctx *c);
+cudaError_t run_resolve(lmc_ctx *c, float *image, float *rows_rgb);
+cudaError_t run_scatter(lmc_ctx *c, const float *all_rows, float *image);
+size_t complete_smem_bytes(int q, int mmax, int G, int solver);
+}  // namespace lmc

@@ -1,0 +1,36 @@
+"""CPU checks of the C-ABI library: it loads without a GPU and exports every symbol that
+include/lmc.h declares (no compute calls here)."""
+import ctypes
+import os
+import re
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared():
+    src = open(os.path.join(ROOT, "include", "lmc.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(lmc_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    import paper_2202_12567_b200.build as b
+    path = b.build()
+    lib = ctypes.CDLL(path)
+    names = declared()
+    assert len(names) >= 20
+    missing = [n for n in names if not hasattr(lib, n)]
+    assert not missing, missing
+
+
+def test_binding_names_match_header():
+    from paper_2202_12567_b200 import lmc
+    assert sorted(lmc.EXPORTS) == declared()
+
+
+def test_status_strings_without_gpu():
+    from paper_2202_12567_b200 import lmc
+    assert lmc.lib.lmc_status_str(0) == b"LMC_OK"
+    assert lmc.lib.lmc_status_str(5) == b"LMC_EOVERFLOW"
+    # a NULL config is rejected before any CUDA call
+    assert lmc.lib.lmc_create(None, None, None, None, None, None) == lmc.LMC_EINVAL
