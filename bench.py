@@ -1,0 +1,344 @@
+#!/usr/bin/env python3
+"""Benchmark of the lighting-matrix hot path (arXiv 2202.12567) on B200.
+
+A step = one frame of the whole hot path: lmc_build_slices,
+lmc_sample_pass1, lmc_coarsen_cut, lmc_sample_pass2, lmc_complete, lmc_resolve_image (+ for
+N > 1 the NCCL gather of the packed image tiles to rank 0 and the scatter into the image), on
+one batch of seeded synthetic input (scenegen) resident in HBM.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--solver adm|mals]
+  python bench.py --impl reference ...     # the fp64 CPU oracle on a bounded sample
+
+Prints ONE JSON line (rank 0).  metric/unit: BASELINE.json's "ms/frame and lighting-matrix
+entries completed/s"; value = sum_s m_s n_s (entries of the completed slice matrices of the
+whole frame) / (ms/frame); ms_per_step = ms/frame.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ms/frame and lighting-matrix entries completed/s at 1/2/4/8 B200"
+UNIT = "entries/s"
+FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # 74.4: 148 SMs x 128 FP32 lanes x FMA x max clock
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--config", default="c4")
+    p.add_argument("--solver", default="adm", choices=["adm", "mals"])
+    p.add_argument("--impl", default="lmc", choices=["lmc", "reference"])
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-sample-slices", type=int, default=0)
+    return p.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu):
+        self.gpu = gpu
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([s.strip() for s in line.split(",")])
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.t.join(timeout=2)
+        sm = [float(r[1]) for r in self.rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            if len(r) < 9:
+                continue
+            for k, nm in enumerate(names):
+                if r[5 + k].lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def adm_flops(q, sum_N, sum_m, sum_n, nslices, iters):
+    """Algorithmic flops of ADM per frame: per iteration and slice
+    6 q N (SDDMM + S Y^T + X^T S) + 6 m q^2 (X update + 2 Grams) + 6 n q^2 (Y update + Gram)
+    + 2 q^3 (two q x q SPD inverses)."""
+    return iters * (6.0 * q * sum_N + 6.0 * q * q * sum_m + 6.0 * q * q * sum_n + 2.0 * q ** 3 * nslices)
+
+
+def mals_flops(q, sum_N, sum_m, sum_n, nslices, iters):
+    """per iteration and slice: Gram + rhs 2 N (q(q+1)/2 + q) twice (rows then columns)
+    + (m + n)(q^3/3 + 2 q^2) (Cholesky + two triangular solves)."""
+    per_sample = 2.0 * (q * (q + 1) / 2 + q)
+    return iters * (2 * per_sample * sum_N + (sum_m + sum_n) * (q ** 3 / 3.0 + 2.0 * q * q))
+
+
+def cpu_oracle_sample(x, nslices_sample, solver):
+    """Time the fp64 oracle (as it stands) on a bounded sample of the workload's slices."""
+    import oracle
+    o = oracle.Oracle(x, solver=solver)
+    off, _ = o.slices()
+    S = off.size - 1
+    ids = np.linspace(0, S - 1, min(nslices_sample, S)).astype(np.int32)
+    t0 = time.perf_counter()
+    res = o.run_slices(ids, stage=4)
+    dt = time.perf_counter() - t0
+    entries = sum(r["m"] * r["n"] for r in res)
+    return entries / dt, dt, len(ids), entries
+
+
+def omp_threads():
+    return int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the fp64 oracle on the host cores, each step a bounded sample."""
+    if rank != 0:
+        return
+    import scenegen
+    x = scenegen.make_inputs(scenegen.preset(args.config, solver=1 if args.solver == "mals" else 0))
+    cores = omp_threads()
+    nsamp = args.cpu_sample_slices or max(cores, 8)
+    for _ in range(args.warmup if args.warmup < 1 else 1):
+        cpu_oracle_sample(x, max(1, nsamp // 4), x.cfg.solver)
+    vals, times = [], []
+    for _ in range(args.steps):
+        v, dt, k, ent = cpu_oracle_sample(x, nsamp, x.cfg.solver)
+        vals.append(v)
+        times.append(dt)
+    value = statistics.median(vals)
+    S = len(__import__("oracle").Oracle(x).slices()[0]) - 1
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": statistics.median(times) * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": f"{args.config}: {x.width}x{x.height} px, {x.vpls['px'].size} VPLs, "
+                                   f"{S} slices, q={x.cfg.rank_q}, rate={x.cfg.rate}, solver={args.solver}",
+                       "sample": f"{nsamp} of {S} slices per step (whole per-slice pipeline)"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": f"{nsamp} of {S} slices per step"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    import torch
+    import torch.distributed as dist
+
+    import scenegen
+    from paper_2202_12567_b200 import lmc
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    solver = 1 if args.solver == "mals" else 0
+    x = scenegen.make_inputs(scenegen.preset(args.config, solver=solver))
+    stream = torch.cuda.current_stream(dev)
+    fr = lmc.Frame(x, rank=rank, world=world, stream=stream)
+    fr.set_timing(True)
+    npix = x.height * x.width
+    img = torch.zeros(npix * 3, device=dev)
+    st0 = fr.stats()
+    rows_local = int(st0["rows"])
+    # slice-ordered row ranges of every rank (identical slicing everywhere) for the tile gather
+    if world > 1:
+        counts = torch.zeros(world, dtype=torch.int64, device=dev)
+        counts[rank] = rows_local
+        dist.all_reduce(counts)
+        counts = counts.tolist()
+        maxrows = max(counts)
+        tile = torch.zeros(maxrows * 3, device=dev)
+        gathered = torch.zeros(world * maxrows * 3, device=dev) if True else None
+        all_rows = torch.zeros(x.m * 3, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > L2 (126 MB)
+
+    def frame_once():
+        fr.build_slices()
+        fr.sample_pass1()
+        fr.coarsen_cut()
+        fr.sample_pass2()
+        fr.complete()
+        if world == 1:
+            fr.resolve_image(img)
+        else:
+            fr.resolve_rows(tile)
+            dist.all_gather_into_tensor(gathered, tile)
+            if rank == 0:
+                off = 0
+                g3 = gathered.view(world, maxrows * 3)
+                for r in range(world):
+                    all_rows[off * 3:(off + counts[r]) * 3] = g3[r, :counts[r] * 3]
+                    off += counts[r]
+                fr.scatter_rows(all_rows, img)
+
+    for _ in range(args.warmup):
+        frame_once()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    times, ms_complete, stage = [], [], {k: [] for k in ("slices", "pass1", "coarsen", "pass2", "complete", "resolve")}
+    launches0 = fr.stats()["launches"]
+    for _ in range(args.steps):
+        flush.fill_(1.0)                      # flush L2 between timed frames (outside the events)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        frame_once()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1))
+        st = fr.stats()
+        for k in stage:
+            stage[k].append(st["ms_" + k])
+    cl = clocks.stop()
+    launches = fr.stats()["launches"] - launches0
+    ms = statistics.mean(times)
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        tc = torch.tensor([statistics.mean(stage["complete"])], device=dev, dtype=torch.float64)
+        dist.all_reduce(tc, op=dist.ReduceOp.MAX)
+    st = fr.stats()
+    tot = torch.tensor([st["sum_completed"], st["sum_samples"], st["sum_cols"], st["rows"],
+                        st["slice_end"] - st["slice_begin"], st["evals_pass1"] + st["evals_coarsen"] + st["evals_pass2"]],
+                       dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tot)
+    sum_completed, sum_N, sum_n, sum_m, nsl, evals = [float(v) for v in tot.tolist()]
+    value = sum_completed / (ms * 1e-3)
+    # roofline of the dominant kernel (completion) from its stage events on the launching stream
+    ms_c = statistics.mean(stage["complete"])
+    q = x.cfg.rank_q
+    K = x.cfg.max_iter
+    fl = (adm_flops if solver == 0 else mals_flops)(q, st["sum_samples"], st["rows"], st["sum_cols"],
+                                                     st["slice_end"] - st["slice_begin"], K)
+    achieved = fl / (ms_c * 1e-3) / 1e12
+    e2e = None
+    if not args.no_e2e and world == 1:
+        e2e = measure_e2e(x, args, solver, dev)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cores = omp_threads()
+        nsamp = args.cpu_sample_slices or max(cores, 8)
+        v, dt, k, ent = cpu_oracle_sample(x, nsamp, solver)
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": f"{k} of {int(nsl)} slices of {args.config} (full per-slice pipeline, literal dense-Z "
+                         f"ADM), {dt:.1f} s wall"}
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": f"{args.config}: {x.width}x{x.height} px, {x.vpls['px'].size} VPLs, {int(nsl)} slices, "
+                               f"q={q}, rate={x.cfg.rate}, K={K}, solver={args.solver}",
+                   "l2": "flushed between timed frames (256 MiB write)",
+                   "decisions": "f64 (entries, sampling, coarsening)", "completion": "f32"},
+        "ms_per_stage": {k: statistics.mean(v) for k, v in stage.items()},
+        "completed_entries": sum_completed, "samples": sum_N, "rays_per_pixel": evals / max(sum_m, 1.0),
+        "roofline": {"bound": "alu", "kernel": "k_adm" if solver == 0 else "k_mals", "achieved": achieved,
+                     "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP32_PEAK_TFLOPS,
+                     "traffic": None, "peak_source": "derived: 148 SMs x 128 FP32 FMA lanes x 2 x 1.965 GHz"},
+        "clocks": cl,
+        "gpu_launches": launches,
+    }
+    if e2e:
+        line["e2e"] = e2e
+    if cpu:
+        line["cpu_baseline"] = cpu
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def measure_e2e(x, args, solver, dev):
+    """Same metric through the C-ABI with HOST buffers: per step, H2D of the frame's inputs
+    (G-buffer + VPLs from pinned memory), the seven calls, D2H of the image."""
+    import torch
+    from paper_2202_12567_b200 import lmc
+    fr = lmc.Frame(x, memory=lmc.MEM_HOST, stream=torch.cuda.current_stream(dev))
+    npix = x.height * x.width
+    host_img = torch.zeros(npix * 3, dtype=torch.float32).pin_memory()
+    h2d = x.m * (14 * 4) + x.vpls["px"].size * 6 * 4
+    d2h = npix * 3 * 4
+
+    def step():
+        fr.upload_inputs()
+        fr.build_slices()
+        fr.sample_pass1()
+        fr.coarsen_cut()
+        fr.sample_pass2()
+        fr.complete()
+        fr.resolve_image(host_img.numpy(), lmc.MEM_HOST)
+
+    for _ in range(max(1, args.warmup)):
+        step()
+    ts = []
+    for _ in range(args.steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        step()
+        torch.cuda.synchronize()
+        ts.append(time.perf_counter() - t0)
+    st = fr.stats()
+    fr.close()
+    return {"value": st["sum_completed"] / statistics.mean(ts), "unit": UNIT, "ms_per_step": statistics.mean(ts) * 1e3,
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+
+
+if __name__ == "__main__":
+    main()

@@ -116,6 +116,7 @@ typedef struct {
     int64_t evals_pass1, evals_coarsen, evals_pass2; /* entry evaluations (shadow rays) */
     int64_t n_direct, n_zero, n_diverged;
     int64_t pool_used_max, pool_cap; /* coarsening sample pool per slice (entries) */
+    int64_t launches;          /* kernel launches issued by the stage calls since lmc_create */
     float ms_slices, ms_pass1, ms_coarsen, ms_pass2, ms_complete, ms_resolve; /* last frame, if timed */
 } lmc_stats;
 

@@ -1,17 +1,18 @@
-// complete.cu — per-slice low-rank completion and factored image rendering (sm_100a, fp32).
+// complete.cu — per-slice ADM completion, Omega layout and factored image rendering (sm_100a).
 //
-//   ADM      PAPER.md:149 and Appendix A, typo readings R18; Z kept implicit:
-//            Z_k = X_k Y_k + S_k with S_k = P_Omega(M^ - X_k Y_k), so
-//              Z_k Y_k^T   = X_k (Y_k Y_k^T) + S_k Y_k^T
-//              X^T Z_k     = (X^T X_k) Y_k + X^T S_k
-//            and X_{k+1} = X_k + (S_k Y_k^T + a U_k - L_k - a X_k)(Y_k Y_k^T + a I)^{-1}.
-//   MALS     BASELINE north_star: per-row / per-column ridge normal equations over Omega,
-//            accumulated in registers, solved by in-register Cholesky.
+//   ADM      PAPER.md:149 and Appendix A, typo readings R18, fp32.  Z is never
+//            formed: Z_k = X_k Y_k + S_k with S_k = P_Omega(M^ - X_k Y_k), so
+//              Z_k Y_k^T = X_k (Y_k Y_k^T) + S_k Y_k^T,   X^T Z_k = (X^T X_k) Y_k + X^T S_k
+//            and X_{k+1} = X_k + (S_k Y_k^T + a U_k - L_k - a X_k)(Y_k Y_k^T + a I)^{-1}
+//            (Z_0 = P_Omega(M^) has no X_0 Y_0 part: the k = 0 step drops the X_k terms).
 //   resolve  I(s) = X (Y e) with RGB weights w^k_c = I^k_c / lum(I_c) (R4).
 //
-// One CTA per slice; X (m x q) and Y (n x q, column j contiguous) stay in shared memory for
-// all K iterations; Omega (CSR + CSC) streams from L2; U, Lambda, V, Pi and S live in global
-// memory (L2-resident at the working-set sizes of a frame).
+// Work decomposition (one CTA per slice, X and Y resident in shared memory for all K
+// iterations): a row (column) is owned by a group of L = q/4 lanes, each holding four of its q
+// components as a float4, so a warp advances R = 32/L rows at once.  Omega streams from L2 in a
+// sliced-ELL layout (k_layout: rows sorted by length, groups of R rows interleaved) so every
+// warp-wide load of column ids / values is coalesced and the y_j / x_i gathers are 64-byte
+// contiguous per lane group.
 #include <cub/cub.cuh>
 
 #include "lmc_internal.h"
@@ -20,27 +21,6 @@
 namespace lmc {
 
 #define FULLM 0xffffffffu
-
-struct CArgs {
-    const int32_t *slice_off;
-    int32_t s0, lbase, G, mmax;
-    int64_t ncap;
-    int K;
-    float alpha, beta, gamma, tol, lambda;
-    uint64_t seed;
-    const int32_t *cut_n, *rowptr, *colptr, *csc_src, *nnz;
-    const uint16_t *col, *csc_row;
-    const float *val;
-    float *U, *V, *Lam, *Pi, *Xold, *S, *resid;
-    int32_t *flags, *iters;
-};
-
-template <int Q>
-struct Cfg {
-    static constexpr int QP = (Q >= 32) ? Q : Q + 4;          // padded row stride (floats)
-    static constexpr int NT = (Q >= 32) ? 256 : 512;          // threads per CTA
-    static constexpr int PART = 4096;                          // floats of Gram partials / GJ workspace
-};
 
 __device__ __forceinline__ float warp_sum(float v)
 {
@@ -71,17 +51,153 @@ __device__ float block_reduce(float v, float *red)
     return red[32];
 }
 
-// out[a][b] = sum_i A[i][a] * B[i][b] over `rows` rows (A, B row-major with strides lda, ldb).
-// Deterministic: fixed partition of rows and a fixed-order sum of the partials.
-template <int Q>
-__device__ void gram(const float *A, int lda, const float *B, int ldb, int rows, float *out, float *part)
+__device__ __forceinline__ float4 f4fma(float s, float4 y, float4 a)
 {
-    constexpr int TQ = Q / 4;
-    constexpr int T = TQ * TQ;                 // 4x4 tiles
-    int P = (int)blockDim.x / T;
+    return make_float4(fmaf(s, y.x, a.x), fmaf(s, y.y, a.y), fmaf(s, y.z, a.z), fmaf(s, y.w, a.w));
+}
+__device__ __forceinline__ float f4dot(float4 a, float4 b) { return fmaf(a.w, b.w, fmaf(a.z, b.z, fmaf(a.y, b.y, a.x * b.x))); }
+__device__ __forceinline__ float f4get(float4 v, int c) { return c == 0 ? v.x : c == 1 ? v.y : c == 2 ? v.z : v.w; }
+
+// ------------------------------------------------------------------------------------------
+// Omega layout: sliced ELL over rows and over columns (groups of R, sorted by length).
+// Row entries: (float bits of M^ = M~/sigma) << 32 | column;  column entries: (index of the
+// entry in the row layout) << 10 | row.  Also the per-slice normalisation (R23).
+// ------------------------------------------------------------------------------------------
+struct LArgs {
+    const int32_t *slice_off, *cut_n, *rowptr, *colptr, *csc_src, *nnz;
+    const uint16_t *col, *csc_row;
+    const float *val;
+    int32_t s0, G, mmax, R;
+    int64_t ncap, scap;
+    uint16_t *r_perm, *r_len, *c_perm, *c_len;
+    int32_t *r_goff, *c_goff, *map;
+    unsigned long long *r_ent;
+    uint32_t *c_ent;
+    float4 *norm;
+};
+
+constexpr int LT = 1024;
+
+__global__ void __launch_bounds__(LT, 1) k_layout(LArgs A)
+{
+    typedef cub::BlockRadixSort<uint32_t, LT, 1> Sort;
+    typedef cub::BlockScan<int32_t, LT> Scan;
+    extern __shared__ __align__(16) unsigned char lsm[];
+    typename Sort::TempStorage &sort_tmp = *reinterpret_cast<typename Sort::TempStorage *>(lsm);
+    __shared__ typename Scan::TempStorage scan_tmp;
+    __shared__ int32_t sh_goff[LT + 1];
+    __shared__ int32_t sh_len[LT];
+    __shared__ float red[33];
+    const int ls = blockIdx.x, s = A.s0 + ls, tid = threadIdx.x, R = A.R;
+    const int m = A.slice_off[s + 1] - A.slice_off[s], n = A.cut_n[ls];
+    const int64_t ob = (int64_t)ls * A.ncap, sb = (int64_t)ls * A.scap;
+    const int32_t *rp = A.rowptr + (int64_t)ls * (A.mmax + 1);
+    const int32_t *cp = A.colptr + (int64_t)ls * (A.G + 1);
+    const int nnz = A.nnz[ls];
+    // sigma = max_Omega M~, then sum and sum of squares of M^ = M~ / sigma
+    float mx = 0.f;
+    for (int k = tid; k < nnz; k += LT) mx = fmaxf(mx, A.val[ob + k]);
+    const float sigma = block_reduce<true>(mx, red);
+    const float inv_sigma = sigma > 0.f ? 1.0f / sigma : 0.f;
+    float sum = 0.f, sq = 0.f;
+    for (int k = tid; k < nnz; k += LT) {
+        const float v = A.val[ob + k] * inv_sigma;
+        sum += v;
+        sq = fmaf(v, v, sq);
+    }
+    sum = block_reduce<false>(sum, red);
+    sq = block_reduce<false>(sq, red);
+    if (tid == 0) A.norm[ls] = make_float4(sigma, inv_sigma, sum, sq);
+    for (int pass = 0; pass < 2; ++pass) {
+        const int cnt = pass == 0 ? m : n;
+        const int32_t *ptr = pass == 0 ? rp : cp;
+        uint16_t *perm = (pass == 0 ? A.r_perm : A.c_perm) + (int64_t)ls * (pass == 0 ? A.mmax : A.G);
+        uint16_t *lens = (pass == 0 ? A.r_len : A.c_len) + (int64_t)ls * (pass == 0 ? A.mmax : A.G);
+        int32_t *goff = (pass == 0 ? A.r_goff : A.c_goff) + (int64_t)ls * ((pass == 0 ? A.mmax : A.G) + 1);
+        // sort by (length desc, index asc): unique keys -> deterministic permutation
+        int len = tid < cnt ? ptr[tid + 1] - ptr[tid] : 0;
+        uint32_t key[1] = {tid < cnt ? ((uint32_t)(2047 - len) << 10) | (uint32_t)tid : 0xFFFFFFFFu};
+        Sort(sort_tmp).Sort(key, 0, 32);
+        const int rank = tid;                       // blocked arrangement: thread = rank
+        const int who = (int)(key[0] & 1023u);
+        const int wlen = rank < cnt ? 2047 - (int)(key[0] >> 10) : 0;
+        if (rank < cnt) {
+            perm[rank] = (uint16_t)who;
+            lens[rank] = (uint16_t)wlen;
+        }
+        sh_len[rank] = wlen;
+        __syncthreads();
+        const int ng = (cnt + R - 1) / R;
+        int gsz = (tid < ng) ? R * sh_len[tid * R] : 0;
+        int pre, tot;
+        Scan(scan_tmp).ExclusiveSum(gsz, pre, tot);
+        if (tid < ng) { sh_goff[tid] = pre; goff[tid] = pre; }
+        if (tid == 0) { sh_goff[ng] = tot; goff[ng] = tot; }
+        __syncthreads();
+        if (rank < ng * R) {
+            const int g = rank / R, r = rank % R;
+            const int lg = sh_len[g * R];
+            const int base = sh_goff[g];
+            const int own = rank < cnt ? wlen : 0;
+            const int p0 = rank < cnt ? ptr[who] : 0;
+            for (int k = 0; k < lg; ++k) {
+                const int idx = base + k * R + r;
+                if (pass == 0) {
+                    unsigned long long e = 0ull;
+                    if (k < own) {
+                        const float mh = A.val[ob + p0 + k] * inv_sigma;
+                        e = ((unsigned long long)__float_as_uint(mh) << 32) | (unsigned long long)A.col[ob + p0 + k];
+                        A.map[ob + p0 + k] = idx;
+                    }
+                    A.r_ent[sb + idx] = e;
+                } else {
+                    uint32_t e = 0u;
+                    if (k < own) e = ((uint32_t)A.map[ob + A.csc_src[ob + p0 + k]] << 10) | (uint32_t)A.csc_row[ob + p0 + k];
+                    A.c_ent[sb + idx] = e;
+                }
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// ADM
+// ------------------------------------------------------------------------------------------
+struct CArgs {
+    const int32_t *slice_off;
+    int32_t s0, lbase, G, mmax, nmax;
+    int64_t scap;
+    int K;
+    float alpha, beta, gamma, tol;
+    uint64_t seed;
+    const int32_t *cut_n, *nnz;
+    const float4 *norm;
+    const uint16_t *r_perm, *r_len, *c_perm, *c_len;
+    const int32_t *r_goff, *c_goff;
+    const unsigned long long *r_ent;
+    const uint32_t *c_ent;
+    float *U, *V, *Lam, *Pi, *Xold, *S, *resid;
+    int32_t *flags, *iters;
+};
+
+template <int Q>
+struct Cfg {
+    static constexpr int L = Q / 4;           // lanes per row / column
+    static constexpr int R = 32 / L;          // rows per warp step
+    static constexpr int PART = 2048;         // floats of Gram partials
+};
+
+// partial Gram sums of out[a][b] = sum_i A[i][a] B[i][b] over threads [t0, t0 + nthr):
+// P = nthr / (Q/4)^2 row partitions, each producing a Q x Q partial in part[p]
+template <int Q>
+__device__ __forceinline__ int gram_partial(const float *A, const float *B, int rows, float *part, int t0, int nthr)
+{
+    constexpr int TQ = Q / 4, T = TQ * TQ;
+    int P = nthr / T;
     if (P * Q * Q > Cfg<Q>::PART) P = Cfg<Q>::PART / (Q * Q);
-    const int tid = threadIdx.x;
-    if (tid < P * T) {
+    const int tid = (int)threadIdx.x - t0;
+    if (tid >= 0 && tid < P * T) {
         const int p = tid / T, tile = tid % T, ta = tile / TQ, tb = tile % TQ;
         float acc[4][4];
 #pragma unroll
@@ -89,8 +205,8 @@ __device__ void gram(const float *A, int lda, const float *B, int ldb, int rows,
 #pragma unroll
             for (int y = 0; y < 4; ++y) acc[x][y] = 0.f;
         for (int i = p; i < rows; i += P) {
-            const float4 a = *reinterpret_cast<const float4 *>(A + (size_t)i * lda + 4 * ta);
-            const float4 b = *reinterpret_cast<const float4 *>(B + (size_t)i * ldb + 4 * tb);
+            const float4 a = *reinterpret_cast<const float4 *>(A + (size_t)i * Q + 4 * ta);
+            const float4 b = *reinterpret_cast<const float4 *>(B + (size_t)i * Q + 4 * tb);
             const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
             for (int x = 0; x < 4; ++x)
@@ -102,272 +218,320 @@ __device__ void gram(const float *A, int lda, const float *B, int ldb, int rows,
 #pragma unroll
             for (int y = 0; y < 4; ++y) part[(size_t)p * Q * Q + (4 * ta + x) * Q + 4 * tb + y] = acc[x][y];
     }
-    __syncthreads();
-    for (int e = tid; e < Q * Q; e += blockDim.x) {
+    return P;
+}
+
+template <int Q>
+__device__ __forceinline__ void gram_reduce(float *out, const float *part, int P)
+{
+    for (int e = threadIdx.x; e < Q * Q; e += blockDim.x) {
         float s = 0.f;
         for (int p = 0; p < P; ++p) s += part[(size_t)p * Q * Q + e];
         out[e] = s;
     }
-    __syncthreads();
 }
 
-// M <- (M + d I)^{-1} for SPD M (q x q), Gauss-Jordan without pivoting by warp 0; aug: 2 Q^2 floats
+// M <- (M + d I)^{-1} for SPD M (Q x Q) by Gauss-Jordan without pivoting in the registers of the
+// calling warp (lane r holds row r of [M + dI | I]); pivot rows are broadcast by shuffles.
 template <int Q>
-__device__ void inv_spd(float *M, float d, float *aug)
+__device__ void inv_spd_warp(float *M, float d)
 {
-    if (threadIdx.x < 32) {
-        const int lane = threadIdx.x;
-        constexpr int C2 = 2 * Q;
-        for (int idx = lane; idx < Q * C2; idx += 32) {
-            int r = idx / C2, c = idx % C2;
-            aug[idx] = c < Q ? M[r * Q + c] + (r == c ? d : 0.f) : (c - Q == r ? 1.f : 0.f);
-        }
-        __syncwarp();
-        for (int k = 0; k < Q; ++k) {
-            const float ip = 1.0f / aug[k * C2 + k];
-            __syncwarp();
-            for (int c = lane; c < C2; c += 32) aug[k * C2 + c] *= ip;
-            __syncwarp();
-            for (int r = lane; r < Q; r += 32) {
-                if (r == k) continue;
-                const float f = aug[r * C2 + k];
-#pragma unroll 8
-                for (int c = 0; c < C2; ++c) aug[r * C2 + c] = fmaf(-f, aug[k * C2 + c], aug[r * C2 + c]);
-            }
-            __syncwarp();
-        }
-        for (int idx = lane; idx < Q * Q; idx += 32) M[idx] = aug[(idx / Q) * C2 + Q + idx % Q];
-    }
-    __syncthreads();
-}
-
-template <int Q>
-__device__ __forceinline__ void load_vec(const float *p, float (&v)[Q])
-{
+    const int lane = threadIdx.x & 31;
+    const int r = lane < Q ? lane : 0;
+    float a[Q], b[Q];
 #pragma unroll
-    for (int l = 0; l < Q; l += 4) {
-        float4 t = *reinterpret_cast<const float4 *>(p + l);
-        v[l] = t.x; v[l + 1] = t.y; v[l + 2] = t.z; v[l + 3] = t.w;
+    for (int c = 0; c < Q; ++c) {
+        a[c] = M[r * Q + c] + (r == c ? d : 0.f);
+        b[c] = (r == c) ? 1.f : 0.f;
+    }
+#pragma unroll
+    for (int k = 0; k < Q; ++k) {
+        float pa[Q], pb[Q];
+#pragma unroll
+        for (int c = k; c < Q; ++c) pa[c] = __shfl_sync(FULLM, a[c], k);
+#pragma unroll
+        for (int c = 0; c <= k; ++c) pb[c] = __shfl_sync(FULLM, b[c], k);
+        const float ip = 1.0f / pa[k];
+        const float f = (lane == k) ? 0.f : a[k] * ip;
+#pragma unroll
+        for (int c = k; c < Q; ++c) a[c] = (lane == k) ? pa[c] * ip : fmaf(-f, pa[c], a[c]);
+#pragma unroll
+        for (int c = 0; c <= k; ++c) b[c] = (lane == k) ? pb[c] * ip : fmaf(-f, pb[c], b[c]);
+    }
+    __syncwarp();
+    if (lane < Q) {
+#pragma unroll
+        for (int c = 0; c < Q; ++c) M[lane * Q + c] = b[c];
     }
 }
+
+// out[4sub..] = sum_m t[m] * Mt[m][4sub..] with t spread over the L lanes of the lane group
 template <int Q>
-__device__ __forceinline__ void store_vec(float *p, const float (&v)[Q])
+__device__ __forceinline__ float4 group_matvec(float4 t4, const float *Mt, int grp_lane0, int sub, float4 acc)
 {
+    constexpr int L = Q / 4;
 #pragma unroll
-    for (int l = 0; l < Q; l += 4) *reinterpret_cast<float4 *>(p + l) = make_float4(v[l], v[l + 1], v[l + 2], v[l + 3]);
+    for (int sp = 0; sp < L; ++sp) {
+        float4 tt;
+        tt.x = __shfl_sync(FULLM, t4.x, grp_lane0 + sp);
+        tt.y = __shfl_sync(FULLM, t4.y, grp_lane0 + sp);
+        tt.z = __shfl_sync(FULLM, t4.z, grp_lane0 + sp);
+        tt.w = __shfl_sync(FULLM, t4.w, grp_lane0 + sp);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const float4 mrow = *reinterpret_cast<const float4 *>(Mt + (4 * sp + c) * Q + 4 * sub);
+            acc = f4fma(f4get(tt, c), mrow, acc);
+        }
+    }
+    return acc;
 }
 
-// ------------------------------------------------------------------------------------------
-// ADM (App. A): one CTA per slice
-// ------------------------------------------------------------------------------------------
 template <int Q>
-__global__ void __launch_bounds__(Cfg<Q>::NT, 1) k_adm(CArgs A)
+__device__ __forceinline__ float group_sum(float v)
 {
-    constexpr int QP = Cfg<Q>::QP;
+#pragma unroll
+    for (int o = 1; o < Q / 4; o <<= 1) v += __shfl_xor_sync(FULLM, v, o);
+    return v;
+}
+
+__device__ __forceinline__ int next_group(int *ctr, int lane)
+{
+    int g = 0;
+    if (lane == 0) g = atomicAdd(ctr, 1);
+    return __shfl_sync(FULLM, g, 0);
+}
+
+template <int Q>
+__device__ __forceinline__ float row_residual_ss(const float *X, const float *Y, const CArgs &A, int ls, int m,
+                                                 int warp, int nwarps, int lane)
+{
+    constexpr int L = Cfg<Q>::L, R = Cfg<Q>::R;
+    const int grp = lane / L, sub = lane % L;
+    const uint16_t *rperm = A.r_perm + (int64_t)ls * A.mmax, *rlen = A.r_len + (int64_t)ls * A.mmax;
+    const int32_t *rgoff = A.r_goff + (int64_t)ls * (A.mmax + 1);
+    const unsigned long long *rent = A.r_ent + (int64_t)ls * A.scap;
+    const int ngr = (m + R - 1) / R;
+    float ss = 0.f;
+    for (int g = warp; g < ngr; g += nwarps) {
+        const int rank = g * R + grp;
+        const bool valid = rank < m;
+        const int row = valid ? rperm[rank] : 0, len = valid ? rlen[rank] : 0;
+        const int lg = rlen[g * R];
+        const unsigned long long *e = rent + rgoff[g] + grp;
+        const float4 x4 = *reinterpret_cast<const float4 *>(X + row * Q + 4 * sub);
+        for (int k = 0; k < lg; ++k) {
+            const unsigned long long w = e[k * R];
+            const float4 y4 = *reinterpret_cast<const float4 *>(Y + (int)(w & 0xFFFFu) * Q + 4 * sub);
+            const float err = __uint_as_float((uint32_t)(w >> 32)) - group_sum<Q>(f4dot(x4, y4));
+            if (k < len && sub == 0) ss = fmaf(err, err, ss);
+        }
+    }
+    return ss;
+}
+
+template <int Q>
+__global__ void __launch_bounds__(512, 1) k_adm(CArgs A)
+{
+    constexpr int L = Cfg<Q>::L, R = Cfg<Q>::R, UNR = 4;
     extern __shared__ __align__(16) float sm[];
     __shared__ float red[33];
+    __shared__ int sh_ctr[2];
     const int ls = blockIdx.x, s = A.s0 + ls, tid = threadIdx.x, NT = blockDim.x;
+    const int lane = tid & 31, warp = tid >> 5, nwarps = NT >> 5;
+    const int grp = lane / L, sub = lane % L, lane0 = grp * L;
     const int m = A.slice_off[s + 1] - A.slice_off[s];
     const int n = A.cut_n[ls];
     const int64_t lrow0 = A.slice_off[s] - A.lbase;
-    const int64_t ob = (int64_t)ls * A.ncap, vb = (int64_t)ls * A.G * Q;
-    const int32_t *rp = A.rowptr + (int64_t)ls * (A.mmax + 1);
-    const int32_t *cp = A.colptr + (int64_t)ls * (A.G + 1);
-    const int nnz = A.nnz[ls];
-    float *X = sm;                                  // mmax x QP
-    float *Y = X + (size_t)A.mmax * QP;             // G x QP
-    float *Bm = Y + (size_t)A.G * QP;               // Q x Q : (Y Y^T + aI)^{-1}
+    const int64_t sb = (int64_t)ls * A.scap, vb = (int64_t)ls * A.G * Q;
+    const uint16_t *rperm = A.r_perm + (int64_t)ls * A.mmax, *rlen = A.r_len + (int64_t)ls * A.mmax;
+    const uint16_t *cperm = A.c_perm + (int64_t)ls * A.G, *clen = A.c_len + (int64_t)ls * A.G;
+    const int32_t *rgoff = A.r_goff + (int64_t)ls * (A.mmax + 1), *cgoff = A.c_goff + (int64_t)ls * (A.G + 1);
+    const unsigned long long *rent = A.r_ent + sb;
+    const uint32_t *cent = A.c_ent + sb;
+    float *S = A.S + sb;
+    float *X = sm;                                  // mmax x Q
+    float *Y = X + (size_t)A.mmax * Q;              // nmax x Q (column j contiguous)
+    float *Bm = Y + (size_t)A.nmax * Q;             // (Y Y^T + aI)^{-1}
     float *Dm = Bm + Q * Q;                         // (X^T X + bI)^{-1}
-    float *Cm = Dm + Q * Q;                         // X_{k+1}^T X_k
-    float *part = Cm + Q * Q;                       // PART
-    float *Ug = A.U + (lrow0 * Q), *Lg = A.Lam + lrow0 * Q, *Xo = A.Xold + lrow0 * Q;
+    float *Cm = Dm + Q * Q;                         // (X_{k+1}^T X_k)^T
+    float *part = Cm + Q * Q;
+    float *Ug = A.U + lrow0 * Q, *Lg = A.Lam + lrow0 * Q, *Xo = A.Xold + lrow0 * Q;
     float *Vg = A.V + vb, *Pg = A.Pi + vb;
     if (m <= Q || n <= Q) {   // R25: rank not below the slice dimensions -> direct rendering
         if (tid == 0) { A.flags[ls] = LMC_SLICE_DIRECT; A.iters[ls] = 0; A.resid[ls] = 0.f; }
         return;
     }
-    // sigma = max_Omega M~ (R23); mean for the initial scale (R20)
-    float mx = 0.f;
-    for (int k = tid; k < nnz; k += NT) mx = fmaxf(mx, A.val[ob + k]);
-    const float sigma = block_reduce<true>(mx, red);
-    if (sigma == 0.f) {   // zero slice
+    const float4 nm = A.norm[ls];            // sigma, 1/sigma, sum M^, sum M^^2
+    const float sigma = nm.x;
+    if (sigma == 0.f) {
         for (int k = tid; k < m * Q; k += NT) Ug[k] = 0.f;
         for (int k = tid; k < n * Q; k += NT) Vg[k] = 0.f;
         if (tid == 0) { A.flags[ls] = LMC_SLICE_ZERO; A.iters[ls] = 0; A.resid[ls] = 0.f; }
         return;
     }
-    const float inv_sigma = 1.0f / sigma;
-    float sum = 0.f, sq = 0.f;
-    for (int k = tid; k < nnz; k += NT) {
-        float v = A.val[ob + k] * inv_sigma;
-        sum += v;
-        sq = fmaf(v, v, sq);
-    }
-    sum = block_reduce<false>(sum, red);
-    const float nrmM2 = block_reduce<false>(sq, red);
-    const float mu = sum / (float)nnz;
-    const float c0 = 2.0f * sqrtf(mu / (float)Q);
-    // X_0, Y_0 (Philox uniform), U_0 = X_0, V_0 = Y_0, Lambda_0 = Pi_0 = 0
+    const float nrmM2 = nm.w;
+    // R20: X_0, Y_0 Philox-uniform with E[X_0 Y_0] = mean_Omega M^
+    const float c0 = 2.0f * sqrtf((nm.z / (float)A.nnz[ls]) / (float)Q);
     for (int e = tid; e < m * Q; e += NT) {
-        int i = e / Q, l = e % Q;
-        float x = c0 * unif_f(philox4((uint32_t)i, (uint32_t)l, (uint32_t)s, TAG_X0, A.seed).x);
-        X[i * QP + l] = x;
+        const int i = e / Q, l = e % Q;
+        const float x = c0 * unif_f(philox4((uint32_t)i, (uint32_t)l, (uint32_t)s, TAG_X0, A.seed).x);
+        X[e] = x;
         Ug[e] = x;
         Lg[e] = 0.f;
     }
     for (int e = tid; e < n * Q; e += NT) {
-        int j = e / Q, l = e % Q;
-        float y = c0 * unif_f(philox4((uint32_t)l, (uint32_t)j, (uint32_t)s, TAG_Y0, A.seed).x);
-        Y[j * QP + l] = y;
+        const int j = e / Q, l = e % Q;
+        const float y = c0 * unif_f(philox4((uint32_t)l, (uint32_t)j, (uint32_t)s, TAG_Y0, A.seed).x);
+        Y[e] = y;
         Vg[e] = y;
         Pg[e] = 0.f;
     }
+    if (tid == 0) { sh_ctr[0] = 0; sh_ctr[1] = 0; }
     __syncthreads();
-    gram<Q>(Y, QP, Y, QP, n, Bm, part);
-    inv_spd<Q>(Bm, A.alpha, part);
+    {
+        const int P = gram_partial<Q>(Y, Y, n, part, 0, NT);
+        __syncthreads();
+        gram_reduce<Q>(Bm, part, P);
+        __syncthreads();
+        if (warp == 0) inv_spd_warp<Q>(Bm, A.alpha);
+        __syncthreads();
+    }
     const float al = A.alpha, be = A.beta, ga = A.gamma;
+    const float inv_al = 1.0f / al, inv_be = 1.0f / be;
+    const int ngr = (m + R - 1) / R, ngc = (n + R - 1) / R;
     int it = 0;
     for (; it < A.K; ++it) {
         const bool first = (it == 0);
-        // ---- X_{k+1} = (Z_k Y_k^T + a U_k - L_k)(Y_k Y_k^T + a I)^{-1}; U, Lambda updates
-        for (int i = tid; i < m; i += NT) {
-            float x[Q], r[Q];
-            load_vec<Q>(X + i * QP, x);
+        // ---- row phase: s_ij = M^_ij - x_i.y_j on Omega_i, r_i = sum_j s_ij y_j, X/U/Lambda update
+        for (int g = next_group(&sh_ctr[0], lane); g < ngr; g = next_group(&sh_ctr[0], lane)) {
+            const int rank = g * R + grp;
+            const bool valid = rank < m;
+            const int row = valid ? rperm[rank] : 0;
+            const int len = valid ? rlen[rank] : 0;
+            const int lg = rlen[g * R];
+            const unsigned long long *e = rent + rgoff[g] + grp;
+            float *Sp = S + rgoff[g] + grp;
+            const float4 x4 = *reinterpret_cast<const float4 *>(X + row * Q + 4 * sub);
+            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int k0 = 0; k0 < lg; k0 += UNR) {
+                unsigned long long w[UNR];
 #pragma unroll
-            for (int l = 0; l < Q; ++l) r[l] = 0.f;
-            const int k1 = rp[i + 1];
-            for (int k = rp[i]; k < k1; ++k) {
-                const int j = A.col[ob + k];
-                const float mh = A.val[ob + k] * inv_sigma;
-                float y[Q];
-                load_vec<Q>(Y + j * QP, y);
-                float d = 0.f;
-                if (!first) {
+                for (int u = 0; u < UNR; ++u) w[u] = (k0 + u < lg) ? e[(k0 + u) * R] : 0ull;
+                float4 y4[UNR];
 #pragma unroll
-                    for (int l = 0; l < Q; ++l) d = fmaf(x[l], y[l], d);
+                for (int u = 0; u < UNR; ++u) y4[u] = *reinterpret_cast<const float4 *>(Y + (int)(w[u] & 0xFFFFu) * Q + 4 * sub);
+#pragma unroll
+                for (int u = 0; u < UNR; ++u) {
+                    const float d = group_sum<Q>(f4dot(x4, y4[u]));
+                    const float sv = __uint_as_float((uint32_t)(w[u] >> 32)) - (first ? 0.f : d);
+                    const bool on = (k0 + u) < len;
+                    acc = f4fma(on ? sv : 0.f, y4[u], acc);
+                    if (on && sub == 0) Sp[(k0 + u) * R] = sv;
                 }
-                const float sv = mh - d;
-                A.S[ob + k] = sv;
-#pragma unroll
-                for (int l = 0; l < Q; ++l) r[l] = fmaf(sv, y[l], r[l]);
             }
-            float u[Q], lam[Q];
-            load_vec<Q>(Ug + i * Q, u);
-            load_vec<Q>(Lg + i * Q, lam);
-            float t[Q], xn[Q];
-#pragma unroll
-            for (int l = 0; l < Q; ++l) t[l] = r[l] + al * u[l] - lam[l] - (first ? 0.f : al * x[l]);
-#pragma unroll
-            for (int l = 0; l < Q; ++l) {
-                float acc = first ? 0.f : x[l];
-#pragma unroll
-                for (int mm = 0; mm < Q; ++mm) acc = fmaf(t[mm], Bm[mm * Q + l], acc);
-                xn[l] = acc;
+            const float4 u4 = *reinterpret_cast<const float4 *>(Ug + row * Q + 4 * sub);
+            const float4 l4 = *reinterpret_cast<const float4 *>(Lg + row * Q + 4 * sub);
+            const float fx = first ? 0.f : al;
+            float4 t4;
+            t4.x = acc.x + al * u4.x - l4.x - fx * x4.x;
+            t4.y = acc.y + al * u4.y - l4.y - fx * x4.y;
+            t4.z = acc.z + al * u4.z - l4.z - fx * x4.z;
+            t4.w = acc.w + al * u4.w - l4.w - fx * x4.w;
+            const float4 xn = group_matvec<Q>(t4, Bm, lane0, sub, first ? make_float4(0.f, 0.f, 0.f, 0.f) : x4);
+            float4 un, ln;
+            un.x = fmaxf(0.f, xn.x + l4.x * inv_al); ln.x = l4.x + ga * al * (xn.x - un.x);
+            un.y = fmaxf(0.f, xn.y + l4.y * inv_al); ln.y = l4.y + ga * al * (xn.y - un.y);
+            un.z = fmaxf(0.f, xn.z + l4.z * inv_al); ln.z = l4.z + ga * al * (xn.z - un.z);
+            un.w = fmaxf(0.f, xn.w + l4.w * inv_al); ln.w = l4.w + ga * al * (xn.w - un.w);
+            if (valid) {
+                *reinterpret_cast<float4 *>(Xo + row * Q + 4 * sub) = x4;
+                *reinterpret_cast<float4 *>(X + row * Q + 4 * sub) = xn;
+                *reinterpret_cast<float4 *>(Ug + row * Q + 4 * sub) = un;
+                *reinterpret_cast<float4 *>(Lg + row * Q + 4 * sub) = ln;
             }
-#pragma unroll
-            for (int l = 0; l < Q; ++l) {
-                const float un = fmaxf(0.f, xn[l] + lam[l] / al);
-                lam[l] = lam[l] + ga * al * (xn[l] - un);
-                u[l] = un;
-            }
-            store_vec<Q>(Xo + i * Q, x);
-            store_vec<Q>(X + i * QP, xn);
-            store_vec<Q>(Ug + i * Q, u);
-            store_vec<Q>(Lg + i * Q, lam);
         }
         __syncthreads();
-        // ---- (X^T X + bI)^{-1} and X_{k+1}^T X_k
-        gram<Q>(X, QP, X, QP, m, Dm, part);
-        inv_spd<Q>(Dm, be, part);
-        if (!first) gram<Q>(X, QP, Xo, Q, m, Cm, part);
-        // ---- Y_{k+1} = (X^T X + bI)^{-1} (X^T Z_k + b V_k - Pi_k); V, Pi updates
-        for (int j = tid; j < n; j += NT) {
-            float y[Q], t[Q];
-            load_vec<Q>(Y + j * QP, y);
+        // ---- (X^T X + bI)^{-1}; warp 0 inverts while the other warps form X_{k+1}^T X_k
+        {
+            int P = gram_partial<Q>(X, X, m, part, 0, NT);
+            __syncthreads();
+            gram_reduce<Q>(Dm, part, P);
+            if (tid == 0) sh_ctr[0] = 0;
+            __syncthreads();
+            if (warp == 0) {
+                inv_spd_warp<Q>(Dm, be);
+            } else if (!first) {
+                P = gram_partial<Q>(Xo, X, m, part, 32, NT - 32);
+            }
+            __syncthreads();
+            if (!first) {
+                P = (NT - 32) / ((Q / 4) * (Q / 4));
+                if (P * Q * Q > Cfg<Q>::PART) P = Cfg<Q>::PART / (Q * Q);
+                gram_reduce<Q>(Cm, part, P);   // Cm[b][a] = (X_{k+1}^T X_k)[a][b]
+                __syncthreads();
+            }
+        }
+        // ---- column phase: Y_{k+1} = (X^T X + bI)^{-1}(X^T Z_k + b V_k - Pi_k), V/Pi update
+        for (int g = next_group(&sh_ctr[1], lane); g < ngc; g = next_group(&sh_ctr[1], lane)) {
+            const int rank = g * R + grp;
+            const bool valid = rank < n;
+            const int colj = valid ? cperm[rank] : 0;
+            const int len = valid ? clen[rank] : 0;
+            const int lg = clen[g * R];
+            const uint32_t *e = cent + cgoff[g] + grp;
+            const float4 y4 = *reinterpret_cast<const float4 *>(Y + colj * Q + 4 * sub);
+            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (!first) acc = group_matvec<Q>(y4, Cm, lane0, sub, acc);   // (X_{k+1}^T X_k) y_j
+            for (int k0 = 0; k0 < lg; k0 += UNR) {
+                uint32_t w[UNR];
 #pragma unroll
-            for (int a = 0; a < Q; ++a) {
-                float acc = 0.f;
-                if (!first) {
+                for (int u = 0; u < UNR; ++u) w[u] = (k0 + u < len) ? e[(k0 + u) * R] : 0u;
+                float sv[UNR];
 #pragma unroll
-                    for (int b = 0; b < Q; ++b) acc = fmaf(Cm[a * Q + b], y[b], acc);
+                for (int u = 0; u < UNR; ++u) sv[u] = (k0 + u < len) ? S[w[u] >> 10] : 0.f;
+#pragma unroll
+                for (int u = 0; u < UNR; ++u) {
+                    const float4 xv = *reinterpret_cast<const float4 *>(X + (int)(w[u] & 1023u) * Q + 4 * sub);
+                    acc = f4fma(sv[u], xv, acc);
                 }
-                t[a] = acc;
             }
-            const int k1 = cp[j + 1];
-            for (int k = cp[j]; k < k1; ++k) {
-                const int i = A.csc_row[ob + k];
-                const float sv = A.S[ob + A.csc_src[ob + k]];
-                float xv[Q];
-                load_vec<Q>(X + i * QP, xv);
-#pragma unroll
-                for (int l = 0; l < Q; ++l) t[l] = fmaf(sv, xv[l], t[l]);
+            const float4 v4 = *reinterpret_cast<const float4 *>(Vg + colj * Q + 4 * sub);
+            const float4 p4 = *reinterpret_cast<const float4 *>(Pg + colj * Q + 4 * sub);
+            float4 t4;
+            t4.x = acc.x + be * v4.x - p4.x;
+            t4.y = acc.y + be * v4.y - p4.y;
+            t4.z = acc.z + be * v4.z - p4.z;
+            t4.w = acc.w + be * v4.w - p4.w;
+            const float4 yn = group_matvec<Q>(t4, Dm, lane0, sub, make_float4(0.f, 0.f, 0.f, 0.f));
+            float4 vn, pn;
+            vn.x = fmaxf(0.f, yn.x + p4.x * inv_be); pn.x = p4.x + ga * be * (yn.x - vn.x);
+            vn.y = fmaxf(0.f, yn.y + p4.y * inv_be); pn.y = p4.y + ga * be * (yn.y - vn.y);
+            vn.z = fmaxf(0.f, yn.z + p4.z * inv_be); pn.z = p4.z + ga * be * (yn.z - vn.z);
+            vn.w = fmaxf(0.f, yn.w + p4.w * inv_be); pn.w = p4.w + ga * be * (yn.w - vn.w);
+            if (valid) {
+                *reinterpret_cast<float4 *>(Y + colj * Q + 4 * sub) = yn;
+                *reinterpret_cast<float4 *>(Vg + colj * Q + 4 * sub) = vn;
+                *reinterpret_cast<float4 *>(Pg + colj * Q + 4 * sub) = pn;
             }
-            float v[Q], pi[Q], yn[Q];
-            load_vec<Q>(Vg + j * Q, v);
-            load_vec<Q>(Pg + j * Q, pi);
-#pragma unroll
-            for (int l = 0; l < Q; ++l) t[l] = t[l] + be * v[l] - pi[l];
-#pragma unroll
-            for (int a = 0; a < Q; ++a) {
-                float acc = 0.f;
-#pragma unroll
-                for (int b = 0; b < Q; ++b) acc = fmaf(Dm[a * Q + b], t[b], acc);
-                yn[a] = acc;
-            }
-#pragma unroll
-            for (int l = 0; l < Q; ++l) {
-                const float vn = fmaxf(0.f, yn[l] + pi[l] / be);
-                pi[l] = pi[l] + ga * be * (yn[l] - vn);
-                v[l] = vn;
-            }
-            store_vec<Q>(Y + j * QP, yn);
-            store_vec<Q>(Vg + j * Q, v);
-            store_vec<Q>(Pg + j * Q, pi);
         }
         __syncthreads();
-        // ---- (Y Y^T + aI)^{-1} for the next X step
-        gram<Q>(Y, QP, Y, QP, n, Bm, part);
-        inv_spd<Q>(Bm, al, part);
-        // ---- optional tolerance stop on r_{k+1} = ||P_Omega(M^ - X_{k+1} Y_{k+1})|| / ||P_Omega M^||
-        if (A.tol > 0.f) {
-            float ss = 0.f;
-            for (int i = tid; i < m; i += NT) {
-                float x[Q];
-                load_vec<Q>(X + i * QP, x);
-                for (int k = rp[i]; k < rp[i + 1]; ++k) {
-                    float y[Q];
-                    load_vec<Q>(Y + A.col[ob + k] * QP, y);
-                    float d = 0.f;
-#pragma unroll
-                    for (int l = 0; l < Q; ++l) d = fmaf(x[l], y[l], d);
-                    const float e = A.val[ob + k] * inv_sigma - d;
-                    ss = fmaf(e, e, ss);
-                }
-            }
-            ss = block_reduce<false>(ss, red);
-            if (!(ss == ss) || isinf(ss)) { ++it; break; }
-            if (sqrtf(ss / nrmM2) < A.tol) { ++it; break; }
+        {
+            const int P = gram_partial<Q>(Y, Y, n, part, 0, NT);
+            __syncthreads();
+            gram_reduce<Q>(Bm, part, P);
+            if (tid == 0) sh_ctr[1] = 0;
+            __syncthreads();
+            if (warp == 0) inv_spd_warp<Q>(Bm, al);
+            __syncthreads();
+        }
+        if (A.tol > 0.f) {   // r_{k+1} = ||P_Omega(M^ - X_{k+1} Y_{k+1})|| / ||P_Omega M^|| (R21)
+            const float ss = block_reduce<false>(row_residual_ss<Q>(X, Y, A, ls, m, warp, nwarps, lane), red);
+            if (!(ss == ss) || isinf(ss) || sqrtf(ss / nrmM2) < A.tol) { ++it; break; }
         }
     }
-    // final residual on Omega and non-finite check
-    float ss = 0.f;
-    for (int i = tid; i < m; i += NT) {
-        float x[Q];
-        load_vec<Q>(X + i * QP, x);
-        for (int k = rp[i]; k < rp[i + 1]; ++k) {
-            float y[Q];
-            load_vec<Q>(Y + A.col[ob + k] * QP, y);
-            float d = 0.f;
-#pragma unroll
-            for (int l = 0; l < Q; ++l) d = fmaf(x[l], y[l], d);
-            const float e = A.val[ob + k] * inv_sigma - d;
-            ss = fmaf(e, e, ss);
-        }
-    }
-    ss = block_reduce<false>(ss, red);
+    const float ss = block_reduce<false>(row_residual_ss<Q>(X, Y, A, ls, m, warp, nwarps, lane), red);
     const float res = sqrtf(ss / nrmM2);
-    // output (U_K, sigma V_K) (R22)
-    for (int e = tid; e < n * Q; e += NT) Vg[e] *= sigma;
+    for (int e = tid; e < n * Q; e += NT) Vg[e] *= sigma;   // R22: output (U_K, sigma V_K)
     if (tid == 0) {
         const bool bad = !(res == res) || isinf(res);
         A.flags[ls] = bad ? (LMC_SLICE_DIVERGED | LMC_SLICE_DIRECT) : 0;
@@ -376,188 +540,18 @@ __global__ void __launch_bounds__(Cfg<Q>::NT, 1) k_adm(CArgs A)
     }
 }
 
-// ------------------------------------------------------------------------------------------
-// Masked ALS: x_i = (sum_{j in Omega_i} y_j y_j^T + lam I)^{-1} sum_j M^_ij y_j, then y_j alike.
-// One thread per row (column); the packed upper triangle of the q x q Gram stays in registers.
-// ------------------------------------------------------------------------------------------
-template <int Q>
-__device__ __forceinline__ void ridge_solve(float (&Ap)[Q * (Q + 1) / 2], float (&b)[Q], float lam, float (&x)[Q])
+size_t adm_smem_bytes(int q, int mmax, int nmax)
 {
-    // packed lower-triangular Cholesky in place: index (r, c<=r) -> r(r+1)/2 + c
-#pragma unroll
-    for (int r = 0; r < Q; ++r) Ap[r * (r + 1) / 2 + r] += lam;
-#pragma unroll
-    for (int j = 0; j < Q; ++j) {
-        float d = Ap[j * (j + 1) / 2 + j];
-#pragma unroll
-        for (int k = 0; k < j; ++k) d = fmaf(-Ap[j * (j + 1) / 2 + k], Ap[j * (j + 1) / 2 + k], d);
-        d = sqrtf(fmaxf(d, 1e-30f));
-        const float id = 1.0f / d;
-        Ap[j * (j + 1) / 2 + j] = d;
-#pragma unroll
-        for (int i = j + 1; i < Q; ++i) {
-            float s = Ap[i * (i + 1) / 2 + j];
-#pragma unroll
-            for (int k = 0; k < j; ++k) s = fmaf(-Ap[i * (i + 1) / 2 + k], Ap[j * (j + 1) / 2 + k], s);
-            Ap[i * (i + 1) / 2 + j] = s * id;
-        }
-    }
-#pragma unroll
-    for (int i = 0; i < Q; ++i) {
-        float s = b[i];
-#pragma unroll
-        for (int k = 0; k < i; ++k) s = fmaf(-Ap[i * (i + 1) / 2 + k], x[k], s);
-        x[i] = s / Ap[i * (i + 1) / 2 + i];
-    }
-#pragma unroll
-    for (int i = Q - 1; i >= 0; --i) {
-        float s = x[i];
-#pragma unroll
-        for (int k = i + 1; k < Q; ++k) s = fmaf(-Ap[k * (k + 1) / 2 + i], x[k], s);
-        x[i] = s / Ap[i * (i + 1) / 2 + i];
-    }
+    return ((size_t)mmax + (size_t)nmax) * q * sizeof(float) + (3 * (size_t)q * q + 2048) * sizeof(float);
 }
 
-template <int Q>
-__global__ void __launch_bounds__(256, 1) k_mals(CArgs A)
-{
-    constexpr int QP = Cfg<Q>::QP;
-    constexpr int NP = Q * (Q + 1) / 2;
-    extern __shared__ __align__(16) float sm[];
-    __shared__ float red[33];
-    const int ls = blockIdx.x, s = A.s0 + ls, tid = threadIdx.x, NT = blockDim.x;
-    const int m = A.slice_off[s + 1] - A.slice_off[s];
-    const int n = A.cut_n[ls];
-    const int64_t lrow0 = A.slice_off[s] - A.lbase;
-    const int64_t ob = (int64_t)ls * A.ncap, vb = (int64_t)ls * A.G * Q;
-    const int32_t *rp = A.rowptr + (int64_t)ls * (A.mmax + 1);
-    const int32_t *cp = A.colptr + (int64_t)ls * (A.G + 1);
-    const int nnz = A.nnz[ls];
-    float *X = sm;
-    float *Y = X + (size_t)A.mmax * QP;
-    float *Ug = A.U + lrow0 * Q, *Vg = A.V + vb;
-    if (m <= Q || n <= Q) {
-        if (tid == 0) { A.flags[ls] = LMC_SLICE_DIRECT; A.iters[ls] = 0; A.resid[ls] = 0.f; }
-        return;
-    }
-    float mx = 0.f;
-    for (int k = tid; k < nnz; k += NT) mx = fmaxf(mx, A.val[ob + k]);
-    const float sigma = block_reduce<true>(mx, red);
-    if (sigma == 0.f) {
-        for (int k = tid; k < m * Q; k += NT) Ug[k] = 0.f;
-        for (int k = tid; k < n * Q; k += NT) Vg[k] = 0.f;
-        if (tid == 0) { A.flags[ls] = LMC_SLICE_ZERO; A.iters[ls] = 0; A.resid[ls] = 0.f; }
-        return;
-    }
-    const float inv_sigma = 1.0f / sigma;
-    float sum = 0.f, sq = 0.f;
-    for (int k = tid; k < nnz; k += NT) {
-        float v = A.val[ob + k] * inv_sigma;
-        sum += v;
-        sq = fmaf(v, v, sq);
-    }
-    sum = block_reduce<false>(sum, red);
-    const float nrmM2 = block_reduce<false>(sq, red);
-    const float c0 = 2.0f * sqrtf((sum / (float)nnz) / (float)Q);
-    for (int e = tid; e < m * Q; e += NT)
-        X[(e / Q) * QP + e % Q] = c0 * unif_f(philox4((uint32_t)(e / Q), (uint32_t)(e % Q), (uint32_t)s, TAG_X0, A.seed).x);
-    for (int e = tid; e < n * Q; e += NT)
-        Y[(e / Q) * QP + e % Q] = c0 * unif_f(philox4((uint32_t)(e % Q), (uint32_t)(e / Q), (uint32_t)s, TAG_Y0, A.seed).x);
-    __syncthreads();
-    for (int it = 0; it < A.K; ++it) {
-        for (int i = tid; i < m; i += NT) {
-            float Ap[NP], b[Q], x[Q];
-#pragma unroll
-            for (int e = 0; e < NP; ++e) Ap[e] = 0.f;
-#pragma unroll
-            for (int l = 0; l < Q; ++l) b[l] = 0.f;
-            for (int k = rp[i]; k < rp[i + 1]; ++k) {
-                float y[Q];
-                load_vec<Q>(Y + A.col[ob + k] * QP, y);
-                const float mh = A.val[ob + k] * inv_sigma;
-#pragma unroll
-                for (int r = 0; r < Q; ++r) {
-#pragma unroll
-                    for (int c = 0; c <= r; ++c) Ap[r * (r + 1) / 2 + c] = fmaf(y[r], y[c], Ap[r * (r + 1) / 2 + c]);
-                    b[r] = fmaf(mh, y[r], b[r]);
-                }
-            }
-            ridge_solve<Q>(Ap, b, A.lambda, x);
-            store_vec<Q>(X + i * QP, x);
-        }
-        __syncthreads();
-        for (int j = tid; j < n; j += NT) {
-            float Ap[NP], b[Q], y[Q];
-#pragma unroll
-            for (int e = 0; e < NP; ++e) Ap[e] = 0.f;
-#pragma unroll
-            for (int l = 0; l < Q; ++l) b[l] = 0.f;
-            for (int k = cp[j]; k < cp[j + 1]; ++k) {
-                float xv[Q];
-                load_vec<Q>(X + A.csc_row[ob + k] * QP, xv);
-                const float mh = A.val[ob + A.csc_src[ob + k]] * inv_sigma;
-#pragma unroll
-                for (int r = 0; r < Q; ++r) {
-#pragma unroll
-                    for (int c = 0; c <= r; ++c) Ap[r * (r + 1) / 2 + c] = fmaf(xv[r], xv[c], Ap[r * (r + 1) / 2 + c]);
-                    b[r] = fmaf(mh, xv[r], b[r]);
-                }
-            }
-            ridge_solve<Q>(Ap, b, A.lambda, y);
-            store_vec<Q>(Y + j * QP, y);
-        }
-        __syncthreads();
-    }
-    float ss = 0.f;
-    for (int i = tid; i < m; i += NT) {
-        float x[Q];
-        load_vec<Q>(X + i * QP, x);
-        for (int k = rp[i]; k < rp[i + 1]; ++k) {
-            float y[Q];
-            load_vec<Q>(Y + A.col[ob + k] * QP, y);
-            float d = 0.f;
-#pragma unroll
-            for (int l = 0; l < Q; ++l) d = fmaf(x[l], y[l], d);
-            const float e = A.val[ob + k] * inv_sigma - d;
-            ss = fmaf(e, e, ss);
-        }
-    }
-    ss = block_reduce<false>(ss, red);
-    const float res = sqrtf(ss / nrmM2);
-    for (int e = tid; e < m * Q; e += NT) Ug[e] = X[(e / Q) * QP + e % Q];
-    for (int e = tid; e < n * Q; e += NT) Vg[e] = sigma * Y[(e / Q) * QP + e % Q];
-    if (tid == 0) {
-        const bool bad = !(res == res) || isinf(res);
-        A.flags[ls] = bad ? (LMC_SLICE_DIVERGED | LMC_SLICE_DIRECT) : 0;
-        A.iters[ls] = A.K;
-        A.resid[ls] = res;
-    }
-}
+static int layout_R(int q) { return 128 / q; }
 
-size_t complete_smem_bytes(int q, int mmax, int G, int solver)
+cudaError_t run_layout(lmc_ctx *c)
 {
-    int qp = q >= 32 ? q : q + 4;
-    size_t base = ((size_t)mmax + (size_t)G) * qp * sizeof(float);
-    if (solver == LMC_SOLVER_MALS) return base;
-    return base + (3 * (size_t)q * q + 4096) * sizeof(float);
-}
-
-static CArgs cargs(lmc_ctx *c)
-{
-    CArgs A;
+    if (c->SL == 0) return cudaSuccess;
+    LArgs A;
     A.slice_off = c->d.slice_off;
-    A.s0 = c->s0;
-    A.lbase = c->h_slice_off[c->s0];
-    A.G = c->G;
-    A.mmax = c->mmax;
-    A.ncap = c->ncap;
-    A.K = c->cfg.max_iter;
-    A.alpha = (float)c->cfg.alpha;
-    A.beta = (float)c->cfg.beta;
-    A.gamma = (float)c->cfg.gamma;
-    A.tol = (float)c->cfg.tol;
-    A.lambda = (float)c->cfg.lambda;
-    A.seed = c->cfg.seed;
     A.cut_n = c->d.cut_n;
     A.rowptr = c->d.rowptr;
     A.colptr = c->d.colptr;
@@ -566,6 +560,70 @@ static CArgs cargs(lmc_ctx *c)
     A.col = c->d.col;
     A.csc_row = c->d.csc_row;
     A.val = c->d.val;
+    A.s0 = c->s0;
+    A.G = c->G;
+    A.mmax = c->mmax;
+    A.R = layout_R(c->q);
+    A.ncap = c->ncap;
+    A.scap = c->scap;
+    A.r_perm = c->d.r_perm;
+    A.r_len = c->d.r_len;
+    A.c_perm = c->d.c_perm;
+    A.c_len = c->d.c_len;
+    A.r_goff = c->d.r_goff;
+    A.c_goff = c->d.c_goff;
+    A.map = c->d.newpos;
+    A.r_ent = c->d.r_ent;
+    A.c_ent = c->d.c_ent;
+    A.norm = c->d.norm;
+    const size_t sm = sizeof(typename cub::BlockRadixSort<uint32_t, LT, 1>::TempStorage);
+    cudaError_t e = cudaFuncSetAttribute(k_layout, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    k_layout<<<c->SL, LT, sm, c->stream>>>(A);
+    return cudaGetLastError();
+}
+
+template <int Q>
+static cudaError_t launch_adm(lmc_ctx *c, const CArgs &A)
+{
+    const size_t sm = adm_smem_bytes(Q, c->mmax, A.nmax);
+    cudaError_t e = cudaFuncSetAttribute(k_adm<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    // two CTAs per SM when their shared memory fits (overlaps one slice's serial Gram/inverse
+    // phases with another slice's sample phases), else one CTA of 16 warps
+    const int nt = (2 * (sm + 2048) <= 227 * 1024) ? 256 : 512;
+    k_adm<Q><<<c->SL, nt, sm, c->stream>>>(A);
+    return cudaGetLastError();
+}
+
+cudaError_t run_adm(lmc_ctx *c, int nmax)
+{
+    if (c->SL == 0) return cudaSuccess;
+    CArgs A;
+    A.slice_off = c->d.slice_off;
+    A.s0 = c->s0;
+    A.lbase = c->h_slice_off[c->s0];
+    A.G = c->G;
+    A.mmax = c->mmax;
+    A.nmax = nmax;
+    A.scap = c->scap;
+    A.K = c->cfg.max_iter;
+    A.alpha = (float)c->cfg.alpha;
+    A.beta = (float)c->cfg.beta;
+    A.gamma = (float)c->cfg.gamma;
+    A.tol = (float)c->cfg.tol;
+    A.seed = c->cfg.seed;
+    A.cut_n = c->d.cut_n;
+    A.nnz = c->d.nnz;
+    A.norm = c->d.norm;
+    A.r_perm = c->d.r_perm;
+    A.r_len = c->d.r_len;
+    A.c_perm = c->d.c_perm;
+    A.c_len = c->d.c_len;
+    A.r_goff = c->d.r_goff;
+    A.c_goff = c->d.c_goff;
+    A.r_ent = c->d.r_ent;
+    A.c_ent = c->d.c_ent;
     A.U = c->d.U;
     A.V = c->d.V;
     A.Lam = c->d.Lam;
@@ -575,35 +633,11 @@ static CArgs cargs(lmc_ctx *c)
     A.resid = c->d.resid;
     A.flags = c->d.flags;
     A.iters = c->d.iters;
-    return A;
-}
-
-template <int Q>
-static cudaError_t launch_q(lmc_ctx *c, const CArgs &A)
-{
-    size_t sm = complete_smem_bytes(Q, c->mmax, c->G, c->cfg.solver);
-    cudaError_t e;
-    if (c->cfg.solver == LMC_SOLVER_MALS) {
-        e = cudaFuncSetAttribute(k_mals<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        if (e != cudaSuccess) return e;
-        k_mals<Q><<<c->SL, 256, sm, c->stream>>>(A);
-    } else {
-        e = cudaFuncSetAttribute(k_adm<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        if (e != cudaSuccess) return e;
-        k_adm<Q><<<c->SL, Cfg<Q>::NT, sm, c->stream>>>(A);
-    }
-    return cudaGetLastError();
-}
-
-cudaError_t run_complete(lmc_ctx *c)
-{
-    if (c->SL == 0) return cudaSuccess;
-    CArgs A = cargs(c);
     switch (c->q) {
-    case 4: return launch_q<4>(c, A);
-    case 8: return launch_q<8>(c, A);
-    case 16: return launch_q<16>(c, A);
-    case 32: return launch_q<32>(c, A);
+    case 4: return launch_adm<4>(c, A);
+    case 8: return launch_adm<8>(c, A);
+    case 16: return launch_adm<16>(c, A);
+    case 32: return launch_adm<32>(c, A);
     default: return cudaErrorInvalidValue;
     }
 }
@@ -631,7 +665,6 @@ __global__ void __launch_bounds__(256) k_resolve(RArgs A)
     const float *V = A.V + (int64_t)ls * A.G * q;
     const int64_t cb = (int64_t)ls * A.G;
     if (!(fl & (LMC_SLICE_DIRECT | LMC_SLICE_ZERO))) {
-        // each warp: partial t over a strided subset of columns
         for (int e = lane; e < 3 * q; e += 32) {
             const int k = e / q, a = e % q;
             float acc = 0.f;

@@ -206,19 +206,28 @@ __global__ void __launch_bounds__(256) k_slice_extent(const int32_t *__restrict_
     }
 }
 
-// sort key of every element: encoded key of the split dimension, 0 for tiles that do not split
-__global__ void k_slice_keys(const int32_t *__restrict__ rows, int64_t M, const int32_t *__restrict__ tbeg,
-                             const int32_t *__restrict__ tslot, int ntiles, const unsigned long long *__restrict__ ext,
-                             unsigned long long *keys, GView g, double diag, double wn)
+__device__ __forceinline__ int tile_of(const int32_t *__restrict__ tbeg, int ntiles, int64_t k)
 {
-    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= M) return;
     int lo = 0, hi = ntiles - 1;   // last tile with begin <= k
     while (lo < hi) {
         int mid = (lo + hi + 1) >> 1;
         if (tbeg[mid] <= k) lo = mid; else hi = mid - 1;
     }
-    int slot = tslot[lo];
+    return lo;
+}
+
+// sort key of every element (encoded key of its tile's split dimension, 0 for tiles that do not
+// split) and the tile of every row
+__global__ void k_slice_keys(const int32_t *__restrict__ rows, int64_t M, const int32_t *__restrict__ tbeg,
+                             const int32_t *__restrict__ tslot, int ntiles, const unsigned long long *__restrict__ ext,
+                             unsigned long long *keys, int32_t *row_tile, GView g, double diag, double wn)
+{
+    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= M) return;
+    const int t = tile_of(tbeg, ntiles, k);
+    const int r = rows[k];
+    row_tile[r] = t;
+    const int slot = tslot[t];
     if (slot < 0) { keys[k] = 0ull; return; }
     int best = 0;
     double bext = -1.0;
@@ -227,7 +236,50 @@ __global__ void k_slice_keys(const int32_t *__restrict__ rows, int64_t M, const 
         double e = dec_key(ext[slot * 12 + d]) - dec_key(ext[slot * 12 + 6 + d]);
         if (e > bext) { bext = e; best = d; }
     }
-    keys[k] = enc_key(slice_key(g, rows[k], best, diag, wn));
+    keys[k] = enc_key(slice_key(g, r, best, diag, wn));
+}
+
+__global__ void k_tile_keys(const int32_t *__restrict__ rows_sorted, const int32_t *__restrict__ row_tile, int64_t M,
+                            uint32_t *tkey)
+{
+    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < M) tkey[k] = (uint32_t)row_tile[rows_sorted[k]];
+}
+
+// rows now in (tile, key, row) order: the lower ceil(n/2) of a splitting tile go left (R26)
+__global__ void k_split_flags(const int32_t *__restrict__ rows_sorted, int64_t M, const int32_t *__restrict__ tbeg,
+                              const int32_t *__restrict__ tend, const int32_t *__restrict__ tslot, int ntiles,
+                              int32_t *left_by_row)
+{
+    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= M) return;
+    const int t = tile_of(tbeg, ntiles, k);
+    const int len = tend[t] - tbeg[t];
+    const int nl = tslot[t] < 0 ? len : (len + 1) / 2;
+    left_by_row[rows_sorted[k]] = (k - tbeg[t]) < nl ? 1 : 0;
+}
+
+__global__ void k_gather_flags(const int32_t *__restrict__ rows, const int32_t *__restrict__ left_by_row, int64_t M,
+                               int32_t *f)
+{
+    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < M) f[k] = left_by_row[rows[k]];
+}
+
+// stable partition of every tile (in its ascending-row input order) into left / right child
+__global__ void k_split_scatter(const int32_t *__restrict__ rows, const int32_t *__restrict__ f,
+                                const int32_t *__restrict__ pre, int64_t M, const int32_t *__restrict__ tbeg,
+                                const int32_t *__restrict__ tend, const int32_t *__restrict__ tslot, int ntiles,
+                                int32_t *rows_out)
+{
+    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= M) return;
+    const int t = tile_of(tbeg, ntiles, k);
+    const int b = tbeg[t], len = tend[t] - b;
+    const int nl = tslot[t] < 0 ? len : (len + 1) / 2;
+    const int before_left = pre[k] - pre[b];
+    const int pos = f[k] ? b + before_left : b + nl + ((int)(k - b) - before_left);
+    rows_out[pos] = rows[k];
 }
 
 __global__ void k_pack_rows(const int32_t *__restrict__ rows, int64_t row0, int64_t ML, GView g,
@@ -263,14 +315,17 @@ cudaError_t upload_scene(const SceneConst &sc) { return cudaMemcpyToSymbol(c_sce
 
 cudaError_t slicing_tmp_bytes(int64_t M, int32_t max_tiles, size_t *bytes)
 {
-    size_t a = 0, b = 0;
-    cudaError_t e = cub::DeviceSegmentedSort::StableSortPairs<unsigned long long, int32_t>(
+    (void)max_tiles;
+    size_t a = 0, b = 0, d = 0;
+    cudaError_t e = cub::DeviceRadixSort::SortPairs<unsigned long long, int32_t>(
         nullptr, a, (const unsigned long long *)nullptr, (unsigned long long *)nullptr, (const int32_t *)nullptr,
-        (int32_t *)nullptr, (int)M, max_tiles, (const int32_t *)nullptr, (const int32_t *)nullptr, 0);
+        (int32_t *)nullptr, (int)M, 0, 64, 0);
     if (e != cudaSuccess) return e;
-    e = cub::DeviceSegmentedSort::SortKeys<int32_t>(nullptr, b, (const int32_t *)nullptr, (int32_t *)nullptr, (int)M,
-                                                     max_tiles, (const int32_t *)nullptr, (const int32_t *)nullptr, 0);
-    *bytes = a > b ? a : b;
+    e = cub::DeviceRadixSort::SortPairs<uint32_t, int32_t>(nullptr, b, (const uint32_t *)nullptr, (uint32_t *)nullptr,
+                                                            (const int32_t *)nullptr, (int32_t *)nullptr, (int)M, 0, 32, 0);
+    if (e != cudaSuccess) return e;
+    e = cub::DeviceScan::ExclusiveSum(nullptr, d, (const int32_t *)nullptr, (int32_t *)nullptr, (int)M, 0);
+    *bytes = std::max(a, std::max(b, d));
     return e;
 }
 
@@ -288,6 +343,8 @@ __global__ void k_iota(int32_t *a, int64_t n)
     if (k < n) a[k] = (int32_t)k;
 }
 
+// per level: extents -> split keys -> radix sort by key (stable, rows ascending within ties) ->
+// stable radix sort by tile -> lower-median flags -> stable partition of the ascending-row tiles.
 cudaError_t run_slicing(lmc_ctx *c)
 {
     cudaStream_t st = c->stream;
@@ -295,24 +352,35 @@ cudaError_t run_slicing(lmc_ctx *c)
     GView g = gview(c);
     const double diag = c->diag, wn = c->cfg.normal_weight;
     if (M == 0) return cudaSuccess;
-    k_iota<<<(unsigned)((M + 255) / 256), 256, 0, st>>>(c->d.rows, M);
+    const unsigned nb = (unsigned)((M + 255) / 256);
+    int32_t *rows = c->d.rows, *alt = c->d.rows_alt;
+    int32_t *row_tile = c->d.sl_i32, *f = c->d.sl_i32 + M, *pre = c->d.sl_i32 + 2 * M, *tmp_rows = c->d.sl_i32 + 3 * M;
+    uint32_t *tkey = reinterpret_cast<uint32_t *>(c->d.keys), *tkey_alt = reinterpret_cast<uint32_t *>(c->d.keys) + M;
+    k_iota<<<nb, 256, 0, st>>>(rows, M);
     for (const auto &L : c->levels) {
         const int32_t *tbeg = c->d.lvl_begin + L.tile_off;
         const int32_t *tend = c->d.lvl_end + L.tile_off;
         const int32_t *tslot = c->d.lvl_slot + L.tile_off;
-        int nslots = L.nslots;
-        k_ext_init<<<(nslots * 12 + 255) / 256, 256, 0, st>>>(c->d.ext, nslots);
-        k_slice_extent<<<L.work_n, 256, 0, st>>>(c->d.rows, c->d.lvl_work + 3 * L.work_off, c->d.ext, g, diag, wn);
-        k_slice_keys<<<(unsigned)((M + 255) / 256), 256, 0, st>>>(c->d.rows, M, tbeg, tslot, L.tile_n, c->d.ext,
-                                                                   c->d.keys, g, diag, wn);
+        k_ext_init<<<(L.nslots * 12 + 255) / 256, 256, 0, st>>>(c->d.ext, L.nslots);
+        k_slice_extent<<<L.work_n, 256, 0, st>>>(rows, c->d.lvl_work + 3 * L.work_off, c->d.ext, g, diag, wn);
+        k_slice_keys<<<nb, 256, 0, st>>>(rows, M, tbeg, tslot, L.tile_n, c->d.ext, c->d.keys_alt, row_tile, g, diag, wn);
         size_t bytes = c->d.cub_tmp_bytes;
-        cudaError_t e = cub::DeviceSegmentedSort::StableSortPairs(c->d.cub_tmp, bytes, c->d.keys, c->d.keys_alt,
-                                                                  c->d.rows, c->d.rows_alt, (int)M, L.tile_n, tbeg,
-                                                                  tend, st);
+        unsigned long long *kin = c->d.keys_alt, *kout = c->d.keys_sorted;
+        cudaError_t e = cub::DeviceRadixSort::SortPairs(c->d.cub_tmp, bytes, kin, kout, rows, alt, (int)M, 0, 64, st);
         if (e != cudaSuccess) return e;
+        k_tile_keys<<<nb, 256, 0, st>>>(alt, row_tile, M, tkey);
+        int tbits = 1;
+        while ((1 << tbits) < L.tile_n) ++tbits;
         bytes = c->d.cub_tmp_bytes;
-        e = cub::DeviceSegmentedSort::SortKeys(c->d.cub_tmp, bytes, c->d.rows_alt, c->d.rows, (int)M, L.next_tile_n,
-                                               c->d.lvl_begin + L.next_tile_off, c->d.lvl_end + L.next_tile_off, st);
+        e = cub::DeviceRadixSort::SortPairs(c->d.cub_tmp, bytes, tkey, tkey_alt, alt, tmp_rows, (int)M, 0, tbits, st);
+        if (e != cudaSuccess) return e;
+        k_split_flags<<<nb, 256, 0, st>>>(tmp_rows, M, tbeg, tend, tslot, L.tile_n, alt /* left_by_row */);
+        k_gather_flags<<<nb, 256, 0, st>>>(rows, alt, M, f);
+        bytes = c->d.cub_tmp_bytes;
+        e = cub::DeviceScan::ExclusiveSum(c->d.cub_tmp, bytes, f, pre, (int)M, st);
+        if (e != cudaSuccess) return e;
+        k_split_scatter<<<nb, 256, 0, st>>>(rows, f, pre, M, tbeg, tend, tslot, L.tile_n, tmp_rows);
+        e = cudaMemcpyAsync(rows, tmp_rows, M * sizeof(int32_t), cudaMemcpyDeviceToDevice, st);
         if (e != cudaSuccess) return e;
     }
     return cudaGetLastError();
@@ -586,7 +654,10 @@ __global__ void __launch_bounds__(CO_THREADS) k_coarsen(
         __syncthreads();
     }
     int col = sh_scan[threadIdx.x] - mine;
-    if (threadIdx.x == CO_THREADS - 1) cut_n[ls] = sh_scan[threadIdx.x];
+    if (threadIdx.x == CO_THREADS - 1) {
+        cut_n[ls] = sh_scan[threadIdx.x];
+        atomicMax(&counters[5], (unsigned long long)sh_scan[threadIdx.x]);
+    }
     const int64_t cb = (int64_t)ls * G;
     for (int u = u0; u < u0 + per && u < U; ++u) {
         if (!(sh_flag[u] & F_INCUT)) continue;
@@ -652,6 +723,7 @@ struct P2Args {
     int32_t *rowptr;
     uint16_t *col;
     float *val;
+    double *val64;                 // fp64 copy of the values (masked ALS only), else null
     uint8_t *carried;
     int32_t *colptr;
     uint16_t *csc_row;
@@ -914,6 +986,7 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2(P2Args A)
             double v = (lum_rho_d(A.prow, lrow0 + i) * lI) * Tv[pb + so + k];
             int pos = csr_pos(bm, P, rp, W, i, c);
             A.val[ob + pos] = (float)v;
+            if (A.val64) A.val64[ob + pos] = v;
             A.carried[ob + pos] = 1;
         }
     }
@@ -938,7 +1011,7 @@ __global__ void __launch_bounds__(256) k_eval_new(Upper up, const int32_t *__res
                                                   const float4 *__restrict__ vpl, const int32_t *__restrict__ cut_n,
                                                   const int32_t *__restrict__ cut_cols, const uint32_t *__restrict__ newcells,
                                                   const int32_t *__restrict__ newpos, const int32_t *__restrict__ n_new,
-                                                  float *val, int64_t ncap, unsigned long long *counters)
+                                                  float *val, double *val64, int64_t ncap, unsigned long long *counters)
 {
     const int ls = blockIdx.y, s = s0 + ls;
     const int n = cut_n[ls], nn = n_new[ls];
@@ -949,7 +1022,9 @@ __global__ void __launch_bounds__(256) k_eval_new(Upper up, const int32_t *__res
         int i = (int)(cell / (uint32_t)n), c = (int)(cell % (uint32_t)n);
         int u = cut_cols[cb + c];
         double T = entry_T(prow, lrow0 + i, vpl, up.rep[u]);
-        val[ob + newpos[ob + k]] = (float)((lum_rho_d(prow, lrow0 + i) * up.lum[u]) * T);
+        const double v = (lum_rho_d(prow, lrow0 + i) * up.lum[u]) * T;
+        val[ob + newpos[ob + k]] = (float)v;
+        if (val64) val64[ob + newpos[ob + k]] = v;
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&counters[2], (unsigned long long)nn);
 }
@@ -990,6 +1065,7 @@ cudaError_t run_pass2(lmc_ctx *c)
     A.rowptr = c->d.rowptr;
     A.col = c->d.col;
     A.val = c->d.val;
+    A.val64 = c->d.val64;
     A.carried = c->d.carried;
     A.colptr = c->d.colptr;
     A.csc_row = c->d.csc_row;
@@ -1009,7 +1085,7 @@ cudaError_t run_pass2(lmc_ctx *c)
     dim3 grid(16, c->SL);
     k_eval_new<<<grid, 256, 0, c->stream>>>(c->up, c->d.slice_off, c->s0, A.lbase, c->G, c->d.prow, c->d.vpl,
                                              c->d.cut_n, c->d.cut_cols, c->d.newcells, c->d.newpos, c->d.n_new,
-                                             c->d.val, c->ncap, c->d.counters);
+                                             c->d.val, c->d.val64, c->ncap, c->d.counters);
     return cudaGetLastError();
 }
 

@@ -82,12 +82,13 @@ void free_all(lmc_ctx *c)
     Dev &d = c->d;
     void *ptrs[] = {d.pixel, d.g[0], d.g[1], d.g[2], d.g[3], d.g[4], d.g[5], d.g[6], d.g[7], d.g[8], d.g[9], d.g[10],
                     d.g[11], d.g[12], d.expo, d.vpl, d.ut_i32, d.ut_lum, d.ut_I, d.rows, d.rows_alt, d.keys,
-                    d.keys_alt, d.lvl_begin, d.lvl_end, d.lvl_slot, d.lvl_work, d.ext, d.slice_off, d.cub_tmp, d.prow,
+                    d.keys_alt, d.keys_sorted, d.sl_i32, d.lvl_begin, d.lvl_end, d.lvl_slot, d.lvl_work, d.ext, d.slice_off, d.cub_tmp, d.prow,
                     d.p1_rows, d.p1_Ta, d.p1_Tb, d.p1_cnt, d.pool_rows, d.pool_Ta, d.pool_Tb, d.pool_used, d.cs_flags,
                     d.cs_eps, d.cs_cost, d.cs_zoff, d.cs_zlen, d.cut_n, d.cut_cols, d.src_off, d.src_len, d.src_side,
-                    d.rowptr, d.col, d.val, d.carried, d.colptr, d.csc_row, d.csc_src, d.nnz, d.target_n, d.n_new,
+                    d.rowptr, d.col, d.val, d.val64, d.carried, d.colptr, d.csc_row, d.csc_src, d.nnz, d.target_n, d.n_new,
                     d.newcells, d.newpos, d.U, d.V, d.Lam, d.Pi, d.Xold, d.S, d.flags, d.iters, d.resid,
-                    d.direct_rgb, d.counters, d.img, d.rows_rgb, d.vpl_soa};
+                    d.direct_rgb, d.counters, d.img, d.rows_rgb, d.vpl_soa, d.r_perm, d.r_len, d.c_perm, d.c_len,
+                    d.r_goff, d.c_goff, d.r_ent, d.c_ent, d.norm};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (c->h_stage) cudaFreeHost(c->h_stage);
@@ -418,6 +419,7 @@ static lmc_status create_impl(lmc_ctx *c, const lmc_gbuffer *g, const lmc_vpls *
     if (!(cfg.rank_q == 4 || cfg.rank_q == 8 || cfg.rank_q == 16 || cfg.rank_q == 32))
         return fail(c, LMC_EINVAL, "rank_q must be one of 4, 8, 16, 32");
     if (cfg.solver == LMC_SOLVER_MALS && cfg.rank_q > 16) return fail(c, LMC_EINVAL, "MALS supports rank_q <= 16");
+    if (cfg.solver == LMC_SOLVER_MALS && !(cfg.lambda > 0.0)) return fail(c, LMC_EINVAL, "MALS needs lambda > 0");
     if (cfg.solver != LMC_SOLVER_ADM && cfg.solver != LMC_SOLVER_MALS) return fail(c, LMC_EINVAL, "unknown solver");
     if (cfg.p1_nmax < 1 || cfg.p1_nmax > MAX_NMAX || cfg.p1_nmin < 1) return fail(c, LMC_EINVAL, "p1_nmax must be in [1, 32], p1_nmin >= 1");
     if (cfg.max_iter < 0) return fail(c, LMC_EINVAL, "max_iter must be >= 0");
@@ -482,6 +484,7 @@ static lmc_status create_impl(lmc_ctx *c, const lmc_gbuffer *g, const lmc_vpls *
     {
         int64_t nt = (int64_t)std::ceil((double)(c->mmax * G) * cfg.rate);
         c->ncap = std::min<int64_t>((int64_t)c->mmax * G, std::max<int64_t>(nt, 2 * c->pool_cap) + G);
+        c->scap = c->ncap + 32 * (int64_t)std::max<int64_t>(c->mmax, G);   // sliced-ELL padding bound
     }
     // device arena
     Dev &d = c->d;
@@ -494,6 +497,8 @@ static lmc_status create_impl(lmc_ctx *c, const lmc_gbuffer *g, const lmc_vpls *
     CK(dalloc(&d.rows_alt, M), "alloc slicing");
     CK(dalloc(&d.keys, M), "alloc slicing");
     CK(dalloc(&d.keys_alt, M), "alloc slicing");
+    CK(dalloc(&d.keys_sorted, M), "alloc slicing");
+    CK(dalloc(&d.sl_i32, 4 * M), "alloc slicing");
     CK(slicing_tmp_bytes(std::max<int64_t>(M, 1), c->max_tiles, &d.cub_tmp_bytes), "cub sizing");
     CK(cudaMalloc(&d.cub_tmp, std::max<size_t>(d.cub_tmp_bytes, 16)), "alloc cub");
     CK(dalloc(&d.prow, 4 * (size_t)ML), "alloc rows");
@@ -519,6 +524,7 @@ static lmc_status create_impl(lmc_ctx *c, const lmc_gbuffer *g, const lmc_vpls *
     CK(dalloc(&d.rowptr, SL * (c->mmax + 1)), "alloc pass2");
     CK(dalloc(&d.col, SL * c->ncap), "alloc pass2");
     CK(dalloc(&d.val, SL * c->ncap), "alloc pass2");
+    if (cfg.solver == LMC_SOLVER_MALS) CK(dalloc(&d.val64, SL * c->ncap), "alloc pass2");
     CK(dalloc(&d.carried, SL * c->ncap), "alloc pass2");
     CK(dalloc(&d.colptr, SL * (G + 1)), "alloc pass2");
     CK(dalloc(&d.csc_row, SL * c->ncap), "alloc pass2");
@@ -533,7 +539,16 @@ static lmc_status create_impl(lmc_ctx *c, const lmc_gbuffer *g, const lmc_vpls *
     CK(dalloc(&d.Xold, ML * c->q), "alloc factors");
     CK(dalloc(&d.V, SL * G * c->q), "alloc factors");
     CK(dalloc(&d.Pi, SL * G * c->q), "alloc factors");
-    CK(dalloc(&d.S, SL * c->ncap), "alloc factors");
+    CK(dalloc(&d.S, SL * c->scap), "alloc factors");
+    CK(dalloc(&d.r_perm, SL * c->mmax), "alloc layout");
+    CK(dalloc(&d.r_len, SL * c->mmax), "alloc layout");
+    CK(dalloc(&d.c_perm, SL * G), "alloc layout");
+    CK(dalloc(&d.c_len, SL * G), "alloc layout");
+    CK(dalloc(&d.r_goff, SL * (c->mmax + 1)), "alloc layout");
+    CK(dalloc(&d.c_goff, SL * (G + 1)), "alloc layout");
+    CK(dalloc(&d.r_ent, SL * c->scap), "alloc layout");
+    CK(dalloc(&d.c_ent, SL * c->scap), "alloc layout");
+    CK(dalloc(&d.norm, SL), "alloc layout");
     CK(dalloc(&d.flags, SL), "alloc factors");
     CK(dalloc(&d.iters, SL), "alloc factors");
     CK(dalloc(&d.resid, SL), "alloc factors");
@@ -545,7 +560,8 @@ static lmc_status create_impl(lmc_ctx *c, const lmc_gbuffer *g, const lmc_vpls *
     CK(cudaMemsetAsync(d.counters, 0, 8 * sizeof(unsigned long long), c->stream), "memset");
     CK(cudaMemsetAsync(d.flags, 0, SL * sizeof(int32_t), c->stream), "memset");
     CK(cudaMemsetAsync(d.img, 0, 3 * sizeof(float) * (size_t)std::max<int64_t>((int64_t)c->W * c->H, 1), c->stream), "memset");
-    size_t need = complete_smem_bytes(c->q, c->mmax, (int)G, cfg.solver);
+    size_t need = cfg.solver == LMC_SOLVER_MALS ? mals_smem_bytes(c->q, c->mmax, (int)G) : adm_smem_bytes(c->q, c->mmax, (int)G);
+    if (c->scap >= (1ll << 22)) return fail(c, LMC_EINVAL, "per-slice sample capacity %lld exceeds 2^22", (long long)c->scap);
     int maxsm = 0, dev = 0;
     CK(cudaGetDevice(&dev), "device");
     CK(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev), "device attr");
@@ -617,6 +633,7 @@ lmc_status lmc_build_slices(lmc_ctx *c)
     CK(cudaMemsetAsync(c->d.counters, 0, 8 * sizeof(unsigned long long), c->stream), "memset counters");
     CK(run_slicing(c), "slicing");
     CK(run_pack_rows(c), "pack rows");
+    c->launches += (c->M > 0 ? 2 : 0) + 11 * (int64_t)c->levels.size();   // CUB sorts / scan: 1 each
     ev_rec(c, 1);
     c->state = 1;
     return LMC_OK;
@@ -627,6 +644,7 @@ lmc_status lmc_sample_pass1(lmc_ctx *c)
     lmc_status s = check_stage(c, 1);
     if (s != LMC_OK) return s;
     CK(run_pass1(c), "pass 1");
+    c->launches += (c->SL > 0 && c->up.nB > 0) ? 1 : 0;
     ev_rec(c, 2);
     c->state = 2;
     return LMC_OK;
@@ -637,6 +655,7 @@ lmc_status lmc_coarsen_cut(lmc_ctx *c)
     lmc_status s = check_stage(c, 2);
     if (s != LMC_OK) return s;
     CK(run_coarsen(c), "coarsening");
+    c->launches += c->SL > 0 ? 1 : 0;
     ev_rec(c, 3);
     c->state = 3;
     return LMC_OK;
@@ -647,6 +666,7 @@ lmc_status lmc_sample_pass2(lmc_ctx *c)
     lmc_status s = check_stage(c, 3);
     if (s != LMC_OK) return s;
     CK(run_pass2(c), "pass 2");
+    c->launches += c->SL > 0 ? 2 : 0;
     ev_rec(c, 4);
     c->state = 4;
     return LMC_OK;
@@ -656,8 +676,20 @@ lmc_status lmc_complete(lmc_ctx *c)
 {
     lmc_status s = check_stage(c, 4);
     if (s != LMC_OK) return s;
-    CK(run_complete(c), "completion");
+    if (c->cfg.solver == LMC_SOLVER_MALS) {
+        CK(run_mals(c), "completion (MALS)");
+    } else {
+        CK(run_layout(c), "Omega layout");
+        // shared memory of the ADM kernel is sized by this frame's largest coarsened cut
+        unsigned long long nmx = 0;
+        CK(cudaMemcpyAsync(&nmx, c->d.counters + 5, sizeof nmx, cudaMemcpyDeviceToHost, c->stream), "read max n");
+        CK(cudaStreamSynchronize(c->stream), "sync");
+        const int nmax = std::max(1, (int)std::min<unsigned long long>(nmx, (unsigned long long)c->G));
+        CK(run_adm(c, nmax), "completion (ADM)");
+        c->launches += c->SL > 0 ? 1 : 0;
+    }
     CK(run_direct(c), "direct slices");
+    c->launches += c->SL > 0 ? 2 : 0;
     ev_rec(c, 5);
     c->state = 5;
     return LMC_OK;
@@ -668,6 +700,7 @@ lmc_status lmc_resolve_image(lmc_ctx *c, float *image, int32_t image_memory)
     lmc_status s = check_stage(c, 5);
     if (s != LMC_OK) return s;
     if (!image) return fail(c, LMC_EINVAL, "null image");
+    c->launches += c->SL > 0 ? 1 : 0;
     if (image_memory == LMC_MEM_DEVICE) {
         CK(run_resolve(c, image, nullptr), "resolve");
         ev_rec(c, 6);
@@ -688,6 +721,7 @@ lmc_status lmc_resolve_rows(lmc_ctx *c, float *rows_rgb)
     if (s != LMC_OK) return s;
     if (!rows_rgb) return fail(c, LMC_EINVAL, "null rows_rgb");
     CK(run_resolve(c, nullptr, rows_rgb), "resolve");
+    c->launches += c->SL > 0 ? 1 : 0;
     ev_rec(c, 6);
     return LMC_OK;
 }
@@ -698,6 +732,7 @@ lmc_status lmc_scatter_rows(lmc_ctx *c, const float *all_rows, float *image)
     if (s != LMC_OK) return s;
     if (!all_rows || !image) return fail(c, LMC_EINVAL, "null buffer");
     CK(run_scatter(c, all_rows, image), "scatter");
+    c->launches += c->M > 0 ? 1 : 0;
     return LMC_OK;
 }
 
@@ -864,6 +899,7 @@ lmc_status lmc_get_stats(lmc_ctx *c, lmc_stats *st)
     st->slice_end = c->s1;
     st->rows = c->ML;
     st->pool_cap = c->pool_cap;
+    st->launches = c->launches;
     unsigned long long cnt[5];
     CK(d2h(cnt, c->d.counters, 5), "stats");
     st->evals_pass1 = (int64_t)cnt[0];

@@ -58,7 +58,8 @@ struct Dev {
     float *ut_I;
     // slicing
     int32_t *rows, *rows_alt;          // M
-    unsigned long long *keys, *keys_alt; // M
+    unsigned long long *keys, *keys_alt, *keys_sorted; // M each (keys also holds 2M uint32 tile keys)
+    int32_t *sl_i32;                   // 4M: row_tile, flags, prefix, rows scratch
     int32_t *lvl_begin, *lvl_end;      // concatenated level tilings
     int32_t *lvl_slot;                 // per tile: extent slot of a splitting tile, -1 otherwise
     int32_t *lvl_work;                 // concatenated extent work items (seg, start, len) triples
@@ -85,6 +86,7 @@ struct Dev {
     int32_t *rowptr;                   // [SL][mmax+1]
     uint16_t *col;                     // [SL][ncap]
     float *val;                        // [SL][ncap]
+    double *val64;                     // [SL][ncap] (MALS only)
     uint8_t *carried;                  // [SL][ncap]
     int32_t *colptr;                   // [SL][G+1]
     uint16_t *csc_row;                 // [SL][ncap]
@@ -93,14 +95,21 @@ struct Dev {
     uint32_t *newcells;                // [SL][ncap] (cell = i*n + c)
     int32_t *newpos;                   // [SL][ncap] CSR position of new cell
     // completion
-    float *U, *V, *Lam, *Pi, *Xold, *S; // U/Lam/Xold [ML][q], V/Pi [SL][G][q], S [SL][ncap]
+    // sliced-ELL layout of Omega for the completion (k_layout)
+    uint16_t *r_perm, *r_len;          // [SL][mmax] rows by (length desc, id)
+    uint16_t *c_perm, *c_len;          // [SL][G]
+    int32_t *r_goff, *c_goff;          // [SL][mmax+1], [SL][G+1]
+    unsigned long long *r_ent;         // [SL][scap] (M^ bits << 32) | column
+    uint32_t *c_ent;                   // [SL][scap] (row-layout index << 10) | row
+    float4 *norm;                      // [SL] sigma, 1/sigma, sum M^, sum M^^2
+    float *U, *V, *Lam, *Pi, *Xold, *S; // U/Lam/Xold [ML][q], V/Pi [SL][G][q], S [SL][scap]
     int32_t *flags, *iters;            // [SL]
     float *resid;                      // [SL]
     float *direct_rgb;                 // [ML][3]
     float *rows_rgb;                   // [ML][3]
     float *img;                        // [H*W][3] staging image for host output
     float *vpl_soa;                    // 6 * NV staging for the VPL packing kernel
-    // counters: 0 evals_pass1, 1 evals_coarsen, 2 evals_pass2, 3 overflow flags, 4 pool_used_max
+    // counters: 0 evals_pass1, 1 evals_coarsen, 2 evals_pass2, 3 overflow flags, 4 pool_used_max, 5 max n_s
     unsigned long long *counters;
 };
 
@@ -124,7 +133,7 @@ struct lmc_ctx {
     int64_t row0 = 0, ML = 0;
     int32_t mmax = 0;
     int32_t q = 0, nmax = 0;
-    int64_t pool_cap = 0, ncap = 0;
+    int64_t pool_cap = 0, ncap = 0, scap = 0;
     // slicing level structure
     struct Level { int32_t tile_off, tile_n, work_off, work_n, next_tile_off, next_tile_n, nslots; };
     std::vector<Level> levels;
@@ -140,6 +149,7 @@ struct lmc_ctx {
     float ms[6] = {0, 0, 0, 0, 0, 0};
     bool ev_ok = false;
     float *h_stage = nullptr;
+    int64_t launches = 0;          // kernels (and CUB dispatches, 1 each) issued by stage calls
 };
 
 namespace lmc {
@@ -156,8 +166,12 @@ cudaError_t run_eval_entries(lmc_ctx *c, int64_t n, const int32_t *d_rows, const
 cudaError_t slicing_tmp_bytes(int64_t M, int32_t max_tiles, size_t *bytes);
 cudaError_t run_pack_vpls(lmc_ctx *c);
 // complete.cu (fp32 completion + resolve)
-cudaError_t run_complete(lmc_ctx *c);
+cudaError_t run_layout(lmc_ctx *c);
+cudaError_t run_adm(lmc_ctx *c, int nmax);
 cudaError_t run_resolve(lmc_ctx *c, float *image, float *rows_rgb);
 cudaError_t run_scatter(lmc_ctx *c, const float *all_rows, float *image);
-size_t complete_smem_bytes(int q, int mmax, int G, int solver);
+size_t adm_smem_bytes(int q, int mmax, int nmax);
+// mals.cu (fp64 masked ALS)
+cudaError_t run_mals(lmc_ctx *c);
+size_t mals_smem_bytes(int q, int mmax, int G);
 }  // namespace lmc

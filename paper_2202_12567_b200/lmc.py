@@ -54,7 +54,7 @@ class Config(C.Structure):
 class Stats(C.Structure):
     _fields_ = [(k, C.c_int64) for k in ("n_slices", "slice_begin", "slice_end", "rows", "sum_cols", "sum_samples",
                                          "sum_completed", "evals_pass1", "evals_coarsen", "evals_pass2", "n_direct",
-                                         "n_zero", "n_diverged", "pool_used_max", "pool_cap")] + \
+                                         "n_zero", "n_diverged", "pool_used_max", "pool_cap", "launches")] + \
               [(k, C.c_float) for k in ("ms_slices", "ms_pass1", "ms_coarsen", "ms_pass2", "ms_complete",
                                         "ms_resolve")]
 

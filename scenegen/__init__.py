@@ -49,7 +49,7 @@ class Config:
     alpha: float = 1.0
     beta: float = 1.0
     gamma: float = 1.6    # PAPER.md:277 gamma in (0, 1.618)
-    lam: float = 1e-3     # MALS ridge
+    lam: float = 1e-2     # MALS ridge on max-normalised data (R34)
     normal_weight: float = 0.3
     seed: int = 12567
     p1_nmax: int = 32
