@@ -140,8 +140,7 @@ def run_reference(args, rank, world):
     x = scenegen.make_inputs(scenegen.preset(args.config, solver=1 if args.solver == "mals" else 0))
     cores = omp_threads()
     nsamp = args.cpu_sample_slices or max(cores, 8)
-    for _ in range(args.warmup if args.warmup < 1 else 1):
-        cpu_oracle_sample(x, max(1, nsamp // 4), x.cfg.solver)
+    cpu_oracle_sample(x, max(1, nsamp // 4), x.cfg.solver)   # warm-up (page-in, OpenMP pool)
     vals, times = [], []
     for _ in range(args.steps):
         v, dt, k, ent = cpu_oracle_sample(x, nsamp, x.cfg.solver)
@@ -269,7 +268,7 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cores = omp_threads()
-        nsamp = args.cpu_sample_slices or max(cores, 8)
+        nsamp = args.cpu_sample_slices or max(4 * cores, 16)   # ~10-30 s of oracle work
         v, dt, k, ent = cpu_oracle_sample(x, nsamp, solver)
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
                "sample": f"{k} of {int(nsl)} slices of {args.config} (full per-slice pipeline, literal dense-Z "

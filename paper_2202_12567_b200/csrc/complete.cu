@@ -60,8 +60,10 @@ __device__ __forceinline__ float f4get(float4 v, int c) { return c == 0 ? v.x : 
 
 // ------------------------------------------------------------------------------------------
 // Omega layout: sliced ELL over rows and over columns (groups of R, sorted by length).
-// Row entries: (float bits of M^ = M~/sigma) << 32 | column;  column entries: (index of the
-// entry in the row layout) << 10 | row.  Also the per-slice normalisation (R23).
+// Row entries: (float bits of M^ = M~/sigma) << 32 | (index of the entry in the column layout)
+// << 10 | column;  column entries: row.  The residual S of the row phase is stored at the
+// column-layout index, so the column phase streams it coalesced.  Also the per-slice
+// normalisation sigma = max_Omega M~ (R23).
 // ------------------------------------------------------------------------------------------
 struct LArgs {
     const int32_t *slice_off, *cut_n, *rowptr, *colptr, *csc_src, *nnz;
@@ -72,7 +74,7 @@ struct LArgs {
     uint16_t *r_perm, *r_len, *c_perm, *c_len;
     int32_t *r_goff, *c_goff, *map;
     unsigned long long *r_ent;
-    uint32_t *c_ent;
+    uint16_t *c_ent;
     float4 *norm;
 };
 
@@ -108,12 +110,15 @@ __global__ void __launch_bounds__(LT, 1) k_layout(LArgs A)
     sum = block_reduce<false>(sum, red);
     sq = block_reduce<false>(sq, red);
     if (tid == 0) A.norm[ls] = make_float4(sigma, inv_sigma, sum, sq);
+    // pass 0: columns (entries: row id; their layout index goes to map[CSR position]),
+    // pass 1: rows (entries: M^ bits << 32 | column-layout index << 10 | column)
     for (int pass = 0; pass < 2; ++pass) {
-        const int cnt = pass == 0 ? m : n;
-        const int32_t *ptr = pass == 0 ? rp : cp;
-        uint16_t *perm = (pass == 0 ? A.r_perm : A.c_perm) + (int64_t)ls * (pass == 0 ? A.mmax : A.G);
-        uint16_t *lens = (pass == 0 ? A.r_len : A.c_len) + (int64_t)ls * (pass == 0 ? A.mmax : A.G);
-        int32_t *goff = (pass == 0 ? A.r_goff : A.c_goff) + (int64_t)ls * ((pass == 0 ? A.mmax : A.G) + 1);
+        const bool rows_pass = pass == 1;
+        const int cnt = rows_pass ? m : n;
+        const int32_t *ptr = rows_pass ? rp : cp;
+        uint16_t *perm = (rows_pass ? A.r_perm : A.c_perm) + (int64_t)ls * (rows_pass ? A.mmax : A.G);
+        uint16_t *lens = (rows_pass ? A.r_len : A.c_len) + (int64_t)ls * (rows_pass ? A.mmax : A.G);
+        int32_t *goff = (rows_pass ? A.r_goff : A.c_goff) + (int64_t)ls * ((rows_pass ? A.mmax : A.G) + 1);
         // sort by (length desc, index asc): unique keys -> deterministic permutation
         int len = tid < cnt ? ptr[tid + 1] - ptr[tid] : 0;
         uint32_t key[1] = {tid < cnt ? ((uint32_t)(2047 - len) << 10) | (uint32_t)tid : 0xFFFFFFFFu};
@@ -128,7 +133,7 @@ __global__ void __launch_bounds__(LT, 1) k_layout(LArgs A)
         sh_len[rank] = wlen;
         __syncthreads();
         const int ng = (cnt + R - 1) / R;
-        int gsz = (tid < ng) ? R * sh_len[tid * R] : 0;
+        int gsz = (tid < ng) ? ((R * sh_len[tid * R] + 7) & ~7) : 0;   // 16-byte aligned groups
         int pre, tot;
         Scan(scan_tmp).ExclusiveSum(gsz, pre, tot);
         if (tid < ng) { sh_goff[tid] = pre; goff[tid] = pre; }
@@ -142,17 +147,20 @@ __global__ void __launch_bounds__(LT, 1) k_layout(LArgs A)
             const int p0 = rank < cnt ? ptr[who] : 0;
             for (int k = 0; k < lg; ++k) {
                 const int idx = base + k * R + r;
-                if (pass == 0) {
+                if (rows_pass) {
                     unsigned long long e = 0ull;
                     if (k < own) {
                         const float mh = A.val[ob + p0 + k] * inv_sigma;
-                        e = ((unsigned long long)__float_as_uint(mh) << 32) | (unsigned long long)A.col[ob + p0 + k];
-                        A.map[ob + p0 + k] = idx;
+                        e = ((unsigned long long)__float_as_uint(mh) << 32) |
+                            ((unsigned long long)(uint32_t)A.map[ob + p0 + k] << 10) | (unsigned long long)A.col[ob + p0 + k];
                     }
                     A.r_ent[sb + idx] = e;
                 } else {
-                    uint32_t e = 0u;
-                    if (k < own) e = ((uint32_t)A.map[ob + A.csc_src[ob + p0 + k]] << 10) | (uint32_t)A.csc_row[ob + p0 + k];
+                    uint16_t e = 0;
+                    if (k < own) {
+                        e = A.csc_row[ob + p0 + k];
+                        A.map[ob + A.csc_src[ob + p0 + k]] = idx;
+                    }
                     A.c_ent[sb + idx] = e;
                 }
             }
@@ -176,7 +184,7 @@ struct CArgs {
     const uint16_t *r_perm, *r_len, *c_perm, *c_len;
     const int32_t *r_goff, *c_goff;
     const unsigned long long *r_ent;
-    const uint32_t *c_ent;
+    const uint16_t *c_ent;
     float *U, *V, *Lam, *Pi, *Xold, *S, *resid;
     int32_t *flags, *iters;
 };
@@ -185,7 +193,7 @@ template <int Q>
 struct Cfg {
     static constexpr int L = Q / 4;           // lanes per row / column
     static constexpr int R = 32 / L;          // rows per warp step
-    static constexpr int PART = 2048;         // floats of Gram partials
+    static constexpr int PART = 16384;        // floats of Gram partials (the 64 KB ring area)
 };
 
 // partial Gram sums of out[a][b] = sum_i A[i][a] B[i][b] over threads [t0, t0 + nthr):
@@ -246,17 +254,20 @@ __device__ void inv_spd_warp(float *M, float d)
     }
 #pragma unroll
     for (int k = 0; k < Q; ++k) {
-        float pa[Q], pb[Q];
+        const float ip = 1.0f / __shfl_sync(FULLM, a[k], k);
+        const bool piv = lane == k;
+        const float f = piv ? 0.f : a[k] * ip;
+        // every pivot-row element is broadcast before the element is updated in this step
 #pragma unroll
-        for (int c = k; c < Q; ++c) pa[c] = __shfl_sync(FULLM, a[c], k);
+        for (int c = k; c < Q; ++c) {
+            const float p = __shfl_sync(FULLM, a[c], k);
+            a[c] = piv ? p * ip : fmaf(-f, p, a[c]);
+        }
 #pragma unroll
-        for (int c = 0; c <= k; ++c) pb[c] = __shfl_sync(FULLM, b[c], k);
-        const float ip = 1.0f / pa[k];
-        const float f = (lane == k) ? 0.f : a[k] * ip;
-#pragma unroll
-        for (int c = k; c < Q; ++c) a[c] = (lane == k) ? pa[c] * ip : fmaf(-f, pa[c], a[c]);
-#pragma unroll
-        for (int c = 0; c <= k; ++c) b[c] = (lane == k) ? pb[c] * ip : fmaf(-f, pb[c], b[c]);
+        for (int c = 0; c <= k; ++c) {
+            const float p = __shfl_sync(FULLM, b[c], k);
+            b[c] = piv ? p * ip : fmaf(-f, p, b[c]);
+        }
     }
     __syncwarp();
     if (lane < Q) {
@@ -301,6 +312,25 @@ __device__ __forceinline__ int next_group(int *ctr, int lane)
     return __shfl_sync(FULLM, g, 0);
 }
 
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem)
+{
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+// predicated global store without a branch
+__device__ __forceinline__ void st_pred(float *addr, float v, bool p)
+{
+    asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q st.global.f32 [%0], %1;\n}\n" ::"l"(addr), "f"(v),
+                 "r"((int)p)
+                 : "memory");
+}
+
+// Omega streaming: each warp double-buffers its group's entries through a 2 x 1 KB ring in shared
+// memory with cp.async (chunk = 512 B of row entries, or 512 B of S + 256 B of rows).
+constexpr int RING_SLOT = 1024;
+
 template <int Q>
 __device__ __forceinline__ float row_residual_ss(const float *X, const float *Y, const CArgs &A, int ls, int m,
                                                  int warp, int nwarps, int lane)
@@ -321,7 +351,7 @@ __device__ __forceinline__ float row_residual_ss(const float *X, const float *Y,
         const float4 x4 = *reinterpret_cast<const float4 *>(X + row * Q + 4 * sub);
         for (int k = 0; k < lg; ++k) {
             const unsigned long long w = e[k * R];
-            const float4 y4 = *reinterpret_cast<const float4 *>(Y + (int)(w & 0xFFFFu) * Q + 4 * sub);
+            const float4 y4 = *reinterpret_cast<const float4 *>(Y + (int)(w & 1023u) * Q + 4 * sub);
             const float err = __uint_as_float((uint32_t)(w >> 32)) - group_sum<Q>(f4dot(x4, y4));
             if (k < len && sub == 0) ss = fmaf(err, err, ss);
         }
@@ -330,9 +360,11 @@ __device__ __forceinline__ float row_residual_ss(const float *X, const float *Y,
 }
 
 template <int Q>
-__global__ void __launch_bounds__(512, 1) k_adm(CArgs A)
+__global__ void __launch_bounds__(1024, 1) k_adm(CArgs A)
 {
-    constexpr int L = Cfg<Q>::L, R = Cfg<Q>::R, UNR = 4;
+    constexpr int L = Cfg<Q>::L, R = Cfg<Q>::R;
+    constexpr int CKR = 64 / R;                 // row-phase k-steps per 512-byte chunk (8-byte entries)
+    constexpr int CKC = 128 / R;                // column-phase k-steps per chunk (4-byte S + 2-byte rows)
     extern __shared__ __align__(16) float sm[];
     __shared__ float red[33];
     __shared__ int sh_ctr[2];
@@ -346,15 +378,17 @@ __global__ void __launch_bounds__(512, 1) k_adm(CArgs A)
     const uint16_t *rperm = A.r_perm + (int64_t)ls * A.mmax, *rlen = A.r_len + (int64_t)ls * A.mmax;
     const uint16_t *cperm = A.c_perm + (int64_t)ls * A.G, *clen = A.c_len + (int64_t)ls * A.G;
     const int32_t *rgoff = A.r_goff + (int64_t)ls * (A.mmax + 1), *cgoff = A.c_goff + (int64_t)ls * (A.G + 1);
-    const unsigned long long *rent = A.r_ent + sb;
-    const uint32_t *cent = A.c_ent + sb;
+    const char *rent = reinterpret_cast<const char *>(A.r_ent + sb);
+    const char *cent = reinterpret_cast<const char *>(A.c_ent + sb);
     float *S = A.S + sb;
     float *X = sm;                                  // mmax x Q
     float *Y = X + (size_t)A.mmax * Q;              // nmax x Q (column j contiguous)
     float *Bm = Y + (size_t)A.nmax * Q;             // (Y Y^T + aI)^{-1}
     float *Dm = Bm + Q * Q;                         // (X^T X + bI)^{-1}
     float *Cm = Dm + Q * Q;                         // (X_{k+1}^T X_k)^T
-    float *part = Cm + Q * Q;
+    char *ring = reinterpret_cast<char *>(Cm + Q * Q);   // nwarps x 2 x RING_SLOT, also Gram partials
+    float *part = reinterpret_cast<float *>(ring);
+    char *slot0 = ring + (size_t)warp * 2 * RING_SLOT;
     float *Ug = A.U + lrow0 * Q, *Lg = A.Lam + lrow0 * Q, *Xo = A.Xold + lrow0 * Q;
     float *Vg = A.V + vb, *Pg = A.Pi + vb;
     if (m <= Q || n <= Q) {   // R25: rank not below the slice dimensions -> direct rendering
@@ -387,6 +421,7 @@ __global__ void __launch_bounds__(512, 1) k_adm(CArgs A)
         Pg[e] = 0.f;
     }
     if (tid == 0) { sh_ctr[0] = 0; sh_ctr[1] = 0; }
+    for (int e = tid; e < Q * Q; e += NT) Cm[e] = 0.f;   // step 0 multiplies it by 0: keep it finite
     __syncthreads();
     {
         const int P = gram_partial<Q>(Y, Y, n, part, 0, NT);
@@ -401,7 +436,7 @@ __global__ void __launch_bounds__(512, 1) k_adm(CArgs A)
     const int ngr = (m + R - 1) / R, ngc = (n + R - 1) / R;
     int it = 0;
     for (; it < A.K; ++it) {
-        const bool first = (it == 0);
+        const float fd = (it == 0) ? 0.f : 1.f;   // Z_0 = P_Omega(M^): no X_0 Y_0 part in step 0
         // ---- row phase: s_ij = M^_ij - x_i.y_j on Omega_i, r_i = sum_j s_ij y_j, X/U/Lambda update
         for (int g = next_group(&sh_ctr[0], lane); g < ngr; g = next_group(&sh_ctr[0], lane)) {
             const int rank = g * R + grp;
@@ -409,35 +444,42 @@ __global__ void __launch_bounds__(512, 1) k_adm(CArgs A)
             const int row = valid ? rperm[rank] : 0;
             const int len = valid ? rlen[rank] : 0;
             const int lg = rlen[g * R];
-            const unsigned long long *e = rent + rgoff[g] + grp;
-            float *Sp = S + rgoff[g] + grp;
+            const char *eg = rent + (size_t)rgoff[g] * 8;
+            const int nch = (lg + CKR - 1) / CKR;
             const float4 x4 = *reinterpret_cast<const float4 *>(X + row * Q + 4 * sub);
             float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-            for (int k0 = 0; k0 < lg; k0 += UNR) {
-                unsigned long long w[UNR];
+            cp_async16(slot0 + lane * 16, eg + lane * 16);
+            cp_commit();
+            for (int c = 0; c < nch; ++c) {
+                if (c + 1 < nch) cp_async16(slot0 + ((c + 1) & 1) * RING_SLOT + lane * 16, eg + (c + 1) * 512 + lane * 16);
+                cp_commit();
+                cp_wait1();
+                __syncwarp();
+                const unsigned long long *wb = reinterpret_cast<const unsigned long long *>(slot0 + (c & 1) * RING_SLOT) + grp;
 #pragma unroll
-                for (int u = 0; u < UNR; ++u) w[u] = (k0 + u < lg) ? e[(k0 + u) * R] : 0ull;
-                float4 y4[UNR];
-#pragma unroll
-                for (int u = 0; u < UNR; ++u) y4[u] = *reinterpret_cast<const float4 *>(Y + (int)(w[u] & 0xFFFFu) * Q + 4 * sub);
-#pragma unroll
-                for (int u = 0; u < UNR; ++u) {
-                    const float d = group_sum<Q>(f4dot(x4, y4[u]));
-                    const float sv = __uint_as_float((uint32_t)(w[u] >> 32)) - (first ? 0.f : d);
-                    const bool on = (k0 + u) < len;
-                    acc = f4fma(on ? sv : 0.f, y4[u], acc);
-                    if (on && sub == 0) Sp[(k0 + u) * R] = sv;
+                for (int kk = 0; kk < CKR; ++kk) {
+                    const int k = c * CKR + kk;
+                    const unsigned long long w = wb[kk * R];
+                    const bool on = k < len;   // entries past the row (or the group) are masked
+                    const int j = on ? (int)((uint32_t)w & 1023u) : 0;
+                    const float4 y4 = *reinterpret_cast<const float4 *>(Y + j * Q + 4 * sub);
+                    const float d = group_sum<Q>(f4dot(x4, y4));
+                    const float sv = __uint_as_float((uint32_t)(w >> 32)) - fd * d;
+                    acc = f4fma(on ? sv : 0.f, y4, acc);
+                    st_pred(S + (((uint32_t)w) >> 10), sv, on && sub == 0);
                 }
+                __syncwarp();
             }
             const float4 u4 = *reinterpret_cast<const float4 *>(Ug + row * Q + 4 * sub);
             const float4 l4 = *reinterpret_cast<const float4 *>(Lg + row * Q + 4 * sub);
-            const float fx = first ? 0.f : al;
+            const float fx = fd * al;
             float4 t4;
             t4.x = acc.x + al * u4.x - l4.x - fx * x4.x;
             t4.y = acc.y + al * u4.y - l4.y - fx * x4.y;
             t4.z = acc.z + al * u4.z - l4.z - fx * x4.z;
             t4.w = acc.w + al * u4.w - l4.w - fx * x4.w;
-            const float4 xn = group_matvec<Q>(t4, Bm, lane0, sub, first ? make_float4(0.f, 0.f, 0.f, 0.f) : x4);
+            const float4 x0 = make_float4(fd * x4.x, fd * x4.y, fd * x4.z, fd * x4.w);
+            const float4 xn = group_matvec<Q>(t4, Bm, lane0, sub, x0);
             float4 un, ln;
             un.x = fmaxf(0.f, xn.x + l4.x * inv_al); ln.x = l4.x + ga * al * (xn.x - un.x);
             un.y = fmaxf(0.f, xn.y + l4.y * inv_al); ln.y = l4.y + ga * al * (xn.y - un.y);
@@ -460,11 +502,11 @@ __global__ void __launch_bounds__(512, 1) k_adm(CArgs A)
             __syncthreads();
             if (warp == 0) {
                 inv_spd_warp<Q>(Dm, be);
-            } else if (!first) {
+            } else if (it > 0) {
                 P = gram_partial<Q>(Xo, X, m, part, 32, NT - 32);
             }
             __syncthreads();
-            if (!first) {
+            if (it > 0) {
                 P = (NT - 32) / ((Q / 4) * (Q / 4));
                 if (P * Q * Q > Cfg<Q>::PART) P = Cfg<Q>::PART / (Q * Q);
                 gram_reduce<Q>(Cm, part, P);   // Cm[b][a] = (X_{k+1}^T X_k)[a][b]
@@ -478,22 +520,38 @@ __global__ void __launch_bounds__(512, 1) k_adm(CArgs A)
             const int colj = valid ? cperm[rank] : 0;
             const int len = valid ? clen[rank] : 0;
             const int lg = clen[g * R];
-            const uint32_t *e = cent + cgoff[g] + grp;
+            const int cb = cgoff[g];
+            const char *sg = reinterpret_cast<const char *>(S + cb);
+            const char *rg = cent + (size_t)cb * 2;
+            const int nch = (lg + CKC - 1) / CKC;
             const float4 y4 = *reinterpret_cast<const float4 *>(Y + colj * Q + 4 * sub);
             float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (!first) acc = group_matvec<Q>(y4, Cm, lane0, sub, acc);   // (X_{k+1}^T X_k) y_j
-            for (int k0 = 0; k0 < lg; k0 += UNR) {
-                uint32_t w[UNR];
-#pragma unroll
-                for (int u = 0; u < UNR; ++u) w[u] = (k0 + u < len) ? e[(k0 + u) * R] : 0u;
-                float sv[UNR];
-#pragma unroll
-                for (int u = 0; u < UNR; ++u) sv[u] = (k0 + u < len) ? S[w[u] >> 10] : 0.f;
-#pragma unroll
-                for (int u = 0; u < UNR; ++u) {
-                    const float4 xv = *reinterpret_cast<const float4 *>(X + (int)(w[u] & 1023u) * Q + 4 * sub);
-                    acc = f4fma(sv[u], xv, acc);
+            acc = group_matvec<Q>(make_float4(fd * y4.x, fd * y4.y, fd * y4.z, fd * y4.w), Cm, lane0, sub, acc);
+            cp_async16(slot0 + lane * 16, sg + lane * 16);
+            if (lane < 16) cp_async16(slot0 + 512 + lane * 16, rg + lane * 16);
+            cp_commit();
+            for (int c = 0; c < nch; ++c) {
+                if (c + 1 < nch) {
+                    char *nx = slot0 + ((c + 1) & 1) * RING_SLOT;
+                    cp_async16(nx + lane * 16, sg + (c + 1) * 512 + lane * 16);
+                    if (lane < 16) cp_async16(nx + 512 + lane * 16, rg + (c + 1) * 256 + lane * 16);
                 }
+                cp_commit();
+                cp_wait1();
+                __syncwarp();
+                const char *cur = slot0 + (c & 1) * RING_SLOT;
+                const float *sbuf = reinterpret_cast<const float *>(cur) + grp;
+                const uint16_t *rbuf = reinterpret_cast<const uint16_t *>(cur + 512) + grp;
+#pragma unroll
+                for (int kk = 0; kk < CKC; ++kk) {
+                    const int k = c * CKC + kk;
+                    const bool on = k < len;
+                    const float sv = on ? sbuf[kk * R] : 0.f;
+                    const int i = on ? (int)rbuf[kk * R] : 0;
+                    const float4 xv = *reinterpret_cast<const float4 *>(X + i * Q + 4 * sub);
+                    acc = f4fma(sv, xv, acc);
+                }
+                __syncwarp();
             }
             const float4 v4 = *reinterpret_cast<const float4 *>(Vg + colj * Q + 4 * sub);
             const float4 p4 = *reinterpret_cast<const float4 *>(Pg + colj * Q + 4 * sub);
@@ -542,7 +600,8 @@ __global__ void __launch_bounds__(512, 1) k_adm(CArgs A)
 
 size_t adm_smem_bytes(int q, int mmax, int nmax)
 {
-    return ((size_t)mmax + (size_t)nmax) * q * sizeof(float) + (3 * (size_t)q * q + 2048) * sizeof(float);
+    // X, Y, three q x q matrices, 32 warps x 2 ring slots (reused for the Gram partials)
+    return ((size_t)mmax + (size_t)nmax) * q * sizeof(float) + 3 * (size_t)q * q * sizeof(float) + 32 * 2 * RING_SLOT;
 }
 
 static int layout_R(int q) { return 128 / q; }
@@ -589,9 +648,7 @@ static cudaError_t launch_adm(lmc_ctx *c, const CArgs &A)
     const size_t sm = adm_smem_bytes(Q, c->mmax, A.nmax);
     cudaError_t e = cudaFuncSetAttribute(k_adm<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
-    // two CTAs per SM when their shared memory fits (overlaps one slice's serial Gram/inverse
-    // phases with another slice's sample phases), else one CTA of 16 warps
-    const int nt = (2 * (sm + 2048) <= 227 * 1024) ? 256 : 512;
+    const int nt = 1024;   // 32 warps (64 registers per thread), one CTA per SM
     k_adm<Q><<<c->SL, nt, sm, c->stream>>>(A);
     return cudaGetLastError();
 }

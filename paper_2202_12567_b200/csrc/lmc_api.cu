@@ -484,7 +484,8 @@ static lmc_status create_impl(lmc_ctx *c, const lmc_gbuffer *g, const lmc_vpls *
     {
         int64_t nt = (int64_t)std::ceil((double)(c->mmax * G) * cfg.rate);
         c->ncap = std::min<int64_t>((int64_t)c->mmax * G, std::max<int64_t>(nt, 2 * c->pool_cap) + G);
-        c->scap = c->ncap + 32 * (int64_t)std::max<int64_t>(c->mmax, G);   // sliced-ELL padding bound
+        // sliced-ELL padding bound (+ 8-entry group alignment + one trailing 128-entry chunk), multiple of 8
+        c->scap = ((c->ncap + 32 * (int64_t)std::max<int64_t>(c->mmax, G) + 8 * (int64_t)std::max<int64_t>(c->mmax, G) + 256) + 7) & ~7ll;
     }
     // device arena
     Dev &d = c->d;

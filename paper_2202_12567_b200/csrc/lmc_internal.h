@@ -99,8 +99,8 @@ struct Dev {
     uint16_t *r_perm, *r_len;          // [SL][mmax] rows by (length desc, id)
     uint16_t *c_perm, *c_len;          // [SL][G]
     int32_t *r_goff, *c_goff;          // [SL][mmax+1], [SL][G+1]
-    unsigned long long *r_ent;         // [SL][scap] (M^ bits << 32) | column
-    uint32_t *c_ent;                   // [SL][scap] (row-layout index << 10) | row
+    unsigned long long *r_ent;         // [SL][scap] (M^ bits << 32) | (column-layout index << 10) | column
+    uint16_t *c_ent;                   // [SL][scap] row of the column-layout entry
     float4 *norm;                      // [SL] sigma, 1/sigma, sum M^, sum M^^2
     float *U, *V, *Lam, *Pi, *Xold, *S; // U/Lam/Xold [ML][q], V/Pi [SL][G][q], S [SL][scap]
     int32_t *flags, *iters;            // [SL]
