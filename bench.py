@@ -262,6 +262,13 @@ def main():
     fl = (adm_flops if solver == 0 else mals_flops)(q, st["sum_samples"], st["rows"], st["sum_cols"],
                                                      st["slice_end"] - st["slice_begin"], K)
     achieved = fl / (ms_c * 1e-3) / 1e12
+    traffic = None
+    try:   # DRAM bytes per launch of the dominant kernel from the committed ncu --set full capture
+        tj = json.load(open(os.path.join(ROOT, "profiles", "r01_traffic.json")))
+        ent = tj.get(f"{args.config}/{args.solver}/q{x.cfg.rank_q}")
+        traffic = ent["bytes"] if ent else None
+    except Exception:
+        traffic = None
     e2e = None
     if not args.no_e2e and world == 1:
         e2e = measure_e2e(x, args, solver, dev)
@@ -290,7 +297,8 @@ def main():
         "completed_entries": sum_completed, "samples": sum_N, "rays_per_pixel": evals / max(sum_m, 1.0),
         "roofline": {"bound": "alu", "kernel": "k_adm" if solver == 0 else "k_mals", "achieved": achieved,
                      "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP32_PEAK_TFLOPS,
-                     "traffic": None, "peak_source": "derived: 148 SMs x 128 FP32 FMA lanes x 2 x 1.965 GHz"},
+                     "traffic": traffic, "peak_source": "derived: 148 SMs x 128 FP32 FMA lanes x 2 x 1.965 GHz",
+                     "flops_per_launch": fl},
         "clocks": cl,
         "gpu_launches": launches,
     }
