@@ -187,14 +187,11 @@ def main():
     rows_local = int(st0["rows"])
     # slice-ordered row ranges of every rank (identical slicing everywhere) for the tile gather
     if world > 1:
-        counts = torch.zeros(world, dtype=torch.int64, device=dev)
-        counts[rank] = rows_local
-        dist.all_reduce(counts)
-        counts = counts.tolist()
-        maxrows = max(counts)
-        tile = torch.zeros(maxrows * 3, device=dev)
-        gathered = torch.zeros(world * maxrows * 3, device=dev) if True else None
-        all_rows = torch.zeros(x.m * 3, device=dev)
+        from paper_2202_12567_b200 import dist as pdist
+        fr.build_slices()
+        off, _ = fr.slices()
+        counts = pdist.row_counts(off, world)
+        tile = torch.zeros(rows_local * 3, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > L2 (126 MB)
 
     def frame_once():
@@ -207,13 +204,8 @@ def main():
             fr.resolve_image(img)
         else:
             fr.resolve_rows(tile)
-            dist.all_gather_into_tensor(gathered, tile)
+            all_rows = pdist.gather_rows(tile, counts)     # one NCCL all-gather over NVLink
             if rank == 0:
-                off = 0
-                g3 = gathered.view(world, maxrows * 3)
-                for r in range(world):
-                    all_rows[off * 3:(off + counts[r]) * 3] = g3[r, :counts[r] * 3]
-                    off += counts[r]
                 fr.scatter_rows(all_rows, img)
 
     for _ in range(args.warmup):

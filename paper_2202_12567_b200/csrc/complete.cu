@@ -69,17 +69,21 @@ struct LArgs {
     const int32_t *slice_off, *cut_n, *rowptr, *colptr, *csc_src, *nnz;
     const uint16_t *col, *csc_row;
     const float *val;
-    int32_t s0, G, mmax, R;
+    int32_t s0, G, mmax, R, P, KAR, KAC;
     int64_t ncap, scap;
     uint16_t *r_perm, *r_len, *c_perm, *c_len;
     int32_t *r_goff, *c_goff, *map;
     unsigned long long *r_ent;
     uint16_t *c_ent;
+    float *S;
     float4 *norm;
 };
 
 constexpr int LT = 1024;
 
+// The entries of the P rows (columns) that share a shared-memory phase of the ADM kernel are
+// scheduled so that at step k member t takes, when it can, an entry whose gathered index has
+// residue (t + k) mod P: the P gathers of a phase then fall into different bank sets.
 __global__ void __launch_bounds__(LT, 1) k_layout(LArgs A)
 {
     typedef cub::BlockRadixSort<uint32_t, LT, 1> Sort;
@@ -90,16 +94,15 @@ __global__ void __launch_bounds__(LT, 1) k_layout(LArgs A)
     __shared__ int32_t sh_goff[LT + 1];
     __shared__ int32_t sh_len[LT];
     __shared__ float red[33];
-    const int ls = blockIdx.x, s = A.s0 + ls, tid = threadIdx.x, R = A.R;
+    const int ls = blockIdx.x, s = A.s0 + ls, tid = threadIdx.x, R = A.R, P = A.P;
     const int m = A.slice_off[s + 1] - A.slice_off[s], n = A.cut_n[ls];
     const int64_t ob = (int64_t)ls * A.ncap, sb = (int64_t)ls * A.scap;
     const int32_t *rp = A.rowptr + (int64_t)ls * (A.mmax + 1);
     const int32_t *cp = A.colptr + (int64_t)ls * (A.G + 1);
     const int nnz = A.nnz[ls];
-    // sigma = max_Omega M~, then sum and sum of squares of M^ = M~ / sigma
     float mx = 0.f;
     for (int k = tid; k < nnz; k += LT) mx = fmaxf(mx, A.val[ob + k]);
-    const float sigma = block_reduce<true>(mx, red);
+    const float sigma = block_reduce<true>(mx, red);   // R23: sigma = max_Omega M~
     const float inv_sigma = sigma > 0.f ? 1.0f / sigma : 0.f;
     float sum = 0.f, sq = 0.f;
     for (int k = tid; k < nnz; k += LT) {
@@ -110,17 +113,17 @@ __global__ void __launch_bounds__(LT, 1) k_layout(LArgs A)
     sum = block_reduce<false>(sum, red);
     sq = block_reduce<false>(sq, red);
     if (tid == 0) A.norm[ls] = make_float4(sigma, inv_sigma, sum, sq);
-    // pass 0: columns (entries: row id; their layout index goes to map[CSR position]),
-    // pass 1: rows (entries: M^ bits << 32 | column-layout index << 10 | column)
+    int dummy = 0;   // row-layout padding stores its (zero) residual here, after the column layout
     for (int pass = 0; pass < 2; ++pass) {
         const bool rows_pass = pass == 1;
         const int cnt = rows_pass ? m : n;
+        const int KA = rows_pass ? A.KAR : A.KAC;   // k-steps per cp.async chunk
         const int32_t *ptr = rows_pass ? rp : cp;
         uint16_t *perm = (rows_pass ? A.r_perm : A.c_perm) + (int64_t)ls * (rows_pass ? A.mmax : A.G);
         uint16_t *lens = (rows_pass ? A.r_len : A.c_len) + (int64_t)ls * (rows_pass ? A.mmax : A.G);
         int32_t *goff = (rows_pass ? A.r_goff : A.c_goff) + (int64_t)ls * ((rows_pass ? A.mmax : A.G) + 1);
         // sort by (length desc, index asc): unique keys -> deterministic permutation
-        int len = tid < cnt ? ptr[tid + 1] - ptr[tid] : 0;
+        const int len = tid < cnt ? ptr[tid + 1] - ptr[tid] : 0;
         uint32_t key[1] = {tid < cnt ? ((uint32_t)(2047 - len) << 10) | (uint32_t)tid : 0xFFFFFFFFu};
         Sort(sort_tmp).Sort(key, 0, 32);
         const int rank = tid;                       // blocked arrangement: thread = rank
@@ -132,41 +135,65 @@ __global__ void __launch_bounds__(LT, 1) k_layout(LArgs A)
         }
         sh_len[rank] = wlen;
         __syncthreads();
+        // groups of R, padded to whole cp.async chunks (KA k-steps)
         const int ng = (cnt + R - 1) / R;
-        int gsz = (tid < ng) ? ((R * sh_len[tid * R] + 7) & ~7) : 0;   // 16-byte aligned groups
+        const int lgp_t = tid < ng ? ((sh_len[tid * R] + KA - 1) / KA) * KA : 0;
+        int gsz = R * lgp_t;
         int pre, tot;
         Scan(scan_tmp).ExclusiveSum(gsz, pre, tot);
         if (tid < ng) { sh_goff[tid] = pre; goff[tid] = pre; }
         if (tid == 0) { sh_goff[ng] = tot; goff[ng] = tot; }
+        if (!rows_pass) dummy = tot;
         __syncthreads();
+        // one thread per member (row / column): its entries are placed blocked by residue of the
+        // gathered index mod P, the blocks in the cyclic order starting at the member's slot t
+        // within its phase set, so the P members of a phase gather different bank sets at
+        // (almost) every step; the rest of the group length is sentinel padding.
+        const uint16_t *gidx = rows_pass ? (A.col + ob) : (A.csc_row + ob);   // gathered index per position
         if (rank < ng * R) {
-            const int g = rank / R, r = rank % R;
-            const int lg = sh_len[g * R];
+            const int g = rank / R, r = rank % R, t = r % P;
+            const int lgp = ((sh_len[g * R] + KA - 1) / KA) * KA;
             const int base = sh_goff[g];
             const int own = rank < cnt ? wlen : 0;
             const int p0 = rank < cnt ? ptr[who] : 0;
-            for (int k = 0; k < lg; ++k) {
+            int cntr[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            for (int k = 0; k < own; ++k) cntr[(int)gidx[p0 + k] % P]++;
+            int start[8];
+            int acc = 0;
+            for (int b = 0; b < P; ++b) {
+                const int res = (t + b) % P;
+                start[res] = acc;
+                acc += cntr[res];
+            }
+            for (int k = 0; k < own; ++k) {
+                const int pos = p0 + k;
+                const int res = (int)gidx[pos] % P;
+                const int slot = start[res]++;
+                const int idx = base + slot * R + r;
+                if (rows_pass) {
+                    const float mh = A.val[ob + pos] * inv_sigma;
+                    A.r_ent[sb + idx] = ((unsigned long long)__float_as_uint(mh) << 32) |
+                                        ((unsigned long long)(uint32_t)A.map[ob + pos] << 11) | (unsigned long long)A.col[ob + pos];
+                } else {
+                    A.c_ent[sb + idx] = A.csc_row[ob + pos];
+                    A.map[ob + A.csc_src[ob + pos]] = idx;
+                    A.S[sb + idx] = 0.f;
+                }
+            }
+            for (int k = own; k < lgp; ++k) {
                 const int idx = base + k * R + r;
                 if (rows_pass) {
-                    unsigned long long e = 0ull;
-                    if (k < own) {
-                        const float mh = A.val[ob + p0 + k] * inv_sigma;
-                        e = ((unsigned long long)__float_as_uint(mh) << 32) |
-                            ((unsigned long long)(uint32_t)A.map[ob + p0 + k] << 10) | (unsigned long long)A.col[ob + p0 + k];
-                    }
-                    A.r_ent[sb + idx] = e;
+                    // sentinel: zero row n of Y, residual parked in the dummy slot
+                    A.r_ent[sb + idx] = ((unsigned long long)(uint32_t)dummy << 11) | (unsigned long long)n;
                 } else {
-                    uint16_t e = 0;
-                    if (k < own) {
-                        e = A.csc_row[ob + p0 + k];
-                        A.map[ob + A.csc_src[ob + p0 + k]] = idx;
-                    }
-                    A.c_ent[sb + idx] = e;
+                    A.c_ent[sb + idx] = (uint16_t)m;   // sentinel: zero row m of X
+                    A.S[sb + idx] = 0.f;               // padding slots stay finite
                 }
             }
         }
         __syncthreads();
     }
+    if (tid == 0) A.S[sb + dummy] = 0.f;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -345,15 +372,15 @@ __device__ __forceinline__ float row_residual_ss(const float *X, const float *Y,
     for (int g = warp; g < ngr; g += nwarps) {
         const int rank = g * R + grp;
         const bool valid = rank < m;
-        const int row = valid ? rperm[rank] : 0, len = valid ? rlen[rank] : 0;
-        const int lg = rlen[g * R];
+        const int row = valid ? rperm[rank] : m;
+        const int len = rlen[g * R];   // group length (warp-uniform); padding entries add 0
         const unsigned long long *e = rent + rgoff[g] + grp;
         const float4 x4 = *reinterpret_cast<const float4 *>(X + row * Q + 4 * sub);
-        for (int k = 0; k < lg; ++k) {
+        for (int k = 0; k < len; ++k) {
             const unsigned long long w = e[k * R];
-            const float4 y4 = *reinterpret_cast<const float4 *>(Y + (int)(w & 1023u) * Q + 4 * sub);
+            const float4 y4 = *reinterpret_cast<const float4 *>(Y + (int)((uint32_t)w & 2047u) * Q + 4 * sub);
             const float err = __uint_as_float((uint32_t)(w >> 32)) - group_sum<Q>(f4dot(x4, y4));
-            if (k < len && sub == 0) ss = fmaf(err, err, ss);
+            if (sub == 0) ss = fmaf(err, err, ss);
         }
     }
     return ss;
@@ -381,9 +408,9 @@ __global__ void __launch_bounds__(1024, 1) k_adm(CArgs A)
     const char *rent = reinterpret_cast<const char *>(A.r_ent + sb);
     const char *cent = reinterpret_cast<const char *>(A.c_ent + sb);
     float *S = A.S + sb;
-    float *X = sm;                                  // mmax x Q
-    float *Y = X + (size_t)A.mmax * Q;              // nmax x Q (column j contiguous)
-    float *Bm = Y + (size_t)A.nmax * Q;             // (Y Y^T + aI)^{-1}
+    float *X = sm;                                  // (mmax + 1) x Q, row m_s is the zero sentinel
+    float *Y = X + (size_t)(A.mmax + 1) * Q;        // (nmax + 1) x Q (column j contiguous), row n_s zero
+    float *Bm = Y + (size_t)(A.nmax + 1) * Q;       // (Y Y^T + aI)^{-1}
     float *Dm = Bm + Q * Q;                         // (X^T X + bI)^{-1}
     float *Cm = Dm + Q * Q;                         // (X_{k+1}^T X_k)^T
     char *ring = reinterpret_cast<char *>(Cm + Q * Q);   // nwarps x 2 x RING_SLOT, also Gram partials
@@ -422,6 +449,7 @@ __global__ void __launch_bounds__(1024, 1) k_adm(CArgs A)
     }
     if (tid == 0) { sh_ctr[0] = 0; sh_ctr[1] = 0; }
     for (int e = tid; e < Q * Q; e += NT) Cm[e] = 0.f;   // step 0 multiplies it by 0: keep it finite
+    for (int e = tid; e < Q; e += NT) { X[m * Q + e] = 0.f; Y[n * Q + e] = 0.f; }   // sentinel rows
     __syncthreads();
     {
         const int P = gram_partial<Q>(Y, Y, n, part, 0, NT);
@@ -441,11 +469,9 @@ __global__ void __launch_bounds__(1024, 1) k_adm(CArgs A)
         for (int g = next_group(&sh_ctr[0], lane); g < ngr; g = next_group(&sh_ctr[0], lane)) {
             const int rank = g * R + grp;
             const bool valid = rank < m;
-            const int row = valid ? rperm[rank] : 0;
-            const int len = valid ? rlen[rank] : 0;
-            const int lg = rlen[g * R];
+            const int row = valid ? rperm[rank] : m;          // m: the zero sentinel row
+            const int nch = (rgoff[g + 1] - rgoff[g]) / (CKR * R);
             const char *eg = rent + (size_t)rgoff[g] * 8;
-            const int nch = (lg + CKR - 1) / CKR;
             const float4 x4 = *reinterpret_cast<const float4 *>(X + row * Q + 4 * sub);
             float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
             cp_async16(slot0 + lane * 16, eg + lane * 16);
@@ -458,15 +484,14 @@ __global__ void __launch_bounds__(1024, 1) k_adm(CArgs A)
                 const unsigned long long *wb = reinterpret_cast<const unsigned long long *>(slot0 + (c & 1) * RING_SLOT) + grp;
 #pragma unroll
                 for (int kk = 0; kk < CKR; ++kk) {
-                    const int k = c * CKR + kk;
+                    // padding entries gather the zero row n of Y: they add exactly 0 and park a
+                    // zero residual in the dummy slot, so no masking is needed
                     const unsigned long long w = wb[kk * R];
-                    const bool on = k < len;   // entries past the row (or the group) are masked
-                    const int j = on ? (int)((uint32_t)w & 1023u) : 0;
-                    const float4 y4 = *reinterpret_cast<const float4 *>(Y + j * Q + 4 * sub);
+                    const float4 y4 = *reinterpret_cast<const float4 *>(Y + (int)((uint32_t)w & 2047u) * Q + 4 * sub);
                     const float d = group_sum<Q>(f4dot(x4, y4));
-                    const float sv = __uint_as_float((uint32_t)(w >> 32)) - fd * d;
-                    acc = f4fma(on ? sv : 0.f, y4, acc);
-                    st_pred(S + (((uint32_t)w) >> 10), sv, on && sub == 0);
+                    const float sv = fmaf(-fd, d, __uint_as_float((uint32_t)(w >> 32)));
+                    acc = f4fma(sv, y4, acc);
+                    st_pred(S + (((uint32_t)w) >> 11), sv, sub == 0);
                 }
                 __syncwarp();
             }
@@ -517,13 +542,11 @@ __global__ void __launch_bounds__(1024, 1) k_adm(CArgs A)
         for (int g = next_group(&sh_ctr[1], lane); g < ngc; g = next_group(&sh_ctr[1], lane)) {
             const int rank = g * R + grp;
             const bool valid = rank < n;
-            const int colj = valid ? cperm[rank] : 0;
-            const int len = valid ? clen[rank] : 0;
-            const int lg = clen[g * R];
+            const int colj = valid ? cperm[rank] : n;         // n: the zero sentinel column
             const int cb = cgoff[g];
+            const int nch = (cgoff[g + 1] - cb) / (CKC * R);
             const char *sg = reinterpret_cast<const char *>(S + cb);
             const char *rg = cent + (size_t)cb * 2;
-            const int nch = (lg + CKC - 1) / CKC;
             const float4 y4 = *reinterpret_cast<const float4 *>(Y + colj * Q + 4 * sub);
             float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
             acc = group_matvec<Q>(make_float4(fd * y4.x, fd * y4.y, fd * y4.z, fd * y4.w), Cm, lane0, sub, acc);
@@ -544,12 +567,9 @@ __global__ void __launch_bounds__(1024, 1) k_adm(CArgs A)
                 const uint16_t *rbuf = reinterpret_cast<const uint16_t *>(cur + 512) + grp;
 #pragma unroll
                 for (int kk = 0; kk < CKC; ++kk) {
-                    const int k = c * CKC + kk;
-                    const bool on = k < len;
-                    const float sv = on ? sbuf[kk * R] : 0.f;
-                    const int i = on ? (int)rbuf[kk * R] : 0;
-                    const float4 xv = *reinterpret_cast<const float4 *>(X + i * Q + 4 * sub);
-                    acc = f4fma(sv, xv, acc);
+                    // padding: zero row m of X and a zero S slot
+                    const float4 xv = *reinterpret_cast<const float4 *>(X + (int)rbuf[kk * R] * Q + 4 * sub);
+                    acc = f4fma(sbuf[kk * R], xv, acc);
                 }
                 __syncwarp();
             }
@@ -601,7 +621,7 @@ __global__ void __launch_bounds__(1024, 1) k_adm(CArgs A)
 size_t adm_smem_bytes(int q, int mmax, int nmax)
 {
     // X, Y, three q x q matrices, 32 warps x 2 ring slots (reused for the Gram partials)
-    return ((size_t)mmax + (size_t)nmax) * q * sizeof(float) + 3 * (size_t)q * q * sizeof(float) + 32 * 2 * RING_SLOT;
+    return ((size_t)mmax + (size_t)nmax + 2) * q * sizeof(float) + 3 * (size_t)q * q * sizeof(float) + 32 * 2 * RING_SLOT;
 }
 
 static int layout_R(int q) { return 128 / q; }
@@ -635,6 +655,10 @@ cudaError_t run_layout(lmc_ctx *c)
     A.r_ent = c->d.r_ent;
     A.c_ent = c->d.c_ent;
     A.norm = c->d.norm;
+    A.S = c->d.S;
+    A.P = c->q >= 32 ? 1 : 32 / c->q;
+    A.KAR = 64 / A.R;      // k-steps per 512-byte chunk of 8-byte row entries
+    A.KAC = 128 / A.R;     // k-steps per chunk of 4-byte S (+ 2-byte rows)
     const size_t sm = sizeof(typename cub::BlockRadixSort<uint32_t, LT, 1>::TempStorage);
     cudaError_t e = cudaFuncSetAttribute(k_layout, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;

@@ -484,8 +484,10 @@ static lmc_status create_impl(lmc_ctx *c, const lmc_gbuffer *g, const lmc_vpls *
     {
         int64_t nt = (int64_t)std::ceil((double)(c->mmax * G) * cfg.rate);
         c->ncap = std::min<int64_t>((int64_t)c->mmax * G, std::max<int64_t>(nt, 2 * c->pool_cap) + G);
-        // sliced-ELL padding bound (+ 8-entry group alignment + one trailing 128-entry chunk), multiple of 8
-        c->scap = ((c->ncap + 32 * (int64_t)std::max<int64_t>(c->mmax, G) + 8 * (int64_t)std::max<int64_t>(c->mmax, G) + 256) + 7) & ~7ll;
+        // sliced-ELL bound: padding to the longest row of a group (<= 32 max(m, G)) plus whole
+        // cp.async chunks per group (<= 128 entries per group) plus the dummy slot; multiple of 8
+        const int64_t mg = std::max<int64_t>(c->mmax, G);
+        c->scap = (c->ncap + 32 * mg + 128 * mg + 256 + 7) & ~7ll;
     }
     // device arena
     Dev &d = c->d;
@@ -562,7 +564,8 @@ static lmc_status create_impl(lmc_ctx *c, const lmc_gbuffer *g, const lmc_vpls *
     CK(cudaMemsetAsync(d.flags, 0, SL * sizeof(int32_t), c->stream), "memset");
     CK(cudaMemsetAsync(d.img, 0, 3 * sizeof(float) * (size_t)std::max<int64_t>((int64_t)c->W * c->H, 1), c->stream), "memset");
     size_t need = cfg.solver == LMC_SOLVER_MALS ? mals_smem_bytes(c->q, c->mmax, (int)G) : adm_smem_bytes(c->q, c->mmax, (int)G);
-    if (c->scap >= (1ll << 22)) return fail(c, LMC_EINVAL, "per-slice sample capacity %lld exceeds 2^22", (long long)c->scap);
+    if (c->scap >= (1ll << 21)) return fail(c, LMC_EINVAL, "per-slice sample capacity %lld exceeds 2^21", (long long)c->scap);
+
     int maxsm = 0, dev = 0;
     CK(cudaGetDevice(&dev), "device");
     CK(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev), "device attr");
