@@ -22,7 +22,7 @@
  *     allocation failed;  LMC_ECUDA a CUDA error (sticky: the ctx must be destroyed);
  *     LMC_EOVERFLOW a per-slice capacity was exceeded (reported by the stage that detects it).
  *   - Thread safety: a ctx is not thread-safe; distinct ctxs are independent.  One ctx per
- *     GPU / rank.
+ *     GPU / rank; at most 16 live contexts per process (LMC_EINVAL beyond).
  */
 #ifndef LMC_H
 #define LMC_H
@@ -79,7 +79,7 @@ typedef struct {
 
 /* Analytic occluders for the shadow-ray visibility test (BASELINE north_star "procedural
  * analytic scene").  HOST pointers, float32: sph[4*k] = (cx,cy,cz,r); box[6*k] = (lo3, hi3);
- * rect[12*k] = (p0, e1, e2, nrm = e1 x e2).  At most 64 of each.  clamp_dist = d_c of the
+ * rect[12*k] = (p0, e1, e2, nrm = e1 x e2).  At most 32 of each.  clamp_dist = d_c of the
  * d^2 clamp (DESIGN R2); shadow_eps = segment shrink at both ends (R3); diag = scene
  * diagonal D used by the slicing keys (R26). */
 typedef struct {

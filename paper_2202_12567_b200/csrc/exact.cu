@@ -13,12 +13,15 @@
 //   entry A(i,j) P:61, P:48, P:50        (R1-R3, R32)
 #include <cub/cub.cuh>
 
+#include <mutex>
+
 #include "lmc_internal.h"
 #include "philox.cuh"
 
 namespace lmc {
 
-__constant__ SceneConst c_scene;
+// one scene per live context (slot acquired in lmc_create): uniform reads hit the constant cache
+__constant__ SceneConst c_scenes[SCENE_SLOTS];
 
 #define LMC_INV_PI 0.31830988618379067
 #define LMC_INV_2PI 0.15915494309189535
@@ -44,12 +47,31 @@ __device__ __forceinline__ double powi_d(double base, int e)
     return r;
 }
 
-// 1 iff the open segment x + t l, t in (eps, dist - eps), misses every occluder
-__device__ bool visible_d(double x0, double x1, double x2, double l0, double l1, double l2, double dist)
+// 1 iff the open segment x + t l, t in (eps, dist - eps), misses every occluder.
+// Each primitive is first screened by a conservative fp32 test on the segment [x, y] (y = VPL
+// position) with a margin of 1e-3 D, orders of magnitude above fp32 rounding: a primitive is
+// skipped only when the exact fp64 test below cannot report a hit, so the visibility decision is
+// exactly the reference's (an OR over primitives does not depend on which misses are skipped).
+__device__ bool visible_d(int slot, double x0, double x1, double x2, double l0, double l1,
+                          double l2, double dist, float y0f, float y1f, float y2f)
 {
-    const double tmin = c_scene.eps, tmax = dist - c_scene.eps;
-    for (int k = 0; k < c_scene.nsph; ++k) {
-        const float *s = c_scene.sph + 4 * k;
+    const SceneConst *sc = &c_scenes[slot];
+    const double tmin = sc->eps, tmax = dist - sc->eps;
+    const float x0f = (float)x0, x1f = (float)x1, x2f = (float)x2;   // exact: the inputs are float32
+    const float mg = sc->margin;
+    const float lo0 = fminf(x0f, y0f), lo1 = fminf(x1f, y1f), lo2 = fminf(x2f, y2f);
+    const float hi0 = fmaxf(x0f, y0f), hi1 = fmaxf(x1f, y1f), hi2 = fmaxf(x2f, y2f);
+    const float w0 = y0f - x0f, w1 = y1f - x1f, w2 = y2f - x2f;
+    const float ww = w0 * w0 + w1 * w1 + w2 * w2;
+    for (int k = 0; k < sc->nsph; ++k) {
+        const float *s = sc->sph + 4 * k;
+        {   // screen: distance from the segment to the centre against r + margin
+            const float v0 = s[0] - x0f, v1 = s[1] - x1f, v2 = s[2] - x2f;
+            const float tt = fminf(fmaxf((v0 * w0 + v1 * w1 + v2 * w2) / ww, 0.f), 1.f);
+            const float d0 = v0 - tt * w0, d1 = v1 - tt * w1, d2 = v2 - tt * w2;
+            const float rr = s[3] + mg;
+            if (d0 * d0 + d1 * d1 + d2 * d2 > rr * rr) continue;
+        }
         double o0 = x0 - (double)s[0], o1 = x1 - (double)s[1], o2 = x2 - (double)s[2];
         double r = s[3];
         double b = dot3d(o0, o1, o2, l0, l1, l2);
@@ -60,10 +82,16 @@ __device__ bool visible_d(double x0, double x1, double x2, double l0, double l1,
         double t0 = -b - sq, t1 = -b + sq;
         if ((t0 > tmin && t0 < tmax) || (t1 > tmin && t1 < tmax)) return false;
     }
-    if (c_scene.nbox > 0) {
-        const double i0 = 1.0 / l0, i1 = 1.0 / l1, i2 = 1.0 / l2;
-        for (int k = 0; k < c_scene.nbox; ++k) {
-            const float *bx = c_scene.box + 6 * k;
+    if (sc->nbox > 0) {
+        double i0 = 0.0, i1 = 0.0, i2 = 0.0;
+        bool inv = false;
+        for (int k = 0; k < sc->nbox; ++k) {
+            const float *bx = sc->box + 6 * k;
+            // screen: segment bounding box against the box grown by the margin
+            if (hi0 < bx[0] - mg || lo0 > bx[3] + mg || hi1 < bx[1] - mg || lo1 > bx[4] + mg || hi2 < bx[2] - mg ||
+                lo2 > bx[5] + mg)
+                continue;
+            if (!inv) { i0 = 1.0 / l0; i1 = 1.0 / l1; i2 = 1.0 / l2; inv = true; }
             double a1 = ((double)bx[0] - x0) * i0, a2 = ((double)bx[3] - x0) * i0;
             double b1 = ((double)bx[1] - x1) * i1, b2 = ((double)bx[4] - x1) * i1;
             double e1 = ((double)bx[2] - x2) * i2, e2 = ((double)bx[5] - x2) * i2;
@@ -72,8 +100,18 @@ __device__ bool visible_d(double x0, double x1, double x2, double l0, double l1,
             if (tnear <= tfar && tfar > tmin && tnear < tmax) return false;
         }
     }
-    for (int k = 0; k < c_scene.nrect; ++k) {
-        const float *rc = c_scene.rect + 12 * k;
+    for (int k = 0; k < sc->nrect; ++k) {
+        const float *rc = sc->rect + 12 * k;
+        {   // screen: bounding boxes, then both end points strictly on one side of the plane
+            const float *rb = sc->rbox + 6 * k;
+            if (hi0 < rb[0] - mg || lo0 > rb[3] + mg || hi1 < rb[1] - mg || lo1 > rb[4] + mg || hi2 < rb[2] - mg ||
+                lo2 > rb[5] + mg)
+                continue;
+            const float sx = (x0f - rc[0]) * rc[9] + (x1f - rc[1]) * rc[10] + (x2f - rc[2]) * rc[11];
+            const float sy = (y0f - rc[0]) * rc[9] + (y1f - rc[1]) * rc[10] + (y2f - rc[2]) * rc[11];
+            const float dl = mg * sc->rnorm[k];
+            if ((sx > dl && sy > dl) || (sx < -dl && sy < -dl)) continue;
+        }
         double p0 = rc[0], p1 = rc[1], p2 = rc[2];
         double e10 = rc[3], e11 = rc[4], e12 = rc[5];
         double e20 = rc[6], e21 = rc[7], e22 = rc[8];
@@ -91,7 +129,8 @@ __device__ bool visible_d(double x0, double x1, double x2, double l0, double l1,
     return true;
 }
 
-__device__ double entry_T(const float4 *__restrict__ prow, int64_t li, const float4 *__restrict__ vpl, int32_t v)
+__device__ double entry_T(int slot, const float4 *__restrict__ prow, int64_t li,
+                          const float4 *__restrict__ vpl, int32_t v)
 {
     const float4 A = prow[4 * li], B = prow[4 * li + 1], C = prow[4 * li + 2], D = prow[4 * li + 3];
     const float4 P = vpl[2 * (int64_t)v], Q = vpl[2 * (int64_t)v + 1];
@@ -105,7 +144,7 @@ __device__ double entry_T(const float4 *__restrict__ prow, int64_t li, const flo
     double ci = dot3d(n0, n1, n2, l0, l1, l2);
     double cj = -dot3d((double)P.w, (double)Q.x, (double)Q.y, l0, l1, l2);
     if (ci <= 0.0 || cj <= 0.0) return 0.0;
-    double G = (ci * cj) / fmax(dd, c_scene.dc2);
+    double G = (ci * cj) / fmax(dd, c_scenes[slot].dc2);
     double s = C.y;
     double phi;
     if (s == 0.0) {
@@ -117,7 +156,7 @@ __device__ double entry_T(const float4 *__restrict__ prow, int64_t li, const flo
         double lobe = rv > 0.0 ? powi_d(rv, e) : 0.0;
         phi = (1.0 - s) * LMC_INV_PI + (s * (((double)(e + 2)) * LMC_INV_2PI)) * lobe;
     }
-    if (!visible_d(x0, x1, x2, l0, l1, l2, dist)) return 0.0;
+    if (!visible_d(slot, x0, x1, x2, l0, l1, l2, dist, P.x, P.y, P.z)) return 0.0;
     return phi * G;
 }
 
@@ -304,6 +343,28 @@ __global__ void k_pack_vpls(const float *__restrict__ soa, int64_t nv, float4 *v
     vpl[2 * k + 1] = make_float4(soa[4 * nv + k], soa[5 * nv + k], 0.f, 0.f);
 }
 
+static std::mutex g_slot_mu;
+static bool g_slot_used[SCENE_SLOTS];
+
+int acquire_scene_slot()
+{
+    std::lock_guard<std::mutex> lk(g_slot_mu);
+    for (int k = 0; k < SCENE_SLOTS; ++k)
+        if (!g_slot_used[k]) { g_slot_used[k] = true; return k; }
+    return -1;
+}
+
+void release_scene_slot(int slot)
+{
+    std::lock_guard<std::mutex> lk(g_slot_mu);
+    if (slot >= 0 && slot < SCENE_SLOTS) g_slot_used[slot] = false;
+}
+
+cudaError_t upload_scene(int slot, const SceneConst &sc)
+{
+    return cudaMemcpyToSymbol(c_scenes, &sc, sizeof(SceneConst), (size_t)slot * sizeof(SceneConst));
+}
+
 cudaError_t run_pack_vpls(lmc_ctx *c)
 {
     if (c->NV == 0) return cudaSuccess;
@@ -311,7 +372,7 @@ cudaError_t run_pack_vpls(lmc_ctx *c)
     return cudaGetLastError();
 }
 
-cudaError_t upload_scene(const SceneConst &sc) { return cudaMemcpyToSymbol(c_scene, &sc, sizeof(SceneConst)); }
+
 
 cudaError_t slicing_tmp_bytes(int64_t M, int32_t max_tiles, size_t *bytes)
 {
@@ -428,7 +489,7 @@ __device__ int warp_floyd(int m, int n, uint32_t a, int s, uint64_t seed, int la
     return out;
 }
 
-__global__ void __launch_bounds__(256) k_pass1(Upper up, const int32_t *__restrict__ slice_off, int32_t s0, int32_t SL,
+__global__ void __launch_bounds__(256) k_pass1(int slot, Upper up, const int32_t *__restrict__ slice_off, int32_t s0, int32_t SL,
                                                int32_t lbase, const float4 *__restrict__ prow,
                                                const float4 *__restrict__ vpl, uint64_t seed, int nmax,
                                                uint16_t *p1_rows, double *p1_Ta, double *p1_Tb, int32_t *p1_cnt,
@@ -449,8 +510,8 @@ __global__ void __launch_bounds__(256) k_pass1(Upper up, const int32_t *__restri
     int row = warp_floyd(m, n, (uint32_t)up.node[f], s, seed, lane);
     const int64_t o = gw * nmax;
     if (lane < n) {
-        double Ta = entry_T(prow, lrow0 + row, vpl, up.rep[a]);
-        double Tb = entry_T(prow, lrow0 + row, vpl, up.rep[bb]);
+        double Ta = entry_T(slot, prow, lrow0 + row, vpl, up.rep[a]);
+        double Tb = entry_T(slot, prow, lrow0 + row, vpl, up.rep[bb]);
         p1_rows[o + lane] = (uint16_t)row;
         p1_Ta[o + lane] = Ta;
         p1_Tb[o + lane] = Tb;
@@ -466,7 +527,7 @@ cudaError_t run_pass1(lmc_ctx *c)
     if (c->SL == 0 || c->up.nB == 0) return cudaSuccess;
     int64_t warps = (int64_t)c->SL * c->up.nB;
     unsigned blocks = (unsigned)((warps * 32 + 255) / 256);
-    k_pass1<<<blocks, 256, 0, c->stream>>>(c->up, c->d.slice_off, c->s0, c->SL, c->h_slice_off[c->s0], c->d.prow,
+    k_pass1<<<blocks, 256, 0, c->stream>>>(c->scene_slot, c->up, c->d.slice_off, c->s0, c->SL, c->h_slice_off[c->s0], c->d.prow,
                                            c->d.vpl, c->cfg.seed, c->nmax, c->d.p1_rows, c->d.p1_Ta, c->d.p1_Tb,
                                            c->d.p1_cnt, c->d.counters);
     return cudaGetLastError();
@@ -488,7 +549,7 @@ __device__ __forceinline__ double warp_max_d(double v)
 }
 
 __global__ void __launch_bounds__(CO_THREADS) k_coarsen(
-    Upper up, const int32_t *__restrict__ slice_off, int32_t s0, int32_t lbase, const float4 *__restrict__ prow,
+    int slot, Upper up, const int32_t *__restrict__ slice_off, int32_t s0, int32_t lbase, const float4 *__restrict__ prow,
     const float4 *__restrict__ vpl, uint64_t seed, int nmax, double tau, const uint16_t *__restrict__ p1_rows,
     const double *__restrict__ p1_Ta, const double *__restrict__ p1_Tb, const int32_t *__restrict__ p1_cnt,
     uint16_t *pool_rows, double *pool_Ta, double *pool_Tb, int32_t *pool_used, int64_t pool_cap, uint8_t *cs_flags,
@@ -598,8 +659,8 @@ __global__ void __launch_bounds__(CO_THREADS) k_coarsen(
                 __syncwarp();
                 for (int k = lane; k < total; k += 32) {
                     int i = pool_rows[pbase + off + k];
-                    double Ta = entry_T(prow, lrow0 + i, vpl, va);
-                    double Tb = entry_T(prow, lrow0 + i, vpl, vb);
+                    double Ta = entry_T(slot, prow, lrow0 + i, vpl, va);
+                    double Tb = entry_T(slot, prow, lrow0 + i, vpl, vb);
                     pool_Ta[pbase + off + k] = Ta;
                     pool_Tb[pbase + off + k] = Tb;
                     double lr = lum_rho_d(prow, lrow0 + i);
@@ -694,7 +755,7 @@ cudaError_t run_coarsen(lmc_ctx *c)
     cudaError_t e = cudaFuncSetAttribute(k_coarsen, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
     k_coarsen<<<c->SL, CO_THREADS, sm, c->stream>>>(
-        c->up, c->d.slice_off, c->s0, c->h_slice_off[c->s0], c->d.prow, c->d.vpl, c->cfg.seed, c->nmax,
+        c->scene_slot, c->up, c->d.slice_off, c->s0, c->h_slice_off[c->s0], c->d.prow, c->d.vpl, c->cfg.seed, c->nmax,
         c->cfg.coarsen_tau, c->d.p1_rows, c->d.p1_Ta, c->d.p1_Tb, c->d.p1_cnt, c->d.pool_rows, c->d.pool_Ta,
         c->d.pool_Tb, c->d.pool_used, c->pool_cap, c->d.cs_flags, c->d.cs_eps, c->d.cs_cost, c->d.cs_zoff,
         c->d.cs_zlen, c->d.cut_n, c->d.cut_cols, c->d.src_off, c->d.src_len, c->d.src_side, c->G, c->d.counters);
@@ -706,7 +767,9 @@ cudaError_t run_coarsen(lmc_ctx *c)
 // shared memory (m x n <= 2^20 bits).
 // ------------------------------------------------------------------------------------------
 constexpr int P2_THREADS = 1024;
-constexpr unsigned P2_INVALID = 0x1FFFFFu;   // 21-bit sort key sentinel (cells < 2^20)
+constexpr unsigned P2_INVALID = 0xFFFFFFFFu; // empty hash slot / no candidate (cells < 2^20)
+constexpr int P2_HBITS = 11;
+constexpr int P2_HSLOTS = 1 << P2_HBITS;     // 2 x P2_THREADS hash slots
 
 struct P2Args {
     Upper up;
@@ -743,7 +806,6 @@ __device__ __forceinline__ int csr_pos(const uint32_t *bm, const uint16_t *P, co
 __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2(P2Args A)
 {
     extern __shared__ __align__(16) unsigned char smem[];
-    typedef cub::BlockRadixSort<uint32_t, P2_THREADS, 1, int32_t> Sort;
     typedef cub::BlockScan<int32_t, P2_THREADS> ScanI;
     typedef cub::BlockScan<unsigned long long, P2_THREADS> ScanU;
     const int ls = blockIdx.x, s = A.s0 + ls, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -758,10 +820,8 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2(P2Args A)
     unsigned char *phase = (unsigned char *)(colcnt + A.G);
     // phase A
     unsigned long long *cdf = (unsigned long long *)phase;              // G (also holds g as double)
-    int32_t *firstf = (int32_t *)(cdf + A.G);                           // P2_THREADS
-    uint32_t *skeys = (uint32_t *)(firstf + P2_THREADS);                // P2_THREADS
-    unsigned char *tmp = (unsigned char *)(skeys + P2_THREADS);
-    typename Sort::TempStorage &sort_tmp = *reinterpret_cast<typename Sort::TempStorage *>(tmp);
+    uint32_t *hkey = (uint32_t *)(cdf + A.G);                           // P2_HSLOTS
+    uint32_t *hmin = hkey + P2_HSLOTS;                                  // P2_HSLOTS
     __shared__ typename ScanI::TempStorage scani_tmp;
     __shared__ typename ScanU::TempStorage scanu_tmp;
     // phase B
@@ -857,6 +917,7 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2(P2Args A)
     const int64_t N = (int64_t)ceil(((double)((int64_t)m * (int64_t)n)) * A.rate);
     const int64_t cap = 64 * N;
     if (tid == 0) { sh_count = sh_obs; sh_nnew = 0; sh_draws = 0; }
+    for (int e = tid; e < P2_HSLOTS; e += P2_THREADS) { hkey[e] = P2_INVALID; hmin[e] = 0xFFFFFFFFu; }
     __syncthreads();
     // draws: column by the CDF, row uniformly; skip observed entries (R15, R16)
     for (int64_t t0 = 0; t0 < cap; t0 += P2_THREADS) {
@@ -878,16 +939,24 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2(P2Args A)
             cell = i * n + cc;
             if (!(bm[i * W + (cc >> 5)] & (1u << (cc & 31)))) key = (uint32_t)cell;
         }
-        uint32_t k1[1] = {key};
-        int32_t v1[1] = {tid};
-        Sort(sort_tmp).Sort(k1, v1, 0, 21);
-        skeys[tid] = k1[0];
+        // first occurrence of each new cell within the batch: a shared hash table keeps the
+        // smallest draw index per cell (linear probing, 2 x P2_THREADS slots)
+        int slot = -1;
+        if (key != P2_INVALID) {
+            uint32_t h = (key * 2654435761u) >> (32 - P2_HBITS);
+            for (;;) {
+                const uint32_t old = atomicCAS(&hkey[h], P2_INVALID, key);
+                if (old == P2_INVALID || old == key) break;
+                h = (h + 1) & (P2_HSLOTS - 1);
+            }
+            atomicMin(&hmin[h], (uint32_t)tid);
+            slot = (int)h;
+        }
         __syncthreads();
-        bool first = k1[0] != P2_INVALID && (tid == 0 || skeys[tid - 1] != k1[0]);
-        firstf[v1[0]] = first ? 1 : 0;
-        __syncthreads();
-        int acc = firstf[tid], pre, tot;
+        const int acc = (slot >= 0 && hmin[slot] == (uint32_t)tid) ? 1 : 0;
+        int pre, tot;
         ScanI(scani_tmp).ExclusiveSum(acc, pre, tot);
+        for (int e = tid; e < P2_HSLOTS; e += P2_THREADS) { hkey[e] = P2_INVALID; hmin[e] = 0xFFFFFFFFu; }
         const int64_t remaining = N - count;
         const bool accept = acc && pre < remaining;
         if (accept) {
@@ -1006,7 +1075,7 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2(P2Args A)
     }
 }
 
-__global__ void __launch_bounds__(256) k_eval_new(Upper up, const int32_t *__restrict__ slice_off, int32_t s0,
+__global__ void __launch_bounds__(256) k_eval_new(int slot, Upper up, const int32_t *__restrict__ slice_off, int32_t s0,
                                                   int32_t lbase, int G, const float4 *__restrict__ prow,
                                                   const float4 *__restrict__ vpl, const int32_t *__restrict__ cut_n,
                                                   const int32_t *__restrict__ cut_cols, const uint32_t *__restrict__ newcells,
@@ -1021,7 +1090,7 @@ __global__ void __launch_bounds__(256) k_eval_new(Upper up, const int32_t *__res
         uint32_t cell = newcells[ob + k];
         int i = (int)(cell / (uint32_t)n), c = (int)(cell % (uint32_t)n);
         int u = cut_cols[cb + c];
-        double T = entry_T(prow, lrow0 + i, vpl, up.rep[u]);
+        double T = entry_T(slot, prow, lrow0 + i, vpl, up.rep[u]);
         const double v = (lum_rho_d(prow, lrow0 + i) * up.lum[u]) * T;
         val[ob + newpos[ob + k]] = (float)v;
         if (val64) val64[ob + newpos[ob + k]] = v;
@@ -1031,9 +1100,7 @@ __global__ void __launch_bounds__(256) k_eval_new(Upper up, const int32_t *__res
 
 static size_t pass2_smem(int mmax, int G)
 {
-    typedef cub::BlockRadixSort<uint32_t, P2_THREADS, 1, int32_t> Sort;
-    size_t tmp = sizeof(typename Sort::TempStorage);
-    size_t phaseA = (size_t)G * 8 + P2_THREADS * 4 * 2 + tmp;
+    size_t phaseA = (size_t)G * 8 + (size_t)P2_HSLOTS * 4 * 2;
     size_t phaseB = ((((size_t)mmax * 33 + 7) & ~(size_t)7) * 2) + ((size_t)mmax + 1) * 4;
     size_t base = (size_t)mmax * 32 * 4 + (size_t)G * 4;
     return base + (phaseA > phaseB ? phaseA : phaseB) + 64;
@@ -1083,7 +1150,7 @@ cudaError_t run_pass2(lmc_ctx *c)
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     dim3 grid(16, c->SL);
-    k_eval_new<<<grid, 256, 0, c->stream>>>(c->up, c->d.slice_off, c->s0, A.lbase, c->G, c->d.prow, c->d.vpl,
+    k_eval_new<<<grid, 256, 0, c->stream>>>(c->scene_slot, c->up, c->d.slice_off, c->s0, A.lbase, c->G, c->d.prow, c->d.vpl,
                                              c->d.cut_n, c->d.cut_cols, c->d.newcells, c->d.newpos, c->d.n_new,
                                              c->d.val, c->d.val64, c->ncap, c->d.counters);
     return cudaGetLastError();
@@ -1092,14 +1159,14 @@ cudaError_t run_pass2(lmc_ctx *c)
 // ------------------------------------------------------------------------------------------
 // Direct rendering of flagged slices (R25 / non-finite fallback): every entry, fp64 sums
 // ------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_direct(Upper up, const int32_t *__restrict__ slice_off, int32_t s0,
+__global__ void __launch_bounds__(256) k_direct(int slot, Upper up, const int32_t *__restrict__ slice_off, int32_t s0,
                                                 int32_t lbase, int G, const float4 *__restrict__ prow,
                                                 const float4 *__restrict__ vpl, const int32_t *__restrict__ cut_n,
                                                 const int32_t *__restrict__ cut_cols, const int32_t *__restrict__ flags,
                                                 float *direct_rgb)
 {
     const int ls = blockIdx.x, s = s0 + ls;
-    if (!(flags[ls] & LMC_SLICE_DIRECT)) return;
+    if (!(flags[ls] & LMC_SLICE_DIRECT)) return;   // uniform per block
     const int m = slice_off[s + 1] - slice_off[s], n = cut_n[ls];
     const int64_t lrow0 = slice_off[s] - lbase, cb = (int64_t)ls * G;
     for (int i = threadIdx.x; i < m; i += blockDim.x) {
@@ -1108,7 +1175,7 @@ __global__ void __launch_bounds__(256) k_direct(Upper up, const int32_t *__restr
         for (int c = 0; c < n; ++c) {
             int u = cut_cols[cb + c];
             double lI = up.lum[u];
-            double T = entry_T(prow, lrow0 + i, vpl, up.rep[u]);
+            double T = entry_T(slot, prow, lrow0 + i, vpl, up.rep[u]);
             double v = (lr * lI) * T;
             double w0 = lI != 0.0 ? (double)up.I[3 * u + 0] / lI : 0.0;
             double w1 = lI != 0.0 ? (double)up.I[3 * u + 1] / lI : 0.0;
@@ -1130,7 +1197,7 @@ __global__ void __launch_bounds__(256) k_direct(Upper up, const int32_t *__restr
 cudaError_t run_direct(lmc_ctx *c)
 {
     if (c->SL == 0) return cudaSuccess;
-    k_direct<<<c->SL, 256, 0, c->stream>>>(c->up, c->d.slice_off, c->s0, c->h_slice_off[c->s0], c->G, c->d.prow,
+    k_direct<<<c->SL, 256, 0, c->stream>>>(c->scene_slot, c->up, c->d.slice_off, c->s0, c->h_slice_off[c->s0], c->G, c->d.prow,
                                             c->d.vpl, c->d.cut_n, c->d.cut_cols, c->d.flags, c->d.direct_rgb);
     return cudaGetLastError();
 }
@@ -1138,7 +1205,7 @@ cudaError_t run_direct(lmc_ctx *c)
 // ------------------------------------------------------------------------------------------
 // Test hook: T on arbitrary (row, vpl) pairs through the same entry function
 // ------------------------------------------------------------------------------------------
-__global__ void k_eval_pairs(int64_t n, const int32_t *rows, const int32_t *vpls, GView g, const float *vx,
+__global__ void k_eval_pairs(int slot, int64_t n, const int32_t *rows, const int32_t *vpls, GView g, const float *vx,
                              const float *vy, const float *vz, const float *rr, const float *rg, const float *rb,
                              const float *spec, const int32_t *expo, float4 *tmp, const float4 *vpl, double *out)
 {
@@ -1149,7 +1216,7 @@ __global__ void k_eval_pairs(int64_t n, const int32_t *rows, const int32_t *vpls
     tmp[4 * k + 1] = make_float4(g.ny[r], g.nz[r], vx[r], vy[r]);
     tmp[4 * k + 2] = make_float4(vz[r], spec[r], rr[r], rg[r]);
     tmp[4 * k + 3] = make_float4(rb[r], __int_as_float(expo[r]), 0.f, 0.f);
-    out[k] = entry_T(tmp, k, vpl, vpls[k]);
+    out[k] = entry_T(slot, tmp, k, vpl, vpls[k]);
 }
 
 cudaError_t run_eval_entries(lmc_ctx *c, int64_t n, const int32_t *d_rows, const int32_t *d_vpls, double *d_out,
@@ -1158,7 +1225,7 @@ cudaError_t run_eval_entries(lmc_ctx *c, int64_t n, const int32_t *d_rows, const
     if (n == 0) return cudaSuccess;
     GView g = gview(c);
     k_eval_pairs<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(
-        n, d_rows, d_vpls, g, c->d.g[6], c->d.g[7], c->d.g[8], c->d.g[9], c->d.g[10], c->d.g[11], c->d.g[12],
+        c->scene_slot, n, d_rows, d_vpls, g, c->d.g[6], c->d.g[7], c->d.g[8], c->d.g[9], c->d.g[10], c->d.g[11], c->d.g[12],
         c->d.expo, d_tmp_rows, c->d.vpl, d_out);
     return cudaGetLastError();
 }

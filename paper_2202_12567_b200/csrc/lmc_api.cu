@@ -97,6 +97,8 @@ void free_all(lmc_ctx *c)
     if (c->ev_ok)
         for (auto &e : c->ev) cudaEventDestroy(e);
     c->ev_ok = false;
+    release_scene_slot(c->scene_slot);
+    c->scene_slot = -1;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -458,7 +460,19 @@ static lmc_status create_impl(lmc_ctx *c, const lmc_gbuffer *g, const lmc_vpls *
     if (sc->n_sph) memcpy(c->scene.sph, sc->sph, sizeof(float) * 4 * sc->n_sph);
     if (sc->n_box) memcpy(c->scene.box, sc->box, sizeof(float) * 6 * sc->n_box);
     if (sc->n_rect) memcpy(c->scene.rect, sc->rect, sizeof(float) * 12 * sc->n_rect);
-    CK(upload_scene(c->scene), "upload scene");
+    c->scene.margin = (float)(1e-3 * sc->diag);
+    for (int k = 0; k < sc->n_rect; ++k) {   // screening data of the rectangles (not used by exact tests)
+        const float *r = sc->rect + 12 * k;
+        for (int a = 0; a < 3; ++a) {
+            float c0 = r[a], c1 = r[a] + r[3 + a], c2 = r[a] + r[6 + a], c3 = r[a] + r[3 + a] + r[6 + a];
+            c->scene.rbox[6 * k + a] = std::min(std::min(c0, c1), std::min(c2, c3));
+            c->scene.rbox[6 * k + 3 + a] = std::max(std::max(c0, c1), std::max(c2, c3));
+        }
+        c->scene.rnorm[k] = (float)std::sqrt((double)r[9] * r[9] + (double)r[10] * r[10] + (double)r[11] * r[11]);
+    }
+    c->scene_slot = acquire_scene_slot();
+    if (c->scene_slot < 0) return fail(c, LMC_EINVAL, "more than %d live contexts in this process", SCENE_SLOTS);
+    CK(upload_scene(c->scene_slot, c->scene), "upload scene");
     // slicing structure and this rank's share
     lmc_status st = build_levels(c);
     if (st != LMC_OK) return st;

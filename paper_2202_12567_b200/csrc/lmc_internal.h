@@ -12,7 +12,8 @@
 namespace lmc {
 
 constexpr int TAG_P1 = 1, TAG_P2 = 2, TAG_FORCE = 3, TAG_X0 = 4, TAG_Y0 = 5;
-constexpr int MAX_PRIMS = 64;
+constexpr int MAX_PRIMS = 32;
+constexpr int SCENE_SLOTS = 16;   // live contexts per process (one __constant__ scene each)
 constexpr int MAX_Q = 32;
 constexpr int MAX_SLICE = 1024;   // rows per slice (bitmap words per row set = 32)
 constexpr int MAX_CUT = 1024;     // |global cut| (columns per slice)
@@ -23,10 +24,15 @@ struct SceneConst {
     int32_t nsph, nbox, nrect, pad;
     double dc2;        // clamp_dist * clamp_dist
     double eps;        // shadow_eps
+    float margin;      // conservative screening margin (1e-3 D) of the fp32 visibility pre-tests
+    float pad3[3];
     float sph[MAX_PRIMS * 4];
     float box[MAX_PRIMS * 6];
     float rect[MAX_PRIMS * 12];
+    float rbox[MAX_PRIMS * 6];   // bounding boxes of the rectangles (lo3, hi3)
+    float rnorm[MAX_PRIMS];      // |e1 x e2| (scale of the plane-side screen)
 };
+static_assert(sizeof(SceneConst) % 16 == 0, "SceneConst is copied as int4 words");
 
 // Upper light tree: the global cut g and all its ancestors, local ids in ascending node id.
 struct Upper {
@@ -140,6 +146,7 @@ struct lmc_ctx {
     int32_t max_tiles = 0;
     // scene + upper tree
     lmc::SceneConst scene;
+    int scene_slot = -1;           // index into the __constant__ scene table
     lmc::Upper up;
     std::vector<int32_t> h_up_node;   // for getters
     lmc::Dev d;
@@ -154,7 +161,6 @@ struct lmc_ctx {
 
 namespace lmc {
 // exact.cu (fp64 decision precision, compiled with -fmad=false)
-cudaError_t upload_scene(const SceneConst &sc);
 cudaError_t run_slicing(lmc_ctx *c);
 cudaError_t run_pack_rows(lmc_ctx *c);
 cudaError_t run_pass1(lmc_ctx *c);
@@ -165,6 +171,9 @@ cudaError_t run_eval_entries(lmc_ctx *c, int64_t n, const int32_t *d_rows, const
                              float4 *d_tmp_rows);
 cudaError_t slicing_tmp_bytes(int64_t M, int32_t max_tiles, size_t *bytes);
 cudaError_t run_pack_vpls(lmc_ctx *c);
+int acquire_scene_slot();
+void release_scene_slot(int slot);
+cudaError_t upload_scene(int slot, const SceneConst &sc);
 // complete.cu (fp32 completion + resolve)
 cudaError_t run_layout(lmc_ctx *c);
 cudaError_t run_adm(lmc_ctx *c, int nmax);
