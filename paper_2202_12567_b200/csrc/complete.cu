@@ -14,6 +14,8 @@
 // warp-wide load of column ids / values is coalesced and the y_j / x_i gathers are 64-byte
 // contiguous per lane group.
 #include <cub/cub.cuh>
+#include <cstdio>
+#include <cstdlib>
 
 #include "lmc_internal.h"
 #include "philox.cuh"
@@ -69,10 +71,10 @@ struct LArgs {
     const int32_t *slice_off, *cut_n, *rowptr, *colptr, *csc_src, *nnz;
     const uint16_t *col, *csc_row;
     const float *val;
-    int32_t s0, G, mmax, R, P, KAR, KAC;
+    int32_t s0, G, mmax, R, P, D, KAR, KAC, solo_min;
     int64_t ncap, scap;
     uint16_t *r_perm, *r_len, *c_perm, *c_len;
-    int32_t *r_goff, *c_goff, *map;
+    int32_t *r_goff, *c_goff, *map, *c_nsolo;
     unsigned long long *r_ent;
     uint16_t *c_ent;
     float *S;
@@ -83,7 +85,8 @@ constexpr int LT = 1024;
 
 // The entries of the P rows (columns) that share a shared-memory phase of the ADM kernel are
 // scheduled so that at step k member t takes, when it can, an entry whose gathered index has
-// residue (t + k) mod P: the P gathers of a phase then fall into different bank sets.
+// residue (t + k) mod P: the P gathers of a phase then fall into different bank sets.  Member
+// r of a group has t = (r / D) mod P (D = 1: a lane group owns a row).
 __global__ void __launch_bounds__(LT, 1) k_layout(LArgs A)
 {
     typedef cub::BlockRadixSort<uint32_t, LT, 1> Sort;
@@ -134,28 +137,58 @@ __global__ void __launch_bounds__(LT, 1) k_layout(LArgs A)
             lens[rank] = (uint16_t)wlen;
         }
         sh_len[rank] = wlen;
-        __syncthreads();
-        // groups of R, padded to whole cp.async chunks (KA k-steps)
-        const int ng = (cnt + R - 1) / R;
-        const int lgp_t = tid < ng ? ((sh_len[tid * R] + KA - 1) / KA) * KA : 0;
-        int gsz = R * lgp_t;
+        // solo members (columns only): at least one chunk of entries; each gets a group of its own
+        // whose R lane groups split its entries (the longest columns no longer bound the phase)
+        const int solo_min = rows_pass ? (1 << 30) : A.solo_min;
+        const int nsolo = __syncthreads_count(rank < cnt && wlen >= solo_min);
+        if (!rows_pass && tid == 0) A.c_nsolo[ls] = nsolo;
+        // groups: nsolo solo groups, then groups of R members, all padded to whole cp.async chunks
+        const int ng = nsolo + (cnt - nsolo + R - 1) / R;
+        int gsz = 0;
+        if (tid < nsolo) {
+            gsz = ((sh_len[tid] + R * KA - 1) / (R * KA)) * (R * KA);
+        } else if (tid < ng) {
+            gsz = R * (((sh_len[nsolo + (tid - nsolo) * R] + KA - 1) / KA) * KA);
+        }
         int pre, tot;
         Scan(scan_tmp).ExclusiveSum(gsz, pre, tot);
         if (tid < ng) { sh_goff[tid] = pre; goff[tid] = pre; }
         if (tid == 0) { sh_goff[ng] = tot; goff[ng] = tot; }
         if (!rows_pass) dummy = tot;
         __syncthreads();
-        // one thread per member (row / column): its entries are placed blocked by residue of the
-        // gathered index mod P, the blocks in the cyclic order starting at the member's slot t
-        // within its phase set, so the P members of a phase gather different bank sets at
-        // (almost) every step; the rest of the group length is sentinel padding.
         const uint16_t *gidx = rows_pass ? (A.col + ob) : (A.csc_row + ob);   // gathered index per position
-        if (rank < ng * R) {
-            const int g = rank / R, r = rank % R, t = r % P;
-            const int lgp = ((sh_len[g * R] + KA - 1) / KA) * KA;
+        const int own = rank < cnt ? wlen : 0;
+        const int p0 = rank < cnt ? ptr[who] : 0;
+        if (rank < nsolo) {
+            // solo: position p = k R + r is gathered by lane group r; the P lane groups of a
+            // shared-memory phase take residues r mod P when they can
+            const int base = sh_goff[rank], gs = sh_goff[rank + 1] - base;
+            int cntr[8] = {0, 0, 0, 0, 0, 0, 0, 0}, nxt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            for (int k = 0; k < own; ++k) cntr[(int)gidx[p0 + k] % P]++;
+            for (int pos = 0; pos < own; ++pos) {
+                int b = ((pos % R) / A.D) % P;
+                while (cntr[b] == 0) b = (b + 1) % P;
+                cntr[b]--;
+                int k = nxt[b];
+                while ((int)gidx[p0 + k] % P != b) ++k;
+                nxt[b] = k + 1;
+                const int src = p0 + k, idx = base + pos;
+                A.c_ent[sb + idx] = A.csc_row[ob + src];
+                A.map[ob + A.csc_src[ob + src]] = idx;
+                A.S[sb + idx] = 0.f;
+            }
+            for (int pos = own; pos < gs; ++pos) {
+                A.c_ent[sb + base + pos] = (uint16_t)m;   // sentinel: zero row m of X
+                A.S[sb + base + pos] = 0.f;
+            }
+        } else if (rank < nsolo + (ng - nsolo) * R) {
+            // one thread per member (row / column): its entries are placed blocked by residue of
+            // the gathered index mod P, the blocks in the cyclic order starting at the member's
+            // slot t within its phase set, so the P members of a phase gather different bank
+            // sets at (almost) every step; the rest of the group length is sentinel padding.
+            const int g = nsolo + (rank - nsolo) / R, r = (rank - nsolo) % R, t = (r / A.D) % P;
+            const int lgp = (sh_goff[g + 1] - sh_goff[g]) / R;
             const int base = sh_goff[g];
-            const int own = rank < cnt ? wlen : 0;
-            const int p0 = rank < cnt ? ptr[who] : 0;
             int cntr[8] = {0, 0, 0, 0, 0, 0, 0, 0};
             for (int k = 0; k < own; ++k) cntr[(int)gidx[p0 + k] % P]++;
             int start[8];
@@ -209,11 +242,12 @@ struct CArgs {
     const int32_t *cut_n, *nnz;
     const float4 *norm;
     const uint16_t *r_perm, *r_len, *c_perm, *c_len;
-    const int32_t *r_goff, *c_goff;
+    const int32_t *r_goff, *c_goff, *c_nsolo;
     const unsigned long long *r_ent;
     const uint16_t *c_ent;
     float *U, *V, *Lam, *Pi, *Xold, *S, *resid;
     int32_t *flags, *iters;
+    unsigned long long *prof;   // optional phase clocks (LMC_ADM_PROF=1), else null
 };
 
 template <int Q>
@@ -239,6 +273,7 @@ __device__ __forceinline__ int gram_partial(const float *A, const float *B, int 
         for (int x = 0; x < 4; ++x)
 #pragma unroll
             for (int y = 0; y < 4; ++y) acc[x][y] = 0.f;
+#pragma unroll 4
         for (int i = p; i < rows; i += P) {
             const float4 a = *reinterpret_cast<const float4 *>(A + (size_t)i * Q + 4 * ta);
             const float4 b = *reinterpret_cast<const float4 *>(B + (size_t)i * Q + 4 * tb);
@@ -317,8 +352,7 @@ __device__ __forceinline__ float4 group_matvec(float4 t4, const float *Mt, int g
         tt.w = __shfl_sync(FULLM, t4.w, grp_lane0 + sp);
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-            const float4 mrow = *reinterpret_cast<const float4 *>(Mt + (4 * sp + c) * Q + 4 * sub);
-            acc = f4fma(f4get(tt, c), mrow, acc);
+            acc = f4fma(f4get(tt, c), *reinterpret_cast<const float4 *>(Mt + (4 * sp + c) * Q + 4 * sub), acc);
         }
     }
     return acc;
@@ -339,10 +373,10 @@ __device__ __forceinline__ int next_group(int *ctr, int lane)
     return __shfl_sync(FULLM, g, 0);
 }
 
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem)
 {
-    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
@@ -386,7 +420,34 @@ __device__ __forceinline__ float row_residual_ss(const float *X, const float *Y,
     return ss;
 }
 
-template <int Q>
+// phase clocks of the instrumented builds (PROF): PMARK(k) charges the time since the last mark
+// to phase k; PEXIT(k) closes a dynamically scheduled loop (own time -> k - 1, wait for the
+// slowest warp -> k) and is the phase barrier.
+#define PEXIT(k)                                                  \
+    if (PROF) {                                                   \
+        long long pt1;                                            \
+        asm volatile("mov.u64 %0, %%clock64;" : "=l"(pt1)::"memory"); \
+        pacc[k - 1] += (unsigned long long)(pt1 - pt0);           \
+        pt0 = pt1;                                                \
+        if (lane == 0) sh_exit[warp] = pt1;                       \
+        __syncthreads();                                          \
+        long long mx = sh_exit[0];                                \
+        for (int w = 1; w < nwarps; ++w) mx = max(mx, sh_exit[w]); \
+        pacc[k] += (unsigned long long)(mx - pt0);                \
+        __syncthreads();                                          \
+        asm volatile("mov.u64 %0, %%clock64;" : "=l"(pt0)::"memory"); \
+    } else {                                                      \
+        __syncthreads();                                          \
+    }
+#define PMARK(k)                                                  \
+    if (PROF) {                                                   \
+        long long pt1;                                            \
+        asm volatile("mov.u64 %0, %%clock64;" : "=l"(pt1)::"memory"); \
+        pacc[k] += (unsigned long long)(pt1 - pt0);               \
+        pt0 = pt1;                                                \
+    }
+
+template <int Q, bool PROF>
 __global__ void __launch_bounds__(1024, 1) k_adm(CArgs A)
 {
     constexpr int L = Cfg<Q>::L, R = Cfg<Q>::R;
@@ -395,7 +456,11 @@ __global__ void __launch_bounds__(1024, 1) k_adm(CArgs A)
     extern __shared__ __align__(16) float sm[];
     __shared__ float red[33];
     __shared__ int sh_ctr[2];
+    __shared__ unsigned long long sh_prof[8];
+    __shared__ long long sh_exit[32];
     const int ls = blockIdx.x, s = A.s0 + ls, tid = threadIdx.x, NT = blockDim.x;
+    long long pt0 = PROF ? clock64() : 0;
+    unsigned long long pacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     const int lane = tid & 31, warp = tid >> 5, nwarps = NT >> 5;
     const int grp = lane / L, sub = lane % L, lane0 = grp * L;
     const int m = A.slice_off[s + 1] - A.slice_off[s];
@@ -461,7 +526,8 @@ __global__ void __launch_bounds__(1024, 1) k_adm(CArgs A)
     }
     const float al = A.alpha, be = A.beta, ga = A.gamma;
     const float inv_al = 1.0f / al, inv_be = 1.0f / be;
-    const int ngr = (m + R - 1) / R, ngc = (n + R - 1) / R;
+    const int nsolo = A.c_nsolo[ls];
+    const int ngr = (m + R - 1) / R, ngc = nsolo + (n - nsolo + R - 1) / R;
     int it = 0;
     for (; it < A.K; ++it) {
         const float fd = (it == 0) ? 0.f : 1.f;   // Z_0 = P_Omega(M^): no X_0 Y_0 part in step 0
@@ -517,7 +583,7 @@ __global__ void __launch_bounds__(1024, 1) k_adm(CArgs A)
                 *reinterpret_cast<float4 *>(Lg + row * Q + 4 * sub) = ln;
             }
         }
-        __syncthreads();
+        PEXIT(1);
         // ---- (X^T X + bI)^{-1}; warp 0 inverts while the other warps form X_{k+1}^T X_k
         {
             int P = gram_partial<Q>(X, X, m, part, 0, NT);
@@ -525,6 +591,7 @@ __global__ void __launch_bounds__(1024, 1) k_adm(CArgs A)
             gram_reduce<Q>(Dm, part, P);
             if (tid == 0) sh_ctr[0] = 0;
             __syncthreads();
+            PMARK(2);
             if (warp == 0) {
                 inv_spd_warp<Q>(Dm, be);
             } else if (it > 0) {
@@ -538,9 +605,11 @@ __global__ void __launch_bounds__(1024, 1) k_adm(CArgs A)
                 __syncthreads();
             }
         }
+        PMARK(3);
         // ---- column phase: Y_{k+1} = (X^T X + bI)^{-1}(X^T Z_k + b V_k - Pi_k), V/Pi update
         for (int g = next_group(&sh_ctr[1], lane); g < ngc; g = next_group(&sh_ctr[1], lane)) {
-            const int rank = g * R + grp;
+            const bool solo = g < nsolo;                       // warp-uniform
+            const int rank = solo ? g : nsolo + (g - nsolo) * R + grp;
             const bool valid = rank < n;
             const int colj = valid ? cperm[rank] : n;         // n: the zero sentinel column
             const int cb = cgoff[g];
@@ -549,7 +618,6 @@ __global__ void __launch_bounds__(1024, 1) k_adm(CArgs A)
             const char *rg = cent + (size_t)cb * 2;
             const float4 y4 = *reinterpret_cast<const float4 *>(Y + colj * Q + 4 * sub);
             float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-            acc = group_matvec<Q>(make_float4(fd * y4.x, fd * y4.y, fd * y4.z, fd * y4.w), Cm, lane0, sub, acc);
             cp_async16(slot0 + lane * 16, sg + lane * 16);
             if (lane < 16) cp_async16(slot0 + 512 + lane * 16, rg + lane * 16);
             cp_commit();
@@ -573,6 +641,16 @@ __global__ void __launch_bounds__(1024, 1) k_adm(CArgs A)
                 }
                 __syncwarp();
             }
+            if (solo) {   // the R lane groups hold partial sums of one column
+#pragma unroll
+                for (int o = L; o < 32; o <<= 1) {
+                    acc.x += __shfl_xor_sync(FULLM, acc.x, o);
+                    acc.y += __shfl_xor_sync(FULLM, acc.y, o);
+                    acc.z += __shfl_xor_sync(FULLM, acc.z, o);
+                    acc.w += __shfl_xor_sync(FULLM, acc.w, o);
+                }
+            }
+            acc = group_matvec<Q>(make_float4(fd * y4.x, fd * y4.y, fd * y4.z, fd * y4.w), Cm, lane0, sub, acc);
             const float4 v4 = *reinterpret_cast<const float4 *>(Vg + colj * Q + 4 * sub);
             const float4 p4 = *reinterpret_cast<const float4 *>(Pg + colj * Q + 4 * sub);
             float4 t4;
@@ -586,22 +664,24 @@ __global__ void __launch_bounds__(1024, 1) k_adm(CArgs A)
             vn.y = fmaxf(0.f, yn.y + p4.y * inv_be); pn.y = p4.y + ga * be * (yn.y - vn.y);
             vn.z = fmaxf(0.f, yn.z + p4.z * inv_be); pn.z = p4.z + ga * be * (yn.z - vn.z);
             vn.w = fmaxf(0.f, yn.w + p4.w * inv_be); pn.w = p4.w + ga * be * (yn.w - vn.w);
-            if (valid) {
+            if (valid && (!solo || grp == 0)) {
                 *reinterpret_cast<float4 *>(Y + colj * Q + 4 * sub) = yn;
                 *reinterpret_cast<float4 *>(Vg + colj * Q + 4 * sub) = vn;
                 *reinterpret_cast<float4 *>(Pg + colj * Q + 4 * sub) = pn;
             }
         }
-        __syncthreads();
+        PEXIT(5);
         {
             const int P = gram_partial<Q>(Y, Y, n, part, 0, NT);
             __syncthreads();
             gram_reduce<Q>(Bm, part, P);
             if (tid == 0) sh_ctr[1] = 0;
             __syncthreads();
+            PMARK(6);
             if (warp == 0) inv_spd_warp<Q>(Bm, al);
             __syncthreads();
         }
+        PMARK(7);
         if (A.tol > 0.f) {   // r_{k+1} = ||P_Omega(M^ - X_{k+1} Y_{k+1})|| / ||P_Omega M^|| (R21)
             const float ss = block_reduce<false>(row_residual_ss<Q>(X, Y, A, ls, m, warp, nwarps, lane), red);
             if (!(ss == ss) || isinf(ss) || sqrtf(ss / nrmM2) < A.tol) { ++it; break; }
@@ -610,6 +690,14 @@ __global__ void __launch_bounds__(1024, 1) k_adm(CArgs A)
     const float ss = block_reduce<false>(row_residual_ss<Q>(X, Y, A, ls, m, warp, nwarps, lane), red);
     const float res = sqrtf(ss / nrmM2);
     for (int e = tid; e < n * Q; e += NT) Vg[e] *= sigma;   // R22: output (U_K, sigma V_K)
+    if (PROF) {
+        if (tid < 8) sh_prof[tid] = 0;
+        __syncthreads();
+        if (lane == 0)
+            for (int k = 0; k < 8; ++k) atomicAdd(&sh_prof[k], pacc[k]);
+        __syncthreads();
+        if (tid < 8) atomicAdd(&A.prof[tid], sh_prof[tid]);
+    }
     if (tid == 0) {
         const bool bad = !(res == res) || isinf(res);
         A.flags[ls] = bad ? (LMC_SLICE_DIVERGED | LMC_SLICE_DIRECT) : 0;
@@ -652,13 +740,16 @@ cudaError_t run_layout(lmc_ctx *c)
     A.r_goff = c->d.r_goff;
     A.c_goff = c->d.c_goff;
     A.map = c->d.newpos;
+    A.c_nsolo = c->d.c_nsolo;
     A.r_ent = c->d.r_ent;
     A.c_ent = c->d.c_ent;
     A.norm = c->d.norm;
     A.S = c->d.S;
     A.P = c->q >= 32 ? 1 : 32 / c->q;
+    A.D = 1;
     A.KAR = 64 / A.R;      // k-steps per 512-byte chunk of 8-byte row entries
     A.KAC = 128 / A.R;     // k-steps per chunk of 4-byte S (+ 2-byte rows)
+    A.solo_min = A.R * A.KAC;   // columns of at least one chunk get a warp of their own
     const size_t sm = sizeof(typename cub::BlockRadixSort<uint32_t, LT, 1>::TempStorage);
     cudaError_t e = cudaFuncSetAttribute(k_layout, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
@@ -666,14 +757,14 @@ cudaError_t run_layout(lmc_ctx *c)
     return cudaGetLastError();
 }
 
-template <int Q>
+template <int Q, bool PROF = false>
 static cudaError_t launch_adm(lmc_ctx *c, const CArgs &A)
 {
     const size_t sm = adm_smem_bytes(Q, c->mmax, A.nmax);
-    cudaError_t e = cudaFuncSetAttribute(k_adm<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaError_t e = cudaFuncSetAttribute(k_adm<Q, PROF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
     const int nt = 1024;   // 32 warps (64 registers per thread), one CTA per SM
-    k_adm<Q><<<c->SL, nt, sm, c->stream>>>(A);
+    k_adm<Q, PROF><<<c->SL, nt, sm, c->stream>>>(A);
     return cudaGetLastError();
 }
 
@@ -703,6 +794,7 @@ cudaError_t run_adm(lmc_ctx *c, int nmax)
     A.c_len = c->d.c_len;
     A.r_goff = c->d.r_goff;
     A.c_goff = c->d.c_goff;
+    A.c_nsolo = c->d.c_nsolo;
     A.r_ent = c->d.r_ent;
     A.c_ent = c->d.c_ent;
     A.U = c->d.U;
@@ -714,13 +806,35 @@ cudaError_t run_adm(lmc_ctx *c, int nmax)
     A.resid = c->d.resid;
     A.flags = c->d.flags;
     A.iters = c->d.iters;
-    switch (c->q) {
-    case 4: return launch_adm<4>(c, A);
-    case 8: return launch_adm<8>(c, A);
-    case 16: return launch_adm<16>(c, A);
-    case 32: return launch_adm<32>(c, A);
-    default: return cudaErrorInvalidValue;
+    A.prof = nullptr;
+    // LMC_ADM_PROF=1: per-phase clock64 totals (diagnostic only; synchronises and prints to stderr)
+    const char *pe = getenv("LMC_ADM_PROF");
+    const bool prof = pe && pe[0] == '1' && c->q == 16;   // instrumented build for q = 16 only
+    if (prof) {
+        if (cudaMalloc(&A.prof, 8 * sizeof(unsigned long long)) != cudaSuccess) return cudaErrorMemoryAllocation;
+        cudaMemsetAsync(A.prof, 0, 8 * sizeof(unsigned long long), c->stream);
     }
+    cudaError_t e;
+    switch (c->q) {
+    case 4: e = launch_adm<4>(c, A); break;
+    case 8: e = launch_adm<8>(c, A); break;
+    case 16: e = prof ? launch_adm<16, true>(c, A) : launch_adm<16>(c, A); break;
+    case 32: e = launch_adm<32>(c, A); break;
+    default: e = cudaErrorInvalidValue;
+    }
+    if (prof) {
+        unsigned long long h[8] = {0};
+        cudaStreamSynchronize(c->stream);
+        cudaMemcpy(h, A.prof, sizeof h, cudaMemcpyDeviceToHost);
+        cudaFree(A.prof);
+        double t = 0;
+        for (int k = 0; k < 8; ++k) t += (double)h[k];
+        const char *nm[8] = {"row-loop", "row-barrier", "gramX", "inv+Cm", "col-loop", "col-barrier", "gramY", "invB"};
+        fprintf(stderr, "[adm prof] warp-cycles:");
+        for (int k = 0; k < 8; ++k) fprintf(stderr, " %s=%.1f%%", nm[k], 100.0 * (double)h[k] / (t > 0 ? t : 1));
+        fprintf(stderr, "\n");
+    }
+    return e;
 }
 
 // ------------------------------------------------------------------------------------------

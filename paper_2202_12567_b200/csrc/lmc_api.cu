@@ -88,7 +88,7 @@ void free_all(lmc_ctx *c)
                     d.rowptr, d.col, d.val, d.val64, d.carried, d.colptr, d.csc_row, d.csc_src, d.nnz, d.target_n, d.n_new,
                     d.newcells, d.newpos, d.U, d.V, d.Lam, d.Pi, d.Xold, d.S, d.flags, d.iters, d.resid,
                     d.direct_rgb, d.counters, d.img, d.rows_rgb, d.vpl_soa, d.r_perm, d.r_len, d.c_perm, d.c_len,
-                    d.r_goff, d.c_goff, d.r_ent, d.c_ent, d.norm};
+                    d.r_goff, d.c_goff, d.c_nsolo, d.r_ent, d.c_ent, d.norm};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (c->h_stage) cudaFreeHost(c->h_stage);
@@ -563,6 +563,7 @@ static lmc_status create_impl(lmc_ctx *c, const lmc_gbuffer *g, const lmc_vpls *
     CK(dalloc(&d.c_len, SL * G), "alloc layout");
     CK(dalloc(&d.r_goff, SL * (c->mmax + 1)), "alloc layout");
     CK(dalloc(&d.c_goff, SL * (G + 1)), "alloc layout");
+    CK(dalloc(&d.c_nsolo, SL), "alloc layout");
     CK(dalloc(&d.r_ent, SL * c->scap), "alloc layout");
     CK(dalloc(&d.c_ent, SL * c->scap), "alloc layout");
     CK(dalloc(&d.norm, SL), "alloc layout");

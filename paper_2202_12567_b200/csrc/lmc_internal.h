@@ -105,6 +105,7 @@ struct Dev {
     uint16_t *r_perm, *r_len;          // [SL][mmax] rows by (length desc, id)
     uint16_t *c_perm, *c_len;          // [SL][G]
     int32_t *r_goff, *c_goff;          // [SL][mmax+1], [SL][G+1]
+    int32_t *c_nsolo;                  // [SL] leading column groups that hold a single (long) column
     unsigned long long *r_ent;         // [SL][scap] (M^ bits << 32) | (column-layout index << 10) | column
     uint16_t *c_ent;                   // [SL][scap] row of the column-layout entry
     float4 *norm;                      // [SL] sigma, 1/sigma, sum M^, sum M^^2

@@ -12,7 +12,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liblmc.so")
+# LMC_LIB: alternative build of the same library (diagnostic builds); default in-tree
+LIB_PATH = os.environ.get("LMC_LIB") or os.path.join(_HERE, "liblmc.so")
 
 LMC_OK, LMC_EINVAL, LMC_ESTATE, LMC_ENOMEM, LMC_ECUDA, LMC_EOVERFLOW = range(6)
 SOLVER_ADM, SOLVER_MALS = 0, 1

@@ -1,0 +1,35 @@
+"""Per CUDA source line ncu metrics (stall samples, instructions, shared wavefronts), top lines by stalls."""
+import csv
+import io
+import subprocess
+import sys
+
+out = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "source", "--csv", "--print-source", "cuda,sass"],
+                     capture_output=True, text=True).stdout
+rows = list(csv.reader(io.StringIO(out)))
+items = []
+fname, h = "?", None
+for r in rows:
+    if not r:
+        continue
+    if r[0] == "File Path":
+        fname = r[1].split("/")[-1]
+        continue
+    if r[0] == "Line No":
+        h = r
+        si, ii, wi = h.index("Warp Stall Sampling (All Samples)"), h.index("Instructions Executed"), h.index("L1 Wavefronts Shared")
+        continue
+    if h is None or not r[0].isdigit():
+        continue
+
+    def f(i):
+        try:
+            return float(r[i].replace(",", ""))
+        except (ValueError, IndexError):
+            return 0.0
+    items.append((f(si), f(ii), f(wi), fname, int(r[0]), r[1]))
+ts = sum(x[0] for x in items) or 1
+ti = sum(x[1] for x in items) or 1
+n = int(sys.argv[2]) if len(sys.argv) > 2 else 40
+for s, i, w, fn, ln, src in sorted(items, key=lambda x: -x[0])[:n]:
+    print(f"{fn[:12]:12s}:{ln:<4d} stall={100*s/ts:5.1f}% inst={100*i/ti:5.1f}% wf={w:.2e}  {src.strip()[:80]}")
