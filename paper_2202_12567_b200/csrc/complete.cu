@@ -83,10 +83,12 @@ struct LArgs {
 
 constexpr int LT = 1024;
 
+
 // The entries of the P rows (columns) that share a shared-memory phase of the ADM kernel are
 // scheduled so that at step k member t takes, when it can, an entry whose gathered index has
 // residue (t + k) mod P: the P gathers of a phase then fall into different bank sets.  Member
 // r of a group has t = (r / D) mod P (D = 1: a lane group owns a row).
+template <int PP>
 __global__ void __launch_bounds__(LT, 1) k_layout(LArgs A)
 {
     typedef cub::BlockRadixSort<uint32_t, LT, 1> Sort;
@@ -96,8 +98,10 @@ __global__ void __launch_bounds__(LT, 1) k_layout(LArgs A)
     __shared__ typename Scan::TempStorage scan_tmp;
     __shared__ int32_t sh_goff[LT + 1];
     __shared__ int32_t sh_len[LT];
+    __shared__ int32_t sh_who[LT];
     __shared__ float red[33];
-    const int ls = blockIdx.x, s = A.s0 + ls, tid = threadIdx.x, R = A.R, P = A.P;
+    const int ls = blockIdx.x, s = A.s0 + ls, tid = threadIdx.x, R = A.R;
+    constexpr int P = PP;   // residues (bank sets) of a shared-memory phase: 32 / q
     const int m = A.slice_off[s + 1] - A.slice_off[s], n = A.cut_n[ls];
     const int64_t ob = (int64_t)ls * A.ncap, sb = (int64_t)ls * A.scap;
     const int32_t *rp = A.rowptr + (int64_t)ls * (A.mmax + 1);
@@ -137,6 +141,7 @@ __global__ void __launch_bounds__(LT, 1) k_layout(LArgs A)
             lens[rank] = (uint16_t)wlen;
         }
         sh_len[rank] = wlen;
+        sh_who[rank] = who;
         // solo members (columns only): at least one chunk of entries; each gets a group of its own
         // whose R lane groups split its entries (the longest columns no longer bound the phase)
         const int solo_min = rows_pass ? (1 << 30) : A.solo_min;
@@ -157,52 +162,105 @@ __global__ void __launch_bounds__(LT, 1) k_layout(LArgs A)
         if (!rows_pass) dummy = tot;
         __syncthreads();
         const uint16_t *gidx = rows_pass ? (A.col + ob) : (A.csc_row + ob);   // gathered index per position
-        const int own = rank < cnt ? wlen : 0;
-        const int p0 = rank < cnt ? ptr[who] : 0;
-        if (rank < nsolo) {
-            // solo: position p = k R + r is gathered by lane group r; the P lane groups of a
-            // shared-memory phase take residues r mod P when they can
-            const int base = sh_goff[rank], gs = sh_goff[rank + 1] - base;
-            int cntr[8] = {0, 0, 0, 0, 0, 0, 0, 0}, nxt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-            for (int k = 0; k < own; ++k) cntr[(int)gidx[p0 + k] % P]++;
-            for (int pos = 0; pos < own; ++pos) {
-                int b = ((pos % R) / A.D) % P;
-                while (cntr[b] == 0) b = (b + 1) % P;
-                cntr[b]--;
-                int k = nxt[b];
-                while ((int)gidx[p0 + k] % P != b) ++k;
-                nxt[b] = k + 1;
-                const int src = p0 + k, idx = base + pos;
-                A.c_ent[sb + idx] = A.csc_row[ob + src];
-                A.map[ob + A.csc_src[ob + src]] = idx;
-                A.S[sb + idx] = 0.f;
+        // a warp per member (ranks lane-strided over the warps, so the long solo members spread):
+        // residue counts and within-residue ranks come from ballots over 32-entry chunks, and
+        // every entry's position has a closed form, so the member's entries are placed in parallel
+        const int lane = tid & 31, warp = tid >> 5;
+        const unsigned lt_mask = (1u << lane) - 1u;
+        for (int mr = warp; mr < nsolo + (ng - nsolo) * R; mr += LT / 32) {
+            const int mown = mr < cnt ? sh_len[mr] : 0;
+            const int mp0 = mr < cnt ? ptr[sh_who[mr]] : 0;
+            int cntr[P];
+#pragma unroll
+            for (int b2 = 0; b2 < P; ++b2) cntr[b2] = 0;
+            for (int k0 = 0; k0 < mown; k0 += 32) {
+                const int k = k0 + lane;
+                const int res = k < mown ? (int)gidx[mp0 + k] % P : -1;
+#pragma unroll
+                for (int b2 = 0; b2 < P; ++b2)
+                    cntr[b2] += __popc(__ballot_sync(FULLM, res == b2));
             }
-            for (int pos = own; pos < gs; ++pos) {
-                A.c_ent[sb + base + pos] = (uint16_t)m;   // sentinel: zero row m of X
-                A.S[sb + base + pos] = 0.f;
+            const bool solo = mr < nsolo;
+            int base, glen, r = 0, start[P], npos[P], fill[P];
+            if (solo) {
+                // position p wants residue p mod P (lane group p mod R, D = 1); residue b fills
+                // its own positions b, b + P, ... first, the overflow takes the positions left
+                // by residues short of entries (in residue order)
+                base = sh_goff[mr];
+                glen = sh_goff[mr + 1] - base;
+#pragma unroll
+                for (int b2 = 0; b2 < P; ++b2) {
+                    npos[b2] = mown > b2 ? (mown - b2 + P - 1) / P : 0;
+                    fill[b2] = min(cntr[b2], npos[b2]);
+                }
+            } else {
+                const int g = nsolo + (mr - nsolo) / R;
+                r = (mr - nsolo) % R;
+                const int t = (r / A.D) % P;
+                base = sh_goff[g];
+                glen = (sh_goff[g + 1] - base) / R;
+                int acc = 0;
+#pragma unroll
+                for (int b2 = 0; b2 < P; ++b2) {
+                    {
+                        const int res = (t + b2) % P;
+                        int c2 = 0;
+#pragma unroll
+                        for (int b3 = 0; b3 < P; ++b3)
+                            if (b3 == res) c2 = cntr[b3];
+#pragma unroll
+                        for (int b3 = 0; b3 < P; ++b3)
+                            if (b3 == res) start[b3] = acc;
+                        acc += c2;
+                    }
+                }
             }
-        } else if (rank < nsolo + (ng - nsolo) * R) {
-            // one thread per member (row / column): its entries are placed blocked by residue of
-            // the gathered index mod P, the blocks in the cyclic order starting at the member's
-            // slot t within its phase set, so the P members of a phase gather different bank
-            // sets at (almost) every step; the rest of the group length is sentinel padding.
-            const int g = nsolo + (rank - nsolo) / R, r = (rank - nsolo) % R, t = (r / A.D) % P;
-            const int lgp = (sh_goff[g + 1] - sh_goff[g]) / R;
-            const int base = sh_goff[g];
-            int cntr[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-            for (int k = 0; k < own; ++k) cntr[(int)gidx[p0 + k] % P]++;
-            int start[8];
-            int acc = 0;
-            for (int b = 0; b < P; ++b) {
-                const int res = (t + b) % P;
-                start[res] = acc;
-                acc += cntr[res];
-            }
-            for (int k = 0; k < own; ++k) {
-                const int pos = p0 + k;
-                const int res = (int)gidx[pos] % P;
-                const int slot = start[res]++;
-                const int idx = base + slot * R + r;
+            int seen[P];   // entries of each residue in earlier chunks
+#pragma unroll
+            for (int b2 = 0; b2 < P; ++b2) seen[b2] = 0;
+            for (int k0 = 0; k0 < mown; k0 += 32) {
+                const int k = k0 + lane;
+                const bool in = k < mown;
+                const int pos = mp0 + k;
+                const int res = in ? (int)gidx[pos] % P : -1;
+                int j = 0, sres = 0, fres = 0;
+#pragma unroll
+                for (int b2 = 0; b2 < P; ++b2) {
+                    {
+                        const unsigned bm = __ballot_sync(FULLM, res == b2);
+                        if (res == b2) {
+                            j = seen[b2] + __popc(bm & lt_mask);
+                            sres = solo ? 0 : start[b2];
+                            fres = solo ? fill[b2] : 0;
+                        }
+                        seen[b2] += __popc(bm);
+                    }
+                }
+                if (!in) continue;
+                int idx;
+                if (solo) {
+                    int p;
+                    if (j < fres) {
+                        p = P * j + res;
+                    } else {
+                        int o = j - fres;
+#pragma unroll
+                        for (int b2 = 0; b2 < P; ++b2)
+                            if (b2 < res) o += max(0, cntr[b2] - npos[b2]);
+                        p = -1;
+#pragma unroll
+                        for (int b2 = 0; b2 < P; ++b2) {
+                            if (p < 0) {
+                                const int def = npos[b2] - fill[b2];
+                                if (o < def) p = P * (fill[b2] + o) + b2;
+                                else o -= def;
+                            }
+                        }
+                    }
+                    idx = base + p;
+                } else {
+                    idx = base + (sres + j) * R + r;
+                }
                 if (rows_pass) {
                     const float mh = A.val[ob + pos] * inv_sigma;
                     A.r_ent[sb + idx] = ((unsigned long long)__float_as_uint(mh) << 32) |
@@ -213,8 +271,9 @@ __global__ void __launch_bounds__(LT, 1) k_layout(LArgs A)
                     A.S[sb + idx] = 0.f;
                 }
             }
-            for (int k = own; k < lgp; ++k) {
-                const int idx = base + k * R + r;
+            // padding: sentinel entries up to the group length
+            for (int k = mown + lane; k < glen; k += 32) {
+                const int idx = solo ? base + k : base + k * R + r;
                 if (rows_pass) {
                     // sentinel: zero row n of Y, residual parked in the dummy slot
                     A.r_ent[sb + idx] = ((unsigned long long)(uint32_t)dummy << 11) | (unsigned long long)n;
@@ -751,9 +810,10 @@ cudaError_t run_layout(lmc_ctx *c)
     A.KAC = 128 / A.R;     // k-steps per chunk of 4-byte S (+ 2-byte rows)
     A.solo_min = A.R * A.KAC;   // columns of at least one chunk get a warp of their own
     const size_t sm = sizeof(typename cub::BlockRadixSort<uint32_t, LT, 1>::TempStorage);
-    cudaError_t e = cudaFuncSetAttribute(k_layout, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    auto kern = A.P == 8 ? k_layout<8> : A.P == 4 ? k_layout<4> : A.P == 2 ? k_layout<2> : k_layout<1>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
-    k_layout<<<c->SL, LT, sm, c->stream>>>(A);
+    kern<<<c->SL, LT, sm, c->stream>>>(A);
     return cudaGetLastError();
 }
 
