@@ -29,7 +29,16 @@ sys.path.insert(0, ROOT)
 
 METRIC = "ms/frame and lighting-matrix entries completed/s at 1/2/4/8 B200"
 UNIT = "entries/s"
-FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # 74.4: 148 SMs x 128 FP32 lanes x FMA x max clock
+FP32_PEAK_DERIVED = 148 * 128 * 2 * 1.965e9 / 1e12   # 74.4: 148 SMs x 128 FP32 lanes x FMA x max clock
+
+
+def fp32_peak():
+    """Measured FP32 FMA peak (tools/peaks.cu on a B200 of this pool, profiles/r01_peaks.json), else derived."""
+    try:
+        pk = json.load(open(os.path.join(ROOT, "profiles", "r01_peaks.json")))
+        return float(pk["fp32_fma_tflops"]), "measured: tools/peaks.cu FP32 FMA microbenchmark (profiles/r01_peaks.json)"
+    except Exception:
+        return FP32_PEAK_DERIVED, "derived: 148 SMs x 128 FP32 FMA lanes x 2 x 1.965 GHz"
 
 
 def parse():
@@ -213,7 +222,7 @@ def main():
     torch.cuda.synchronize()
     clocks = ClockSampler(local)
     clocks.start()
-    times, ms_complete, stage = [], [], {k: [] for k in ("slices", "pass1", "coarsen", "pass2", "complete", "resolve")}
+    times, solver_ms, stage = [], [], {k: [] for k in ("slices", "pass1", "coarsen", "pass2", "complete", "resolve")}
     launches0 = fr.stats()["launches"]
     for _ in range(args.steps):
         flush.fill_(1.0)                      # flush L2 between timed frames (outside the events)
@@ -230,6 +239,7 @@ def main():
         st = fr.stats()
         for k in stage:
             stage[k].append(st["ms_" + k])
+        solver_ms.append(st["ms_solver"])   # the completion kernel alone (events around its launch)
     cl = clocks.stop()
     launches = fr.stats()["launches"] - launches0
     ms = statistics.mean(times)
@@ -237,8 +247,9 @@ def main():
         t = torch.tensor([ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-        tc = torch.tensor([statistics.mean(stage["complete"])], device=dev, dtype=torch.float64)
+        tc = torch.tensor([statistics.mean(solver_ms)], device=dev, dtype=torch.float64)
         dist.all_reduce(tc, op=dist.ReduceOp.MAX)
+        solver_ms = [float(tc.item())]
     st = fr.stats()
     tot = torch.tensor([st["sum_completed"], st["sum_samples"], st["sum_cols"], st["rows"],
                         st["slice_end"] - st["slice_begin"], st["evals_pass1"] + st["evals_coarsen"] + st["evals_pass2"]],
@@ -247,18 +258,21 @@ def main():
         dist.all_reduce(tot)
     sum_completed, sum_N, sum_n, sum_m, nsl, evals = [float(v) for v in tot.tolist()]
     value = sum_completed / (ms * 1e-3)
-    # roofline of the dominant kernel (completion) from its stage events on the launching stream
-    ms_c = statistics.mean(stage["complete"])
+    # roofline of the dominant kernel (the completion kernel) from CUDA events recorded around its
+    # launch on the launching stream (lmc_stats.ms_solver), averaged over the timed frames
+    ms_c = statistics.mean(solver_ms)
     q = x.cfg.rank_q
     K = x.cfg.max_iter
     fl = (adm_flops if solver == 0 else mals_flops)(q, st["sum_samples"], st["rows"], st["sum_cols"],
                                                      st["slice_end"] - st["slice_begin"], K)
     achieved = fl / (ms_c * 1e-3) / 1e12
-    traffic = None
+    peak, peak_src = fp32_peak()
+    traffic, limiter = None, None
     try:   # DRAM bytes per launch of the dominant kernel from the committed ncu --set full capture
         tj = json.load(open(os.path.join(ROOT, "profiles", "r01_traffic.json")))
         ent = tj.get(f"{args.config}/{args.solver}/q{x.cfg.rank_q}")
         traffic = ent["bytes"] if ent else None
+        limiter = ent.get("limiter") if ent else None
     except Exception:
         traffic = None
     e2e = None
@@ -288,9 +302,9 @@ def main():
         "ms_per_stage": {k: statistics.mean(v) for k, v in stage.items()},
         "completed_entries": sum_completed, "samples": sum_N, "rays_per_pixel": evals / max(sum_m, 1.0),
         "roofline": {"bound": "alu", "kernel": "k_adm" if solver == 0 else "k_mals", "achieved": achieved,
-                     "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP32_PEAK_TFLOPS,
-                     "traffic": traffic, "peak_source": "derived: 148 SMs x 128 FP32 FMA lanes x 2 x 1.965 GHz",
-                     "flops_per_launch": fl},
+                     "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                     "traffic": traffic, "peak_source": peak_src, "flops_per_launch": fl,
+                     "kernel_ms": ms_c, "limiter": limiter},
         "clocks": cl,
         "gpu_launches": launches,
     }

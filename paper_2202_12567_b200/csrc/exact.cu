@@ -129,8 +129,13 @@ __device__ bool visible_d(int slot, double x0, double x1, double x2, double l0, 
     return true;
 }
 
-__device__ double entry_T(int slot, const float4 *__restrict__ prow, int64_t li,
-                          const float4 *__restrict__ vpl, int32_t v)
+// Shading part of T: phi * G, or 0 when the entry is zero without a visibility test; the
+// segment (unit direction l, length dist) the visibility test needs is returned through g.
+struct Seg {
+    double l0, l1, l2, dist;
+};
+__device__ __forceinline__ double entry_shade(int slot, const float4 *__restrict__ prow, int64_t li,
+                                              const float4 *__restrict__ vpl, int32_t v, Seg &g)
 {
     const float4 A = prow[4 * li], B = prow[4 * li + 1], C = prow[4 * li + 2], D = prow[4 * li + 3];
     const float4 P = vpl[2 * (int64_t)v], Q = vpl[2 * (int64_t)v + 1];
@@ -156,8 +161,28 @@ __device__ double entry_T(int slot, const float4 *__restrict__ prow, int64_t li,
         double lobe = rv > 0.0 ? powi_d(rv, e) : 0.0;
         phi = (1.0 - s) * LMC_INV_PI + (s * (((double)(e + 2)) * LMC_INV_2PI)) * lobe;
     }
-    if (!visible_d(slot, x0, x1, x2, l0, l1, l2, dist, P.x, P.y, P.z)) return 0.0;
+    g.l0 = l0;
+    g.l1 = l1;
+    g.l2 = l2;
+    g.dist = dist;
     return phi * G;
+}
+
+__device__ __forceinline__ bool entry_visible(int slot, const float4 *__restrict__ prow, int64_t li,
+                                              const float4 *__restrict__ vpl, int32_t v, const Seg &g)
+{
+    const float4 A = prow[4 * li];
+    const float4 P = vpl[2 * (int64_t)v];
+    return visible_d(slot, A.x, A.y, A.z, g.l0, g.l1, g.l2, g.dist, P.x, P.y, P.z);
+}
+
+__device__ double entry_T(int slot, const float4 *__restrict__ prow, int64_t li,
+                          const float4 *__restrict__ vpl, int32_t v)
+{
+    Seg g;
+    const double pg = entry_shade(slot, prow, li, vpl, v, g);
+    if (pg == 0.0) return 0.0;
+    return entry_visible(slot, prow, li, vpl, v, g) ? pg : 0.0;
 }
 
 __device__ __forceinline__ double lum_rho_d(const float4 *__restrict__ prow, int64_t li)

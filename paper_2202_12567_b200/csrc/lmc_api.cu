@@ -696,7 +696,9 @@ lmc_status lmc_complete(lmc_ctx *c)
     lmc_status s = check_stage(c, 4);
     if (s != LMC_OK) return s;
     if (c->cfg.solver == LMC_SOLVER_MALS) {
+        ev_rec(c, 8);
         CK(run_mals(c), "completion (MALS)");
+        ev_rec(c, 9);
     } else {
         CK(run_layout(c), "Omega layout");
         // shared memory of the ADM kernel is sized by this frame's largest coarsened cut
@@ -704,7 +706,9 @@ lmc_status lmc_complete(lmc_ctx *c)
         CK(cudaMemcpyAsync(&nmx, c->d.counters + 5, sizeof nmx, cudaMemcpyDeviceToHost, c->stream), "read max n");
         CK(cudaStreamSynchronize(c->stream), "sync");
         const int nmax = std::max(1, (int)std::min<unsigned long long>(nmx, (unsigned long long)c->G));
+        ev_rec(c, 8);
         CK(run_adm(c, nmax), "completion (ADM)");
+        ev_rec(c, 9);
         c->launches += c->SL > 0 ? 1 : 0;
     }
     CK(run_direct(c), "direct slices");
@@ -954,6 +958,8 @@ lmc_status lmc_get_stats(lmc_ctx *c, lmc_stats *st)
             float v = 0.f;
             if (cudaEventElapsedTime(&v, c->ev[k], c->ev[k + 1]) == cudaSuccess) *ms[k] = v;
         }
+        float v = 0.f;
+        if (cudaEventElapsedTime(&v, c->ev[8], c->ev[9]) == cudaSuccess) st->ms_solver = v;
         cudaGetLastError();
     }
     return LMC_OK;

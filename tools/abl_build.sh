@@ -4,7 +4,7 @@
 set -e
 cd "$(dirname "$0")/.."
 name=$1; shift
-out=abl/$name; mkdir -p $out
+out=varlib/$name; mkdir -p $out
 B=paper_2202_12567_b200/build
 nvcc -O3 -std=c++17 -lineinfo -gencode arch=compute_100a,code=sm_100a -Xcompiler -fPIC,-ffp-contract=off \
   -I include -I paper_2202_12567_b200/csrc "$@" -c paper_2202_12567_b200/csrc/complete.cu -o $out/complete.o

@@ -4,7 +4,9 @@ import io
 import subprocess
 import sys
 
-out = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "source", "--csv", "--print-source", "cuda,sass"],
+import os
+flt = ["-k", os.environ["NCU_K"]] if os.environ.get("NCU_K") else []
+out = subprocess.run(["ncu", "-i", sys.argv[1], *flt, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 items = []
@@ -17,7 +19,8 @@ for r in rows:
         continue
     if r[0] == "Line No":
         h = r
-        si, ii, wi = h.index("Warp Stall Sampling (All Samples)"), h.index("Instructions Executed"), h.index("L1 Wavefronts Shared")
+        si, ii = h.index("Warp Stall Sampling (All Samples)"), h.index("Instructions Executed")
+        wi = h.index("L1 Wavefronts Shared") if "L1 Wavefronts Shared" in h else si
         continue
     if h is None or not r[0].isdigit():
         continue
