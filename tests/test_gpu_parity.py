@@ -201,6 +201,18 @@ def test_c2_full_size_sampled_slices():
         check_slice(x, fr, img, r)
 
 
+@pytest.mark.slow
+def test_c4_full_size_sampled_slices():
+    """the headline workload (1920x1080, 1M VPLs, 2048 slices, q=16) in the configuration bench.py
+    times: slicing of the whole frame bit-exact, three sampled slices through every stage"""
+    x, fr, img = frame("c4")
+    off, rows = fr.slices()
+    ooff, orows = oracle.Oracle(x).slices()
+    assert np.array_equal(off, ooff) and np.array_equal(rows, orows)
+    for r in oracle_slices(x, pick(off.size - 1, 3)):
+        check_slice(x, fr, img, r)
+
+
 def test_empty_gbuffer():
     """no valid pixel: zero slices, every stage is a no-op, the image is untouched"""
     import dataclasses

@@ -30,7 +30,7 @@ for k in range(frames):
     torch.cuda.synchronize()
     st = fr.stats()
     print(f"frame {k}: {e0.elapsed_time(e1):.2f} ms | " + " ".join(f"{s}={st['ms_'+s]:.2f}" for s in
-          ("slices", "pass1", "coarsen", "pass2", "complete", "resolve")), flush=True)
+          ("slices", "pass1", "coarsen", "pass2", "complete", "resolve", "solver")), flush=True)
 print({k: v for k, v in st.items() if not k.startswith("ms_")})
 print("completed entries/s: %.3e" % (st["sum_completed"] / (e0.elapsed_time(e1) * 1e-3)))
 print("rays/pixel: %.1f" % ((st["evals_pass1"] + st["evals_coarsen"] + st["evals_pass2"]) / st["rows"]))
