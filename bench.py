@@ -181,10 +181,18 @@ def main():
     import scenegen
     from paper_2202_12567_b200 import lmc
 
+    # BENCH_DIST_BACKEND=gloo + BENCH_SAME_DEVICE=1: diagnostic run of the multi-rank path with every
+    # rank on GPU 0 (the production path is NCCL, one rank per GPU)
+    if os.environ.get("BENCH_SAME_DEVICE") == "1":
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     solver = 1 if args.solver == "mals" else 0
     x = scenegen.make_inputs(scenegen.preset(args.config, solver=solver))
     stream = torch.cuda.current_stream(dev)

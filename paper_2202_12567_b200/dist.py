@@ -35,6 +35,9 @@ def gather_rows(tile, counts, group=None):
     mx = max(counts)
     pad = torch.zeros(mx * 3, dtype=tile.dtype, device=tile.device)
     pad[: counts[rank] * 3] = tile.reshape(-1)[: counts[rank] * 3]
+    dev = pad.device
+    if pad.is_cuda and dist.get_backend(group) == "gloo":   # gloo moves host tensors (CPU tests)
+        pad = pad.cpu()
     parts = [torch.empty_like(pad) for _ in range(world)]
     dist.all_gather(parts, pad, group=group)
-    return torch.cat([parts[r][: counts[r] * 3] for r in range(world)]).view(-1, 3)
+    return torch.cat([parts[r][: counts[r] * 3] for r in range(world)]).view(-1, 3).to(dev)

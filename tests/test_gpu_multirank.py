@@ -1,0 +1,87 @@
+"""The slice-sharded multi-rank frame on the GPU: world-size 2 and 3, every rank on
+GPU 0 with the gloo transport (one GPU is available to the tests; the production path is NCCL
+with one rank per GPU).  Each rank runs the CUDA path on its slice range (lmc_config.rank/world),
+packs its rows (lmc_resolve_rows), the tiles are all-gathered and rank 0 scatters them
+(lmc_scatter_rows): the image must equal the single-rank image bit for bit, since a slice's
+computation does not depend on which rank runs it."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no GPU", allow_module_level=True)
+
+import torch.multiprocessing as mp  # noqa: E402
+
+import scenegen  # noqa: E402
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, name, q):
+    import torch.distributed as dist
+
+    from paper_2202_12567_b200 import dist as pdist
+    from paper_2202_12567_b200 import lmc
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    x = scenegen.make_inputs(name)
+    fr = lmc.Frame(x, rank=rank, world=world)
+    fr.build_slices()
+    off, _ = fr.slices()
+    counts = pdist.row_counts(off, world)
+    st = fr.stats()
+    assert st["rows"] == counts[rank]
+    fr.sample_pass1()
+    fr.coarsen_cut()
+    fr.sample_pass2()
+    fr.complete()
+    tile = torch.zeros(counts[rank] * 3, device="cuda")
+    fr.resolve_rows(tile)
+    allrows = pdist.gather_rows(tile, counts)
+    if rank == 0:
+        img = torch.zeros(x.height * x.width * 3, device="cuda")
+        fr.scatter_rows(allrows, img)
+        torch.cuda.synchronize()
+        q.put(img.cpu().numpy())
+    dist.barrier()
+    fr.close()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_frame_equals_single_rank(world):
+    from paper_2202_12567_b200 import lmc
+    name = "t_interior"
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, name, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    x = scenegen.make_inputs(name)
+    fr = lmc.Frame(x)
+    img = torch.zeros(x.height * x.width * 3, device="cuda")
+    fr.run(img)
+    torch.cuda.synchronize()
+    ref = img.cpu().numpy()
+    fr.close()
+    assert np.array_equal(got, ref)
+    assert np.count_nonzero(ref) > 0.5 * ref.size
