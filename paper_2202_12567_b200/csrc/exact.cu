@@ -129,6 +129,137 @@ __device__ bool visible_d(int slot, double x0, double x1, double x2, double l0, 
     return true;
 }
 
+// Visibility with the scene staged in shared memory and the exact tests batched per warp: every
+// lane first runs the fp32 screens of all primitives (uniform loop) and keeps a bitmask of the
+// primitives that need the exact fp64 test; the warp then runs those tests type by type, each lane
+// on its own next primitive, until every lane has a hit or no candidate left.  The decision is the
+// same OR over primitives as visible_d (only the order of the exact tests differs), but the exact
+// tests run with most lanes busy instead of with the few lanes whose screen passed for the
+// primitive of the moment.
+__device__ __forceinline__ bool sphere_hit(const float *s, double x0, double x1, double x2, double l0, double l1, double l2,
+                                           double tmin, double tmax)
+{
+    double o0 = x0 - (double)s[0], o1 = x1 - (double)s[1], o2 = x2 - (double)s[2];
+    double r = s[3];
+    double b = dot3d(o0, o1, o2, l0, l1, l2);
+    double cc = dot3d(o0, o1, o2, o0, o1, o2) - r * r;
+    double disc = b * b - cc;
+    if (disc < 0.0) return false;
+    double sq = sqrt(disc);
+    double t0 = -b - sq, t1 = -b + sq;
+    return (t0 > tmin && t0 < tmax) || (t1 > tmin && t1 < tmax);
+}
+
+__device__ __forceinline__ bool box_hit(const float *bx, double x0, double x1, double x2, double i0, double i1, double i2,
+                                        double tmin, double tmax)
+{
+    double a1 = ((double)bx[0] - x0) * i0, a2 = ((double)bx[3] - x0) * i0;
+    double b1 = ((double)bx[1] - x1) * i1, b2 = ((double)bx[4] - x1) * i1;
+    double e1 = ((double)bx[2] - x2) * i2, e2 = ((double)bx[5] - x2) * i2;
+    double tnear = fmax(fmax(fmin(a1, a2), fmin(b1, b2)), fmin(e1, e2));
+    double tfar = fmin(fmin(fmax(a1, a2), fmax(b1, b2)), fmax(e1, e2));
+    return tnear <= tfar && tfar > tmin && tnear < tmax;
+}
+
+__device__ __forceinline__ bool rect_hit(const float *rc, double x0, double x1, double x2, double l0, double l1, double l2,
+                                         double tmin, double tmax)
+{
+    double p0 = rc[0], p1 = rc[1], p2 = rc[2];
+    double e10 = rc[3], e11 = rc[4], e12 = rc[5];
+    double e20 = rc[6], e21 = rc[7], e22 = rc[8];
+    double n0 = rc[9], n1 = rc[10], n2 = rc[11];
+    double den = dot3d(n0, n1, n2, l0, l1, l2);
+    if (den == 0.0) return false;
+    double t = dot3d(p0 - x0, p1 - x1, p2 - x2, n0, n1, n2) / den;
+    if (!(t > tmin && t < tmax)) return false;
+    double h0 = x0 + t * l0, h1 = x1 + t * l1, h2 = x2 + t * l2;
+    double q0 = h0 - p0, q1 = h1 - p1, q2 = h2 - p2;
+    double a = dot3d(q0, q1, q2, e10, e11, e12) / dot3d(e10, e11, e12, e10, e11, e12);
+    double b = dot3d(q0, q1, q2, e20, e21, e22) / dot3d(e20, e21, e22, e20, e21, e22);
+    return a >= 0.0 && a <= 1.0 && b >= 0.0 && b <= 1.0;
+}
+
+// copy the context's scene into shared memory (all threads of the block; barrier inside)
+__device__ __forceinline__ void stage_scene(SceneConst *dst, int slot)
+{
+    const int4 *src = reinterpret_cast<const int4 *>(&c_scenes[slot]);
+    int4 *d = reinterpret_cast<int4 *>(dst);
+    for (int k = threadIdx.x; k < (int)(sizeof(SceneConst) / 16); k += blockDim.x) d[k] = src[k];
+    __syncthreads();
+}
+
+__device__ bool visible_w(const SceneConst *sc, double x0, double x1, double x2, double l0, double l1, double l2,
+                          double dist, float y0f, float y1f, float y2f)
+{
+    const double tmin = sc->eps, tmax = dist - sc->eps;
+    const float x0f = (float)x0, x1f = (float)x1, x2f = (float)x2;   // exact: the inputs are float32
+    const float mg = sc->margin;
+    const float lo0 = fminf(x0f, y0f), lo1 = fminf(x1f, y1f), lo2 = fminf(x2f, y2f);
+    const float hi0 = fmaxf(x0f, y0f), hi1 = fmaxf(x1f, y1f), hi2 = fmaxf(x2f, y2f);
+    const float w0 = y0f - x0f, w1 = y1f - x1f, w2 = y2f - x2f;
+    const float ww = w0 * w0 + w1 * w1 + w2 * w2;
+    // screens (identical arithmetic to visible_d)
+    uint32_t ms = 0u, mb = 0u, mr = 0u;
+    for (int k = 0; k < sc->nsph; ++k) {
+        const float *s = sc->sph + 4 * k;
+        const float v0 = s[0] - x0f, v1 = s[1] - x1f, v2 = s[2] - x2f;
+        const float tt = fminf(fmaxf((v0 * w0 + v1 * w1 + v2 * w2) / ww, 0.f), 1.f);
+        const float d0 = v0 - tt * w0, d1 = v1 - tt * w1, d2 = v2 - tt * w2;
+        const float rr = s[3] + mg;
+        if (!(d0 * d0 + d1 * d1 + d2 * d2 > rr * rr)) ms |= 1u << k;
+    }
+    for (int k = 0; k < sc->nbox; ++k) {
+        const float *bx = sc->box + 6 * k;
+        if (!(hi0 < bx[0] - mg || lo0 > bx[3] + mg || hi1 < bx[1] - mg || lo1 > bx[4] + mg || hi2 < bx[2] - mg ||
+              lo2 > bx[5] + mg))
+            mb |= 1u << k;
+    }
+    for (int k = 0; k < sc->nrect; ++k) {
+        const float *rc = sc->rect + 12 * k;
+        const float *rb = sc->rbox + 6 * k;
+        if (hi0 < rb[0] - mg || lo0 > rb[3] + mg || hi1 < rb[1] - mg || lo1 > rb[4] + mg || hi2 < rb[2] - mg ||
+            lo2 > rb[5] + mg)
+            continue;
+        const float sx = (x0f - rc[0]) * rc[9] + (x1f - rc[1]) * rc[10] + (x2f - rc[2]) * rc[11];
+        const float sy = (y0f - rc[0]) * rc[9] + (y1f - rc[1]) * rc[10] + (y2f - rc[2]) * rc[11];
+        const float dl = mg * sc->rnorm[k];
+        if ((sx > dl && sy > dl) || (sx < -dl && sy < -dl)) continue;
+        mr |= 1u << k;
+    }
+    // exact tests, batched across the active lanes
+    const unsigned act = __activemask();
+    bool hit = false;
+    while (__any_sync(act, ms != 0u)) {
+        if (ms) {
+            const int k = __ffs(ms) - 1;
+            ms &= ms - 1u;
+            if (sphere_hit(sc->sph + 4 * k, x0, x1, x2, l0, l1, l2, tmin, tmax)) { hit = true; ms = mb = mr = 0u; }
+        }
+    }
+    if (__any_sync(act, mb != 0u)) {
+        const double i0 = 1.0 / l0, i1 = 1.0 / l1, i2 = 1.0 / l2;
+        while (__any_sync(act, mb != 0u)) {
+            if (mb) {
+                const int k = __ffs(mb) - 1;
+                mb &= mb - 1u;
+                if (box_hit(sc->box + 6 * k, x0, x1, x2, i0, i1, i2, tmin, tmax)) { hit = true; mb = mr = 0u; }
+            }
+        }
+    }
+    while (__any_sync(act, mr != 0u)) {
+        if (mr) {
+            const int k = __ffs(mr) - 1;
+            mr &= mr - 1u;
+            if (rect_hit(sc->rect + 12 * k, x0, x1, x2, l0, l1, l2, tmin, tmax)) { hit = true; mr = 0u; }
+        }
+    }
+    return !hit;
+}
+
+// entry T with the warp-batched visibility (sc: the scene staged in shared memory)
+__device__ __forceinline__ double entry_T_w(const SceneConst *sc, int slot, const float4 *__restrict__ prow, int64_t li,
+                                            const float4 *__restrict__ vpl, int32_t v);
+
 // Shading part of T: phi * G, or 0 when the entry is zero without a visibility test; the
 // segment (unit direction l, length dist) the visibility test needs is returned through g.
 struct Seg {
@@ -183,6 +314,19 @@ __device__ double entry_T(int slot, const float4 *__restrict__ prow, int64_t li,
     const double pg = entry_shade(slot, prow, li, vpl, v, g);
     if (pg == 0.0) return 0.0;
     return entry_visible(slot, prow, li, vpl, v, g) ? pg : 0.0;
+}
+
+__device__ __forceinline__ double entry_T_w(const SceneConst *sc, int slot, const float4 *__restrict__ prow, int64_t li,
+                                            const float4 *__restrict__ vpl, int32_t v)
+{
+    Seg g;
+    const double pg = entry_shade(slot, prow, li, vpl, v, g);
+    bool vis = false;
+    // every lane takes part in the batched test (a lane with pg == 0 brings no candidates)
+    const float4 A = prow[4 * li];
+    const float4 P = vpl[2 * (int64_t)v];
+    if (pg != 0.0) vis = visible_w(sc, A.x, A.y, A.z, g.l0, g.l1, g.l2, g.dist, P.x, P.y, P.z);
+    return vis ? pg : 0.0;
 }
 
 __device__ __forceinline__ double lum_rho_d(const float4 *__restrict__ prow, int64_t li)
@@ -520,6 +664,8 @@ __global__ void __launch_bounds__(256) k_pass1(int slot, Upper up, const int32_t
                                                uint16_t *p1_rows, double *p1_Ta, double *p1_Tb, int32_t *p1_cnt,
                                                unsigned long long *counters)
 {
+    __shared__ __align__(16) SceneConst sc;
+    stage_scene(&sc, slot);
     const int lane = threadIdx.x & 31;
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (gw >= (int64_t)SL * up.nB) return;
@@ -534,12 +680,17 @@ __global__ void __launch_bounds__(256) k_pass1(int slot, Upper up, const int32_t
     int n = up.nunc[f] < m ? up.nunc[f] : m;
     int row = warp_floyd(m, n, (uint32_t)up.node[f], s, seed, lane);
     const int64_t o = gw * nmax;
-    if (lane < n) {
-        double Ta = entry_T(slot, prow, lrow0 + row, vpl, up.rep[a]);
-        double Tb = entry_T(slot, prow, lrow0 + row, vpl, up.rep[bb]);
-        p1_rows[o + lane] = (uint16_t)row;
-        p1_Ta[o + lane] = Ta;
-        p1_Tb[o + lane] = Tb;
+    if (lane < n) p1_rows[o + lane] = (uint16_t)row;
+    // the 2n evaluations T(row_j, rep a), T(row_j, rep b) spread over the warp's lanes
+    for (int base = 0; base < 2 * n; base += 32) {
+        const int j = base + lane;
+        const int jr = j < n ? j : j - n;
+        const int rj = __shfl_sync(FULL_MASK, row, jr & 31);
+        if (j < 2 * n) {
+            const double T = entry_T_w(&sc, slot, prow, lrow0 + rj, vpl, j < n ? up.rep[a] : up.rep[bb]);
+            if (j < n) p1_Ta[o + j] = T;
+            else p1_Tb[o + jr] = T;
+        }
     }
     if (lane == 0) {
         p1_cnt[gw] = n;
@@ -1107,6 +1258,8 @@ __global__ void __launch_bounds__(256) k_eval_new(int slot, Upper up, const int3
                                                   const int32_t *__restrict__ newpos, const int32_t *__restrict__ n_new,
                                                   float *val, double *val64, int64_t ncap, unsigned long long *counters)
 {
+    __shared__ __align__(16) SceneConst sc;
+    stage_scene(&sc, slot);
     const int ls = blockIdx.y, s = s0 + ls;
     const int n = cut_n[ls], nn = n_new[ls];
     const int64_t lrow0 = slice_off[s] - lbase;
@@ -1115,7 +1268,7 @@ __global__ void __launch_bounds__(256) k_eval_new(int slot, Upper up, const int3
         uint32_t cell = newcells[ob + k];
         int i = (int)(cell / (uint32_t)n), c = (int)(cell % (uint32_t)n);
         int u = cut_cols[cb + c];
-        double T = entry_T(slot, prow, lrow0 + i, vpl, up.rep[u]);
+        double T = entry_T_w(&sc, slot, prow, lrow0 + i, vpl, up.rep[u]);
         const double v = (lum_rho_d(prow, lrow0 + i) * up.lum[u]) * T;
         val[ob + newpos[ob + k]] = (float)v;
         if (val64) val64[ob + newpos[ob + k]] = v;
