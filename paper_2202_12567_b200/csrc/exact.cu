@@ -943,7 +943,7 @@ cudaError_t run_coarsen(lmc_ctx *c)
 // shared memory (m x n <= 2^20 bits).
 // ------------------------------------------------------------------------------------------
 constexpr int P2_THREADS = 1024;
-constexpr unsigned P2_INVALID = 0xFFFFFFFFu; // empty hash slot / no candidate (cells < 2^20)
+constexpr unsigned P2_INVALID = 0xFFFFFFFFu; // empty hash slot / no candidate (cells < 2^21)
 constexpr int P2_HBITS = 11;
 constexpr int P2_HSLOTS = 1 << P2_HBITS;     // 2 x P2_THREADS hash slots
 
@@ -1007,34 +1007,53 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2(P2Args A)
     __shared__ unsigned long long sh_ured[32];
     __shared__ int sh_ired[32];
     __shared__ int sh_count, sh_obs, sh_nnew, sh_draws;
+    __shared__ int sh_cpre[P2_THREADS];   // per-column prefix offsets (carried entries, CSC)
 
     for (int k = tid; k < m * W; k += P2_THREADS) bm[k] = 0u;
     for (int c = tid; c < n; c += P2_THREADS) colcnt[c] = 0;
     __syncthreads();
-    // carried observations (R13) and light importance g(c) = max C_c - min C_c
+    // carried observations (R13) and light importance g(c) = max C_c - min C_c.
+    // The carried entries of all columns form one flat list (prefix of the per-column counts), so
+    // all threads work on them at once; values are >= +0, so their bit patterns order like the
+    // values and the per-column max / min are integer atomics (order-free: exact).
     double *gcol = (double *)cdf;
+    unsigned long long *chi = (unsigned long long *)cdf;   // per column max (bits), then g
+    unsigned long long *clo = (unsigned long long *)hkey;  // per column min (bits); hash area is free
     int obs_local = 0;
-    for (int c = w; c < n; c += 32) {
-        const int so = A.src_off[cb + c], sl = A.src_len[cb + c], sd = A.src_side[cb + c];
-        const int u = A.cut_cols[cb + c];
-        const double lI = A.up.lum[u];
-        const double *Tv = sd ? A.pool_Tb : A.pool_Ta;
-        double lo = INFINITY, hi = -INFINITY;
-        for (int k = lane; k < sl; k += 32) {
-            int i = A.pool_rows[pb + so + k];
-            double v = (lum_rho_d(A.prow, lrow0 + i) * lI) * Tv[pb + so + k];
-            lo = fmin(lo, v);
-            hi = fmax(hi, v);
+    {
+        const int sl_t = tid < n ? A.src_len[cb + tid] : 0;
+        int pre, tot;
+        ScanI(scani_tmp).ExclusiveSum(sl_t, pre, tot);
+        if (tid < n) {
+            sh_cpre[tid] = pre;
+            colcnt[tid] = sl_t;
+            chi[tid] = 0ull;
+            clo[tid] = 0x7FF0000000000000ull;   // +inf
+        }
+        if (tid == 0) obs_local = tot;
+        __syncthreads();
+        for (int e = tid; e < tot; e += P2_THREADS) {
+            int lo = 0, hi = n - 1;   // last column whose entries start at or before e
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (sh_cpre[mid] <= e) lo = mid; else hi = mid - 1;
+            }
+            const int c = lo, k = e - sh_cpre[c];
+            const int so = A.src_off[cb + c], sd = A.src_side[cb + c];
+            const double lI = A.up.lum[A.cut_cols[cb + c]];
+            const double *Tv = sd ? A.pool_Tb : A.pool_Ta;
+            const int i = A.pool_rows[pb + so + k];
+            const double v = (lum_rho_d(A.prow, lrow0 + i) * lI) * Tv[pb + so + k];
+            const unsigned long long vb = (unsigned long long)__double_as_longlong(v);
+            atomicMax(&chi[c], vb);
+            atomicMin(&clo[c], vb);
             atomicOr(&bm[i * W + (c >> 5)], 1u << (c & 31));
         }
-        for (int o = 16; o > 0; o >>= 1) {
-            lo = fmin(lo, __shfl_xor_sync(FULL_MASK, lo, o));
-            hi = fmax(hi, __shfl_xor_sync(FULL_MASK, hi, o));
-        }
-        if (lane == 0) {
-            colcnt[c] = sl;
-            gcol[c] = sl > 0 ? hi - lo : -1.0;
-            obs_local += sl;
+        __syncthreads();
+        if (tid < n) {
+            const int sl = colcnt[tid];
+            const double hv = __longlong_as_double((long long)chi[tid]), lv = __longlong_as_double((long long)clo[tid]);
+            gcol[tid] = sl > 0 ? hv - lv : -1.0;
         }
     }
     __syncthreads();
@@ -1112,7 +1131,7 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2(P2Args A)
             }
             cc = lo;
             int i = (int)randint_u(u.y, (uint32_t)m);
-            cell = i * n + cc;
+            cell = (i << 11) | cc;   // i < 1024, cc < 2048
             if (!(bm[i * W + (cc >> 5)] & (1u << (cc & 31)))) key = (uint32_t)cell;
         }
         // first occurrence of each new cell within the batch: a shared hash table keeps the
@@ -1136,7 +1155,7 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2(P2Args A)
         const int64_t remaining = N - count;
         const bool accept = acc && pre < remaining;
         if (accept) {
-            atomicOr(&bm[(cell / n) * W + (cc >> 5)], 1u << (cc & 31));
+            atomicOr(&bm[(cell >> 11) * W + (cc >> 5)], 1u << (cc & 31));
             atomicAdd(&colcnt[cc], 1);
             A.newcells[ob + (count - sh_obs) + pre] = (uint32_t)cell;
             if (pre == remaining - 1) sh_draws = (int)(t + 1);
@@ -1152,14 +1171,14 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2(P2Args A)
         if (tid < n && colcnt[tid] == 0) {
             uint4 u = philox4((uint32_t)tid, 0u, (uint32_t)s, TAG_FORCE, A.seed);
             int i = (int)randint_u(u.x, (uint32_t)m);
-            cell = i * n + tid;
+            cell = (i << 11) | tid;
             need = 1;
         }
         int pre, tot;
         ScanI(scani_tmp).ExclusiveSum(need, pre, tot);
         if (need) {
-            int c = cell % n;
-            atomicOr(&bm[(cell / n) * W + (c >> 5)], 1u << (c & 31));
+            int c = cell & 2047;
+            atomicOr(&bm[(cell >> 11) * W + (c >> 5)], 1u << (c & 31));
             colcnt[c] = 1;
             A.newcells[ob + nd + pre] = (uint32_t)cell;
         }
@@ -1209,27 +1228,51 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2(P2Args A)
     int32_t *gcp = A.colptr + (int64_t)ls * (A.G + 1);
     if (tid < n) gcp[tid] = cpre;
     if (tid == 0) gcp[n] = ctot;
-    if (tid < n) {
-        int k = cpre;
-        const int wi = tid >> 5;
-        const uint32_t bit = 1u << (tid & 31);
-        for (int i = 0; i < m; ++i) {
-            if (bm[i * W + wi] & bit) {
+    sh_cpre[tid] = cpre;
+    __syncthreads();
+    // a warp per 32-column strip: 32x32 bit blocks of the row-major bitmap are transposed with
+    // ballots, lane b then walks the rows of column 32 wi + b in ascending order
+    for (int wi = w; wi < W; wi += 32) {
+        const int c = wi * 32 + lane;
+        int k = c < n ? sh_cpre[c] : 0;
+        for (int r0 = 0; r0 < m; r0 += 32) {
+            const uint32_t word = r0 + lane < m ? bm[(r0 + lane) * W + wi] : 0u;
+            uint32_t colw = 0u;   // rows r0..r0+31 of column c
+#pragma unroll
+            for (int b = 0; b < 32; ++b) {
+                const uint32_t bal = __ballot_sync(FULL_MASK, (word >> b) & 1u);
+                if (lane == b) colw = bal;
+            }
+            while (colw) {
+                const int i = r0 + __ffs(colw) - 1;
+                colw &= colw - 1u;
                 A.csc_row[ob + k] = (uint16_t)i;
-                A.csc_src[ob + k] = csr_pos(bm, P, rp, W, i, tid);
+                A.csc_src[ob + k] = csr_pos(bm, P, rp, W, i, c);
                 ++k;
             }
         }
     }
-    // carried values at their CSR positions
-    for (int c = w; c < n; c += 32) {
-        const int so = A.src_off[cb + c], sl = A.src_len[cb + c], sd = A.src_side[cb + c];
-        const double lI = A.up.lum[A.cut_cols[cb + c]];
-        const double *Tv = sd ? A.pool_Tb : A.pool_Ta;
-        for (int k = lane; k < sl; k += 32) {
-            int i = A.pool_rows[pb + so + k];
-            double v = (lum_rho_d(A.prow, lrow0 + i) * lI) * Tv[pb + so + k];
-            int pos = csr_pos(bm, P, rp, W, i, c);
+    // carried values at their CSR positions (flat list over all columns, as above)
+    {
+        const int sl_t = tid < n ? A.src_len[cb + tid] : 0;
+        int pre, tot;
+        __syncthreads();   // sh_cpre of the CSC pass fully read
+        ScanI(scani_tmp).ExclusiveSum(sl_t, pre, tot);
+        if (tid < n) sh_cpre[tid] = pre;
+        __syncthreads();
+        for (int e = tid; e < tot; e += P2_THREADS) {
+            int lo = 0, hi = n - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (sh_cpre[mid] <= e) lo = mid; else hi = mid - 1;
+            }
+            const int c = lo, k = e - sh_cpre[c];
+            const int so = A.src_off[cb + c], sd = A.src_side[cb + c];
+            const double lI = A.up.lum[A.cut_cols[cb + c]];
+            const double *Tv = sd ? A.pool_Tb : A.pool_Ta;
+            const int i = A.pool_rows[pb + so + k];
+            const double v = (lum_rho_d(A.prow, lrow0 + i) * lI) * Tv[pb + so + k];
+            const int pos = csr_pos(bm, P, rp, W, i, c);
             A.val[ob + pos] = (float)v;
             if (A.val64) A.val64[ob + pos] = v;
             A.carried[ob + pos] = 1;
@@ -1238,7 +1281,7 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2(P2Args A)
     // new entries: CSR positions (values are evaluated by k_eval_new)
     for (int k = tid; k < nnew; k += P2_THREADS) {
         uint32_t cell = A.newcells[ob + k];
-        int i = (int)(cell / (uint32_t)n), c = (int)(cell % (uint32_t)n);
+        int i = (int)(cell >> 11), c = (int)(cell & 2047u);
         int pos = csr_pos(bm, P, rp, W, i, c);
         A.newpos[ob + k] = pos;
         A.carried[ob + pos] = 0;
@@ -1266,7 +1309,7 @@ __global__ void __launch_bounds__(256) k_eval_new(int slot, Upper up, const int3
     const int64_t ob = (int64_t)ls * ncap, cb = (int64_t)ls * G;
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nn; k += gridDim.x * blockDim.x) {
         uint32_t cell = newcells[ob + k];
-        int i = (int)(cell / (uint32_t)n), c = (int)(cell % (uint32_t)n);
+        int i = (int)(cell >> 11), c = (int)(cell & 2047u);
         int u = cut_cols[cb + c];
         double T = entry_T_w(&sc, slot, prow, lrow0 + i, vpl, up.rep[u]);
         const double v = (lum_rho_d(prow, lrow0 + i) * up.lum[u]) * T;

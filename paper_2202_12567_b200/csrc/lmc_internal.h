@@ -98,7 +98,7 @@ struct Dev {
     uint16_t *csc_row;                 // [SL][ncap]
     int32_t *csc_src;                  // [SL][ncap]
     int32_t *nnz, *target_n, *n_new;   // [SL]
-    uint32_t *newcells;                // [SL][ncap] (cell = i*n + c)
+    uint32_t *newcells;                // [SL][ncap] (cell = i << 11 | c)
     int32_t *newpos;                   // [SL][ncap] CSR position of new cell
     // completion
     // sliced-ELL layout of Omega for the completion (k_layout)
