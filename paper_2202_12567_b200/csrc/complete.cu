@@ -450,6 +450,12 @@ __device__ __forceinline__ void st_pred(float *addr, float v, bool p)
 // Omega streaming: each warp double-buffers its group's entries through a 2 x 1 KB ring in shared
 // memory with cp.async (chunk = 512 B of row entries, or 512 B of S + 256 B of rows).
 constexpr int RING_SLOT = 1024;
+#ifndef ADM_COL_CHUNK
+#define ADM_COL_CHUNK 128
+#endif
+// entries per column-phase chunk (4-byte S + 2-byte row each).  64 pads the column groups less
+// (14% -> 7% padding at C4) but measured no faster (more chunk waits)
+constexpr int COL_CHUNK = ADM_COL_CHUNK;
 
 template <int Q>
 __device__ __forceinline__ float row_residual_ss(const float *X, const float *Y, const CArgs &A, int ls, int m,
@@ -511,7 +517,8 @@ __global__ void __launch_bounds__(1024, 1) k_adm(CArgs A)
 {
     constexpr int L = Cfg<Q>::L, R = Cfg<Q>::R;
     constexpr int CKR = 64 / R;                 // row-phase k-steps per 512-byte chunk (8-byte entries)
-    constexpr int CKC = 128 / R;                // column-phase k-steps per chunk (4-byte S + 2-byte rows)
+    constexpr int CKC = COL_CHUNK / R;          // column-phase k-steps per chunk (4-byte S + 2-byte rows)
+    constexpr int SB = COL_CHUNK * 4, RB = COL_CHUNK * 2;   // bytes of S and of rows per chunk
     extern __shared__ __align__(16) float sm[];
     __shared__ float red[33];
     __shared__ int sh_ctr[2];
@@ -526,8 +533,8 @@ __global__ void __launch_bounds__(1024, 1) k_adm(CArgs A)
     const int n = A.cut_n[ls];
     const int64_t lrow0 = A.slice_off[s] - A.lbase;
     const int64_t sb = (int64_t)ls * A.scap, vb = (int64_t)ls * A.G * Q;
-    const uint16_t *rperm = A.r_perm + (int64_t)ls * A.mmax, *rlen = A.r_len + (int64_t)ls * A.mmax;
-    const uint16_t *cperm = A.c_perm + (int64_t)ls * A.G, *clen = A.c_len + (int64_t)ls * A.G;
+    const uint16_t *rperm = A.r_perm + (int64_t)ls * A.mmax;
+    const uint16_t *cperm = A.c_perm + (int64_t)ls * A.G;
     const int32_t *rgoff = A.r_goff + (int64_t)ls * (A.mmax + 1), *cgoff = A.c_goff + (int64_t)ls * (A.G + 1);
     const char *rent = reinterpret_cast<const char *>(A.r_ent + sb);
     const char *cent = reinterpret_cast<const char *>(A.c_ent + sb);
@@ -677,14 +684,14 @@ __global__ void __launch_bounds__(1024, 1) k_adm(CArgs A)
             const char *rg = cent + (size_t)cb * 2;
             const float4 y4 = *reinterpret_cast<const float4 *>(Y + colj * Q + 4 * sub);
             float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-            cp_async16(slot0 + lane * 16, sg + lane * 16);
-            if (lane < 16) cp_async16(slot0 + 512 + lane * 16, rg + lane * 16);
+            if (lane < SB / 16) cp_async16(slot0 + lane * 16, sg + lane * 16);
+            if (lane < RB / 16) cp_async16(slot0 + 512 + lane * 16, rg + lane * 16);
             cp_commit();
             for (int c = 0; c < nch; ++c) {
                 if (c + 1 < nch) {
                     char *nx = slot0 + ((c + 1) & 1) * RING_SLOT;
-                    cp_async16(nx + lane * 16, sg + (c + 1) * 512 + lane * 16);
-                    if (lane < 16) cp_async16(nx + 512 + lane * 16, rg + (c + 1) * 256 + lane * 16);
+                    if (lane < SB / 16) cp_async16(nx + lane * 16, sg + (c + 1) * SB + lane * 16);
+                    if (lane < RB / 16) cp_async16(nx + 512 + lane * 16, rg + (c + 1) * RB + lane * 16);
                 }
                 cp_commit();
                 cp_wait1();
@@ -807,8 +814,9 @@ cudaError_t run_layout(lmc_ctx *c)
     A.P = c->q >= 32 ? 1 : 32 / c->q;
     A.D = 1;
     A.KAR = 64 / A.R;      // k-steps per 512-byte chunk of 8-byte row entries
-    A.KAC = 128 / A.R;     // k-steps per chunk of 4-byte S (+ 2-byte rows)
-    A.solo_min = A.R * A.KAC;   // columns of at least one chunk get a warp of their own
+    A.KAC = COL_CHUNK / A.R;   // k-steps per chunk of 4-byte S (+ 2-byte rows)
+    A.solo_min = 128;      // columns of >= 128 entries get a warp of their own (a solo column pays the
+                           // whole warp's update, so the threshold stays well above a group's share)
     const size_t sm = sizeof(typename cub::BlockRadixSort<uint32_t, LT, 1>::TempStorage);
     auto kern = A.P == 8 ? k_layout<8> : A.P == 4 ? k_layout<4> : A.P == 2 ? k_layout<2> : k_layout<1>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
