@@ -85,7 +85,7 @@ void free_all(lmc_ctx *c)
                     d.keys_alt, d.keys_sorted, d.sl_i32, d.lvl_begin, d.lvl_end, d.lvl_slot, d.lvl_work, d.ext, d.slice_off, d.cub_tmp, d.prow,
                     d.p1_rows, d.p1_Ta, d.p1_Tb, d.p1_cnt, d.pool_rows, d.pool_Ta, d.pool_Tb, d.pool_used, d.cs_flags,
                     d.cs_eps, d.cs_cost, d.cs_zoff, d.cs_zlen, d.cut_n, d.cut_cols, d.src_off, d.src_len, d.src_side,
-                    d.rowptr, d.col, d.val, d.val64, d.carried, d.colptr, d.csc_row, d.csc_src, d.nnz, d.target_n, d.n_new,
+                    d.rowptr, d.col, d.val, d.val64, d.Xd, d.Yd, d.val64c, d.carried, d.colptr, d.csc_row, d.csc_src, d.nnz, d.target_n, d.n_new,
                     d.newcells, d.newpos, d.U, d.V, d.Lam, d.Pi, d.Xold, d.S, d.flags, d.iters, d.resid,
                     d.direct_rgb, d.counters, d.img, d.rows_rgb, d.vpl_soa, d.r_perm, d.r_len, d.c_perm, d.c_len,
                     d.r_goff, d.c_goff, d.c_nsolo, d.r_ent, d.c_ent, d.norm};
@@ -541,7 +541,12 @@ static lmc_status create_impl(lmc_ctx *c, const lmc_gbuffer *g, const lmc_vpls *
     CK(dalloc(&d.rowptr, SL * (c->mmax + 1)), "alloc pass2");
     CK(dalloc(&d.col, SL * c->ncap), "alloc pass2");
     CK(dalloc(&d.val, SL * c->ncap), "alloc pass2");
-    if (cfg.solver == LMC_SOLVER_MALS) CK(dalloc(&d.val64, SL * c->ncap), "alloc pass2");
+    if (cfg.solver == LMC_SOLVER_MALS) {
+        CK(dalloc(&d.val64, SL * c->ncap), "alloc pass2");
+        CK(dalloc(&d.Xd, ML * c->q), "alloc MALS factors");
+        CK(dalloc(&d.val64c, SL * c->ncap), "alloc MALS values");
+        CK(dalloc(&d.Yd, SL * G * c->q), "alloc MALS factors");
+    }
     CK(dalloc(&d.carried, SL * c->ncap), "alloc pass2");
     CK(dalloc(&d.colptr, SL * (G + 1)), "alloc pass2");
     CK(dalloc(&d.csc_row, SL * c->ncap), "alloc pass2");

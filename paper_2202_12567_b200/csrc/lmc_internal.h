@@ -93,6 +93,8 @@ struct Dev {
     uint16_t *col;                     // [SL][ncap]
     float *val;                        // [SL][ncap]
     double *val64;                     // [SL][ncap] (MALS only)
+    double *Xd, *Yd;                   // MALS fp64 factors [ML][q], [SL][G][q] (MALS only)
+    double *val64c;                    // [SL][ncap] values in CSC order (MALS only)
     uint8_t *carried;                  // [SL][ncap]
     int32_t *colptr;                   // [SL][G+1]
     uint16_t *csc_row;                 // [SL][ncap]

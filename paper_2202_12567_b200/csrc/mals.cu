@@ -8,7 +8,11 @@
 // solved in fp64 (B200 runs fp64 FMA at half the fp32 rate).  One CTA per slice, X and Y in
 // shared memory as fp64; each q x q system is owned by a group of q lanes, lane l holding row
 // l of [A | b]; the solve is Gauss-Jordan without pivoting (A is SPD), pivot rows broadcast by
-// shuffles.
+// shuffles.  Only the operand of the current half-step (Y for the row half, X for the column half)
+// is gathered, so only it lives in shared memory (fp64, (max(m, n) + 1) x q: 131 KB at C4); both
+// factors are kept in fp64 in global memory and the operand is reloaded at each half-step.
+#include <algorithm>
+
 #include "lmc_internal.h"
 #include "philox.cuh"
 
@@ -24,11 +28,27 @@ struct MArgs {
     const int32_t *cut_n, *rowptr, *colptr, *csc_src, *nnz;
     const uint16_t *col, *csc_row;
     const double *val;             // fp64 entry values (the fp32 copy would perturb MALS, R34)
+    double *valc;                  // the same values in CSC order (filled per slice at start)
     float *U, *V, *resid;
+    double *Xd, *Yd;               // fp64 factors [rows][q], [slice][G][q]
+    int32_t fmax;                  // rows of the operand buffer in shared memory (max(mmax, G))
     int32_t *flags, *iters;
 };
 
 constexpr int MT = 256;
+// threads per CTA: q = 16 runs the tensor-core accumulation (few registers) with 16 warps
+template <int Q>
+struct MCfg {
+    static constexpr int NT = Q == 16 ? 512 : MT;
+};
+// operand layout in shared memory: at q = 16 the two 64-byte halves of odd rows are swapped, so the
+// four rows a tensor-core fragment load touches fall into both bank halves
+template <int Q>
+__device__ __forceinline__ int fidx(int r, int c)
+{
+    if constexpr (Q == 16) return r * 16 + (c ^ ((r & 1) << 3));
+    return r * Q + c;
+}
 
 __device__ __forceinline__ double dwarp_sum(double v)
 {
@@ -84,13 +104,78 @@ __device__ __forceinline__ double solve_group(double (&a)[Q], double b, int l, i
     return b;
 }
 
+// ---- q = 16: normal equations on the fp64 tensor cores ------------------------------------
+// mma.sync m8n8k4 f64 (g = lane/4, t = lane%4): A (8x4) a0 = A[g][t]; B (4x8) b0 = B[t][g];
+// C (8x8) c0, c1 = C[g][2t], C[g][2t+1].  For a system with samples k (gathered operand rows
+// f_k): sum_k f_k f_k^T = F^T F and sum_k m_k f_k = F^T m are products with K = 4 samples per
+// instruction; lane (g, t) loads f_t[g] and f_t[8 + g], which serve as both the A fragment (rows
+// 8mt + g of F^T) and the B fragment (columns 8nt + g of F).  Exact fp64 products and sums
+// (only the summation order differs from a sample-by-sample loop).
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b)
+{
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d[0]), "+d"(d[1])
+                 : "d"(a), "d"(b));
+}
+
+// accumulate [F^T F | F^T m] of one system (samples [p0, p1)) into the warp's scratch (16 x 17,
+// row-major); `half` selects CSR (row system) or CSC (column system) indexing
+__device__ __forceinline__ void accumulate_tc(const double *F, int nf, const MArgs &A, int64_t ob, int half, int p0,
+                                              int p1, double inv_sigma, double *scr)
+{
+    const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+    double c00[2] = {0.0, 0.0}, c01[2] = {0.0, 0.0}, c10[2] = {0.0, 0.0}, c11[2] = {0.0, 0.0};
+    double cb0[2] = {0.0, 0.0}, cb1[2] = {0.0, 0.0};
+    // the sample (index, value) of the next 4-sample step is loaded one step ahead
+    auto fetch = [&](int pp, int &other, double &v) {
+        other = nf;   // zero row: padding samples add nothing
+        v = 0.0;
+        if (pp < p1) {
+            if (half == 0) {
+                other = A.col[ob + pp];
+                v = A.val[ob + pp];
+            } else {
+                other = A.csc_row[ob + pp];
+                v = A.valc[ob + pp];
+            }
+        }
+    };
+    int oc;
+    double vc;
+    fetch(p0 + t, oc, vc);
+    for (int p = p0; p < p1; p += 4) {
+        int on;
+        double vn;
+        fetch(p + 4 + t, on, vn);
+        const double f0 = F[fidx<16>(oc, g)], f1 = F[fidx<16>(oc, 8 + g)];
+        const double bm = g == 0 ? vc * inv_sigma : 0.0;
+        dmma(c00, f0, f0);
+        dmma(c01, f0, f1);
+        dmma(c10, f1, f0);
+        dmma(c11, f1, f1);
+        dmma(cb0, f0, bm);
+        dmma(cb1, f1, bm);
+        oc = on;
+        vc = vn;
+    }
+    double *r0 = scr + (size_t)g * 17, *r1 = scr + (size_t)(8 + g) * 17;
+    r0[2 * t] = c00[0]; r0[2 * t + 1] = c00[1];
+    r0[8 + 2 * t] = c01[0]; r0[8 + 2 * t + 1] = c01[1];
+    r1[2 * t] = c10[0]; r1[2 * t + 1] = c10[1];
+    r1[8 + 2 * t] = c11[0]; r1[8 + 2 * t + 1] = c11[1];
+    if (t == 0) {
+        r0[16] = cb0[0];
+        r1[16] = cb1[0];
+    }
+}
+
 template <int Q>
-__global__ void __launch_bounds__(MT, 1) k_mals(MArgs A)
+__global__ void __launch_bounds__(MCfg<Q>::NT, 1) k_mals(MArgs A)
 {
     extern __shared__ __align__(16) double dsm[];
     __shared__ double red[33];
     const int ls = blockIdx.x, s = A.s0 + ls, tid = threadIdx.x;
-    const int lane = tid & 31, warp = tid >> 5, nwarps = MT >> 5;
+    const int lane = tid & 31, warp = tid >> 5, nwarps = MCfg<Q>::NT >> 5;
     constexpr int GPW = 32 / Q;                  // systems per warp
     const int gi = lane / Q, l = lane % Q, lane0 = gi * Q;
     const int m = A.slice_off[s + 1] - A.slice_off[s];
@@ -100,24 +185,25 @@ __global__ void __launch_bounds__(MT, 1) k_mals(MArgs A)
     const int32_t *rp = A.rowptr + (int64_t)ls * (A.mmax + 1);
     const int32_t *cp = A.colptr + (int64_t)ls * (A.G + 1);
     const int nnz = A.nnz[ls];
-    double *X = dsm;
-    double *Y = X + (size_t)A.mmax * Q;
+    double *F = dsm;                              // operand of the current half-step
+    double *Xg = A.Xd + lrow0 * Q, *Yg = A.Yd + vb;
     float *Ug = A.U + lrow0 * Q, *Vg = A.V + vb;
     if (m <= Q || n <= Q) {
         if (tid == 0) { A.flags[ls] = LMC_SLICE_DIRECT; A.iters[ls] = 0; A.resid[ls] = 0.f; }
         return;
     }
     double mx = 0.0;
-    for (int k = tid; k < nnz; k += MT) mx = fmax(mx, A.val[ob + k]);
+    for (int k = tid; k < nnz; k += MCfg<Q>::NT) mx = fmax(mx, A.val[ob + k]);
     const double sigma = dblock_reduce<true>(mx, red);
     if (sigma == 0.0) {
-        for (int k = tid; k < m * Q; k += MT) Ug[k] = 0.f;
-        for (int k = tid; k < n * Q; k += MT) Vg[k] = 0.f;
+        for (int k = tid; k < m * Q; k += MCfg<Q>::NT) Ug[k] = 0.f;
+        for (int k = tid; k < n * Q; k += MCfg<Q>::NT) Vg[k] = 0.f;
         if (tid == 0) { A.flags[ls] = LMC_SLICE_ZERO; A.iters[ls] = 0; A.resid[ls] = 0.f; }
         return;
     }
+    for (int k = tid; k < nnz; k += MCfg<Q>::NT) A.valc[ob + k] = A.val[ob + A.csc_src[ob + k]];
     double sum = 0.0, sq = 0.0;
-    for (int k = tid; k < nnz; k += MT) {
+    for (int k = tid; k < nnz; k += MCfg<Q>::NT) {
         const double v = A.val[ob + k] / sigma;
         sum += v;
         sq = fma(v, v, sq);
@@ -125,18 +211,47 @@ __global__ void __launch_bounds__(MT, 1) k_mals(MArgs A)
     sum = dblock_reduce<false>(sum, red);
     const double nrmM2 = dblock_reduce<false>(sq, red);
     const double c0 = 2.0 * sqrt((sum / (double)nnz) / (double)Q);
-    for (int e = tid; e < m * Q; e += MT)
-        X[e] = c0 * (double)unif_f(philox4((uint32_t)(e / Q), (uint32_t)(e % Q), (uint32_t)s, TAG_X0, A.seed).x);
-    for (int e = tid; e < n * Q; e += MT)
-        Y[e] = c0 * (double)unif_f(philox4((uint32_t)(e % Q), (uint32_t)(e / Q), (uint32_t)s, TAG_Y0, A.seed).x);
+    for (int e = tid; e < m * Q; e += MCfg<Q>::NT)
+        Xg[e] = c0 * (double)unif_f(philox4((uint32_t)(e / Q), (uint32_t)(e % Q), (uint32_t)s, TAG_X0, A.seed).x);
+    for (int e = tid; e < n * Q; e += MCfg<Q>::NT)
+        Yg[e] = c0 * (double)unif_f(philox4((uint32_t)(e % Q), (uint32_t)(e / Q), (uint32_t)s, TAG_Y0, A.seed).x);
     __syncthreads();
     const double lam = A.lambda;
     for (int it = 0; it < A.K; ++it) {
         for (int half = 0; half < 2; ++half) {
-            const int nsys = half == 0 ? m : n;
+            const int nsys = half == 0 ? m : n, nf = half == 0 ? n : m;
             const int32_t *ptr = half == 0 ? rp : cp;
-            const double *F = half == 0 ? Y : X;     // operand gathered per sample
-            double *O = half == 0 ? X : Y;           // unknowns solved for
+            const double *src = half == 0 ? Yg : Xg;     // operand gathered per sample
+            double *O = half == 0 ? Xg : Yg;             // unknowns solved for
+            for (int e = tid; e < nf * Q; e += MCfg<Q>::NT) F[fidx<Q>(e / Q, e % Q)] = src[e];
+            for (int e = tid; e < Q; e += MCfg<Q>::NT) F[nf * Q + e] = 0.0;   // zero row for padding samples
+            __syncthreads();
+            if constexpr (Q == 16) {
+                // two systems per warp: tensor-core accumulation one after the other into the
+                // warp's scratch, then one 16-lane Gauss-Jordan solve per system side by side
+                double *scr = F + (size_t)(A.fmax + 1) * Q + (size_t)warp * 2 * 16 * 17;
+                for (int sys0 = warp * 2; sys0 < nsys; sys0 += nwarps * 2) {
+                    for (int h2 = 0; h2 < 2; ++h2) {
+                        const int sy = sys0 + h2;
+                        const int q0 = sy < nsys ? ptr[sy] : 0, q1 = sy < nsys ? ptr[sy + 1] : 0;
+                        accumulate_tc(F, nf, A, ob, half, q0, q1, 1.0 / sigma, scr + h2 * 16 * 17);
+                    }
+                    __syncwarp();
+                    const int sys = sys0 + gi;
+                    double a[Q];
+                    const double *row = scr + gi * 16 * 17 + l * 17;
+#pragma unroll
+                    for (int c = 0; c < Q; ++c) a[c] = row[c];
+                    double b = row[16];
+                    __syncwarp();
+#pragma unroll
+                    for (int c = 0; c < Q; ++c)
+                        if (c == l) a[c] += lam;
+                    const double x = solve_group<Q>(a, b, l, lane0);
+                    if (sys < nsys) O[(size_t)sys * Q + l] = x;
+                }
+                __syncthreads();
+            } else {
             for (int sys0 = warp * GPW; sys0 < nsys; sys0 += nwarps * GPW) {
                 const int sys = sys0 + gi;
                 const bool valid = sys < nsys;
@@ -153,7 +268,7 @@ __global__ void __launch_bounds__(MT, 1) k_mals(MArgs A)
                         v = A.val[ob + p];
                     } else {
                         other = A.csc_row[ob + p];
-                        v = A.val[ob + A.csc_src[ob + p]];
+                        v = A.valc[ob + p];
                     }
                     const double mh = v / sigma;
                     const double *f = F + (size_t)other * Q;
@@ -173,24 +288,25 @@ __global__ void __launch_bounds__(MT, 1) k_mals(MArgs A)
                 if (valid) O[(size_t)sys * Q + l] = x;
             }
             __syncthreads();
+            }
         }
     }
-    // residual on Omega, outputs (X, sigma Y)
+    // after the last column half F holds X: residual on Omega (y from global), outputs (X, sigma Y)
     double ss = 0.0;
-    for (int i = tid; i < m; i += MT) {
+    for (int i = tid; i < m; i += MCfg<Q>::NT) {
         for (int p = rp[i]; p < rp[i + 1]; ++p) {
-            const double *x = X + (size_t)i * Q, *y = Y + (size_t)A.col[ob + p] * Q;
+            const double *y = Yg + (size_t)A.col[ob + p] * Q;
             double d = 0.0;
 #pragma unroll
-            for (int c = 0; c < Q; ++c) d = fma(x[c], y[c], d);
+            for (int c = 0; c < Q; ++c) d = fma(F[fidx<Q>(i, c)], y[c], d);
             const double e = A.val[ob + p] / sigma - d;
             ss = fma(e, e, ss);
         }
     }
     ss = dblock_reduce<false>(ss, red);
     const double res = sqrt(ss / nrmM2);
-    for (int e = tid; e < m * Q; e += MT) Ug[e] = (float)X[e];
-    for (int e = tid; e < n * Q; e += MT) Vg[e] = (float)(sigma * Y[e]);
+    for (int e = tid; e < m * Q; e += MCfg<Q>::NT) Ug[e] = (float)F[fidx<Q>(e / Q, e % Q)];
+    for (int e = tid; e < n * Q; e += MCfg<Q>::NT) Vg[e] = (float)(sigma * Yg[e]);
     if (tid == 0) {
         const bool bad = !(res == res) || isinf(res);
         A.flags[ls] = bad ? (LMC_SLICE_DIVERGED | LMC_SLICE_DIRECT) : 0;
@@ -199,7 +315,12 @@ __global__ void __launch_bounds__(MT, 1) k_mals(MArgs A)
     }
 }
 
-size_t mals_smem_bytes(int q, int mmax, int G) { return ((size_t)mmax + (size_t)G) * q * sizeof(double); }
+size_t mals_smem_bytes(int q, int mmax, int G)
+{
+    // operand (max(m, n) + 1 zero row) x q fp64, plus at q = 16 a 2 x 16 x 17 scratch per warp
+    const size_t scr = q == 16 ? (size_t)(MCfg<16>::NT / 32) * 2 * 16 * 17 * sizeof(double) : 0;
+    return ((size_t)std::max(mmax, G) + 1) * q * sizeof(double) + scr;
+}
 
 template <int Q>
 static cudaError_t launch_mals(lmc_ctx *c, const MArgs &A)
@@ -207,7 +328,7 @@ static cudaError_t launch_mals(lmc_ctx *c, const MArgs &A)
     size_t sm = mals_smem_bytes(Q, c->mmax, c->G);
     cudaError_t e = cudaFuncSetAttribute(k_mals<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
-    k_mals<Q><<<c->SL, MT, sm, c->stream>>>(A);
+    k_mals<Q><<<c->SL, MCfg<Q>::NT, sm, c->stream>>>(A);
     return cudaGetLastError();
 }
 
@@ -235,6 +356,10 @@ cudaError_t run_mals(lmc_ctx *c)
     A.U = c->d.U;
     A.V = c->d.V;
     A.resid = c->d.resid;
+    A.Xd = c->d.Xd;
+    A.Yd = c->d.Yd;
+    A.valc = c->d.val64c;
+    A.fmax = std::max(c->mmax, c->G);
     A.flags = c->d.flags;
     A.iters = c->d.iters;
     switch (c->q) {
