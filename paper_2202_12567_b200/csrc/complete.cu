@@ -316,6 +316,61 @@ struct Cfg {
     static constexpr int PART = 16384;        // floats of Gram partials (the 64 KB ring area)
 };
 
+// ---- q = 16: the q x q products of the updates on the fp64 tensor cores ---------------------
+// mma.sync m8n8k4 f64 (g = lane / 4, t = lane % 4): a0 = A[g][t], b0 = B[t][g], c = C[g][2t..2t+1].
+// A warp step holds 8 rows (g = lane group) x 16 components, lane t holding components 4t..4t+3
+// as a float4.  Taking k-step kk over the components {4t + kk : t = 0..3}, the A fragment is the
+// lane's own component kk (no shuffles); with output column n of half h standing for component
+// 4(n / 2) + 2h + n % 2, lane (g, t) receives components 4t + 2h, 4t + 2h + 1 of row g -- its own
+// float4 again.  The matrix is kept in shared memory in this fragment order (MatFrag16), 8 floats
+// per lane as two float4.  Products and sums are exact fp64 (one rounding to fp32 at the end):
+// 8 DMMA instead of 16 shuffles and 16 16-byte shared loads per warp step.
+#ifndef ADM_TC_MATVEC
+#define ADM_TC_MATVEC 1
+#endif
+__device__ __forceinline__ int frag16(int r, int c)
+{
+    // element (r, c) of the 16 x 16 matrix -> its slot in the fragment-ordered copy
+    const int t = r >> 2, kk = r & 3, g = 2 * (c >> 2) + (c & 1), h = (c >> 1) & 1;
+    return (kk >> 1) * 128 + (4 * g + t) * 4 + (kk & 1) * 2 + h;
+}
+__device__ __forceinline__ void dmma16(double (&d)[2], double a, double b)
+{
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d[0]), "+d"(d[1])
+                 : "d"(a), "d"(b));
+}
+__device__ __forceinline__ float4 matvec_tc16(float4 t4, const float *Mf, float4 acc)
+{
+    const int lane = threadIdx.x & 31;
+    const float4 f0 = reinterpret_cast<const float4 *>(Mf)[lane];        // kk 0, 1 (h 0, 1)
+    const float4 f1 = reinterpret_cast<const float4 *>(Mf + 128)[lane];  // kk 2, 3
+    double c0[2] = {0.0, 0.0}, c1[2] = {0.0, 0.0};
+    dmma16(c0, (double)t4.x, (double)f0.x);
+    dmma16(c1, (double)t4.x, (double)f0.y);
+    dmma16(c0, (double)t4.y, (double)f0.z);
+    dmma16(c1, (double)t4.y, (double)f0.w);
+    dmma16(c0, (double)t4.z, (double)f1.x);
+    dmma16(c1, (double)t4.z, (double)f1.y);
+    dmma16(c0, (double)t4.w, (double)f1.z);
+    dmma16(c1, (double)t4.w, (double)f1.w);
+    acc.x += (float)c0[0];
+    acc.y += (float)c0[1];
+    acc.z += (float)c1[0];
+    acc.w += (float)c1[1];
+    return acc;
+}
+template <int Q>
+struct TcMatvec {
+    static constexpr bool on = Q == 16 && ADM_TC_MATVEC;
+};
+// index of element (r, c) of a q x q matrix consumed by matvec(): fragment order at q = 16
+template <int Q>
+__device__ __forceinline__ int mat_idx(int r, int c)
+{
+    if constexpr (TcMatvec<Q>::on) return frag16(r, c);
+    return r * Q + c;
+}
 // partial Gram sums of out[a][b] = sum_i A[i][a] B[i][b] over threads [t0, t0 + nthr):
 // P = nthr / (Q/4)^2 row partitions, each producing a Q x Q partial in part[p]
 template <int Q>
@@ -350,13 +405,14 @@ __device__ __forceinline__ int gram_partial(const float *A, const float *B, int 
     return P;
 }
 
-template <int Q>
+template <int Q, bool MATVEC_ORDER = false>
 __device__ __forceinline__ void gram_reduce(float *out, const float *part, int P)
 {
     for (int e = threadIdx.x; e < Q * Q; e += blockDim.x) {
         float s = 0.f;
         for (int p = 0; p < P; ++p) s += part[(size_t)p * Q * Q + e];
-        out[e] = s;
+        if constexpr (MATVEC_ORDER) out[mat_idx<Q>(e / Q, e % Q)] = s;
+        else out[e] = s;
     }
 }
 
@@ -393,7 +449,7 @@ __device__ void inv_spd_warp(float *M, float d)
     __syncwarp();
     if (lane < Q) {
 #pragma unroll
-        for (int c = 0; c < Q; ++c) M[lane * Q + c] = b[c];
+        for (int c = 0; c < Q; ++c) M[mat_idx<Q>(lane, c)] = b[c];
     }
 }
 
@@ -418,6 +474,13 @@ __device__ __forceinline__ float4 group_matvec(float4 t4, const float *Mt, int g
 }
 
 template <int Q>
+__device__ __forceinline__ float4 matvec(float4 t4, const float *Mt, int grp_lane0, int sub, float4 acc)
+{
+    if constexpr (TcMatvec<Q>::on) return matvec_tc16(t4, Mt, acc);
+    return group_matvec<Q>(t4, Mt, grp_lane0, sub, acc);
+}
+
+template <int Q>
 __device__ __forceinline__ float group_sum(float v)
 {
 #pragma unroll
@@ -438,7 +501,8 @@ __device__ __forceinline__ void cp_async16(void *smem, const void *gmem)
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-__device__ __forceinline__ void cp_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 // predicated global store without a branch
 __device__ __forceinline__ void st_pred(float *addr, float v, bool p)
 {
@@ -450,6 +514,16 @@ __device__ __forceinline__ void st_pred(float *addr, float v, bool p)
 // Omega streaming: each warp double-buffers its group's entries through a 2 x 1 KB ring in shared
 // memory with cp.async (chunk = 512 B of row entries, or 512 B of S + 256 B of rows).
 constexpr int RING_SLOT = 1024;
+// stages of the per-warp ring (2 x RING_SLOT bytes): row phase 512-byte chunks, column phase
+// chunks of COL_CHUNK (S, row) entries
+#ifndef ADM_ROW_NS
+#define ADM_ROW_NS 2
+#endif
+#ifndef ADM_COL_NS
+#define ADM_COL_NS 2
+#endif
+constexpr int ROW_NS = ADM_ROW_NS, COL_NS = ADM_COL_NS;
+static_assert(ROW_NS >= 2 && ROW_NS * 512 <= 2 * RING_SLOT, "row ring stages");
 #ifndef ADM_COL_CHUNK
 #define ADM_COL_CHUNK 128
 #endif
@@ -519,6 +593,8 @@ __global__ void __launch_bounds__(1024, 1) k_adm(CArgs A)
     constexpr int CKR = 64 / R;                 // row-phase k-steps per 512-byte chunk (8-byte entries)
     constexpr int CKC = COL_CHUNK / R;          // column-phase k-steps per chunk (4-byte S + 2-byte rows)
     constexpr int SB = COL_CHUNK * 4, RB = COL_CHUNK * 2;   // bytes of S and of rows per chunk
+    constexpr int CST = (SB + RB + 127) / 128 * 128;       // bytes per column-phase ring stage
+    static_assert(COL_NS >= 2 && COL_NS * CST <= 2 * RING_SLOT, "column ring stages");
     extern __shared__ __align__(16) float sm[];
     __shared__ float red[33];
     __shared__ int sh_ctr[2];
@@ -606,14 +682,20 @@ __global__ void __launch_bounds__(1024, 1) k_adm(CArgs A)
             const char *eg = rent + (size_t)rgoff[g] * 8;
             const float4 x4 = *reinterpret_cast<const float4 *>(X + row * Q + 4 * sub);
             float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-            cp_async16(slot0 + lane * 16, eg + lane * 16);
-            cp_commit();
-            for (int c = 0; c < nch; ++c) {
-                if (c + 1 < nch) cp_async16(slot0 + ((c + 1) & 1) * RING_SLOT + lane * 16, eg + (c + 1) * 512 + lane * 16);
+#pragma unroll
+            for (int p = 0; p < ROW_NS - 1; ++p) {
+                if (p < nch) cp_async16(slot0 + p * 512 + lane * 16, eg + p * 512 + lane * 16);
                 cp_commit();
-                cp_wait1();
+            }
+            int cs = 0;   // ring stage of chunk c
+            for (int c = 0; c < nch; ++c) {
+                const int pf = c + ROW_NS - 1;
+                if (pf < nch) cp_async16(slot0 + (cs == 0 ? ROW_NS - 1 : cs - 1) * 512 + lane * 16, eg + pf * 512 + lane * 16);
+                cp_commit();
+                cp_wait<ROW_NS - 1>();
                 __syncwarp();
-                const unsigned long long *wb = reinterpret_cast<const unsigned long long *>(slot0 + (c & 1) * RING_SLOT) + grp;
+                const unsigned long long *wb = reinterpret_cast<const unsigned long long *>(slot0 + cs * 512) + grp;
+                cs = cs + 1 == ROW_NS ? 0 : cs + 1;
 #pragma unroll
                 for (int kk = 0; kk < CKR; ++kk) {
                     // padding entries gather the zero row n of Y: they add exactly 0 and park a
@@ -636,7 +718,7 @@ __global__ void __launch_bounds__(1024, 1) k_adm(CArgs A)
             t4.z = acc.z + al * u4.z - l4.z - fx * x4.z;
             t4.w = acc.w + al * u4.w - l4.w - fx * x4.w;
             const float4 x0 = make_float4(fd * x4.x, fd * x4.y, fd * x4.z, fd * x4.w);
-            const float4 xn = group_matvec<Q>(t4, Bm, lane0, sub, x0);
+            const float4 xn = matvec<Q>(t4, Bm, lane0, sub, x0);
             float4 un, ln;
             un.x = fmaxf(0.f, xn.x + l4.x * inv_al); ln.x = l4.x + ga * al * (xn.x - un.x);
             un.y = fmaxf(0.f, xn.y + l4.y * inv_al); ln.y = l4.y + ga * al * (xn.y - un.y);
@@ -667,7 +749,7 @@ __global__ void __launch_bounds__(1024, 1) k_adm(CArgs A)
             if (it > 0) {
                 P = (NT - 32) / ((Q / 4) * (Q / 4));
                 if (P * Q * Q > Cfg<Q>::PART) P = Cfg<Q>::PART / (Q * Q);
-                gram_reduce<Q>(Cm, part, P);   // Cm[b][a] = (X_{k+1}^T X_k)[a][b]
+                gram_reduce<Q, true>(Cm, part, P);   // Cm[b][a] = (X_{k+1}^T X_k)[a][b]
                 __syncthreads();
             }
         }
@@ -684,21 +766,29 @@ __global__ void __launch_bounds__(1024, 1) k_adm(CArgs A)
             const char *rg = cent + (size_t)cb * 2;
             const float4 y4 = *reinterpret_cast<const float4 *>(Y + colj * Q + 4 * sub);
             float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (lane < SB / 16) cp_async16(slot0 + lane * 16, sg + lane * 16);
-            if (lane < RB / 16) cp_async16(slot0 + 512 + lane * 16, rg + lane * 16);
-            cp_commit();
-            for (int c = 0; c < nch; ++c) {
-                if (c + 1 < nch) {
-                    char *nx = slot0 + ((c + 1) & 1) * RING_SLOT;
-                    if (lane < SB / 16) cp_async16(nx + lane * 16, sg + (c + 1) * SB + lane * 16);
-                    if (lane < RB / 16) cp_async16(nx + 512 + lane * 16, rg + (c + 1) * RB + lane * 16);
+#pragma unroll
+            for (int p = 0; p < COL_NS - 1; ++p) {
+                if (p < nch) {
+                    if (lane < SB / 16) cp_async16(slot0 + p * CST + lane * 16, sg + p * SB + lane * 16);
+                    if (lane < RB / 16) cp_async16(slot0 + p * CST + SB + lane * 16, rg + p * RB + lane * 16);
                 }
                 cp_commit();
-                cp_wait1();
+            }
+            int cs = 0;   // ring stage of chunk c
+            for (int c = 0; c < nch; ++c) {
+                const int pf = c + COL_NS - 1;
+                if (pf < nch) {
+                    char *nx = slot0 + (cs == 0 ? COL_NS - 1 : cs - 1) * CST;
+                    if (lane < SB / 16) cp_async16(nx + lane * 16, sg + pf * SB + lane * 16);
+                    if (lane < RB / 16) cp_async16(nx + SB + lane * 16, rg + pf * RB + lane * 16);
+                }
+                cp_commit();
+                cp_wait<COL_NS - 1>();
                 __syncwarp();
-                const char *cur = slot0 + (c & 1) * RING_SLOT;
+                const char *cur = slot0 + cs * CST;
+                cs = cs + 1 == COL_NS ? 0 : cs + 1;
                 const float *sbuf = reinterpret_cast<const float *>(cur) + grp;
-                const uint16_t *rbuf = reinterpret_cast<const uint16_t *>(cur + 512) + grp;
+                const uint16_t *rbuf = reinterpret_cast<const uint16_t *>(cur + SB) + grp;
 #pragma unroll
                 for (int kk = 0; kk < CKC; ++kk) {
                     // padding: zero row m of X and a zero S slot
@@ -716,7 +806,7 @@ __global__ void __launch_bounds__(1024, 1) k_adm(CArgs A)
                     acc.w += __shfl_xor_sync(FULLM, acc.w, o);
                 }
             }
-            acc = group_matvec<Q>(make_float4(fd * y4.x, fd * y4.y, fd * y4.z, fd * y4.w), Cm, lane0, sub, acc);
+            acc = matvec<Q>(make_float4(fd * y4.x, fd * y4.y, fd * y4.z, fd * y4.w), Cm, lane0, sub, acc);
             const float4 v4 = *reinterpret_cast<const float4 *>(Vg + colj * Q + 4 * sub);
             const float4 p4 = *reinterpret_cast<const float4 *>(Pg + colj * Q + 4 * sub);
             float4 t4;
@@ -724,7 +814,7 @@ __global__ void __launch_bounds__(1024, 1) k_adm(CArgs A)
             t4.y = acc.y + be * v4.y - p4.y;
             t4.z = acc.z + be * v4.z - p4.z;
             t4.w = acc.w + be * v4.w - p4.w;
-            const float4 yn = group_matvec<Q>(t4, Dm, lane0, sub, make_float4(0.f, 0.f, 0.f, 0.f));
+            const float4 yn = matvec<Q>(t4, Dm, lane0, sub, make_float4(0.f, 0.f, 0.f, 0.f));
             float4 vn, pn;
             vn.x = fmaxf(0.f, yn.x + p4.x * inv_be); pn.x = p4.x + ga * be * (yn.x - vn.x);
             vn.y = fmaxf(0.f, yn.y + p4.y * inv_be); pn.y = p4.y + ga * be * (yn.y - vn.y);
