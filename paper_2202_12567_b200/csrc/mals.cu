@@ -119,53 +119,54 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b)
 }
 
 // accumulate [F^T F | F^T m] of one system (samples [p0, p1)) into the warp's scratch (16 x 17,
-// row-major); `half` selects CSR (row system) or CSC (column system) indexing
+// row-major); `half` selects CSR (row system) or CSC (column system) indexing.  The system's
+// (index, value) lists are read 32 entries at a time with coalesced loads, one batch ahead, and
+// handed to the 4-sample steps by shuffles.  F^T F is symmetric: the tensor cores form the blocks
+// (0,0), (0,1), (1,1) and (1,0) is written as the transpose of (0,1); F^T m is a per-lane fp64
+// FMA sum over the lane's samples, reduced over the 4 lanes of a component at the end.
 __device__ __forceinline__ void accumulate_tc(const double *F, int nf, const MArgs &A, int64_t ob, int half, int p0,
                                               int p1, double inv_sigma, double *scr)
 {
     const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-    double c00[2] = {0.0, 0.0}, c01[2] = {0.0, 0.0}, c10[2] = {0.0, 0.0}, c11[2] = {0.0, 0.0};
-    double cb0[2] = {0.0, 0.0}, cb1[2] = {0.0, 0.0};
-    // the sample (index, value) of the next 4-sample step is loaded one step ahead
-    auto fetch = [&](int pp, int &other, double &v) {
-        other = nf;   // zero row: padding samples add nothing
-        v = 0.0;
-        if (pp < p1) {
-            if (half == 0) {
-                other = A.col[ob + pp];
-                v = A.val[ob + pp];
-            } else {
-                other = A.csc_row[ob + pp];
-                v = A.valc[ob + pp];
-            }
+    double c00[2] = {0.0, 0.0}, c01[2] = {0.0, 0.0}, c11[2] = {0.0, 0.0};
+    double b0 = 0.0, b1 = 0.0;
+    const uint16_t *idx = half == 0 ? A.col + ob : A.csc_row + ob;
+    const double *val = half == 0 ? A.val + ob : A.valc + ob;
+    // lane k holds entry pb + k of the current batch (zero row nf and value 0 past the end)
+    int bcol = nf;
+    double bval = 0.0;
+    if (p0 + lane < p1) { bcol = idx[p0 + lane]; bval = val[p0 + lane]; }
+    for (int pb = p0; pb < p1; pb += 32) {
+        int ncol = nf;
+        double nval = 0.0;
+        if (pb + 32 + lane < p1) { ncol = idx[pb + 32 + lane]; nval = val[pb + 32 + lane]; }
+        const int nst = min(8, (p1 - pb + 3) >> 2);   // warp-uniform
+        for (int st = 0; st < nst; ++st) {
+            const int oc = __shfl_sync(0xffffffffu, bcol, 4 * st + t);
+            const double vc = __shfl_sync(0xffffffffu, bval, 4 * st + t);
+            const double f0 = F[fidx<16>(oc, g)], f1 = F[fidx<16>(oc, 8 + g)];
+            dmma(c00, f0, f0);
+            dmma(c01, f0, f1);
+            dmma(c11, f1, f1);
+            b0 = fma(f0, vc, b0);
+            b1 = fma(f1, vc, b1);
         }
-    };
-    int oc;
-    double vc;
-    fetch(p0 + t, oc, vc);
-    for (int p = p0; p < p1; p += 4) {
-        int on;
-        double vn;
-        fetch(p + 4 + t, on, vn);
-        const double f0 = F[fidx<16>(oc, g)], f1 = F[fidx<16>(oc, 8 + g)];
-        const double bm = g == 0 ? vc * inv_sigma : 0.0;
-        dmma(c00, f0, f0);
-        dmma(c01, f0, f1);
-        dmma(c10, f1, f0);
-        dmma(c11, f1, f1);
-        dmma(cb0, f0, bm);
-        dmma(cb1, f1, bm);
-        oc = on;
-        vc = vn;
+        bcol = ncol;
+        bval = nval;
     }
+    b0 += __shfl_xor_sync(0xffffffffu, b0, 1);
+    b0 += __shfl_xor_sync(0xffffffffu, b0, 2);
+    b1 += __shfl_xor_sync(0xffffffffu, b1, 1);
+    b1 += __shfl_xor_sync(0xffffffffu, b1, 2);
     double *r0 = scr + (size_t)g * 17, *r1 = scr + (size_t)(8 + g) * 17;
     r0[2 * t] = c00[0]; r0[2 * t + 1] = c00[1];
     r0[8 + 2 * t] = c01[0]; r0[8 + 2 * t + 1] = c01[1];
-    r1[2 * t] = c10[0]; r1[2 * t + 1] = c10[1];
+    scr[(size_t)(8 + 2 * t) * 17 + g] = c01[0];        // block (1,0) = (0,1)^T
+    scr[(size_t)(8 + 2 * t + 1) * 17 + g] = c01[1];
     r1[8 + 2 * t] = c11[0]; r1[8 + 2 * t + 1] = c11[1];
     if (t == 0) {
-        r0[16] = cb0[0];
-        r1[16] = cb1[0];
+        r0[16] = b0 * inv_sigma;
+        r1[16] = b1 * inv_sigma;
     }
 }
 
