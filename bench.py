@@ -41,6 +41,15 @@ def fp32_peak():
         return FP32_PEAK_DERIVED, "derived: 148 SMs x 128 FP32 FMA lanes x 2 x 1.965 GHz"
 
 
+def fp64_peak():
+    """Measured FP64 FMA peak (tools/peaks.cu, profiles/r01_peaks.json): the denominator of the fp64 MALS kernel."""
+    try:
+        pk = json.load(open(os.path.join(ROOT, "profiles", "r01_peaks.json")))
+        return float(pk["fp64_fma_tflops"]), "measured: tools/peaks.cu FP64 FMA microbenchmark (profiles/r01_peaks.json)"
+    except Exception:
+        return FP32_PEAK_DERIVED / 2, "derived: half the FP32 rate (148 SMs x 64 FP64 FMA lanes x 2 x 1.965 GHz)"
+
+
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
@@ -274,7 +283,7 @@ def main():
     fl = (adm_flops if solver == 0 else mals_flops)(q, st["sum_samples"], st["rows"], st["sum_cols"],
                                                      st["slice_end"] - st["slice_begin"], K)
     achieved = fl / (ms_c * 1e-3) / 1e12
-    peak, peak_src = fp32_peak()
+    peak, peak_src = fp32_peak() if solver == 0 else fp64_peak()
     traffic, limiter = None, None
     try:   # DRAM bytes per launch of the dominant kernel from the committed ncu --set full capture
         tj = json.load(open(os.path.join(ROOT, "profiles", "r01_traffic.json")))
@@ -292,8 +301,8 @@ def main():
         nsamp = args.cpu_sample_slices or max(4 * cores, 16)   # ~10-30 s of oracle work
         v, dt, k, ent = cpu_oracle_sample(x, nsamp, solver)
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
-               "sample": f"{k} of {int(nsl)} slices of {args.config} (full per-slice pipeline, literal dense-Z "
-                         f"ADM), {dt:.1f} s wall"}
+               "sample": f"{k} of {int(nsl)} slices of {args.config} (full per-slice pipeline, "
+                         f"{'literal dense-Z ADM' if solver == 0 else 'masked ALS'}), {dt:.1f} s wall"}
     if rank != 0:
         if world > 1:
             dist.barrier()
@@ -301,12 +310,13 @@ def main():
         return
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f32" if solver == 0 else "f64",
         "data": "synthetic",
         "config": {"workload": f"{args.config}: {x.width}x{x.height} px, {x.vpls['px'].size} VPLs, {int(nsl)} slices, "
                                f"q={q}, rate={x.cfg.rate}, K={K}, solver={args.solver}",
                    "l2": "flushed between timed frames (256 MiB write)",
-                   "decisions": "f64 (entries, sampling, coarsening)", "completion": "f32"},
+                   "decisions": "f64 (entries, sampling, coarsening)", "completion": "f32" if solver == 0 else "f64"},
         "ms_per_stage": {k: statistics.mean(v) for k, v in stage.items()},
         "completed_entries": sum_completed, "samples": sum_N, "rays_per_pixel": evals / max(sum_m, 1.0),
         "roofline": {"bound": "alu", "kernel": "k_adm" if solver == 0 else "k_mals", "achieved": achieved,
