@@ -82,7 +82,7 @@ void free_all(lmc_ctx *c)
     Dev &d = c->d;
     void *ptrs[] = {d.pixel, d.g[0], d.g[1], d.g[2], d.g[3], d.g[4], d.g[5], d.g[6], d.g[7], d.g[8], d.g[9], d.g[10],
                     d.g[11], d.g[12], d.expo, d.vpl, d.ut_i32, d.ut_lum, d.ut_I, d.rows, d.rows_alt, d.keys,
-                    d.keys_alt, d.keys_sorted, d.sl_i32, d.lvl_begin, d.lvl_end, d.lvl_slot, d.lvl_work, d.ext, d.slice_off, d.cub_tmp, d.prow,
+                    d.keys_alt, d.keys_sorted, d.sl_i32, d.lvl_begin, d.lvl_end, d.lvl_slot, d.lvl_work, d.ext, d.slice_off, d.cub_tmp, d.prow, d.sbox,
                     d.p1_rows, d.p1_Ta, d.p1_Tb, d.p1_cnt, d.pool_rows, d.pool_Ta, d.pool_Tb, d.pool_used, d.cs_flags,
                     d.cs_eps, d.cs_cost, d.cs_zoff, d.cs_zlen, d.cut_n, d.cut_cols, d.src_off, d.src_len, d.src_side,
                     d.rowptr, d.col, d.val, d.val64, d.Xd, d.Yd, d.val64c, d.carried, d.colptr, d.csc_row, d.csc_src, d.nnz, d.target_n, d.n_new,
@@ -572,6 +572,7 @@ static lmc_status create_impl(lmc_ctx *c, const lmc_gbuffer *g, const lmc_vpls *
     CK(dalloc(&d.r_ent, SL * c->scap), "alloc layout");
     CK(dalloc(&d.c_ent, SL * c->scap), "alloc layout");
     CK(dalloc(&d.norm, SL), "alloc layout");
+    CK(dalloc(&d.sbox, 6 * SL), "alloc slices");
     CK(dalloc(&d.flags, SL), "alloc factors");
     CK(dalloc(&d.iters, SL), "alloc factors");
     CK(dalloc(&d.resid, SL), "alloc factors");
@@ -668,7 +669,7 @@ lmc_status lmc_sample_pass1(lmc_ctx *c)
     lmc_status s = check_stage(c, 1);
     if (s != LMC_OK) return s;
     CK(run_pass1(c), "pass 1");
-    c->launches += (c->SL > 0 && c->up.nB > 0) ? 1 : 0;
+    c->launches += (c->SL > 0 ? 1 : 0) + ((c->SL > 0 && c->up.nB > 0) ? 1 : 0);   // k_slice_bbox, k_pass1
     ev_rec(c, 2);
     c->state = 2;
     return LMC_OK;

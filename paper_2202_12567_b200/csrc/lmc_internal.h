@@ -74,6 +74,7 @@ struct Dev {
     void *cub_tmp;
     size_t cub_tmp_bytes;
     float4 *prow;                      // 4 per local row (slice order)
+    float *sbox;                       // [SL][6] bounding box (lo3, hi3) of each slice's points (fp32, exact)
     // pass 1: [SL][nB][nmax]
     uint16_t *p1_rows;
     double *p1_Ta, *p1_Tb;
