@@ -306,6 +306,7 @@ struct CArgs {
     const uint16_t *c_ent;
     float *U, *V, *Lam, *Pi, *Xold, *S, *resid;
     int32_t *flags, *iters;
+    const int32_t *order;       // CTA -> slice, or null for CTA = slice
     unsigned long long *prof;   // optional phase clocks (LMC_ADM_PROF=1), else null
 };
 
@@ -600,7 +601,7 @@ __global__ void __launch_bounds__(1024, 1) k_adm(CArgs A)
     __shared__ int sh_ctr[2];
     __shared__ unsigned long long sh_prof[8];
     __shared__ long long sh_exit[32];
-    const int ls = blockIdx.x, s = A.s0 + ls, tid = threadIdx.x, NT = blockDim.x;
+    const int ls = A.order ? A.order[blockIdx.x] : (int)blockIdx.x, s = A.s0 + ls, tid = threadIdx.x, NT = blockDim.x;
     long long pt0 = PROF ? clock64() : 0;
     unsigned long long pacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     const int lane = tid & 31, warp = tid >> 5, nwarps = NT >> 5;
@@ -965,6 +966,7 @@ cudaError_t run_adm(lmc_ctx *c, int nmax)
     A.flags = c->d.flags;
     A.iters = c->d.iters;
     A.prof = nullptr;
+    A.order = c->adm_ordered ? c->d.adm_order : nullptr;
     // LMC_ADM_PROF=1: per-phase clock64 totals (diagnostic only; synchronises and prints to stderr)
     const char *pe = getenv("LMC_ADM_PROF");
     const bool prof = pe && pe[0] == '1' && c->q == 16;   // instrumented build for q = 16 only

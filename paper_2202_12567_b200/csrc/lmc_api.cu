@@ -88,7 +88,7 @@ void free_all(lmc_ctx *c)
                     d.rowptr, d.col, d.val, d.val64, d.Xd, d.Yd, d.val64c, d.carried, d.colptr, d.csc_row, d.csc_src, d.nnz, d.target_n, d.n_new,
                     d.newcells, d.newpos, d.U, d.V, d.Lam, d.Pi, d.Xold, d.S, d.flags, d.iters, d.resid,
                     d.direct_rgb, d.counters, d.img, d.rows_rgb, d.vpl_soa, d.r_perm, d.r_len, d.c_perm, d.c_len,
-                    d.r_goff, d.c_goff, d.c_nsolo, d.r_ent, d.c_ent, d.norm};
+                    d.r_goff, d.c_goff, d.c_nsolo, d.adm_order, d.r_ent, d.c_ent, d.norm};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (c->h_stage) cudaFreeHost(c->h_stage);
@@ -569,6 +569,7 @@ static lmc_status create_impl(lmc_ctx *c, const lmc_gbuffer *g, const lmc_vpls *
     CK(dalloc(&d.r_goff, SL * (c->mmax + 1)), "alloc layout");
     CK(dalloc(&d.c_goff, SL * (G + 1)), "alloc layout");
     CK(dalloc(&d.c_nsolo, SL), "alloc layout");
+    CK(dalloc(&d.adm_order, SL), "alloc layout");
     CK(dalloc(&d.r_ent, SL * c->scap), "alloc layout");
     CK(dalloc(&d.c_ent, SL * c->scap), "alloc layout");
     CK(dalloc(&d.norm, SL), "alloc layout");
@@ -590,6 +591,7 @@ static lmc_status create_impl(lmc_ctx *c, const lmc_gbuffer *g, const lmc_vpls *
     int maxsm = 0, dev = 0;
     CK(cudaGetDevice(&dev), "device");
     CK(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev), "device attr");
+    CK(cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, dev), "device attr");
     if (need > (size_t)maxsm)
         return fail(c, LMC_EINVAL, "rank %d with slices of %d rows and a %lld-node cut needs %zu B of shared memory (max %d)",
                     c->q, c->mmax, (long long)G, need, maxsm);
@@ -710,8 +712,33 @@ lmc_status lmc_complete(lmc_ctx *c)
         // shared memory of the ADM kernel is sized by this frame's largest coarsened cut
         unsigned long long nmx = 0;
         CK(cudaMemcpyAsync(&nmx, c->d.counters + 5, sizeof nmx, cudaMemcpyDeviceToHost, c->stream), "read max n");
+        // launch order of the completion CTAs: slice order, except that the nsm slices with the
+        // fewest samples run last, largest first, so the final wave holds the shortest CTAs (a
+        // slice's result does not depend on when its CTA runs; LMC_ADM_TAIL=0 keeps slice order)
+        const char *te = getenv("LMC_ADM_TAIL");   // multiple of nsm slices moved last (diagnostic)
+        const int ntail = (te ? atoi(te) : 1) * c->nsm;
+        const bool tail = ntail > 0 && c->SL > ntail;
+        if (tail) {
+            c->h_nnz.resize(c->SL);
+            CK(cudaMemcpyAsync(c->h_nnz.data(), c->d.nnz, c->SL * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream), "read nnz");
+        }
         CK(cudaStreamSynchronize(c->stream), "sync");
         const int nmax = std::max(1, (int)std::min<unsigned long long>(nmx, (unsigned long long)c->G));
+        c->adm_ordered = false;
+        if (tail) {
+            std::vector<int32_t> byn(c->SL);
+            for (int k = 0; k < c->SL; ++k) byn[k] = k;
+            std::stable_sort(byn.begin(), byn.end(), [&](int a, int b) { return c->h_nnz[a] < c->h_nnz[b]; });
+            std::vector<char> last(c->SL, 0);
+            for (int k = 0; k < ntail; ++k) last[byn[k]] = 1;
+            c->h_order.clear();
+            for (int k = 0; k < c->SL; ++k)
+                if (!last[k]) c->h_order.push_back(k);
+            for (int k = ntail - 1; k >= 0; --k) c->h_order.push_back(byn[k]);
+            CK(cudaMemcpyAsync(c->d.adm_order, c->h_order.data(), c->SL * sizeof(int32_t), cudaMemcpyHostToDevice, c->stream),
+               "upload order");
+            c->adm_ordered = true;
+        }
         ev_rec(c, 8);
         CK(run_adm(c, nmax), "completion (ADM)");
         ev_rec(c, 9);

@@ -109,6 +109,7 @@ struct Dev {
     uint16_t *c_perm, *c_len;          // [SL][G]
     int32_t *r_goff, *c_goff;          // [SL][mmax+1], [SL][G+1]
     int32_t *c_nsolo;                  // [SL] leading column groups that hold a single (long) column
+    int32_t *adm_order;                // [SL] completion CTA -> slice (the smallest slices last)
     unsigned long long *r_ent;         // [SL][scap] (M^ bits << 32) | (column-layout index << 10) | column
     uint16_t *c_ent;                   // [SL][scap] row of the column-layout entry
     float4 *norm;                      // [SL] sigma, 1/sigma, sum M^, sum M^^2
@@ -153,6 +154,9 @@ struct lmc_ctx {
     int scene_slot = -1;           // index into the __constant__ scene table
     lmc::Upper up;
     std::vector<int32_t> h_up_node;   // for getters
+    int nsm = 0;                      // SMs of the device
+    bool adm_ordered = false;         // d.adm_order holds this frame's completion launch order
+    std::vector<int32_t> h_nnz, h_order;   // completion launch order (lmc_complete)
     lmc::Dev d;
     // timing
     int timing = 0;
