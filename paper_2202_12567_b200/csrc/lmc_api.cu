@@ -699,11 +699,42 @@ lmc_status lmc_sample_pass2(lmc_ctx *c)
     return LMC_OK;
 }
 
+// Launch order of the completion CTAs: slice order, except that the nsm slices with the fewest
+// samples run last, largest first, so the final wave holds the shortest CTAs (a slice's result
+// does not depend on when its CTA runs).  Reads the per-slice sample counts (synchronises the
+// stream, as the ADM shared-memory sizing does anyway).  LMC_ADM_TAIL=k moves k x nsm slices
+// (diagnostic; 0 keeps slice order).
+static cudaError_t completion_order(lmc_ctx *c)
+{
+    const char *te = getenv("LMC_ADM_TAIL");
+    const int ntail = (te ? atoi(te) : 1) * c->nsm;
+    c->adm_ordered = false;
+    if (!(ntail > 0 && c->SL > ntail)) return cudaStreamSynchronize(c->stream);
+    c->h_nnz.resize(c->SL);
+    cudaError_t e = cudaMemcpyAsync(c->h_nnz.data(), c->d.nnz, c->SL * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    if (e != cudaSuccess) return e;
+    std::vector<int32_t> byn(c->SL);
+    for (int k = 0; k < c->SL; ++k) byn[k] = k;
+    std::stable_sort(byn.begin(), byn.end(), [&](int a, int b) { return c->h_nnz[a] < c->h_nnz[b]; });
+    std::vector<char> last(c->SL, 0);
+    for (int k = 0; k < ntail; ++k) last[byn[k]] = 1;
+    c->h_order.clear();
+    for (int k = 0; k < c->SL; ++k)
+        if (!last[k]) c->h_order.push_back(k);
+    for (int k = ntail - 1; k >= 0; --k) c->h_order.push_back(byn[k]);
+    e = cudaMemcpyAsync(c->d.adm_order, c->h_order.data(), c->SL * sizeof(int32_t), cudaMemcpyHostToDevice, c->stream);
+    if (e != cudaSuccess) return e;
+    c->adm_ordered = true;
+    return cudaSuccess;
+}
+
 lmc_status lmc_complete(lmc_ctx *c)
 {
     lmc_status s = check_stage(c, 4);
     if (s != LMC_OK) return s;
     if (c->cfg.solver == LMC_SOLVER_MALS) {
+        CK(completion_order(c), "completion order");
         ev_rec(c, 8);
         CK(run_mals(c), "completion (MALS)");
         ev_rec(c, 9);
@@ -712,33 +743,8 @@ lmc_status lmc_complete(lmc_ctx *c)
         // shared memory of the ADM kernel is sized by this frame's largest coarsened cut
         unsigned long long nmx = 0;
         CK(cudaMemcpyAsync(&nmx, c->d.counters + 5, sizeof nmx, cudaMemcpyDeviceToHost, c->stream), "read max n");
-        // launch order of the completion CTAs: slice order, except that the nsm slices with the
-        // fewest samples run last, largest first, so the final wave holds the shortest CTAs (a
-        // slice's result does not depend on when its CTA runs; LMC_ADM_TAIL=0 keeps slice order)
-        const char *te = getenv("LMC_ADM_TAIL");   // multiple of nsm slices moved last (diagnostic)
-        const int ntail = (te ? atoi(te) : 1) * c->nsm;
-        const bool tail = ntail > 0 && c->SL > ntail;
-        if (tail) {
-            c->h_nnz.resize(c->SL);
-            CK(cudaMemcpyAsync(c->h_nnz.data(), c->d.nnz, c->SL * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream), "read nnz");
-        }
-        CK(cudaStreamSynchronize(c->stream), "sync");
+        CK(completion_order(c), "completion order");   // synchronises the stream
         const int nmax = std::max(1, (int)std::min<unsigned long long>(nmx, (unsigned long long)c->G));
-        c->adm_ordered = false;
-        if (tail) {
-            std::vector<int32_t> byn(c->SL);
-            for (int k = 0; k < c->SL; ++k) byn[k] = k;
-            std::stable_sort(byn.begin(), byn.end(), [&](int a, int b) { return c->h_nnz[a] < c->h_nnz[b]; });
-            std::vector<char> last(c->SL, 0);
-            for (int k = 0; k < ntail; ++k) last[byn[k]] = 1;
-            c->h_order.clear();
-            for (int k = 0; k < c->SL; ++k)
-                if (!last[k]) c->h_order.push_back(k);
-            for (int k = ntail - 1; k >= 0; --k) c->h_order.push_back(byn[k]);
-            CK(cudaMemcpyAsync(c->d.adm_order, c->h_order.data(), c->SL * sizeof(int32_t), cudaMemcpyHostToDevice, c->stream),
-               "upload order");
-            c->adm_ordered = true;
-        }
         ev_rec(c, 8);
         CK(run_adm(c, nmax), "completion (ADM)");
         ev_rec(c, 9);

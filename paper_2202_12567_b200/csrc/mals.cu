@@ -33,6 +33,7 @@ struct MArgs {
     double *Xd, *Yd;               // fp64 factors [rows][q], [slice][G][q]
     int32_t fmax;                  // rows of the operand buffer in shared memory (max(mmax, G))
     int32_t *flags, *iters;
+    const int32_t *order;          // CTA -> slice, or null for CTA = slice
 };
 
 constexpr int MT = 256;
@@ -175,7 +176,7 @@ __global__ void __launch_bounds__(MCfg<Q>::NT, 1) k_mals(MArgs A)
 {
     extern __shared__ __align__(16) double dsm[];
     __shared__ double red[33];
-    const int ls = blockIdx.x, s = A.s0 + ls, tid = threadIdx.x;
+    const int ls = A.order ? A.order[blockIdx.x] : (int)blockIdx.x, s = A.s0 + ls, tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5, nwarps = MCfg<Q>::NT >> 5;
     constexpr int GPW = 32 / Q;                  // systems per warp
     const int gi = lane / Q, l = lane % Q, lane0 = gi * Q;
@@ -363,6 +364,7 @@ cudaError_t run_mals(lmc_ctx *c)
     A.fmax = std::max(c->mmax, c->G);
     A.flags = c->d.flags;
     A.iters = c->d.iters;
+    A.order = c->adm_ordered ? c->d.adm_order : nullptr;
     switch (c->q) {
     case 4: return launch_mals<4>(c, A);
     case 8: return launch_mals<8>(c, A);
