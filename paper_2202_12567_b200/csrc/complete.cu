@@ -83,6 +83,20 @@ struct LArgs {
 
 constexpr int LT = 1024;
 
+// Within a cp.async chunk (KA k-steps of R members, canonical position k * R + r) the entries are
+// stored V k-steps per member together: position (k - k % V) * R + r * V + k % V.  A lane group
+// then reads V consecutive k-steps of its member with one vector load, and the R groups of a warp
+// read one contiguous span (row entries: V = 2 x 8 bytes; column S: V = 4 x 4 bytes; column rows:
+// V = 8 x 2 bytes) -- a quarter to a half of the shared-memory wavefronts of per-k-step loads.
+constexpr int VROW = 2, VS = 4, VCR = 8;
+__host__ __device__ __forceinline__ int vperm(int rel, int R, int KA, int V)
+{
+    // rel: canonical position relative to a chunk-aligned group base
+    const int ch = R * KA, c = rel / ch, w = rel - c * ch, k = w / R, r = w - k * R;
+    const int v = V < KA ? V : KA;
+    return c * ch + (k - k % v) * R + r * v + k % v;
+}
+
 
 // The entries of the P rows (columns) that share a shared-memory phase of the ADM kernel are
 // scheduled so that at step k member t takes, when it can, an entry whose gathered index has
@@ -237,7 +251,7 @@ __global__ void __launch_bounds__(LT, 1) k_layout(LArgs A)
                     }
                 }
                 if (!in) continue;
-                int idx;
+                int rel;
                 if (solo) {
                     int p;
                     if (j < fres) {
@@ -257,29 +271,31 @@ __global__ void __launch_bounds__(LT, 1) k_layout(LArgs A)
                             }
                         }
                     }
-                    idx = base + p;
+                    rel = p;
                 } else {
-                    idx = base + (sres + j) * R + r;
+                    rel = (sres + j) * R + r;
                 }
                 if (rows_pass) {
                     const float mh = A.val[ob + pos] * inv_sigma;
-                    A.r_ent[sb + idx] = ((unsigned long long)__float_as_uint(mh) << 32) |
-                                        ((unsigned long long)(uint32_t)A.map[ob + pos] << 11) | (unsigned long long)A.col[ob + pos];
+                    A.r_ent[sb + base + vperm(rel, R, KA, VROW)] =
+                        ((unsigned long long)__float_as_uint(mh) << 32) |
+                        ((unsigned long long)(uint32_t)A.map[ob + pos] << 11) | (unsigned long long)A.col[ob + pos];
                 } else {
-                    A.c_ent[sb + idx] = A.csc_row[ob + pos];
-                    A.map[ob + A.csc_src[ob + pos]] = idx;
-                    A.S[sb + idx] = 0.f;
+                    const int is = base + vperm(rel, R, KA, VS);
+                    A.c_ent[sb + base + vperm(rel, R, KA, VCR)] = A.csc_row[ob + pos];
+                    A.map[ob + A.csc_src[ob + pos]] = is;
+                    A.S[sb + is] = 0.f;
                 }
             }
             // padding: sentinel entries up to the group length
             for (int k = mown + lane; k < glen; k += 32) {
-                const int idx = solo ? base + k : base + k * R + r;
+                const int rel = solo ? k : k * R + r;
                 if (rows_pass) {
                     // sentinel: zero row n of Y, residual parked in the dummy slot
-                    A.r_ent[sb + idx] = ((unsigned long long)(uint32_t)dummy << 11) | (unsigned long long)n;
+                    A.r_ent[sb + base + vperm(rel, R, KA, VROW)] = ((unsigned long long)(uint32_t)dummy << 11) | (unsigned long long)n;
                 } else {
-                    A.c_ent[sb + idx] = (uint16_t)m;   // sentinel: zero row m of X
-                    A.S[sb + idx] = 0.f;               // padding slots stay finite
+                    A.c_ent[sb + base + vperm(rel, R, KA, VCR)] = (uint16_t)m;   // sentinel: zero row m of X
+                    A.S[sb + base + vperm(rel, R, KA, VS)] = 0.f;                // padding slots stay finite
                 }
             }
         }
@@ -548,10 +564,10 @@ __device__ __forceinline__ float row_residual_ss(const float *X, const float *Y,
         const bool valid = rank < m;
         const int row = valid ? rperm[rank] : m;
         const int len = rlen[g * R];   // group length (warp-uniform); padding entries add 0
-        const unsigned long long *e = rent + rgoff[g] + grp;
+        const unsigned long long *e = rent + rgoff[g];
         const float4 x4 = *reinterpret_cast<const float4 *>(X + row * Q + 4 * sub);
         for (int k = 0; k < len; ++k) {
-            const unsigned long long w = e[k * R];
+            const unsigned long long w = e[vperm(k * R + grp, R, 64 / R, VROW)];
             const float4 y4 = *reinterpret_cast<const float4 *>(Y + (int)((uint32_t)w & 2047u) * Q + 4 * sub);
             const float err = __uint_as_float((uint32_t)(w >> 32)) - group_sum<Q>(f4dot(x4, y4));
             if (sub == 0) ss = fmaf(err, err, ss);
@@ -596,6 +612,8 @@ __global__ void __launch_bounds__(1024, 1) k_adm(CArgs A)
     constexpr int SB = COL_CHUNK * 4, RB = COL_CHUNK * 2;   // bytes of S and of rows per chunk
     constexpr int CST = (SB + RB + 127) / 128 * 128;       // bytes per column-phase ring stage
     static_assert(COL_NS >= 2 && COL_NS * CST <= 2 * RING_SLOT, "column ring stages");
+    constexpr int VC = CKC < VCR ? CKC : VCR;   // column rows per vector load (layout: vperm)
+    static_assert(CKR % VROW == 0 && CKC % VS == 0 && VC % VS == 0 && (VC == 8 || VC == 4), "vector widths");
     extern __shared__ __align__(16) float sm[];
     __shared__ float red[33];
     __shared__ int sh_ctr[2];
@@ -695,18 +713,23 @@ __global__ void __launch_bounds__(1024, 1) k_adm(CArgs A)
                 cp_commit();
                 cp_wait<ROW_NS - 1>();
                 __syncwarp();
-                const unsigned long long *wb = reinterpret_cast<const unsigned long long *>(slot0 + cs * 512) + grp;
+                const unsigned long long *wb = reinterpret_cast<const unsigned long long *>(slot0 + cs * 512) + VROW * grp;
                 cs = cs + 1 == ROW_NS ? 0 : cs + 1;
 #pragma unroll
-                for (int kk = 0; kk < CKR; ++kk) {
-                    // padding entries gather the zero row n of Y: they add exactly 0 and park a
-                    // zero residual in the dummy slot, so no masking is needed
-                    const unsigned long long w = wb[kk * R];
-                    const float4 y4 = *reinterpret_cast<const float4 *>(Y + (int)((uint32_t)w & 2047u) * Q + 4 * sub);
-                    const float d = group_sum<Q>(f4dot(x4, y4));
-                    const float sv = fmaf(-fd, d, __uint_as_float((uint32_t)(w >> 32)));
-                    acc = f4fma(sv, y4, acc);
-                    st_pred(S + (((uint32_t)w) >> 11), sv, sub == 0);
+                for (int kk = 0; kk < CKR; kk += VROW) {
+                    // two k-steps of this row in one 16-byte load (vperm layout)
+                    const ulonglong2 wp = *reinterpret_cast<const ulonglong2 *>(wb + kk * R);
+#pragma unroll
+                    for (int h = 0; h < VROW; ++h) {
+                        // padding entries gather the zero row n of Y: they add exactly 0 and park a
+                        // zero residual in the dummy slot, so no masking is needed
+                        const unsigned long long w = h == 0 ? wp.x : wp.y;
+                        const float4 y4 = *reinterpret_cast<const float4 *>(Y + (int)((uint32_t)w & 2047u) * Q + 4 * sub);
+                        const float d = group_sum<Q>(f4dot(x4, y4));
+                        const float sv = fmaf(-fd, d, __uint_as_float((uint32_t)(w >> 32)));
+                        acc = f4fma(sv, y4, acc);
+                        st_pred(S + (((uint32_t)w) >> 11), sv, sub == 0);
+                    }
                 }
                 __syncwarp();
             }
@@ -788,13 +811,31 @@ __global__ void __launch_bounds__(1024, 1) k_adm(CArgs A)
                 __syncwarp();
                 const char *cur = slot0 + cs * CST;
                 cs = cs + 1 == COL_NS ? 0 : cs + 1;
-                const float *sbuf = reinterpret_cast<const float *>(cur) + grp;
-                const uint16_t *rbuf = reinterpret_cast<const uint16_t *>(cur + SB) + grp;
+                // vperm layout: VS k-steps of S and VC k-steps of rows per vector load
+                const float *sbuf = reinterpret_cast<const float *>(cur) + VS * grp;
+                const uint16_t *rbuf = reinterpret_cast<const uint16_t *>(cur + SB) + VC * grp;
 #pragma unroll
-                for (int kk = 0; kk < CKC; ++kk) {
-                    // padding: zero row m of X and a zero S slot
-                    const float4 xv = *reinterpret_cast<const float4 *>(X + (int)rbuf[kk * R] * Q + 4 * sub);
-                    acc = f4fma(sbuf[kk * R], xv, acc);
+                for (int kq = 0; kq < CKC; kq += VC) {
+                    uint32_t rw[VC / 2];
+                    if constexpr (VC == 8) {
+                        const uint4 t = *reinterpret_cast<const uint4 *>(rbuf + kq * R);
+                        rw[0] = t.x; rw[1] = t.y; rw[2] = t.z; rw[3] = t.w;
+                    } else {
+                        const uint2 t = *reinterpret_cast<const uint2 *>(rbuf + kq * R);
+                        rw[0] = t.x; rw[1] = t.y;
+                    }
+#pragma unroll
+                    for (int k4 = 0; k4 < VC; k4 += VS) {
+                        const float4 s4 = *reinterpret_cast<const float4 *>(sbuf + (kq + k4) * R);
+#pragma unroll
+                        for (int h = 0; h < VS; ++h) {
+                            // padding: zero row m of X and a zero S slot
+                            const int k = k4 + h;
+                            const int row = (int)((rw[k >> 1] >> (16 * (k & 1))) & 0xffffu);
+                            const float4 xv = *reinterpret_cast<const float4 *>(X + row * Q + 4 * sub);
+                            acc = f4fma(f4get(s4, h), xv, acc);
+                        }
+                    }
                 }
                 __syncwarp();
             }
