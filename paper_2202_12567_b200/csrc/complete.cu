@@ -326,12 +326,25 @@ struct CArgs {
     unsigned long long *prof;   // optional phase clocks (LMC_ADM_PROF=1), else null
 };
 
+// Per-rank kernel shape.  q <= 16: 32 warps, a 2 KB ring per warp, 128-entry column chunks.
+// q = 32: X and Y take twice the shared memory (a 1024-node cut at 512-row slices needs 197 KB),
+// so 16 warps with a 1 KB ring each and 64-entry column chunks (the same ring stages in half the
+// bytes); 512 threads leave 128 registers per thread.
+#ifndef ADM_COL_CHUNK
+#define ADM_COL_CHUNK 128
+#endif
 template <int Q>
 struct Cfg {
     static constexpr int L = Q / 4;           // lanes per row / column
     static constexpr int R = 32 / L;          // rows per warp step
-    static constexpr int PART = 16384;        // floats of Gram partials (the 64 KB ring area)
+    static constexpr int NT = Q >= 32 ? 512 : 1024;                  // threads per CTA
+    static constexpr int SLOT = Q >= 32 ? 512 : 1024;                // bytes per ring slot (2 per warp)
+    static constexpr int COL_CHUNK = Q >= 32 ? 64 : ADM_COL_CHUNK;   // (S, row) entries per column chunk
+    static constexpr int PART = NT / 32 * 2 * SLOT / 4;             // floats of Gram partials (the ring area)
 };
+__host__ __device__ constexpr int adm_threads(int q) { return q >= 32 ? 512 : 1024; }
+__host__ __device__ constexpr int adm_slot(int q) { return q >= 32 ? 512 : 1024; }
+__host__ __device__ constexpr int adm_col_chunk(int q) { return q >= 32 ? 64 : ADM_COL_CHUNK; }
 
 // ---- q = 16: the q x q products of the updates on the fp64 tensor cores ---------------------
 // mma.sync m8n8k4 f64 (g = lane / 4, t = lane % 4): a0 = A[g][t], b0 = B[t][g], c = C[g][2t..2t+1].
@@ -530,9 +543,8 @@ __device__ __forceinline__ void st_pred(float *addr, float v, bool p)
 
 // Omega streaming: each warp double-buffers its group's entries through a 2 x 1 KB ring in shared
 // memory with cp.async (chunk = 512 B of row entries, or 512 B of S + 256 B of rows).
-constexpr int RING_SLOT = 1024;
-// stages of the per-warp ring (2 x RING_SLOT bytes): row phase 512-byte chunks, column phase
-// chunks of COL_CHUNK (S, row) entries
+// stages of the per-warp ring (2 x Cfg<Q>::SLOT bytes): row phase 512-byte chunks, column phase
+// chunks of Cfg<Q>::COL_CHUNK (S, row) entries
 #ifndef ADM_ROW_NS
 #define ADM_ROW_NS 2
 #endif
@@ -540,13 +552,9 @@ constexpr int RING_SLOT = 1024;
 #define ADM_COL_NS 2
 #endif
 constexpr int ROW_NS = ADM_ROW_NS, COL_NS = ADM_COL_NS;
-static_assert(ROW_NS >= 2 && ROW_NS * 512 <= 2 * RING_SLOT, "row ring stages");
-#ifndef ADM_COL_CHUNK
-#define ADM_COL_CHUNK 128
-#endif
+
 // entries per column-phase chunk (4-byte S + 2-byte row each).  64 pads the column groups less
 // (14% -> 7% padding at C4) but measured no faster (more chunk waits)
-constexpr int COL_CHUNK = ADM_COL_CHUNK;
 
 template <int Q>
 __device__ __forceinline__ float row_residual_ss(const float *X, const float *Y, const CArgs &A, int ls, int m,
@@ -604,10 +612,12 @@ __device__ __forceinline__ float row_residual_ss(const float *X, const float *Y,
     }
 
 template <int Q, bool PROF>
-__global__ void __launch_bounds__(1024, 1) k_adm(CArgs A)
+__global__ void __launch_bounds__(Cfg<Q>::NT, 1) k_adm(CArgs A)
 {
     constexpr int L = Cfg<Q>::L, R = Cfg<Q>::R;
     constexpr int CKR = 64 / R;                 // row-phase k-steps per 512-byte chunk (8-byte entries)
+    constexpr int COL_CHUNK = Cfg<Q>::COL_CHUNK, RING_SLOT = Cfg<Q>::SLOT;
+    static_assert(ROW_NS >= 2 && ROW_NS * 512 <= 2 * RING_SLOT, "row ring stages");
     constexpr int CKC = COL_CHUNK / R;          // column-phase k-steps per chunk (4-byte S + 2-byte rows)
     constexpr int SB = COL_CHUNK * 4, RB = COL_CHUNK * 2;   // bytes of S and of rows per chunk
     constexpr int CST = (SB + RB + 127) / 128 * 128;       // bytes per column-phase ring stage
@@ -906,8 +916,9 @@ __global__ void __launch_bounds__(1024, 1) k_adm(CArgs A)
 
 size_t adm_smem_bytes(int q, int mmax, int nmax)
 {
-    // X, Y, three q x q matrices, 32 warps x 2 ring slots (reused for the Gram partials)
-    return ((size_t)mmax + (size_t)nmax + 2) * q * sizeof(float) + 3 * (size_t)q * q * sizeof(float) + 32 * 2 * RING_SLOT;
+    // X, Y, three q x q matrices, 2 ring slots per warp (reused for the Gram partials)
+    return ((size_t)mmax + (size_t)nmax + 2) * q * sizeof(float) + 3 * (size_t)q * q * sizeof(float) +
+           (size_t)(adm_threads(q) / 32) * 2 * adm_slot(q);
 }
 
 static int layout_R(int q) { return 128 / q; }
@@ -946,7 +957,7 @@ cudaError_t run_layout(lmc_ctx *c)
     A.P = c->q >= 32 ? 1 : 32 / c->q;
     A.D = 1;
     A.KAR = 64 / A.R;      // k-steps per 512-byte chunk of 8-byte row entries
-    A.KAC = COL_CHUNK / A.R;   // k-steps per chunk of 4-byte S (+ 2-byte rows)
+    A.KAC = adm_col_chunk(c->q) / A.R;   // k-steps per chunk of 4-byte S (+ 2-byte rows)
     A.solo_min = 128;      // columns of >= 128 entries get a warp of their own (a solo column pays the
                            // whole warp's update, so the threshold stays well above a group's share)
     const size_t sm = sizeof(typename cub::BlockRadixSort<uint32_t, LT, 1>::TempStorage);
@@ -963,7 +974,7 @@ static cudaError_t launch_adm(lmc_ctx *c, const CArgs &A)
     const size_t sm = adm_smem_bytes(Q, c->mmax, A.nmax);
     cudaError_t e = cudaFuncSetAttribute(k_adm<Q, PROF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
-    const int nt = 1024;   // 32 warps (64 registers per thread), one CTA per SM
+    const int nt = Cfg<Q>::NT;   // 32 warps (64 registers per thread) or 16 (q = 32), one CTA per SM
     k_adm<Q, PROF><<<c->SL, nt, sm, c->stream>>>(A);
     return cudaGetLastError();
 }

@@ -213,6 +213,17 @@ def test_c4_full_size_sampled_slices():
         check_slice(x, fr, img, r)
 
 
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["c5_q32_r5", "c5_q4_r20"])
+def test_c5_sweep_corners_sampled_slices(name):
+    """BASELINE configs[4] at full size (1024x1024, 300k VPLs, glossy): the sweep's corners -- rank 32
+    at 5% (a 1024-node cut at 512-row slices: the 16-warp q = 32 kernel shape) and rank 4 at 20%"""
+    x, fr, img = frame(name)
+    off, rows = fr.slices()
+    for r in oracle_slices(x, pick(off.size - 1, 3)):
+        check_slice(x, fr, img, r)
+
+
 def test_empty_gbuffer():
     """no valid pixel: zero slices, every stage is a no-op, the image is untouched"""
     import dataclasses

@@ -34,5 +34,6 @@ for r in rows:
 ts = sum(x[0] for x in items) or 1
 ti = sum(x[1] for x in items) or 1
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 40
-for s, i, w, fn, ln, src in sorted(items, key=lambda x: -x[0])[:n]:
+key = 2 if os.environ.get("NCU_SORT") == "wf" else 0
+for s, i, w, fn, ln, src in sorted(items, key=lambda x: -x[key])[:n]:
     print(f"{fn[:12]:12s}:{ln:<4d} stall={100*s/ts:5.1f}% inst={100*i/ti:5.1f}% wf={w:.2e}  {src.strip()[:80]}")
