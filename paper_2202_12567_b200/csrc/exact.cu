@@ -1029,6 +1029,10 @@ constexpr int P2_THREADS = 1024;
 constexpr unsigned P2_INVALID = 0xFFFFFFFFu; // empty hash slot / no candidate (cells < 2^21)
 constexpr int P2_HBITS = 11;
 constexpr int P2_HSLOTS = 1 << P2_HBITS;     // 2 x P2_THREADS hash slots
+#ifndef P2_FAST_DRAWS
+#define P2_FAST_DRAWS 4
+#endif
+constexpr int P2_FAST = P2_FAST_DRAWS;       // draws per thread in a fast (uncut) batch
 
 struct P2Args {
     Upper up;
@@ -1089,7 +1093,7 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2(P2Args A)
     __shared__ double sh_dred[32];
     __shared__ unsigned long long sh_ured[32];
     __shared__ int sh_ired[32];
-    __shared__ int sh_count, sh_obs, sh_nnew, sh_draws;
+    __shared__ int sh_count, sh_obs, sh_nnew, sh_draws, sh_bacc;
     __shared__ int sh_cpre[P2_THREADS];   // per-column prefix offsets (carried entries, CSC)
 
     for (int k = tid; k < m * W; k += P2_THREADS) bm[k] = 0u;
@@ -1194,14 +1198,55 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2(P2Args A)
     const unsigned long long Wsum = n > 0 ? cdf[n - 1] : 0ull;
     const int64_t N = (int64_t)ceil(((double)((int64_t)m * (int64_t)n)) * A.rate);
     const int64_t cap = 64 * N;
-    if (tid == 0) { sh_count = sh_obs; sh_nnew = 0; sh_draws = 0; }
+    if (tid == 0) { sh_count = sh_obs; sh_nnew = 0; sh_draws = 0; sh_bacc = 0; }
     for (int e = tid; e < P2_HSLOTS; e += P2_THREADS) { hkey[e] = P2_INVALID; hmin[e] = 0xFFFFFFFFu; }
     __syncthreads();
-    // draws: column by the CDF, row uniformly; skip observed entries (R15, R16)
-    for (int64_t t0 = 0; t0 < cap; t0 += P2_THREADS) {
+    // draws: column by the CDF, row uniformly; skip observed entries (R15, R16).  The
+    // accepted set is the first N - |carried| distinct unobserved cells in draw order.  While the
+    // budget left is at least a whole fast batch (P2_FAST draws per thread), no draw of the batch can
+    // be cut off, so every new cell of the batch is accepted and duplicates resolve by atomicOr on
+    // the bitmap in any order (same set; newcells order is not used).  The last batches take the
+    // exact path: first occurrence per cell by smallest draw index, cut off at the budget.
+    for (int64_t t0 = 0; t0 < cap;) {
         const int count = sh_count;
         if (count >= N) break;
+        if (N - count >= (int64_t)P2_FAST * P2_THREADS) {
+#pragma unroll
+            for (int u = 0; u < P2_FAST; ++u) {
+                const int64_t t = t0 + (int64_t)u * P2_THREADS + tid;
+                bool isnew = false;
+                int cell = 0, cc = 0;
+                if (t < cap && n > 0) {
+                    uint4 uu = philox4((uint32_t)t, 0u, (uint32_t)s, TAG_P2, A.seed);
+                    unsigned long long x = ((unsigned long long)uu.x * Wsum) >> 32;
+                    int lo = 0, hi = n - 1;
+                    while (lo < hi) {
+                        int mid = (lo + hi) >> 1;
+                        if (cdf[mid] > x) hi = mid; else lo = mid + 1;
+                    }
+                    cc = lo;
+                    const int i = (int)randint_u(uu.y, (uint32_t)m);
+                    cell = (i << 11) | cc;
+                    const uint32_t bit = 1u << (cc & 31);
+                    isnew = !(atomicOr(&bm[i * W + (cc >> 5)], bit) & bit);
+                }
+                const unsigned bal = __ballot_sync(FULL_MASK, isnew);
+                int base = 0;
+                if (lane == 0 && bal) base = atomicAdd(&sh_bacc, __popc(bal));
+                base = __shfl_sync(FULL_MASK, base, 0);
+                if (isnew) {
+                    atomicAdd(&colcnt[cc], 1);
+                    A.newcells[ob + (count - sh_obs) + base + __popc(bal & ((1u << lane) - 1u))] = (uint32_t)cell;
+                }
+            }
+            __syncthreads();
+            if (tid == 0) { sh_count = count + sh_bacc; sh_bacc = 0; }
+            __syncthreads();
+            t0 += (int64_t)P2_FAST * P2_THREADS;
+            continue;
+        }
         const int64_t t = t0 + tid;
+        t0 += P2_THREADS;
         uint32_t key = P2_INVALID;
         int cell = 0, cc = 0;
         if (t < cap && n > 0) {
