@@ -749,7 +749,13 @@ __global__ void __launch_bounds__(256) k_slice_bbox(const int32_t *__restrict__ 
     }
 }
 
-__global__ void __launch_bounds__(256) k_pass1(int slot, Upper up, const int32_t *__restrict__ slice_off, int32_t s0, int32_t SL,
+#ifndef P1_MINB
+#define P1_MINB 4   // 64 registers, 4 CTAs per SM: pass 1 3.27 -> 2.12 ms at C4 (despite spills)
+#endif
+#ifndef CO_MINB
+#define CO_MINB 3   // 80 registers: coarsening 3.5 -> 3.35 ms at C4 (4: 3.6 ms)
+#endif
+__global__ void __launch_bounds__(256, P1_MINB) k_pass1(int slot, Upper up, const int32_t *__restrict__ slice_off, int32_t s0, int32_t SL,
                                                int32_t lbase, const float4 *__restrict__ prow,
                                                const float4 *__restrict__ vpl, uint64_t seed, int nmax,
                                                uint16_t *p1_rows, double *p1_Ta, double *p1_Tb, int32_t *p1_cnt,
@@ -822,7 +828,7 @@ __device__ __forceinline__ double warp_max_d(double v)
     return v;
 }
 
-__global__ void __launch_bounds__(CO_THREADS) k_coarsen(
+__global__ void __launch_bounds__(CO_THREADS, CO_MINB) k_coarsen(
     int slot, Upper up, const int32_t *__restrict__ slice_off, int32_t s0, int32_t lbase, const float4 *__restrict__ prow,
     const float4 *__restrict__ vpl, uint64_t seed, int nmax, double tau, const uint16_t *__restrict__ p1_rows,
     const double *__restrict__ p1_Ta, const double *__restrict__ p1_Tb, const int32_t *__restrict__ p1_cnt,
