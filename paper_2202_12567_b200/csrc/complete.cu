@@ -82,6 +82,11 @@ struct LArgs {
 };
 
 constexpr int LT = 1024;
+#ifndef ADM_COL_CHUNK
+#define ADM_COL_CHUNK 128
+#endif
+// (S, row) entries per column-phase chunk of the ADM kernel (Cfg<Q>::COL_CHUNK)
+__host__ __device__ constexpr int adm_col_chunk(int q) { return q >= 32 ? 64 : ADM_COL_CHUNK; }
 
 // Within a cp.async chunk (KA k-steps of R members, canonical position k * R + r) the entries are
 // stored V k-steps per member together: position (k - k % V) * R + r * V + k % V.  A lane group
@@ -114,8 +119,11 @@ __global__ void __launch_bounds__(LT, 1) k_layout(LArgs A)
     __shared__ int32_t sh_len[LT];
     __shared__ int32_t sh_who[LT];
     __shared__ float red[33];
-    const int ls = blockIdx.x, s = A.s0 + ls, tid = threadIdx.x, R = A.R;
+    const int ls = blockIdx.x, s = A.s0 + ls, tid = threadIdx.x;
     constexpr int P = PP;   // residues (bank sets) of a shared-memory phase: 32 / q
+    // compile-time shape (q = 32 / P): members per group R = 128 / q, k-steps per row chunk
+    // (512 bytes of 8-byte entries) and per column chunk -- the host's A.R / A.KAR / A.KAC
+    constexpr int R = 4 * PP, KAR = 64 / R, KAC = adm_col_chunk(32 / PP) / R;
     const int m = A.slice_off[s + 1] - A.slice_off[s], n = A.cut_n[ls];
     const int64_t ob = (int64_t)ls * A.ncap, sb = (int64_t)ls * A.scap;
     const int32_t *rp = A.rowptr + (int64_t)ls * (A.mmax + 1);
@@ -138,7 +146,7 @@ __global__ void __launch_bounds__(LT, 1) k_layout(LArgs A)
     for (int pass = 0; pass < 2; ++pass) {
         const bool rows_pass = pass == 1;
         const int cnt = rows_pass ? m : n;
-        const int KA = rows_pass ? A.KAR : A.KAC;   // k-steps per cp.async chunk
+        const int KA = rows_pass ? KAR : KAC;   // k-steps per cp.async chunk
         const int32_t *ptr = rows_pass ? rp : cp;
         uint16_t *perm = (rows_pass ? A.r_perm : A.c_perm) + (int64_t)ls * (rows_pass ? A.mmax : A.G);
         uint16_t *lens = (rows_pass ? A.r_len : A.c_len) + (int64_t)ls * (rows_pass ? A.mmax : A.G);
@@ -210,7 +218,7 @@ __global__ void __launch_bounds__(LT, 1) k_layout(LArgs A)
             } else {
                 const int g = nsolo + (mr - nsolo) / R;
                 r = (mr - nsolo) % R;
-                const int t = (r / A.D) % P;
+                const int t = r % P;   // D = 1: a lane group owns a member
                 base = sh_goff[g];
                 glen = (sh_goff[g + 1] - base) / R;
                 int acc = 0;
@@ -277,12 +285,12 @@ __global__ void __launch_bounds__(LT, 1) k_layout(LArgs A)
                 }
                 if (rows_pass) {
                     const float mh = A.val[ob + pos] * inv_sigma;
-                    A.r_ent[sb + base + vperm(rel, R, KA, VROW)] =
+                    A.r_ent[sb + base + vperm(rel, R, KAR, VROW)] =
                         ((unsigned long long)__float_as_uint(mh) << 32) |
                         ((unsigned long long)(uint32_t)A.map[ob + pos] << 11) | (unsigned long long)A.col[ob + pos];
                 } else {
-                    const int is = base + vperm(rel, R, KA, VS);
-                    A.c_ent[sb + base + vperm(rel, R, KA, VCR)] = A.csc_row[ob + pos];
+                    const int is = base + vperm(rel, R, KAC, VS);
+                    A.c_ent[sb + base + vperm(rel, R, KAC, VCR)] = A.csc_row[ob + pos];
                     A.map[ob + A.csc_src[ob + pos]] = is;
                     A.S[sb + is] = 0.f;
                 }
@@ -292,10 +300,10 @@ __global__ void __launch_bounds__(LT, 1) k_layout(LArgs A)
                 const int rel = solo ? k : k * R + r;
                 if (rows_pass) {
                     // sentinel: zero row n of Y, residual parked in the dummy slot
-                    A.r_ent[sb + base + vperm(rel, R, KA, VROW)] = ((unsigned long long)(uint32_t)dummy << 11) | (unsigned long long)n;
+                    A.r_ent[sb + base + vperm(rel, R, KAR, VROW)] = ((unsigned long long)(uint32_t)dummy << 11) | (unsigned long long)n;
                 } else {
-                    A.c_ent[sb + base + vperm(rel, R, KA, VCR)] = (uint16_t)m;   // sentinel: zero row m of X
-                    A.S[sb + base + vperm(rel, R, KA, VS)] = 0.f;                // padding slots stay finite
+                    A.c_ent[sb + base + vperm(rel, R, KAC, VCR)] = (uint16_t)m;   // sentinel: zero row m of X
+                    A.S[sb + base + vperm(rel, R, KAC, VS)] = 0.f;                // padding slots stay finite
                 }
             }
         }
@@ -330,9 +338,6 @@ struct CArgs {
 // q = 32: X and Y take twice the shared memory (a 1024-node cut at 512-row slices needs 197 KB),
 // so 16 warps with a 1 KB ring each and 64-entry column chunks (the same ring stages in half the
 // bytes); 512 threads leave 128 registers per thread.
-#ifndef ADM_COL_CHUNK
-#define ADM_COL_CHUNK 128
-#endif
 template <int Q>
 struct Cfg {
     static constexpr int L = Q / 4;           // lanes per row / column
@@ -344,7 +349,6 @@ struct Cfg {
 };
 __host__ __device__ constexpr int adm_threads(int q) { return q >= 32 ? 512 : 1024; }
 __host__ __device__ constexpr int adm_slot(int q) { return q >= 32 ? 512 : 1024; }
-__host__ __device__ constexpr int adm_col_chunk(int q) { return q >= 32 ? 64 : ADM_COL_CHUNK; }
 
 // ---- q = 16: the q x q products of the updates on the fp64 tensor cores ---------------------
 // mma.sync m8n8k4 f64 (g = lane / 4, t = lane % 4): a0 = A[g][t], b0 = B[t][g], c = C[g][2t..2t+1].
