@@ -405,6 +405,10 @@ __device__ __forceinline__ int mat_idx(int r, int c)
     if constexpr (TcMatvec<Q>::on) return frag16(r, c);
     return r * Q + c;
 }
+#ifndef GRAM_UNROLL
+#define GRAM_UNROLL 8   // 8 rows in flight per thread: k_adm 136.7 -> 136.1 ms at C4 (4: HEAD of round 1)
+#endif
+constexpr int kGramUnroll = GRAM_UNROLL;   // rows per unrolled step of the Gram partials
 // partial Gram sums of out[a][b] = sum_i A[i][a] B[i][b] over threads [t0, t0 + nthr):
 // P = nthr / (Q/4)^2 row partitions, each producing a Q x Q partial in part[p]
 template <int Q>
@@ -421,7 +425,7 @@ __device__ __forceinline__ int gram_partial(const float *A, const float *B, int 
         for (int x = 0; x < 4; ++x)
 #pragma unroll
             for (int y = 0; y < 4; ++y) acc[x][y] = 0.f;
-#pragma unroll 4
+#pragma unroll kGramUnroll
         for (int i = p; i < rows; i += P) {
             const float4 a = *reinterpret_cast<const float4 *>(A + (size_t)i * Q + 4 * ta);
             const float4 b = *reinterpret_cast<const float4 *>(B + (size_t)i * Q + 4 * tb);
@@ -442,6 +446,27 @@ __device__ __forceinline__ int gram_partial(const float *A, const float *B, int 
 template <int Q, bool MATVEC_ORDER = false>
 __device__ __forceinline__ void gram_reduce(float *out, const float *part, int P)
 {
+#if GRAM_RED4
+    // every thread sums a quarter of the partials of one element (a warp reads 32 consecutive
+    // elements: no bank conflicts), the four quarters meet in part[0..3] after a barrier
+    if ((int)blockDim.x >= 4 * Q * Q) {   // block-uniform; called by every thread of the block
+        const int e = threadIdx.x % (Q * Q), j = threadIdx.x / (Q * Q);
+        const int pq = (P + 3) / 4, pa = j * pq, pb = min(P, pa + pq);
+        float s = 0.f;
+        if (j < 4)
+            for (int p = pa; p < pb; ++p) s += part[(size_t)p * Q * Q + e];
+        __syncthreads();
+        float *q4 = const_cast<float *>(part);
+        if (j < 4) q4[j * Q * Q + e] = s;
+        __syncthreads();
+        if (j == 0) {
+            s = (q4[e] + q4[Q * Q + e]) + (q4[2 * Q * Q + e] + q4[3 * Q * Q + e]);
+            if constexpr (MATVEC_ORDER) out[mat_idx<Q>(e / Q, e % Q)] = s;
+            else out[e] = s;
+        }
+        return;
+    }
+#endif
     for (int e = threadIdx.x; e < Q * Q; e += blockDim.x) {
         float s = 0.f;
         for (int p = 0; p < P; ++p) s += part[(size_t)p * Q * Q + e];
