@@ -1481,17 +1481,18 @@ __global__ void __launch_bounds__(EV_WARPS * 32, EV_MINB) k_eval_new(int slot, U
         const Cand cd = col_candidates(&sc, bx, P.x, P.y, P.z);
         const double lu = up.lum[u];
         const int k1 = cp[c + 1];
-        for (int k0 = cp[c]; k0 < k1; k0 += 32) {
-            const int k = k0 + lane;
-            int pos = 0;
-            bool todo = false;
-            if (k < k1) {
-                pos = csc_src[ob + k];
-                todo = !carried[ob + pos];
-            }
+        // the CSR position and row of the next 32 entries are loaded one batch ahead, so only
+        // the carried-flag load is exposed before the evaluation
+        int k0 = cp[c];
+        int pos_n = 0, row_n = 0;
+        if (k0 + lane < k1) { pos_n = csc_src[ob + k0 + lane]; row_n = csc_row[ob + k0 + lane]; }
+        for (; k0 < k1; k0 += 32) {
+            const bool in = k0 + lane < k1;
+            const int pos = pos_n, i = row_n;
+            const bool todo = in && !carried[ob + pos];
+            if (k0 + 32 + lane < k1) { pos_n = csc_src[ob + k0 + 32 + lane]; row_n = csc_row[ob + k0 + 32 + lane]; }
             if (!__any_sync(FULL_MASK, todo)) continue;
             if (todo) {
-                const int i = csc_row[ob + k];
                 const double T = entry_T_w(&sc, slot, prow, lrow0 + i, vpl, v, cd.s, cd.b, cd.r);
                 const double val_d = (lum_rho_d(prow, lrow0 + i) * lu) * T;
                 val[ob + pos] = (float)val_d;
