@@ -85,7 +85,8 @@ def lib():
     global _lib
     with _lock:
         if _lib is None:
-            L = C.CDLL(build())
+            # ORACLE_LIB: a prebuilt alternative (tools/mutants.py loads deliberately broken copies)
+            L = C.CDLL(os.environ.get("ORACLE_LIB") or build())
             P = C.c_void_p
             L.orc_philox.argtypes = [P, P, P]
             L.orc_floyd.argtypes = [C.c_int32, C.c_int32, C.c_uint32, C.c_int32, C.c_uint64, C.c_uint32, P]
@@ -107,6 +108,11 @@ def lib():
             L.orc_mals.restype = C.c_int32
             L.orc_fullcut_slice.argtypes = [C.POINTER(_Inputs), P, C.c_int32, P, C.c_int32, P]
             L.orc_bruteforce_rows.argtypes = [C.POINTER(_Inputs), P, C.c_int32, P]
+            L.orc_light_importance.argtypes = [C.c_int32, C.c_int64, P, P, P, P]
+            L.orc_pdf_weights.argtypes = [C.c_int32, P, P, P]
+            L.orc_cdf_pick.argtypes = [C.c_int32, P, C.c_uint64]
+            L.orc_cdf_pick.restype = C.c_int32
+            L.orc_pass2_draws.argtypes = [C.c_uint64, C.c_int32, C.c_uint32, C.c_int64, P, C.c_int32, C.c_int32, P, P]
             _lib = L
     return _lib
 
@@ -298,3 +304,34 @@ def mals(m, n, row, col, val, q, K=100, lam=1e-3, seed=12567, slice_id=0):
     flags = lib().orc_mals(m, n, row.size, _p(row), _p(col), _p(val), q, K, lam, seed, slice_id, _p(X), _p(Y),
                            _p(obj), _p(sg))
     return dict(X=X, Y=Y, obj=obj, sigma=float(sg[0]), flags=flags)
+
+
+def light_importance(n, col, val):
+    """g(c) = max - min of column c's observations and the observation counts."""
+    col = np.ascontiguousarray(col, np.int32)
+    val = np.ascontiguousarray(val, np.float64)
+    g = np.zeros(max(n, 1))
+    cnt = np.zeros(max(n, 1), np.int32)
+    lib().orc_light_importance(n, col.size, _p(col), _p(val), _p(g), _p(cnt))
+    return g[:n], cnt[:n]
+
+
+def pdf_weights(g, cnt):
+    g = np.ascontiguousarray(g, np.float64)
+    cnt = np.ascontiguousarray(cnt, np.int32)
+    w = np.zeros(max(g.size, 1), np.uint32)
+    lib().orc_pdf_weights(g.size, _p(g), _p(cnt), _p(w))
+    return w[:g.size]
+
+
+def cdf_pick(cdf, x):
+    cdf = np.ascontiguousarray(cdf, np.uint64)
+    return int(lib().orc_cdf_pick(cdf.size, _p(cdf), int(x)))
+
+
+def pass2_draws(w, m, count, seed=12567, slice_id=0, t0=0):
+    w = np.ascontiguousarray(w, np.uint32)
+    rows = np.zeros(count, np.int32)
+    cols = np.zeros(count, np.int32)
+    lib().orc_pass2_draws(seed, slice_id, t0, count, _p(w), w.size, m, _p(rows), _p(cols))
+    return rows, cols

@@ -530,6 +530,90 @@ static void coarsen(slice_ctx *c, orc_slice_result *res, const int32_t *parent)
 }
 
 /* ------------------------------------------------------------------------------------------
+ * Pass-2 building blocks (public so that tests can pin them on hand-made inputs).
+ * ---------------------------------------------------------------------------------------- */
+/* g(c) = max(C_c) - min(C_c) over the observations of column c ("the maximal value
+ * minus the minimal value of the sampled elements of C_j"); cnt[c] = observations of c, g = 0
+ * when cnt[c] <= 1 (R14).  Order-free, exact. */
+void orc_light_importance(int32_t n, int64_t nobs, const int32_t *col, const double *val, double *g, int32_t *cnt)
+{
+    double *lo = malloc((size_t)(n > 0 ? n : 1) * sizeof(double));
+    double *hi = malloc((size_t)(n > 0 ? n : 1) * sizeof(double));
+    for (int32_t c = 0; c < n; ++c) { cnt[c] = 0; lo[c] = INFINITY; hi[c] = -INFINITY; g[c] = 0.0; }
+    for (int64_t k = 0; k < nobs; ++k) {
+        int32_t c = col[k];
+        lo[c] = fmin(lo[c], val[k]);
+        hi[c] = fmax(hi[c], val[k]);
+        cnt[c]++;
+    }
+    for (int32_t c = 0; c < n; ++c)
+        if (cnt[c]) g[c] = hi[c] - lo[c];
+    free(lo);
+    free(hi);
+}
+
+/* Integer pdf weights of the columns (Eq. 2 with f(i) = 1, reading R14): with G = max_c g(c) > 0,
+ * an observed column gets max(2^16, 1 + floor((2^20 - 1) g(c) / G)), an unobserved one the mean
+ * (integer division) of the observed weights (2^19 if none is observed); G = 0 gives 1 everywhere. */
+void orc_pdf_weights(int32_t n, const double *g, const int32_t *cnt, uint32_t *w)
+{
+    double G = 0.0;
+    for (int32_t c = 0; c < n; ++c)
+        if (cnt[c] && g[c] > G) G = g[c];
+    if (G > 0.0) {
+        uint64_t sumw = 0;
+        int32_t nobsc = 0;
+        for (int32_t c = 0; c < n; ++c) {
+            if (!cnt[c]) continue;
+            double x = floor(1048575.0 * (g[c] / G));
+            uint32_t wc = 1u + (uint32_t)x;
+            w[c] = wc > 65536u ? wc : 65536u;
+            sumw += w[c];
+            nobsc++;
+        }
+        uint32_t wu = nobsc ? (uint32_t)(sumw / (uint64_t)nobsc) : 524288u;
+        for (int32_t c = 0; c < n; ++c)
+            if (!cnt[c]) w[c] = wu;
+    } else {
+        for (int32_t c = 0; c < n; ++c) w[c] = 1u;
+    }
+}
+
+/* CDF inversion (R29): the smallest c with cdf[c] > x (cdf inclusive prefix sums of the weights) */
+int32_t orc_cdf_pick(int32_t n, const uint64_t *cdf, uint64_t x)
+{
+    int32_t lo = 0, hi = n - 1;
+    while (lo < hi) {
+        int32_t mid = (lo + hi) / 2;
+        if (cdf[mid] > x) hi = mid; else lo = mid + 1;
+    }
+    return lo;
+}
+
+/* Draw t of pass 2 ("select a column by its importance, then a row uniformly", O7):
+ * u = Philox(t, 0, slice, P2); column = CDF^-1((u0 W) >> 32); row = (u1 m) >> 32. */
+void orc_pass2_draw(uint64_t seed, int32_t slice, uint32_t t, uint64_t W, const uint64_t *cdf, int32_t n, int32_t m,
+                    int32_t *row, int32_t *col)
+{
+    uint32_t u[4];
+    philox_draw(seed, t, 0u, (uint32_t)slice, TAG_P2, u);
+    uint64_t x = ((uint64_t)u[0] * W) >> 32;
+    *col = orc_cdf_pick(n, cdf, x);
+    *row = (int32_t)randint(u[1], (uint32_t)m);
+}
+
+/* draws t0 .. t0+count-1 of pass 2 without the observed-cell test (statistical pins) */
+void orc_pass2_draws(uint64_t seed, int32_t slice, uint32_t t0, int64_t count, const uint32_t *w, int32_t n, int32_t m,
+                     int32_t *rows, int32_t *cols)
+{
+    uint64_t *cdf = malloc((size_t)(n > 0 ? n : 1) * sizeof(uint64_t));
+    uint64_t W = 0;
+    for (int32_t c = 0; c < n; ++c) { W += w[c]; cdf[c] = W; }
+    for (int64_t k = 0; k < count; ++k) orc_pass2_draw(seed, slice, t0 + (uint32_t)k, W, cdf, n, m, rows + k, cols + k);
+    free(cdf);
+}
+
+/* ------------------------------------------------------------------------------------------
  * Sampling pass 2 (Eq. (2); readings R13-R17, R27).
  * ---------------------------------------------------------------------------------------- */
 static void pass2(slice_ctx *c, orc_slice_result *res)
@@ -560,38 +644,24 @@ static void pass2(slice_ctx *c, orc_slice_result *res)
         }
     }
     res->n_carried = n_obs;
-    /* light importance g(j) = max(C_j) - min(C_j) over observed entries (R14) */
-    uint32_t *w = malloc((size_t)(n > 0 ? n : 1) * sizeof(uint32_t));
-    double *g = calloc((size_t)(n > 0 ? n : 1), sizeof(double));
-    double G = 0.0;
-    for (int32_t cc = 0; cc < n; ++cc) {
-        if (!colcnt[cc]) continue;
-        double lo = INFINITY, hi = -INFINITY;
+    /* light importance g(j) = max(C_j) - min(C_j) over the observed entries (R14) */
+    int32_t *ocol = malloc((size_t)(n_obs > 0 ? n_obs : 1) * sizeof(int32_t));
+    double *oval = malloc((size_t)(n_obs > 0 ? n_obs : 1) * sizeof(double));
+    int64_t no = 0;
+    for (int32_t cc = 0; cc < n; ++cc)
         for (int32_t i = 0; i < m; ++i) {
             size_t at = (size_t)i * (size_t)n + (size_t)cc;
-            if (obs[at]) { lo = fmin(lo, val[at]); hi = fmax(hi, val[at]); }
+            if (obs[at]) { ocol[no] = cc; oval[no] = val[at]; no++; }
         }
-        g[cc] = hi - lo;
-        if (g[cc] > G) G = g[cc];
-    }
+    uint32_t *w = malloc((size_t)(n > 0 ? n : 1) * sizeof(uint32_t));
+    double *g = calloc((size_t)(n > 0 ? n : 1), sizeof(double));
+    int32_t *gcnt = calloc((size_t)(n > 0 ? n : 1), sizeof(int32_t));
+    orc_light_importance(n, no, ocol, oval, g, gcnt);
     /* pixel importance f(i) = 1; pdf(i,j) ∝ f(i) g(j) (Eq. 2) as integer weights (R14) */
-    if (G > 0.0) {
-        uint64_t sumw = 0;
-        int32_t nobsc = 0;
-        for (int32_t cc = 0; cc < n; ++cc) {
-            if (!colcnt[cc]) continue;
-            double x = floor(1048575.0 * (g[cc] / G));
-            uint32_t wc = 1u + (uint32_t)x;
-            w[cc] = wc > 65536u ? wc : 65536u;
-            sumw += w[cc];
-            nobsc++;
-        }
-        uint32_t wu = nobsc ? (uint32_t)(sumw / (uint64_t)nobsc) : 524288u;
-        for (int32_t cc = 0; cc < n; ++cc)
-            if (!colcnt[cc]) w[cc] = wu;
-    } else {
-        for (int32_t cc = 0; cc < n; ++cc) w[cc] = 1u;
-    }
+    orc_pdf_weights(n, g, gcnt, w);
+    free(ocol);
+    free(oval);
+    free(gcnt);
     uint64_t *cdf = malloc((size_t)(n > 0 ? n : 1) * sizeof(uint64_t));
     uint64_t W = 0;
     for (int32_t cc = 0; cc < n; ++cc) { W += w[cc]; cdf[cc] = W; }
@@ -600,16 +670,8 @@ static void pass2(slice_ctx *c, orc_slice_result *res)
     res->target_N = N;
     int64_t n_new = 0, t = 0;
     for (t = 0; t < 64 * N && n_obs < N; ++t) {
-        uint32_t u[4];
-        philox_draw(in->seed, (uint32_t)t, 0u, (uint32_t)c->s, TAG_P2, u);
-        uint64_t x = ((uint64_t)u[0] * W) >> 32;
-        int32_t lo = 0, hi = n - 1; /* smallest c with CDF_c > x */
-        while (lo < hi) {
-            int32_t mid = (lo + hi) / 2;
-            if (cdf[mid] > x) hi = mid; else lo = mid + 1;
-        }
-        int32_t cc = lo;
-        int32_t i = (int32_t)randint(u[1], (uint32_t)m);
+        int32_t i, cc;
+        orc_pass2_draw(in->seed, c->s, (uint32_t)t, W, cdf, n, m, &i, &cc);
         size_t at = (size_t)i * (size_t)n + (size_t)cc;
         if (!obs[at]) {
             obs[at] = 1;

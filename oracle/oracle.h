@@ -88,6 +88,15 @@ double orc_entry_T(const orc_inputs *in, int64_t row, int64_t vpl);
 int32_t orc_visible(const orc_inputs *in, const double x[3], const double y[3]);
 /* Matrix slicing, P:71-73 / P:172 with reading R26 */
 int32_t orc_build_slices(const orc_inputs *in, int32_t *off, int32_t *rows, int64_t *nslices);
+/* Pass-2 building blocks (readings R14, R29): light importance g(c) = max - min of
+ * each column's observations, integer pdf weights, CDF inversion, one draw (t) of the pass */
+void orc_light_importance(int32_t n, int64_t nobs, const int32_t *col, const double *val, double *g, int32_t *cnt);
+void orc_pdf_weights(int32_t n, const double *g, const int32_t *cnt, uint32_t *w);
+int32_t orc_cdf_pick(int32_t n, const uint64_t *cdf, uint64_t x);
+void orc_pass2_draw(uint64_t seed, int32_t slice, uint32_t t, uint64_t W, const uint64_t *cdf, int32_t n, int32_t m,
+                    int32_t *row, int32_t *col);
+void orc_pass2_draws(uint64_t seed, int32_t slice, uint32_t t0, int64_t count, const uint32_t *w, int32_t n, int32_t m,
+                     int32_t *rows, int32_t *cols);
 /* Per-slice pipeline: coarsening, sampling, completion (App. A),
  * resolve.  stage: 1 = coarsen, 2 = + pass 2, 3 = + completion, 4 = + resolve */
 orc_slice_result *orc_run_slice(const orc_inputs *in, const int32_t *rows, int32_t m, int32_t slice, int32_t stage);
