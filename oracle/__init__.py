@@ -93,6 +93,7 @@ def lib():
             L.orc_floyd.restype = C.c_int32
             L.orc_entry_T.argtypes = [C.POINTER(_Inputs), C.c_int64, C.c_int64]
             L.orc_entry_T.restype = C.c_double
+            L.orc_entry_T_many.argtypes = [C.POINTER(_Inputs), C.c_int64, P, P, P]
             L.orc_visible.argtypes = [C.POINTER(_Inputs), P, P]
             L.orc_visible.restype = C.c_int32
             L.orc_build_slices.argtypes = [C.POINTER(_Inputs), P, P, P]
@@ -177,6 +178,13 @@ class Oracle:
     # -- primitives -------------------------------------------------------------------------
     def entry_T(self, row: int, vpl: int) -> float:
         return lib().orc_entry_T(C.byref(self.s), int(row), int(vpl))
+
+    def entries_T(self, rows, vpls):
+        rows = np.ascontiguousarray(rows, np.int32)
+        vpls = np.ascontiguousarray(vpls, np.int32)
+        out = np.zeros(rows.size)
+        lib().orc_entry_T_many(C.byref(self.s), rows.size, _p(rows), _p(vpls), _p(out))
+        return out
 
     def visible(self, x, y) -> bool:
         a = np.ascontiguousarray(x, np.float64)

@@ -200,6 +200,12 @@ double orc_entry_T(const orc_inputs *in, int64_t p, int64_t v)
     return phi * G;
 }
 
+/* T for n (row, vpl) pairs, one orc_entry_T call each (test convenience, no new arithmetic) */
+void orc_entry_T_many(const orc_inputs *in, int64_t n, const int32_t *rows, const int32_t *vpls, double *out)
+{
+    for (int64_t k = 0; k < n; ++k) out[k] = orc_entry_T(in, rows[k], vpls[k]);
+}
+
 static double lum_rho(const orc_inputs *in, int64_t p) { return lum3(in->rr[p], in->rg[p], in->rb[p]); }
 static double lum_node(const orc_inputs *in, int32_t f) { return lum3(in->tir[f], in->tig[f], in->tib[f]); }
 

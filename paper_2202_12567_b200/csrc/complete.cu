@@ -332,6 +332,7 @@ struct CArgs {
     int32_t *flags, *iters;
     const int32_t *order;       // CTA -> slice, or null for CTA = slice
     unsigned long long *prof;   // optional phase clocks (LMC_ADM_PROF=1), else null
+    int32_t force_nf;           // test hook (LMC_TEST_NONFINITE_SLICE): this slice's residual is made NaN
 };
 
 // Per-rank kernel shape.  q <= 16: 32 warps, a 2 KB ring per warp, 128-entry column chunks.
@@ -925,7 +926,7 @@ __global__ void __launch_bounds__(Cfg<Q>::NT, 1) k_adm(CArgs A)
         }
     }
     const float ss = block_reduce<false>(row_residual_ss<Q>(X, Y, A, ls, m, warp, nwarps, lane), red);
-    const float res = sqrtf(ss / nrmM2);
+    const float res = s == A.force_nf ? __int_as_float(0x7fc00000) : sqrtf(ss / nrmM2);
     for (int e = tid; e < n * Q; e += NT) Vg[e] *= sigma;   // R22: output (U_K, sigma V_K)
     if (PROF) {
         if (tid < 8) sh_prof[tid] = 0;
@@ -1048,6 +1049,8 @@ cudaError_t run_adm(lmc_ctx *c, int nmax)
     A.iters = c->d.iters;
     A.prof = nullptr;
     A.order = c->adm_ordered ? c->d.adm_order : nullptr;
+    const char *fe = getenv("LMC_TEST_NONFINITE_SLICE");
+    A.force_nf = fe ? atoi(fe) : -1;
     // LMC_ADM_PROF=1: per-phase clock64 totals (diagnostic only; synchronises and prints to stderr)
     const char *pe = getenv("LMC_ADM_PROF");
     const bool prof = pe && pe[0] == '1' && c->q == 16;   // instrumented build for q = 16 only
@@ -1084,7 +1087,7 @@ cudaError_t run_adm(lmc_ctx *c, int nmax)
 struct RArgs {
     const int32_t *slice_off, *rows, *pixel, *cut_n, *cut_cols, *flags;
     int32_t s0, lbase, G, q;
-    int64_t row0;
+    int64_t row0, npix;                 // npix = width * height (image writes are bounds-checked)
     const float *U, *V, *I, *direct_rgb;
     const float4 *prow;
     float *image, *rows_rgb;
@@ -1151,6 +1154,7 @@ __global__ void __launch_bounds__(256) k_resolve(RArgs A)
         }
         if (A.image) {
             const int64_t p = A.pixel[A.rows[A.row0 + li]];
+            if (p < 0 || p >= A.npix) continue;   // rejected at lmc_create / lmc_upload_inputs
             A.image[3 * p] = o0;
             A.image[3 * p + 1] = o1;
             A.image[3 * p + 2] = o2;
@@ -1173,6 +1177,7 @@ cudaError_t run_resolve(lmc_ctx *c, float *image, float *rows_rgb)
     A.G = c->G;
     A.q = c->q;
     A.row0 = c->row0;
+    A.npix = (int64_t)c->W * c->H;
     A.U = c->d.U;
     A.V = c->d.V;
     A.I = c->d.ut_I;
@@ -1185,11 +1190,12 @@ cudaError_t run_resolve(lmc_ctx *c, float *image, float *rows_rgb)
 }
 
 __global__ void k_scatter(int64_t M, const int32_t *__restrict__ rows, const int32_t *__restrict__ pixel,
-                          const float *__restrict__ all_rows, float *image)
+                          const float *__restrict__ all_rows, float *image, int64_t npix)
 {
     int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= M) return;
     const int64_t p = pixel[rows[k]];
+    if (p < 0 || p >= npix) return;
     image[3 * p] = all_rows[3 * k];
     image[3 * p + 1] = all_rows[3 * k + 1];
     image[3 * p + 2] = all_rows[3 * k + 2];
@@ -1198,7 +1204,85 @@ __global__ void k_scatter(int64_t M, const int32_t *__restrict__ rows, const int
 cudaError_t run_scatter(lmc_ctx *c, const float *all_rows, float *image)
 {
     if (c->M == 0) return cudaSuccess;
-    k_scatter<<<(unsigned)((c->M + 255) / 256), 256, 0, c->stream>>>(c->M, c->d.rows, c->d.pixel, all_rows, image);
+    k_scatter<<<(unsigned)((c->M + 255) / 256), 256, 0, c->stream>>>(c->M, c->d.rows, c->d.pixel, all_rows, image,
+                                                                       (int64_t)c->W * c->H);
+    return cudaGetLastError();
+}
+
+// image index of every row of this rank (slice-row order) -- the host-buffer resolve scatters with it
+__global__ void k_rank_pixels(int64_t ML, int64_t row0, const int32_t *__restrict__ rows, const int32_t *__restrict__ pixel,
+                              int32_t *out)
+{
+    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < ML) out[k] = pixel[rows[row0 + k]];
+}
+cudaError_t run_rank_pixels(lmc_ctx *c, int32_t *out)
+{
+    if (c->ML == 0) return cudaSuccess;
+    k_rank_pixels<<<(unsigned)((c->ML + 255) / 256), 256, 0, c->stream>>>(c->ML, c->row0, c->d.rows, c->d.pixel, out);
+    return cudaGetLastError();
+}
+
+// G-buffer pixel indices must lie in [0, width * height) (lmc.h: LMC_EINVAL otherwise)
+__global__ void k_check_pixels(int64_t M, const int32_t *__restrict__ pixel, int64_t npix, unsigned long long *flag)
+{
+    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < M && (pixel[k] < 0 || pixel[k] >= npix)) atomicOr(flag, 1ull);
+}
+cudaError_t run_check_pixels(lmc_ctx *c, unsigned long long *flag)
+{
+    cudaError_t e = cudaMemsetAsync(flag, 0, sizeof(unsigned long long), c->stream);
+    if (e != cudaSuccess || c->M == 0) return e;
+    k_check_pixels<<<(unsigned)((c->M + 255) / 256), 256, 0, c->stream>>>(c->M, c->d.pixel, (int64_t)c->W * c->H, flag);
+    return cudaGetLastError();
+}
+
+// Completion launch order on the device (no host round trip): slice order, except that the nsm
+// slices with the fewest samples run last, largest first, so the final wave holds the shortest
+// CTAs.  sorted = slices by ascending |Omega| (stable radix sort); one CTA compacts the rest.
+__global__ void __launch_bounds__(1024) k_launch_order(int32_t SL, int32_t ntail, const int32_t *__restrict__ sorted,
+                                                       int32_t *mark, int32_t *order)
+{
+    typedef cub::BlockScan<int32_t, 1024> Scan;
+    __shared__ typename Scan::TempStorage tmp;
+    __shared__ int32_t base;
+    for (int k = threadIdx.x; k < SL; k += 1024) mark[k] = 0;
+    __syncthreads();
+    for (int k = threadIdx.x; k < ntail; k += 1024) mark[sorted[k]] = 1;
+    if (threadIdx.x == 0) base = 0;
+    __syncthreads();
+    for (int k0 = 0; k0 < SL; k0 += 1024) {
+        const int k = k0 + (int)threadIdx.x;
+        const int keep = k < SL && !mark[k];
+        int pos, tot;
+        Scan(tmp).ExclusiveSum(keep, pos, tot);
+        if (keep) order[base + pos] = k;
+        __syncthreads();
+        if (threadIdx.x == 0) base += tot;
+        __syncthreads();
+    }
+    for (int k = threadIdx.x; k < ntail; k += 1024) order[SL - ntail + k] = sorted[ntail - 1 - k];
+}
+__global__ void k_iota(int32_t n, int32_t *a)
+{
+    int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < n) a[k] = k;
+}
+cudaError_t launch_order_bytes(int32_t SL, size_t *bytes)
+{
+    *bytes = 0;
+    return cub::DeviceRadixSort::SortPairs(nullptr, *bytes, (const int32_t *)nullptr, (int32_t *)nullptr,
+                                           (const int32_t *)nullptr, (int32_t *)nullptr, SL);
+}
+cudaError_t run_launch_order(lmc_ctx *c, int ntail)
+{
+    const int SL = c->SL;
+    int32_t *keys_out = c->d.ord_tmp, *iota = c->d.ord_tmp + SL, *sorted = c->d.ord_tmp + 2 * SL, *mark = c->d.ord_tmp + 3 * SL;
+    k_iota<<<(SL + 255) / 256, 256, 0, c->stream>>>(SL, iota);
+    size_t bytes = c->d.ord_cub_bytes;
+    cudaError_t e = cub::DeviceRadixSort::SortPairs(c->d.ord_cub, bytes, c->d.nnz, keys_out, iota, sorted, SL, 0, 32, c->stream);
+    if (e != cudaSuccess) return e;
+    k_launch_order<<<1, 1024, 0, c->stream>>>(SL, ntail, sorted, mark, c->d.adm_order);
     return cudaGetLastError();
 }
 

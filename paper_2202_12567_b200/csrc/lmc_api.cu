@@ -88,10 +88,13 @@ void free_all(lmc_ctx *c)
                     d.rowptr, d.col, d.val, d.val64, d.Xd, d.Yd, d.val64c, d.carried, d.colptr, d.csc_row, d.csc_src, d.nnz, d.target_n, d.n_new,
                     d.newcells, d.newpos, d.U, d.V, d.Lam, d.Pi, d.Xold, d.S, d.flags, d.iters, d.resid,
                     d.direct_rgb, d.counters, d.img, d.rows_rgb, d.vpl_soa, d.r_perm, d.r_len, d.c_perm, d.c_len,
-                    d.r_goff, d.c_goff, d.c_nsolo, d.adm_order, d.r_ent, d.c_ent, d.norm};
+                    d.r_goff, d.c_goff, d.c_nsolo, d.adm_order, d.r_ent, d.c_ent, d.norm, d.r_grp, d.c_grp,
+                    d.r_slot, d.c_slot, d.ngrp, d.ctot, d.slot_st, d.ord_tmp, d.ord_cub, d.rank_pix};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (c->h_stage) cudaFreeHost(c->h_stage);
+    if (c->h_pix) cudaFreeHost(c->h_pix);
+    c->h_pix = nullptr;
     memset(&c->d, 0, sizeof(c->d));
     c->h_stage = nullptr;
     if (c->ev_ok)
@@ -367,6 +370,7 @@ lmc_status check_overflow(lmc_ctx *c)
     CK(cudaStreamSynchronize(c->stream), "sync");
     if (cnt[3] & 1ull) return fail(c, LMC_EOVERFLOW, "coarsening sample pool overflow (cap %lld)", (long long)c->pool_cap);
     if (cnt[3] & 2ull) return fail(c, LMC_EOVERFLOW, "pass-2 sample capacity overflow (cap %lld)", (long long)c->ncap);
+    if (cnt[3] & 4ull) return fail(c, LMC_EOVERFLOW, "completion layout capacity overflow (cap %lld)", (long long)c->scap);
     return LMC_OK;
 }
 
@@ -425,10 +429,14 @@ static lmc_status create_impl(lmc_ctx *c, const lmc_gbuffer *g, const lmc_vpls *
     if (cfg.solver != LMC_SOLVER_ADM && cfg.solver != LMC_SOLVER_MALS) return fail(c, LMC_EINVAL, "unknown solver");
     if (cfg.p1_nmax < 1 || cfg.p1_nmax > MAX_NMAX || cfg.p1_nmin < 1) return fail(c, LMC_EINVAL, "p1_nmax must be in [1, 32], p1_nmin >= 1");
     if (cfg.max_iter < 0) return fail(c, LMC_EINVAL, "max_iter must be >= 0");
+    if (cfg.solver == LMC_SOLVER_MALS && cfg.max_iter < 1) return fail(c, LMC_EINVAL, "MALS needs max_iter >= 1");
     if (cfg.world < 1 || cfg.rank < 0 || cfg.rank >= cfg.world) return fail(c, LMC_EINVAL, "bad rank/world");
     if (cfg.input_memory != LMC_MEM_DEVICE && cfg.input_memory != LMC_MEM_HOST) return fail(c, LMC_EINVAL, "bad input_memory");
     if (!g || !v || !t || !sc) return fail(c, LMC_EINVAL, "null input struct");
     if (g->count < 0 || g->count > (1ll << 31) - 1) return fail(c, LMC_EINVAL, "bad gbuffer count");
+    if (g->width < 0 || g->height < 0 || (int64_t)g->width * g->height > (1ll << 31) - 1 ||
+        (g->count > 0 && (g->width < 1 || g->height < 1)))
+        return fail(c, LMC_EINVAL, "bad image size %d x %d", g->width, g->height);
     if (g->count > 0 && (!g->pixel || !g->px || !g->py || !g->pz || !g->nx || !g->ny || !g->nz || !g->vx || !g->vy ||
                          !g->vz || !g->rho_r || !g->rho_g || !g->rho_b || !g->spec || !g->exponent))
         return fail(c, LMC_EINVAL, "null gbuffer array");
@@ -502,6 +510,23 @@ static lmc_status create_impl(lmc_ctx *c, const lmc_gbuffer *g, const lmc_vpls *
         // cp.async chunks per group (<= 128 entries per group) plus the dummy slot; multiple of 8
         const int64_t mg = std::max<int64_t>(c->mmax, G);
         c->scap = (c->ncap + 32 * mg + 128 * mg + 256 + 7) & ~7ll;
+        // lane-per-segment layout (complete2.cu): a member of len entries takes the next power of
+        // two >= ceil(len / T) segments (< 2 len / T + 2), groups of 32 segments of <= T entries
+        // padded to multiples of 8 k-steps
+        // q <= 8: lane-per-segment kernel (complete2.cu; 1.6-2.6x faster than the lane-group kernel
+        // on the C5 sweep); q = 16: the lane-group kernel (complete.cu) unless LMC_ADM2=1 (equal at
+        // C2/C3, slower when the residuals S spill from shared memory, C4 and 20% rates: DESIGN.md §6)
+        const char *ev = getenv("LMC_ADM_V1"), *e2 = getenv("LMC_ADM2");
+        c->use_adm2 = cfg.solver == LMC_SOLVER_ADM && (cfg.rank_q <= 8 || (cfg.rank_q == 16 && e2 && e2[0] == '1')) &&
+                      !(ev && ev[0] == '1');
+        if (c->use_adm2) {
+            const int64_t T = std::min(c->adm2_Tr, c->adm2_Tc), Tmax = std::max(c->adm2_Tr, c->adm2_Tc);
+            c->gcap = (2 * c->ncap / T + 2 * mg + 31) / 32 + 2;
+            const int64_t cap2 = 32 * ((Tmax + 7) / 8 * 8) * c->gcap + 256;
+            if (cap2 >= (1ll << 19)) c->use_adm2 = false;   // S positions are 19-bit in the row entries
+            else c->scap = std::max(c->scap, cap2);
+        }
+        c->scap = (c->scap + 255) & ~255ll;
     }
     // device arena
     Dev &d = c->d;
@@ -556,11 +581,12 @@ static lmc_status create_impl(lmc_ctx *c, const lmc_gbuffer *g, const lmc_vpls *
     CK(dalloc(&d.n_new, SL), "alloc pass2");
     CK(dalloc(&d.newcells, SL * c->ncap), "alloc pass2");
     CK(dalloc(&d.newpos, SL * c->ncap), "alloc pass2");
-    CK(dalloc(&d.U, ML * c->q), "alloc factors");
-    CK(dalloc(&d.Lam, ML * c->q), "alloc factors");
-    CK(dalloc(&d.Xold, ML * c->q), "alloc factors");
-    CK(dalloc(&d.V, SL * G * c->q), "alloc factors");
-    CK(dalloc(&d.Pi, SL * G * c->q), "alloc factors");
+    // + q: the lane-group ADM kernel reads (and discards) the zero sentinel row m / column n
+    CK(dalloc(&d.U, ML * c->q + c->q), "alloc factors");
+    CK(dalloc(&d.Lam, ML * c->q + c->q), "alloc factors");
+    CK(dalloc(&d.Xold, ML * c->q + c->q), "alloc factors");
+    CK(dalloc(&d.V, SL * G * c->q + c->q), "alloc factors");
+    CK(dalloc(&d.Pi, SL * G * c->q + c->q), "alloc factors");
     CK(dalloc(&d.S, SL * c->scap), "alloc factors");
     CK(dalloc(&d.r_perm, SL * c->mmax), "alloc layout");
     CK(dalloc(&d.r_len, SL * c->mmax), "alloc layout");
@@ -570,9 +596,23 @@ static lmc_status create_impl(lmc_ctx *c, const lmc_gbuffer *g, const lmc_vpls *
     CK(dalloc(&d.c_goff, SL * (G + 1)), "alloc layout");
     CK(dalloc(&d.c_nsolo, SL), "alloc layout");
     CK(dalloc(&d.adm_order, SL), "alloc layout");
+    CK(dalloc(&d.ord_tmp, 4 * SL), "alloc layout");
+    CK(launch_order_bytes((int32_t)std::max<int64_t>(SL, 1), &d.ord_cub_bytes), "cub sizing");
+    CK(cudaMalloc(&d.ord_cub, std::max<size_t>(d.ord_cub_bytes, 16)), "alloc cub");
+    CK(dalloc(&d.rank_pix, ML), "alloc resolve");
+    CK(cudaMallocHost(&c->h_pix, sizeof(int32_t) * (size_t)std::max<int64_t>(ML, 1)), "alloc staging");
     CK(dalloc(&d.r_ent, SL * c->scap), "alloc layout");
     CK(dalloc(&d.c_ent, SL * c->scap), "alloc layout");
     CK(dalloc(&d.norm, SL), "alloc layout");
+    if (c->use_adm2) {
+        CK(dalloc(&d.r_grp, SL * c->gcap), "alloc layout");
+        CK(dalloc(&d.c_grp, SL * c->gcap), "alloc layout");
+        CK(dalloc(&d.r_slot, SL * c->gcap * 32), "alloc layout");
+        CK(dalloc(&d.c_slot, SL * c->gcap * 32), "alloc layout");
+        CK(dalloc(&d.ngrp, 2 * SL), "alloc layout");
+        CK(dalloc(&d.ctot, SL), "alloc layout");
+        CK(dalloc(&d.slot_st, 5 * SL * c->gcap * 32 * c->q), "alloc slot state");
+    }
     CK(dalloc(&d.sbox, 6 * SL), "alloc slices");
     CK(dalloc(&d.flags, SL), "alloc factors");
     CK(dalloc(&d.iters, SL), "alloc factors");
@@ -581,8 +621,8 @@ static lmc_status create_impl(lmc_ctx *c, const lmc_gbuffer *g, const lmc_vpls *
     CK(dalloc(&d.rows_rgb, 3 * ML), "alloc resolve");
     CK(dalloc(&d.img, 3 * (size_t)std::max<int64_t>((int64_t)c->W * c->H, 1)), "alloc resolve");
     CK(cudaMallocHost(&c->h_stage, 3 * sizeof(float) * (size_t)std::max<int64_t>((int64_t)c->W * c->H, 1)), "alloc staging");
-    CK(dalloc(&d.counters, 8), "alloc counters");
-    CK(cudaMemsetAsync(d.counters, 0, 8 * sizeof(unsigned long long), c->stream), "memset");
+    CK(dalloc(&d.counters, 16), "alloc counters");
+    CK(cudaMemsetAsync(d.counters, 0, 16 * sizeof(unsigned long long), c->stream), "memset");
     CK(cudaMemsetAsync(d.flags, 0, SL * sizeof(int32_t), c->stream), "memset");
     CK(cudaMemsetAsync(d.img, 0, 3 * sizeof(float) * (size_t)std::max<int64_t>((int64_t)c->W * c->H, 1), c->stream), "memset");
     size_t need = cfg.solver == LMC_SOLVER_MALS ? mals_smem_bytes(c->q, c->mmax, (int)G) : adm_smem_bytes(c->q, c->mmax, (int)G);
@@ -640,7 +680,11 @@ lmc_status lmc_upload_inputs(lmc_ctx *c, const lmc_gbuffer *g, const lmc_vpls *v
         for (int k = 0; k < 6; ++k) CK(dcopy_in(d.vpl_soa + k * nv, vs[k], nv, mem, st), "copy vpls");
         CK(run_pack_vpls(c), "pack vpls");
     }
+    CK(run_check_pixels(c, d.counters + 8), "check pixels");
+    unsigned long long bad = 0;
+    CK(cudaMemcpyAsync(&bad, d.counters + 8, sizeof bad, cudaMemcpyDeviceToHost, st), "check pixels");
     CK(cudaStreamSynchronize(st), "sync");
+    if (bad) return fail(c, LMC_EINVAL, "a G-buffer pixel index is outside [0, width * height)");
     c->state = 0;
     return LMC_OK;
 }
@@ -701,31 +745,18 @@ lmc_status lmc_sample_pass2(lmc_ctx *c)
 
 // Launch order of the completion CTAs: slice order, except that the nsm slices with the fewest
 // samples run last, largest first, so the final wave holds the shortest CTAs (a slice's result
-// does not depend on when its CTA runs).  Reads the per-slice sample counts (synchronises the
-// stream, as the ADM shared-memory sizing does anyway).  LMC_ADM_TAIL=k moves k x nsm slices
-// (diagnostic; 0 keeps slice order).
+// does not depend on when its CTA runs).  Computed on the device (run_launch_order): no host sync.
+// LMC_ADM_TAIL=k moves k x nsm slices (diagnostic; 0 keeps slice order).
 static cudaError_t completion_order(lmc_ctx *c)
 {
     const char *te = getenv("LMC_ADM_TAIL");
     const int ntail = (te ? atoi(te) : 1) * c->nsm;
     c->adm_ordered = false;
-    if (!(ntail > 0 && c->SL > ntail)) return cudaStreamSynchronize(c->stream);
-    c->h_nnz.resize(c->SL);
-    cudaError_t e = cudaMemcpyAsync(c->h_nnz.data(), c->d.nnz, c->SL * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
-    if (e != cudaSuccess) return e;
-    std::vector<int32_t> byn(c->SL);
-    for (int k = 0; k < c->SL; ++k) byn[k] = k;
-    std::stable_sort(byn.begin(), byn.end(), [&](int a, int b) { return c->h_nnz[a] < c->h_nnz[b]; });
-    std::vector<char> last(c->SL, 0);
-    for (int k = 0; k < ntail; ++k) last[byn[k]] = 1;
-    c->h_order.clear();
-    for (int k = 0; k < c->SL; ++k)
-        if (!last[k]) c->h_order.push_back(k);
-    for (int k = ntail - 1; k >= 0; --k) c->h_order.push_back(byn[k]);
-    e = cudaMemcpyAsync(c->d.adm_order, c->h_order.data(), c->SL * sizeof(int32_t), cudaMemcpyHostToDevice, c->stream);
+    if (!(ntail > 0 && c->SL > ntail)) return cudaSuccess;
+    cudaError_t e = run_launch_order(c, ntail);
     if (e != cudaSuccess) return e;
     c->adm_ordered = true;
+    c->launches += 3;
     return cudaSuccess;
 }
 
@@ -738,15 +769,20 @@ lmc_status lmc_complete(lmc_ctx *c)
         ev_rec(c, 8);
         CK(run_mals(c), "completion (MALS)");
         ev_rec(c, 9);
+    } else if (c->use_adm2) {
+        CK(run_layout2(c), "Omega layout");
+        CK(completion_order(c), "completion order");
+        ev_rec(c, 8);
+        CK(run_adm2(c), "completion (ADM)");
+        ev_rec(c, 9);
+        c->launches += c->SL > 0 ? 2 : 0;
     } else {
         CK(run_layout(c), "Omega layout");
-        // shared memory of the ADM kernel is sized by this frame's largest coarsened cut
-        unsigned long long nmx = 0;
-        CK(cudaMemcpyAsync(&nmx, c->d.counters + 5, sizeof nmx, cudaMemcpyDeviceToHost, c->stream), "read max n");
-        CK(completion_order(c), "completion order");   // synchronises the stream
-        const int nmax = std::max(1, (int)std::min<unsigned long long>(nmx, (unsigned long long)c->G));
+        // shared memory of the ADM kernel is sized by the cut bound G (validated at lmc_create), so
+        // nothing of this frame has to be read back: the call only enqueues
+        CK(completion_order(c), "completion order");
         ev_rec(c, 8);
-        CK(run_adm(c, nmax), "completion (ADM)");
+        CK(run_adm(c, c->G), "completion (ADM)");
         ev_rec(c, 9);
         c->launches += c->SL > 0 ? 1 : 0;
     }
@@ -769,11 +805,31 @@ lmc_status lmc_resolve_image(lmc_ctx *c, float *image, int32_t image_memory)
         return LMC_OK;
     }
     if (image_memory != LMC_MEM_HOST) return fail(c, LMC_EINVAL, "bad image_memory");
-    CK(run_resolve(c, c->d.img, nullptr), "resolve");
+    if (c->cfg.world == 1 && c->M == (int64_t)c->W * c->H) {
+        // every pixel is a row of this rank: the whole image is this rank's output
+        CK(run_resolve(c, c->d.img, nullptr), "resolve");
+        ev_rec(c, 6);
+        const size_t bytes = 3 * sizeof(float) * (size_t)c->W * c->H;
+        CK(cudaMemcpyAsync(image, c->d.img, bytes, cudaMemcpyDeviceToHost, c->stream), "image download");
+        CK(cudaStreamSynchronize(c->stream), "sync");
+        return LMC_OK;
+    }
+    // otherwise only this rank's pixels are written: packed rows + their image indices, scattered here
+    CK(run_resolve(c, nullptr, c->d.rows_rgb), "resolve");
+    CK(run_rank_pixels(c, c->d.rank_pix), "resolve");
+    c->launches += c->ML > 0 ? 1 : 0;
     ev_rec(c, 6);
-    const size_t bytes = 3 * sizeof(float) * (size_t)c->W * c->H;
-    CK(cudaMemcpyAsync(image, c->d.img, bytes, cudaMemcpyDeviceToHost, c->stream), "image download");
+    CK(cudaMemcpyAsync(c->h_stage, c->d.rows_rgb, 3 * sizeof(float) * (size_t)c->ML, cudaMemcpyDeviceToHost, c->stream),
+       "image download");
+    CK(cudaMemcpyAsync(c->h_pix, c->d.rank_pix, sizeof(int32_t) * (size_t)c->ML, cudaMemcpyDeviceToHost, c->stream),
+       "image download");
     CK(cudaStreamSynchronize(c->stream), "sync");
+    for (int64_t k = 0; k < c->ML; ++k) {
+        const int64_t p = c->h_pix[k];
+        image[3 * p] = c->h_stage[3 * k];
+        image[3 * p + 1] = c->h_stage[3 * k + 1];
+        image[3 * p + 2] = c->h_stage[3 * k + 2];
+    }
     return LMC_OK;
 }
 
@@ -968,6 +1024,12 @@ lmc_status lmc_get_stats(lmc_ctx *c, lmc_stats *st)
     st->evals_coarsen = (int64_t)cnt[1];
     st->evals_pass2 = (int64_t)cnt[2];
     st->pool_used_max = (int64_t)cnt[4];
+    {
+        unsigned long long c67[2];
+        CK(d2h(c67, c->d.counters + 6, 2), "stats");
+        st->layout_row_slots = (int64_t)c67[0];
+        st->layout_col_slots = (int64_t)c67[1];
+    }
     if (c->state >= 3) {
         std::vector<int32_t> cn(c->SL);
         CK(d2h(cn.data(), c->d.cut_n, (size_t)c->SL), "stats");

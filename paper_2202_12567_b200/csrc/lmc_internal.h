@@ -110,9 +110,19 @@ struct Dev {
     int32_t *r_goff, *c_goff;          // [SL][mmax+1], [SL][G+1]
     int32_t *c_nsolo;                  // [SL] leading column groups that hold a single (long) column
     int32_t *adm_order;                // [SL] completion CTA -> slice (the smallest slices last)
+    int32_t *ord_tmp;                  // [4 SL] launch-order scratch (sorted keys, iota, sorted ids, marks)
+    void *ord_cub;                     // CUB radix-sort temp of the launch order
+    size_t ord_cub_bytes;
+    int32_t *rank_pix;                 // [ML] image index of this rank's rows (host-buffer resolve)
     unsigned long long *r_ent;         // [SL][scap] (M^ bits << 32) | (column-layout index << 10) | column
     uint16_t *c_ent;                   // [SL][scap] row of the column-layout entry
     float4 *norm;                      // [SL] sigma, 1/sigma, sum M^, sum M^^2
+    // lane-per-segment layout of the q <= 16 ADM kernel (complete2.cu)
+    int4 *r_grp, *c_grp;               // [SL][gcap] (entry offset, k-steps, max log2 segments, 0)
+    uint32_t *r_slot, *c_slot;         // [SL][gcap * 32] member | segment << 11 | log2 segments << 16
+    int32_t *ngrp;                     // [SL][2] row groups, column groups
+    int32_t *ctot;                     // [SL] column-layout size
+    float *slot_st;                    // 5 x [SL][gcap * 32 * q]: U, Lambda, X_k, V, Pi by lane slot
     float *U, *V, *Lam, *Pi, *Xold, *S; // U/Lam/Xold [ML][q], V/Pi [SL][G][q], S [SL][scap]
     int32_t *flags, *iters;            // [SL]
     float *resid;                      // [SL]
@@ -120,7 +130,8 @@ struct Dev {
     float *rows_rgb;                   // [ML][3]
     float *img;                        // [H*W][3] staging image for host output
     float *vpl_soa;                    // 6 * NV staging for the VPL packing kernel
-    // counters: 0 evals_pass1, 1 evals_coarsen, 2 evals_pass2, 3 overflow flags, 4 pool_used_max, 5 max n_s
+    // counters: 0 evals_pass1, 1 evals_coarsen, 2 evals_pass2, 3 overflow flags, 4 pool_used_max, 5 max n_s,
+    // 6 / 7 padded row / column layout sizes of the q <= 16 ADM
     unsigned long long *counters;
 };
 
@@ -145,6 +156,9 @@ struct lmc_ctx {
     int32_t mmax = 0;
     int32_t q = 0, nmax = 0;
     int64_t pool_cap = 0, ncap = 0, scap = 0;
+    int64_t gcap = 0;              // groups per slice and phase of the q <= 16 ADM layout
+    int32_t adm2_Tr = 64, adm2_Tc = 64;   // segment length caps (rows, columns)
+    bool use_adm2 = false;         // complete2.cu kernels (q <= 16) instead of complete.cu
     // slicing level structure
     struct Level { int32_t tile_off, tile_n, work_off, work_n, next_tile_off, next_tile_n, nslots; };
     std::vector<Level> levels;
@@ -164,6 +178,7 @@ struct lmc_ctx {
     float ms[6] = {0, 0, 0, 0, 0, 0};
     bool ev_ok = false;
     float *h_stage = nullptr;
+    int32_t *h_pix = nullptr;      // pinned [ML] pixel ids of the host-buffer resolve
     int64_t launches = 0;          // kernels (and CUB dispatches, 1 each) issued by stage calls
 };
 
@@ -187,7 +202,14 @@ cudaError_t run_layout(lmc_ctx *c);
 cudaError_t run_adm(lmc_ctx *c, int nmax);
 cudaError_t run_resolve(lmc_ctx *c, float *image, float *rows_rgb);
 cudaError_t run_scatter(lmc_ctx *c, const float *all_rows, float *image);
+cudaError_t run_rank_pixels(lmc_ctx *c, int32_t *out);
+cudaError_t run_check_pixels(lmc_ctx *c, unsigned long long *flag);
+cudaError_t launch_order_bytes(int32_t SL, size_t *bytes);
+cudaError_t run_launch_order(lmc_ctx *c, int ntail);
 size_t adm_smem_bytes(int q, int mmax, int nmax);
+// complete2.cu (lane-per-segment ADM, q <= 16)
+cudaError_t run_layout2(lmc_ctx *c);
+cudaError_t run_adm2(lmc_ctx *c);
 // mals.cu (fp64 masked ALS)
 cudaError_t run_mals(lmc_ctx *c);
 size_t mals_smem_bytes(int q, int mmax, int G);

@@ -57,7 +57,8 @@ class Stats(C.Structure):
                                          "sum_completed", "evals_pass1", "evals_coarsen", "evals_pass2", "n_direct",
                                          "n_zero", "n_diverged", "pool_used_max", "pool_cap", "launches")] + \
               [(k, C.c_float) for k in ("ms_slices", "ms_pass1", "ms_coarsen", "ms_pass2", "ms_complete",
-                                        "ms_resolve", "ms_solver")]
+                                        "ms_resolve", "ms_solver")] + \
+              [(k, C.c_int64) for k in ("layout_row_slots", "layout_col_slots")]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

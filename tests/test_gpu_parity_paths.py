@@ -1,0 +1,262 @@
+"""GPU parity of the paths the round-1 review found untested (VERDICT.md "Close the parity gaps").
+
+  * 10^6 random entry pairs per scene, bit-exact fp64 (P:61 entry, readings R1-R3)
+  * a sigma = 0 slice (every entry zero: LMC_SLICE_ZERO, R23) next to an ordinary slice
+  * a non-finite residual -> the slice is rendered directly from all its entries (R25)
+  * the tol > 0 early stop ("error below tolerance", R21)
+  * masked ALS at the survey's ridge lambda = 1e-3 (north_star; R34 default is 1e-2)
+  * both ADM kernels at every rank they serve (complete.cu lane groups, complete2.cu lane segments)
+
+Each case runs the CUDA path through the C-ABI and compares with the fp64 oracle on the same
+seeded inputs, with the bars of test_gpu_parity.py.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import scenegen
+from tests._mini import mini
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no GPU", allow_module_level=True)
+from paper_2202_12567_b200 import lmc  # noqa: E402
+from tests.test_gpu_parity import check_slice  # noqa: E402
+
+LUMW = np.array([0.2126, 0.7152, 0.0722])
+
+
+def run_frame(x, env=None, **over):
+    """create + one frame with some environment switches of the library set during the run"""
+    old = {}
+    for k, v in (env or {}).items():
+        old[k] = os.environ.get(k)
+        os.environ[k] = v
+    try:
+        fr = lmc.Frame(x, **over)
+        img = torch.zeros(x.height * x.width * 3, device="cuda")
+        fr.run(img)
+        torch.cuda.synchronize()
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    return fr, img.view(-1, 3).cpu().numpy().astype(np.float64)
+
+
+# ------------------------------------------------------------------------------ entries
+
+@pytest.mark.parametrize("name", ["c1", "t_interior"])
+def test_entries_bit_exact_million_pairs(name):
+    x = scenegen.make_inputs(name)
+    fr = lmc.Frame(x)
+    o = oracle.Oracle(x)
+    rng = np.random.default_rng(2202)
+    n = 1_000_000
+    rows = rng.integers(0, x.m, n).astype(np.int32)
+    vp = rng.integers(0, x.vpls["px"].size, n).astype(np.int32)
+    got = fr.eval_entries(rows, vp)
+    ref = o.entries_T(rows, vp)
+    bad = np.flatnonzero(got != ref)
+    assert bad.size == 0, f"{bad.size} of {n} entries differ, first at pair {bad[:3]}"
+    assert (ref > 0).mean() > 0.1 and (ref == 0).mean() > 0.05   # both lit and shadowed / back-facing pairs
+    fr.close()
+
+
+@pytest.mark.slow
+def test_entries_bit_exact_million_pairs_c3_scene():
+    x = scenegen.make_inputs("c3")
+    fr = lmc.Frame(x)
+    o = oracle.Oracle(x)
+    rng = np.random.default_rng(12567)
+    n = 1_000_000
+    rows = rng.integers(0, x.m, n).astype(np.int32)
+    vp = rng.integers(0, x.vpls["px"].size, n).astype(np.int32)
+    assert np.array_equal(fr.eval_entries(rows, vp), o.entries_T(rows, vp))
+    fr.close()
+
+
+# ------------------------------------------------------------------------------ sigma = 0 slice
+
+def _floor_and_ceiling(q, solver=0):
+    """300 floor points facing the VPLs and 300 ceiling points facing away: the slicing separates
+    them (their y differs), and every entry of the ceiling slice is 0 (cos at the point <= 0)."""
+    rng = np.random.default_rng(9)
+    m = 300
+    floor = np.column_stack([rng.uniform(0, 1, m), np.zeros(m), rng.uniform(0, 1, m)])
+    ceil = np.column_stack([rng.uniform(0, 1, m), np.ones(m), rng.uniform(0, 1, m)])
+    pts = np.concatenate([floor, ceil])
+    nrm = np.tile([0.0, 1.0, 0.0], (2 * m, 1))
+    nv = 40
+    vpos = np.column_stack([rng.uniform(0, 1, nv), np.full(nv, 0.5), rng.uniform(0, 1, nv)])
+    vI = rng.uniform(0.2, 1.0, (nv, 3))
+    return mini(pts, nrm, vpos, np.tile([0, -1, 0], (nv, 1)), vI, tau=0.0, slice_target=300, rank_q=q, rate=0.3,
+                solver=solver, diag=np.sqrt(3.0))
+
+
+@pytest.mark.parametrize("q,solver", [(8, 0), (16, 0), (8, 1)])
+def test_zero_slice(q, solver):
+    x = _floor_and_ceiling(q, solver)
+    fr, img = run_frame(x)
+    off, _ = fr.slices()
+    assert off.size == 3
+    res = oracle.Oracle(x).run_slices([0, 1], stage=4)
+    zero = [r for r in res if r["flags"] & oracle.FLAG_ZERO]
+    assert len(zero) == 1, "one slice of the frame has only zero entries"
+    for r in res:
+        check_slice(x, fr, img, r)
+    z = zero[0]
+    fa = fr.factors(z["slice"])
+    assert fa["flags"] & lmc.SLICE_ZERO
+    assert np.all(img[x.gbuf["pixel"][z["rows"]]] == 0.0)
+    fr.close()
+
+
+# ------------------------------------------------------------------------------ non-finite fallback
+
+@pytest.mark.parametrize("q", [8, 16])
+def test_nonfinite_residual_renders_directly(q):
+    x = scenegen.make_inputs(scenegen.preset("t_interior", rank_q=q))
+    victim = 2
+    fr, img = run_frame(x, env={"LMC_TEST_NONFINITE_SLICE": str(victim)})
+    o = oracle.Oracle(x)
+    off, _ = fr.slices()
+    res = o.run_slices(list(range(off.size - 1)), stage=4)
+    for r in res:
+        if r["slice"] != victim:
+            check_slice(x, fr, img, r)
+            continue
+        fa = fr.factors(victim)
+        assert fa["flags"] & lmc.SLICE_DIVERGED and fa["flags"] & lmc.SLICE_DIRECT
+        # direct rendering = exact column sums of the fully evaluated coarsened slice (R25)
+        ref = o.fullcut_slice(r["rows"], r["cut_nodes"])
+        got = img[x.gbuf["pixel"][r["rows"]]]
+        floor = 1e-3 * max(float((ref @ LUMW).mean()), 1e-30)
+        rel = np.abs(got - ref) / np.maximum(np.abs(ref), floor)
+        assert rel.max() <= 1e-3, f"direct rendering of slice {victim}: max rel {rel.max():.3g}"
+    fr.close()
+
+
+# ------------------------------------------------------------------------------ tol > 0
+
+@pytest.mark.parametrize("q", [8, 16])
+def test_tolerance_early_stop(q):
+    tol = 0.12
+    x = scenegen.make_inputs(scenegen.preset("t_interior", rank_q=q, tol=tol))
+    fr, img = run_frame(x)
+    off, _ = fr.slices()
+    res = oracle.Oracle(x).run_slices(list(range(off.size - 1)), stage=4)
+    stopped = 0
+    for r in res:
+        if r["flags"] & (oracle.FLAG_DIRECT | oracle.FLAG_ZERO):
+            continue
+        fa = fr.factors(r["slice"])
+        if fa["iters"] != r["iters"]:
+            # fp32 against fp64 may cross the threshold one iteration apart only if the residual
+            # sits at the threshold itself
+            assert abs(fa["iters"] - r["iters"]) == 1 and abs(r["resid"] - tol) < 1e-3 * tol, \
+                f"slice {r['slice']}: {fa['iters']} vs {r['iters']} iterations (oracle resid {r['resid']:.6g})"
+            continue
+        stopped += r["iters"] < x.cfg.max_iter
+        check_slice(x, fr, img, r)
+        assert fa["resid"] < tol or r["iters"] == x.cfg.max_iter
+    assert stopped > 0, "the tolerance stopped no slice early"
+    fr.close()
+
+
+# ------------------------------------------------------------------------------ MALS lambda = 1e-3
+
+def test_mals_survey_lambda():
+    x = scenegen.make_inputs(scenegen.preset("t_interior", solver=1, lam=1e-3))
+    fr, img = run_frame(x)
+    off, _ = fr.slices()
+    for r in oracle.Oracle(x).run_slices(list(range(off.size - 1)), stage=4):
+        check_slice(x, fr, img, r)
+    fr.close()
+
+
+# ------------------------------------------------------------------------------ both ADM kernels
+
+@pytest.mark.parametrize("name,q,env", [("t_interior", 16, {"LMC_ADM2": "1"}), ("c1", 16, {"LMC_ADM2": "1"}),
+                                        ("t_interior", 8, {"LMC_ADM_V1": "1"}), ("t_interior", 4, {"LMC_ADM_V1": "1"}),
+                                        ("t_cornell", 8, {}), ("t_cornell", 4, {})])
+def test_adm_kernels_all_ranks(name, q, env):
+    x = scenegen.make_inputs(scenegen.preset(name, rank_q=q))
+    fr, img = run_frame(x, env=env)
+    off, _ = fr.slices()
+    for r in oracle.Oracle(x).run_slices(list(range(off.size - 1)), stage=4):
+        check_slice(x, fr, img, r)
+    fr.close()
+
+
+# ------------------------------------------------------------------------------ asynchronous stages
+
+def test_stage_calls_capture_into_a_cuda_graph():
+    """every stage call only enqueues (lmc.h): the whole frame, completion launch order included,
+    captures into one CUDA graph, and replaying it reproduces the eagerly computed image bit for bit"""
+    x = scenegen.make_inputs("t_interior")
+    s = torch.cuda.Stream()
+    fr = lmc.Frame(x, stream=s)
+    ref = torch.zeros(x.height * x.width * 3, device="cuda")
+    with torch.cuda.stream(s):
+        fr.run(ref)
+    s.synchronize()
+    img = torch.zeros_like(ref)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        fr.build_slices()
+        fr.sample_pass1()
+        fr.coarsen_cut()
+        fr.sample_pass2()
+        fr.complete()
+        fr.resolve_image(img)
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(img, ref)
+    img.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(img, ref)
+    fr.close()
+
+
+def test_bad_pixel_index_rejected():
+    import dataclasses
+    x = scenegen.make_inputs("t_cornell")
+    g = dict(x.gbuf)
+    g["pixel"] = g["pixel"].copy()
+    g["pixel"][5] = x.width * x.height   # one past the image
+    with pytest.raises(lmc.LmcError):
+        lmc.Frame(dataclasses.replace(x, gbuf=g))
+
+
+def test_host_image_leaves_background_untouched():
+    """LMC_MEM_HOST resolve writes only the rows' pixels (the rest of the caller's image keeps its values)"""
+    import dataclasses
+    x = scenegen.make_inputs("t_cornell")
+    keep = np.arange(x.m) % 3 != 0                 # drop a third of the rows: background pixels
+    g = {k: v[keep] for k, v in x.gbuf.items()}
+    x2 = dataclasses.replace(x, gbuf=g)
+    fr = lmc.Frame(x2)
+    dev = torch.zeros(x.height * x.width * 3, device="cuda")
+    fr.run(dev)
+    torch.cuda.synchronize()
+    host = np.full(x.height * x.width * 3, 7.0, np.float32)
+    fr.build_slices()
+    fr.sample_pass1()
+    fr.coarsen_cut()
+    fr.sample_pass2()
+    fr.complete()
+    fr.resolve_image(host, memory=lmc.MEM_HOST)
+    h = host.reshape(-1, 3)
+    pix = g["pixel"]
+    assert np.array_equal(h[pix], dev.view(-1, 3).cpu().numpy()[pix])
+    bg = np.setdiff1d(np.arange(x.height * x.width), pix)
+    assert bg.size > 0 and np.all(h[bg] == 7.0)
+    fr.close()
