@@ -125,6 +125,42 @@ def adm_flops(q, sum_N, sum_m, sum_n, nslices, iters):
     return iters * (6.0 * q * sum_N + 6.0 * q * q * sum_m + 6.0 * q * q * sum_n + 2.0 * q ** 3 * nslices)
 
 
+def adm_flops_survey(q, sum_N, sum_m, sum_n, nslices, iters):
+    """the SURVEY §8(a) a7 count per iteration and slice: 6 q N + 8 m q^2 + 6 n q^2 + 2/3 q^3 (it
+    forms X_k^T G_Y as well; the kernel's reformulation saves that product)"""
+    return iters * (6.0 * q * sum_N + 8.0 * q * q * sum_m + 6.0 * q * q * sum_n + (2.0 / 3.0) * q ** 3 * nslices)
+
+
+def entry_flops_per_entry(x, fr, nslices=8):
+    """Mean fp64 operations (+ - * / sqrt, as the oracle's entry function executes them: early exits
+    taken, primitives tested until the first hit) over a sample of the pairs this frame evaluated:
+    pass 1 + coarsening (rows of every processed candidate x the reps of its two children, from the
+    oracle's record of the same slices) and pass 2 (the frame's new samples)."""
+    import oracle
+    o = oracle.Oracle(x)
+    off, rows = fr.slices()
+    S = off.size - 1
+    ids = sorted(set(np.linspace(0, S - 1, min(nslices, S)).astype(int).tolist()))
+    t = x.tree
+    r1, v1, r2, v2 = [], [], [], []
+    for r in o.run_slices(ids, stage=1):
+        for k, f in enumerate(r["proc_node"]):
+            z = r["rows"][r["proc_zrows"][r["proc_zoff"][k]:r["proc_zoff"][k + 1]]]
+            for ch in (t["left"][f], t["right"][f]):
+                r1.append(z)
+                v1.append(np.full(z.size, t["rep"][ch], np.int32))
+    for s in ids:
+        sm = fr.samples(s)
+        new = sm["carried"] == 0
+        cut = fr.cut(s)
+        r2.append(rows[off[s] + sm["row"][new]])
+        v2.append(t["rep"][cut[sm["col"][new]]].astype(np.int32))
+    r1, v1, r2, v2 = (np.concatenate(a) if a else np.zeros(0, np.int32) for a in (r1, v1, r2, v2))
+    f1 = o.entry_flops(r1, v1) / max(r1.size, 1)
+    f2 = o.entry_flops(r2, v2) / max(r2.size, 1)
+    return f1, f2, int(r1.size), int(r2.size), len(ids)
+
+
 def mals_flops(q, sum_N, sum_m, sum_n, nslices, iters):
     """per iteration and slice: Gram + rhs 2 N (q(q+1)/2 + q) twice (rows then columns)
     + (m + n)(q^3/3 + 2 q^2) (Cholesky + two triangular solves)."""
@@ -239,7 +275,8 @@ def main():
     torch.cuda.synchronize()
     clocks = ClockSampler(local)
     clocks.start()
-    times, solver_ms, stage = [], [], {k: [] for k in ("slices", "pass1", "coarsen", "pass2", "complete", "resolve")}
+    times, solver_ms, eval2_ms = [], [], []
+    stage = {k: [] for k in ("slices", "pass1", "coarsen", "pass2", "complete", "resolve")}
     launches0 = fr.stats()["launches"]
     for _ in range(args.steps):
         flush.fill_(1.0)                      # flush L2 between timed frames (outside the events)
@@ -257,6 +294,7 @@ def main():
         for k in stage:
             stage[k].append(st["ms_" + k])
         solver_ms.append(st["ms_solver"])   # the completion kernel alone (events around its launch)
+        eval2_ms.append(st["ms_eval2"])     # the pass-2 entry kernel alone
     cl = clocks.stop()
     launches = fr.stats()["launches"] - launches0
     ms = statistics.mean(times)
@@ -284,6 +322,8 @@ def main():
                                                      st["slice_end"] - st["slice_begin"], K)
     achieved = fl / (ms_c * 1e-3) / 1e12
     peak, peak_src = fp32_peak() if solver == 0 else fp64_peak()
+    fl_survey = adm_flops_survey(q, st["sum_samples"], st["rows"], st["sum_cols"], st["slice_end"] - st["slice_begin"], K) \
+        if solver == 0 else fl
     traffic, limiter = None, None
     try:   # DRAM bytes per launch of the dominant kernel from the committed ncu --set full capture
         tj = json.load(open(os.path.join(ROOT, "profiles", "r01_traffic.json")))
@@ -292,6 +332,26 @@ def main():
         limiter = ent.get("limiter") if ent else None
     except Exception:
         traffic = None
+    roof_entry = None
+    if rank == 0 and solver in (0, 1) and not os.environ.get("BENCH_NO_ENTRY_ROOFLINE"):
+        # entry evaluation (a3): fp64 flops as the oracle executes them x entries evaluated, over the
+        # CUDA-event time of the kernels that evaluate them (pass 1 incl. its slice-box kernel,
+        # coarsening, the pass-2 entry kernel)
+        f1, f2, n1, n2, nsl_s = entry_flops_per_entry(x, fr)
+        ev1 = float(st["evals_pass1"] + st["evals_coarsen"])
+        ev2 = float(st["evals_pass2"])
+        efl = f1 * ev1 + f2 * ev2
+        ems = statistics.mean(stage["pass1"]) + statistics.mean(stage["coarsen"]) + statistics.mean(eval2_ms)
+        p64, p64_src = fp64_peak()
+        ach = efl / (ems * 1e-3) / 1e12
+        roof_entry = {"bound": "alu", "kernel": "k_pass1 + k_coarsen + k_eval_new (+ k_slice_bbox)",
+                      "achieved": ach, "peak": p64, "unit": "TFLOP/s", "frac": ach / p64, "traffic": None,
+                      "peak_source": p64_src + "; FMA counted as 2 flops: the unfused ops of the exact "
+                                               "(-fmad=false) path cap the fraction at 0.5",
+                      "flops_per_entry": {"pass1+coarsen": f1, "pass2": f2},
+                      "entries": {"pass1+coarsen": ev1, "pass2": ev2}, "flops_per_frame": efl, "kernel_ms": ems,
+                      "sample": f"oracle operation count over {n1} pass-1/coarsening pairs and {n2} pass-2 "
+                                f"entries of {nsl_s} slices of this frame"}
     e2e = None
     if not args.no_e2e and world == 1:
         e2e = measure_e2e(x, args, solver, dev)
@@ -322,7 +382,9 @@ def main():
         "roofline": {"bound": "alu", "kernel": "k_adm" if solver == 0 else "k_mals", "achieved": achieved,
                      "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                      "traffic": traffic, "peak_source": peak_src, "flops_per_launch": fl,
+                     "flops_per_launch_survey_count": fl_survey, "frac_survey_count": fl_survey / (ms_c * 1e-3) / 1e12 / peak,
                      "kernel_ms": ms_c, "limiter": limiter},
+        "roofline_entry": roof_entry,
         "clocks": cl,
         "gpu_launches": launches,
     }

@@ -120,6 +120,7 @@ typedef struct {
     float ms_slices, ms_pass1, ms_coarsen, ms_pass2, ms_complete, ms_resolve; /* last frame, if timed */
     float ms_solver;           /* last frame, if timed: the completion kernel alone (ADM or MALS) */
     int64_t layout_row_slots, layout_col_slots; /* q <= 16 ADM: padded sample slots of the row / column layouts */
+    float ms_eval2;            /* last frame, if timed: the pass-2 entry-evaluation kernel alone */
 } lmc_stats;
 
 typedef struct lmc_ctx lmc_ctx;

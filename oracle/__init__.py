@@ -94,6 +94,8 @@ def lib():
             L.orc_entry_T.argtypes = [C.POINTER(_Inputs), C.c_int64, C.c_int64]
             L.orc_entry_T.restype = C.c_double
             L.orc_entry_T_many.argtypes = [C.POINTER(_Inputs), C.c_int64, P, P, P]
+            L.orc_entry_flops.argtypes = [C.POINTER(_Inputs), C.c_int64, P, P]
+            L.orc_entry_flops.restype = C.c_int64
             L.orc_visible.argtypes = [C.POINTER(_Inputs), P, P]
             L.orc_visible.restype = C.c_int32
             L.orc_build_slices.argtypes = [C.POINTER(_Inputs), P, P, P]
@@ -185,6 +187,12 @@ class Oracle:
         out = np.zeros(rows.size)
         lib().orc_entry_T_many(C.byref(self.s), rows.size, _p(rows), _p(vpls), _p(out))
         return out
+
+    def entry_flops(self, rows, vpls) -> int:
+        """fp64 operations (+ - * / sqrt) the oracle's entry function executes over these pairs"""
+        rows = np.ascontiguousarray(rows, np.int32)
+        vpls = np.ascontiguousarray(vpls, np.int32)
+        return int(lib().orc_entry_flops(C.byref(self.s), rows.size, _p(rows), _p(vpls)))
 
     def visible(self, x, y) -> bool:
         a = np.ascontiguousarray(x, np.float64)

@@ -84,7 +84,13 @@ int32_t orc_floyd(int32_t m, int32_t n, uint32_t a, int32_t slice, uint64_t seed
  * stated — reading R1): cosine-weighted VPL emitter (R32), d^2 clamp (R2),
  * normalised-Phong BRDF (R1), visibility against the analytic occluders (R3).
  * ---------------------------------------------------------------------------------------- */
-static double dot3(const double a[3], const double b[3]) { return (a[0] * b[0] + a[1] * b[1]) + a[2] * b[2]; }
+/* Floating-point operation counter of the entry evaluation (measurement only: bench.py's roofline
+ * of the entry kernels).  FL(k) adds k for every +, -, *, / and sqrt the code below executes
+ * (comparisons, fmin / fmax and negations count 0); it does not change any arithmetic. */
+static _Thread_local int64_t orc_fl;
+#define FL(k) (orc_fl += (k))
+
+static double dot3(const double a[3], const double b[3]) { FL(5); return (a[0] * b[0] + a[1] * b[1]) + a[2] * b[2]; }
 
 static double lum3(double r, double g, double b) { return (0.2126 * r + 0.7152 * g) + 0.0722 * b; }
 
@@ -93,12 +99,15 @@ static int seg_hits_sphere(const float *s, const double x[3], const double l[3],
     double c[3] = {s[0], s[1], s[2]};
     double r = s[3];
     double oc[3] = {x[0] - c[0], x[1] - c[1], x[2] - c[2]};
+    FL(3);
     double b = dot3(oc, l);
     double cc = dot3(oc, oc) - r * r;
     double disc = b * b - cc;
+    FL(4);
     if (disc < 0.0) return 0;
     double sq = sqrt(disc);
     double t0 = -b - sq, t1 = -b + sq;
+    FL(3);
     return (t0 > tmin && t0 < tmax) || (t1 > tmin && t1 < tmax);
 }
 
@@ -109,6 +118,7 @@ static int seg_hits_box(const float *bx, const double x[3], const double l[3], d
         double inv = 1.0 / l[a];
         double t1 = ((double)bx[a] - x[a]) * inv;
         double t2 = ((double)bx[3 + a] - x[a]) * inv;
+        FL(5);
         tn[a] = fmin(t1, t2);
         tf[a] = fmax(t1, t2);
     }
@@ -127,11 +137,14 @@ static int seg_hits_rect(const float *rc, const double x[3], const double l[3], 
     if (den == 0.0) return 0;
     double pd[3] = {p0[0] - x[0], p0[1] - x[1], p0[2] - x[2]};
     double t = dot3(pd, nr) / den;
+    FL(4);
     if (!(t > tmin && t < tmax)) return 0;
     double h[3] = {x[0] + t * l[0], x[1] + t * l[1], x[2] + t * l[2]};
     double hp[3] = {h[0] - p0[0], h[1] - p0[1], h[2] - p0[2]};
+    FL(9);
     double a = dot3(hp, e1) / dot3(e1, e1);
     double b = dot3(hp, e2) / dot3(e2, e2);
+    FL(2);
     return a >= 0.0 && a <= 1.0 && b >= 0.0 && b <= 1.0;
 }
 
@@ -139,6 +152,7 @@ static int seg_hits_rect(const float *rc, const double x[3], const double l[3], 
 static int visible_dir(const orc_inputs *in, const double x[3], const double l[3], double dist)
 {
     double tmin = in->shadow_eps, tmax = dist - in->shadow_eps;
+    FL(1);
     for (int k = 0; k < in->nsph; ++k)
         if (seg_hits_sphere(in->sph + 4 * k, x, l, tmin, tmax)) return 0;
     for (int k = 0; k < in->nbox; ++k)
@@ -162,8 +176,9 @@ static double powi(double base, int32_t e)
 {
     double r = 1.0;
     while (e > 0) {
-        if (e & 1) r = r * base;
+        if (e & 1) { r = r * base; FL(1); }
         base = base * base;
+        FL(1);
         e >>= 1;
     }
     return r;
@@ -177,15 +192,18 @@ double orc_entry_T(const orc_inputs *in, int64_t p, int64_t v)
     double y[3] = {in->lx[v], in->ly[v], in->lz[v]};
     double nv[3] = {in->lnx[v], in->lny[v], in->lnz[v]};
     double d[3] = {y[0] - x[0], y[1] - x[1], y[2] - x[2]};
+    FL(3);
     double d2 = dot3(d, d);
     if (d2 == 0.0) return 0.0;
     double dist = sqrt(d2);
     double l[3] = {d[0] / dist, d[1] / dist, d[2] / dist};
+    FL(4);
     double ci = dot3(np_, l);
     double cj = -dot3(nv, l);
     if (ci <= 0.0 || cj <= 0.0) return 0.0;
     double dc2 = in->clamp_dist * in->clamp_dist;
     double G = (ci * cj) / fmax(d2, dc2);
+    FL(3);
     double s = in->spec[p];
     double phi;
     if (s == 0.0) {
@@ -193,10 +211,13 @@ double orc_entry_T(const orc_inputs *in, int64_t p, int64_t v)
     } else {
         int32_t e = in->expo[p];
         double rv = (2.0 * ci) * dot3(np_, o) - dot3(l, o);
+        FL(3);
         double lobe = rv > 0.0 ? powi(rv, e) : 0.0;
         phi = (1.0 - s) * INV_PI + (s * (((double)(e + 2)) * INV_2PI)) * lobe;
+        FL(6);
     }
     if (!visible_dir(in, x, l, dist)) return 0.0;
+    FL(1);
     return phi * G;
 }
 
@@ -204,6 +225,14 @@ double orc_entry_T(const orc_inputs *in, int64_t p, int64_t v)
 void orc_entry_T_many(const orc_inputs *in, int64_t n, const int32_t *rows, const int32_t *vpls, double *out)
 {
     for (int64_t k = 0; k < n; ++k) out[k] = orc_entry_T(in, rows[k], vpls[k]);
+}
+
+/* floating-point operations executed by orc_entry_T over n pairs (FL counter above) */
+int64_t orc_entry_flops(const orc_inputs *in, int64_t n, const int32_t *rows, const int32_t *vpls)
+{
+    orc_fl = 0;
+    for (int64_t k = 0; k < n; ++k) (void)orc_entry_T(in, rows[k], vpls[k]);
+    return orc_fl;
 }
 
 static double lum_rho(const orc_inputs *in, int64_t p) { return lum3(in->rr[p], in->rg[p], in->rb[p]); }

@@ -85,6 +85,8 @@ int32_t orc_floyd(int32_t m, int32_t n, uint32_t a, int32_t slice, uint64_t seed
 /* Lighting-matrix entry T(p, v) (geometry x BRDF x visibility), P:61 with readings R1-R3 */
 double orc_entry_T(const orc_inputs *in, int64_t row, int64_t vpl);
 void orc_entry_T_many(const orc_inputs *in, int64_t n, const int32_t *rows, const int32_t *vpls, double *out);
+/* floating-point operations (+ - * / sqrt) orc_entry_T executes over n pairs (measurement only) */
+int64_t orc_entry_flops(const orc_inputs *in, int64_t n, const int32_t *rows, const int32_t *vpls);
 /* visibility only (1 visible, 0 occluded) of segment x -> y */
 int32_t orc_visible(const orc_inputs *in, const double x[3], const double y[3]);
 /* Matrix slicing, P:71-73 / P:172 with reading R26 */

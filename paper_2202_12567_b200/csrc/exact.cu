@@ -1555,11 +1555,14 @@ cudaError_t run_pass2(lmc_ctx *c)
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     dim3 grid(64 / EV_WARPS, c->SL);   // 64 warps per slice
+    if (c->timing && c->ev_ok) cudaEventRecord(c->ev[10], c->stream);   // pass-2 entry kernel alone (stats.ms_eval2)
     k_eval_new<<<grid, EV_WARPS * 32, 0, c->stream>>>(c->scene_slot, c->up, c->d.slice_off, c->s0, A.lbase, c->G, c->d.prow,
                                                       c->d.vpl, c->d.cut_n, c->d.cut_cols, c->d.colptr, c->d.csc_row,
                                                       c->d.csc_src, c->d.carried, c->d.n_new, c->d.sbox, c->d.val, c->d.val64,
                                                       c->ncap, c->d.counters);
-    return cudaGetLastError();
+    e = cudaGetLastError();
+    if (c->timing && c->ev_ok) cudaEventRecord(c->ev[11], c->stream);
+    return e;
 }
 
 // ------------------------------------------------------------------------------------------

@@ -1061,6 +1061,8 @@ lmc_status lmc_get_stats(lmc_ctx *c, lmc_stats *st)
         }
         float v = 0.f;
         if (cudaEventElapsedTime(&v, c->ev[8], c->ev[9]) == cudaSuccess) st->ms_solver = v;
+        v = 0.f;
+        if (cudaEventElapsedTime(&v, c->ev[10], c->ev[11]) == cudaSuccess) st->ms_eval2 = v;
         cudaGetLastError();
     }
     return LMC_OK;

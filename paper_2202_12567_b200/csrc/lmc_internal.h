@@ -174,7 +174,7 @@ struct lmc_ctx {
     lmc::Dev d;
     // timing
     int timing = 0;
-    cudaEvent_t ev[10];   // [0, 7) stage boundaries, [8, 10) around the completion kernel
+    cudaEvent_t ev[12];   // [0, 7) stage boundaries, [8, 10) around the completion kernel, [10, 12) the pass-2 entry kernel
     float ms[6] = {0, 0, 0, 0, 0, 0};
     bool ev_ok = false;
     float *h_stage = nullptr;

@@ -58,7 +58,7 @@ class Stats(C.Structure):
                                          "n_zero", "n_diverged", "pool_used_max", "pool_cap", "launches")] + \
               [(k, C.c_float) for k in ("ms_slices", "ms_pass1", "ms_coarsen", "ms_pass2", "ms_complete",
                                         "ms_resolve", "ms_solver")] + \
-              [(k, C.c_int64) for k in ("layout_row_slots", "layout_col_slots")]
+              [(k, C.c_int64) for k in ("layout_row_slots", "layout_col_slots")] + [("ms_eval2", C.c_float)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

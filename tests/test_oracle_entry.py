@@ -141,3 +141,28 @@ def test_glossy_energy_bound_and_peak():
         # mirror direction of o about n maximises the glossy part
         refl = np.array([-o[0], o[1], -o[2]])
         assert np.dot(best_dir, refl) > 0.99
+
+
+def test_entry_flop_count_hand_cases():
+    """the measurement counter of the entry evaluation (bench.py's entry roofline) on hand cases:
+    d (3) + d.d (5) + sqrt and l = d/|d| (4) + two cosines (10) = 22 up to the back-facing exit;
+    + d_c^2, G (3) + segment end (1) + phi G (1) = 27 for a lit diffuse pair with no occluder;
+    a box costs 15 (3 axes x (1 / l_a, two slab distances)); a sphere 17 to the disc < 0 exit,
+    20 when the roots are formed (a hit skips the final product)"""
+    from tests._mini import mini
+    pts = [[0.5, 0.0, 0.5]]
+    lit = dict(points=pts, normals=[[0, 1, 0]], vpl_pos=[[0.5, 1.0, 0.5]], vpl_nrm=[[0, -1, 0]], vpl_I=[[1, 1, 1]])
+    x = mini(**lit)
+    o = oracle.Oracle(x)
+    assert o.entry_flops([0], [0]) == 27
+    xb = mini(**{**lit, "normals": [[0, -1, 0]]})           # back-facing point
+    assert oracle.Oracle(xb).entry_flops([0], [0]) == 22
+    xbox = mini(**lit, box=[[2.0, 2.0, 2.0, 3.0, 3.0, 3.0]])   # a box off the segment
+    assert oracle.Oracle(xbox).entry_flops([0], [0]) == 27 + 15
+    xs_miss = mini(**lit, sph=[[3.0, 0.5, 0.5, 0.1]])        # disc < 0
+    assert oracle.Oracle(xs_miss).entry_flops([0], [0]) == 27 + 17
+    xs_hit = mini(**lit, sph=[[0.5, 0.5, 0.5, 0.1]])         # on the segment: occluded
+    oh = oracle.Oracle(xs_hit)
+    assert oh.entry_T(0, 0) == 0.0
+    assert oh.entry_flops([0], [0]) == 22 + 3 + 1 + 20
+    assert o.entry_flops([0, 0, 0], [0, 0, 0]) == 3 * 27     # additive over pairs
