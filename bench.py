@@ -2,9 +2,10 @@
 """Benchmark of the lighting-matrix hot path (arXiv 2202.12567) on B200.
 
 A step = one frame of the whole hot path: lmc_build_slices,
-lmc_sample_pass1, lmc_coarsen_cut, lmc_sample_pass2, lmc_complete, lmc_resolve_image (+ for
-N > 1 the NCCL gather of the packed image tiles to rank 0 and the scatter into the image), on
-one batch of seeded synthetic input (scenegen) resident in HBM.
+lmc_sample_pass1, lmc_coarsen_cut, lmc_sample_pass2, lmc_complete, lmc_resolve_image (for N > 1
+inside it: the NCCL gather of every rank's packed rows to rank 0 and the scatter into the image),
+on one batch of seeded synthetic input (scenegen) resident in HBM.  N = 2^k ranks each slice only
+the top k levels of the whole G-buffer, then their own subtree.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--solver adm|mals]
   python bench.py --impl reference ...     # the fp64 CPU oracle on a bounded sample
@@ -139,8 +140,9 @@ def entry_flops_per_entry(x, fr, nslices=8):
     import oracle
     o = oracle.Oracle(x)
     off, rows = fr.slices()
-    S = off.size - 1
-    ids = sorted(set(np.linspace(0, S - 1, min(nslices, S)).astype(int).tolist()))
+    st = fr.stats()
+    s0, s1 = int(st["slice_begin"]), int(st["slice_end"])   # this rank's slices
+    ids = sorted(set(np.linspace(s0, s1 - 1, min(nslices, s1 - s0)).astype(int).tolist()))
     t = x.tree
     r1, v1, r2, v2 = [], [], [], []
     for r in o.run_slices(ids, stage=1):
@@ -241,19 +243,26 @@ def main():
     solver = 1 if args.solver == "mals" else 0
     x = scenegen.make_inputs(scenegen.preset(args.config, solver=solver))
     stream = torch.cuda.current_stream(dev)
-    fr = lmc.Frame(x, rank=rank, world=world, stream=stream)
+    # world > 1 over NCCL: the image gather runs inside the library (lmc_resolve_image: every rank's
+    # packed rows to rank 0, one NCCL group); rank 0 makes the NCCL id, torch.distributed broadcasts it
+    lib_gather = world > 1 and os.environ.get("BENCH_DIST_BACKEND", "nccl") == "nccl"
+    nccl_id = None
+    if lib_gather:
+        idt = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            idt.copy_(torch.frombuffer(bytearray(lmc.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(idt, 0)
+        nccl_id = bytes(idt.cpu().tolist())
+    fr = lmc.Frame(x, rank=rank, world=world, stream=stream, nccl_id=nccl_id)
     fr.set_timing(True)
     npix = x.height * x.width
     img = torch.zeros(npix * 3, device=dev)
     st0 = fr.stats()
     rows_local = int(st0["rows"])
-    # slice-ordered row ranges of every rank (identical slicing everywhere) for the tile gather
-    if world > 1:
+    if world > 1 and not lib_gather:   # diagnostic gloo transport (BENCH_DIST_BACKEND=gloo)
         from paper_2202_12567_b200 import dist as pdist
-        fr.build_slices()
-        off, _ = fr.slices()
-        counts = pdist.row_counts(off, world)
-        tile = torch.zeros(rows_local * 3, device=dev)
+        counts = pdist.row_counts(fr.partition()[1])
+        tile = torch.zeros(rows_local * 4, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > L2 (126 MB)
 
     def frame_once():
@@ -262,11 +271,11 @@ def main():
         fr.coarsen_cut()
         fr.sample_pass2()
         fr.complete()
-        if world == 1:
+        if world == 1 or lib_gather:
             fr.resolve_image(img)
         else:
             fr.resolve_rows(tile)
-            all_rows = pdist.gather_rows(tile, counts)     # one NCCL all-gather over NVLink
+            all_rows = pdist.gather_rows(tile, counts)
             if rank == 0:
                 fr.scatter_rows(all_rows, img)
 

@@ -18,9 +18,10 @@
  *     inputs re-runs from build_slices).
  *   - Errors: LMC_EINVAL null pointers / sizes / invariants (rep(f) in {rep(l), rep(r)}, the
  *     global cut is an antichain cover, rate in (0,1], gamma in (0,1.618), 1 <= q <= 32,
- *     slice_target <= 1024, |global cut| <= 1024, p1_nmax <= 32);  LMC_ENOMEM device
- *     allocation failed;  LMC_ECUDA a CUDA error (sticky: the ctx must be destroyed);
- *     LMC_EOVERFLOW a per-slice capacity was exceeded (reported by the stage that detects it).
+ *     slice_target <= 1024, |global cut| <= 1024, p1_nmax <= 32, G-buffer pixel indices in
+ *     [0, width*height));  LMC_ENOMEM device allocation failed;  LMC_ECUDA a CUDA error (sticky:
+ *     the ctx must be destroyed);  LMC_EOVERFLOW a per-slice capacity was exceeded (reported by
+ *     the next getter);  LMC_ENCCL an NCCL call failed (sticky).
  *   - Thread safety: a ctx is not thread-safe; distinct ctxs are independent.  One ctx per
  *     GPU / rank; at most 16 live contexts per process (LMC_EINVAL beyond).
  */
@@ -38,7 +39,8 @@ typedef enum {
     LMC_ESTATE = 2,
     LMC_ENOMEM = 3,
     LMC_ECUDA = 4,
-    LMC_EOVERFLOW = 5
+    LMC_EOVERFLOW = 5,
+    LMC_ENCCL = 6
 } lmc_status;
 
 typedef enum { LMC_SOLVER_ADM = 0, LMC_SOLVER_MALS = 1 } lmc_solver;
@@ -101,9 +103,14 @@ typedef struct {
     double tol;             /* stop when ||P_Omega(M - XY)|| / ||P_Omega M|| < tol (0 = run K) */
     double alpha, beta, gamma; /* ADM penalties / step (R19) */
     double lambda;          /* MALS ridge */
-    int32_t rank, world;    /* this process' share: slices [S*rank/world, S*(rank+1)/world) */
+    int32_t rank, world;    /* this process' share of the slices (lmc_get_partition): for world = 2^k the
+                               rank-th subtree of depth k of the slicing (levels >= k are sliced by
+                               that rank only), otherwise slices [S*rank/world, S*(rank+1)/world) */
     int32_t input_memory;   /* lmc_memory of the gbuffer / vpls / tree arrays */
     void *stream;           /* cudaStream_t */
+    uint8_t nccl_id[128];   /* world > 1: the ncclUniqueId from lmc_nccl_unique_id() on rank 0, broadcast
+                               to every rank by the caller; all zero = no NCCL communicator (then the
+                               image is assembled with lmc_resolve_rows / lmc_scatter_rows) */
 } lmc_config;
 
 typedef struct {
@@ -162,16 +169,33 @@ lmc_status lmc_sample_pass2(lmc_ctx *ctx);
 lmc_status lmc_complete(lmc_ctx *ctx);
 
 /* Image: per slice out^k = tint^k * U (V w^k), written into image_rgb
- * (float32, height*width*3, row-major pixels, RGB interleaved) at this rank's pixels only;
- * other pixels are untouched.  image_memory: LMC_MEM_DEVICE or LMC_MEM_HOST (then the
- * rank's pixels are copied device->host and the call synchronises). */
+ * (float32, height*width*3, row-major pixels, RGB interleaved) at the G-buffer's pixels only;
+ * other pixels are untouched.  image_memory: LMC_MEM_DEVICE (enqueued, no synchronisation) or
+ * LMC_MEM_HOST (the call synchronises).
+ * world = 1: this rank's pixels.  world > 1 (needs the NCCL communicator of lmc_config.nccl_id):
+ * every rank packs its rows, rank 0 receives the other ranks' tiles with ncclRecv (the others
+ * ncclSend theirs; one NCCL group) and writes every pixel of the frame; image_rgb is ignored on
+ * ranks != 0 (may be NULL there).  world > 1 without a communicator: this rank's pixels only. */
 lmc_status lmc_resolve_image(lmc_ctx *ctx, float *image_rgb, int32_t image_memory);
 
-/* This rank's pixels as a packed tile in slice-row order (rows_rgb: float32 rows*3, device)
- * for a cross-rank gather; lmc_scatter_rows() writes a gathered, slice-ordered array of all
- * rows (every rank's tile concatenated in rank order) into a device image. */
-lmc_status lmc_resolve_rows(lmc_ctx *ctx, float *rows_rgb);
-lmc_status lmc_scatter_rows(lmc_ctx *ctx, const float *all_rows_rgb, float *image_rgb);
+/* ncclGetUniqueId for lmc_config.nccl_id (call on rank 0 only; LMC_ENCCL on failure) */
+lmc_status lmc_nccl_unique_id(uint8_t out[128]);
+
+/* The ranks' shares: slice_first[r] / row_first[r] = first slice / first slice-ordered row of rank r
+ * (world + 1 entries each, last = S / M).  Host buffers; either may be NULL. */
+lmc_status lmc_get_partition(lmc_ctx *ctx, int32_t *slice_first, int64_t *row_first);
+/* The same shares without a context or a GPU (host planning only, e.g. for tests): for `rows`
+ * G-buffer rows and slice_target, world + 1 entries each and the frame's slice count. */
+lmc_status lmc_plan_partition(int64_t rows, int32_t slice_target, int32_t world, int32_t *slice_first,
+                              int64_t *row_first, int64_t *n_slices);
+
+/* This rank's pixels as a packed tile for a cross-rank gather done by the caller (e.g. with
+ * torch.distributed): tile = rows x 4 float32 (r, g, b, image pixel index as int32 bits) in this
+ * rank's slice-row order (device buffer, lmc_get_stats().rows rows).  lmc_scatter_rows() writes n
+ * such packed rows (any order, e.g. every rank's tile concatenated) into a device image.  Both
+ * only enqueue. */
+lmc_status lmc_resolve_rows(lmc_ctx *ctx, float *tile);
+lmc_status lmc_scatter_rows(lmc_ctx *ctx, const float *tiles, int64_t n_rows, float *image_rgb);
 
 void lmc_destroy(lmc_ctx *ctx);
 const char *lmc_last_error(const lmc_ctx *ctx);

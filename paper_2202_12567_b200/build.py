@@ -43,7 +43,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
                 f.write(r.stderr)
     if force or _stale(LIB, objs):
         tmp = LIB + f".tmp{os.getpid()}"
-        cmd = [NVCC, "-shared", *ARCH, "-o", tmp, *objs]
+        cmd = [NVCC, "-shared", *ARCH, "-o", tmp, *objs, "-lnccl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)

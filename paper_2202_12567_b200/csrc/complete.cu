@@ -1091,6 +1091,7 @@ struct RArgs {
     const float *U, *V, *I, *direct_rgb;
     const float4 *prow;
     float *image, *rows_rgb;
+    float4 *tile4;   // optional packed (r, g, b, pixel index bits) per row of this rank (image gather)
 };
 
 __global__ void __launch_bounds__(256) k_resolve(RArgs A)
@@ -1147,6 +1148,7 @@ __global__ void __launch_bounds__(256) k_resolve(RArgs A)
             o1 = C.w * ir * d1;
             o2 = D.x * ir * d2;
         }
+        if (A.tile4) A.tile4[li] = make_float4(o0, o1, o2, __int_as_float(A.pixel[A.rows[A.row0 + li]]));
         if (A.rows_rgb) {
             A.rows_rgb[3 * li] = o0;
             A.rows_rgb[3 * li + 1] = o1;
@@ -1162,7 +1164,7 @@ __global__ void __launch_bounds__(256) k_resolve(RArgs A)
     }
 }
 
-cudaError_t run_resolve(lmc_ctx *c, float *image, float *rows_rgb)
+cudaError_t run_resolve(lmc_ctx *c, float *image, float *rows_rgb, float4 *tile4)
 {
     if (c->SL == 0) return cudaSuccess;
     RArgs A;
@@ -1185,6 +1187,7 @@ cudaError_t run_resolve(lmc_ctx *c, float *image, float *rows_rgb)
     A.prow = c->d.prow;
     A.image = image;
     A.rows_rgb = rows_rgb;
+    A.tile4 = tile4;
     k_resolve<<<c->SL, 256, 0, c->stream>>>(A);
     return cudaGetLastError();
 }
@@ -1206,6 +1209,25 @@ cudaError_t run_scatter(lmc_ctx *c, const float *all_rows, float *image)
     if (c->M == 0) return cudaSuccess;
     k_scatter<<<(unsigned)((c->M + 255) / 256), 256, 0, c->stream>>>(c->M, c->d.rows, c->d.pixel, all_rows, image,
                                                                        (int64_t)c->W * c->H);
+    return cudaGetLastError();
+}
+
+// packed (r, g, b, pixel) rows of every rank (rank 0 of an NCCL image gather) into the image
+__global__ void k_scatter4(int64_t n, const float4 *__restrict__ all4, float *image, int64_t npix)
+{
+    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const float4 v = all4[k];
+    const int64_t p = __float_as_int(v.w);
+    if (p < 0 || p >= npix) return;
+    image[3 * p] = v.x;
+    image[3 * p + 1] = v.y;
+    image[3 * p + 2] = v.z;
+}
+cudaError_t run_scatter4(lmc_ctx *c, const float4 *all4, int64_t n, float *image)
+{
+    if (n == 0) return cudaSuccess;
+    k_scatter4<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(n, all4, image, (int64_t)c->W * c->H);
     return cudaGetLastError();
 }
 

@@ -639,38 +639,44 @@ cudaError_t run_slicing(lmc_ctx *c)
     uint32_t *tkey = reinterpret_cast<uint32_t *>(c->d.keys), *tkey_alt = reinterpret_cast<uint32_t *>(c->d.keys) + M;
     k_iota<<<nb, 256, 0, st>>>(rows, M);
     for (const auto &L : c->levels) {
+        // rows [L.lo, L.lo + L.n) of this level (all rows, or this rank's subtree): every position
+        // array is offset by lo; row_tile / left-flags are indexed by the G-buffer row itself
+        const int64_t lo = L.lo, n = L.n;
+        const unsigned nbl = (unsigned)((n + 255) / 256);
+        int32_t *rws = rows + lo, *alt_l = alt + lo, *f_l = f + lo, *pre_l = pre + lo, *tmp_l = tmp_rows + lo;
+        uint32_t *tkey_l = tkey + lo, *tkey_alt_l = tkey_alt + lo;
         const int32_t *tbeg = c->d.lvl_begin + L.tile_off;
         const int32_t *tend = c->d.lvl_end + L.tile_off;
         const int32_t *tslot = c->d.lvl_slot + L.tile_off;
         k_ext_init<<<(L.nslots * 12 + 255) / 256, 256, 0, st>>>(c->d.ext, L.nslots);
-        k_slice_extent<<<L.work_n, 256, 0, st>>>(rows, c->d.lvl_work + 3 * L.work_off, c->d.ext, g, diag, wn);
-        k_slice_keys<<<nb, 256, 0, st>>>(rows, M, tbeg, tslot, L.tile_n, c->d.ext, c->d.keys_alt, row_tile, g, diag, wn);
+        k_slice_extent<<<L.work_n, 256, 0, st>>>(rws, c->d.lvl_work + 3 * L.work_off, c->d.ext, g, diag, wn);
+        k_slice_keys<<<nbl, 256, 0, st>>>(rws, n, tbeg, tslot, L.tile_n, c->d.ext, c->d.keys_alt + lo, row_tile, g, diag, wn);
         size_t bytes = c->d.cub_tmp_bytes;
-        unsigned long long *kin = c->d.keys_alt, *kout = c->d.keys_sorted;
+        unsigned long long *kin = c->d.keys_alt + lo, *kout = c->d.keys_sorted + lo;
         cudaError_t e;
         if (L.tile_n >= SLICE_SEG_MIN) {
             // tiles are contiguous ranges of `rows` (ascending rows inside): one stable segmented
             // sort by key per tile gives the same (tile, key, row) order as the two global sorts
-            e = cub::DeviceSegmentedSort::StableSortPairs(c->d.cub_tmp, bytes, kin, kout, rows, tmp_rows, (int)M,
+            e = cub::DeviceSegmentedSort::StableSortPairs(c->d.cub_tmp, bytes, kin, kout, rws, tmp_l, (int)n,
                                                           L.tile_n, tbeg, tend, st);
             if (e != cudaSuccess) return e;
         } else {
-            e = cub::DeviceRadixSort::SortPairs(c->d.cub_tmp, bytes, kin, kout, rows, alt, (int)M, 0, 64, st);
+            e = cub::DeviceRadixSort::SortPairs(c->d.cub_tmp, bytes, kin, kout, rws, alt_l, (int)n, 0, 64, st);
             if (e != cudaSuccess) return e;
-            k_tile_keys<<<nb, 256, 0, st>>>(alt, row_tile, M, tkey);
+            k_tile_keys<<<nbl, 256, 0, st>>>(alt_l, row_tile, n, tkey_l);
             int tbits = 1;
             while ((1 << tbits) < L.tile_n) ++tbits;
             bytes = c->d.cub_tmp_bytes;
-            e = cub::DeviceRadixSort::SortPairs(c->d.cub_tmp, bytes, tkey, tkey_alt, alt, tmp_rows, (int)M, 0, tbits, st);
+            e = cub::DeviceRadixSort::SortPairs(c->d.cub_tmp, bytes, tkey_l, tkey_alt_l, alt_l, tmp_l, (int)n, 0, tbits, st);
             if (e != cudaSuccess) return e;
         }
-        k_split_flags<<<nb, 256, 0, st>>>(tmp_rows, M, tbeg, tend, tslot, L.tile_n, alt /* left_by_row */);
-        k_gather_flags<<<nb, 256, 0, st>>>(rows, alt, M, f);
+        k_split_flags<<<nbl, 256, 0, st>>>(tmp_l, n, tbeg, tend, tslot, L.tile_n, alt /* left_by_row */);
+        k_gather_flags<<<nbl, 256, 0, st>>>(rws, alt, n, f_l);
         bytes = c->d.cub_tmp_bytes;
-        e = cub::DeviceScan::ExclusiveSum(c->d.cub_tmp, bytes, f, pre, (int)M, st);
+        e = cub::DeviceScan::ExclusiveSum(c->d.cub_tmp, bytes, f_l, pre_l, (int)n, st);
         if (e != cudaSuccess) return e;
-        k_split_scatter<<<nb, 256, 0, st>>>(rows, f, pre, M, tbeg, tend, tslot, L.tile_n, tmp_rows);
-        e = cudaMemcpyAsync(rows, tmp_rows, M * sizeof(int32_t), cudaMemcpyDeviceToDevice, st);
+        k_split_scatter<<<nbl, 256, 0, st>>>(rws, f_l, pre_l, n, tbeg, tend, tslot, L.tile_n, tmp_l);
+        e = cudaMemcpyAsync(rws, tmp_l, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, st);
         if (e != cudaSuccess) return e;
     }
     return cudaGetLastError();

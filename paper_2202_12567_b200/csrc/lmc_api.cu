@@ -2,6 +2,7 @@
 // state machine and getters.  No per-slice arithmetic runs here; every stage of the path is a
 // kernel in exact.cu / complete.cu.
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
@@ -79,6 +80,10 @@ cudaError_t hcopy_in(std::vector<T> &dst, const T *src, size_t n, int memory, cu
 
 void free_all(lmc_ctx *c)
 {
+    if (c->comm) {
+        ncclCommDestroy((ncclComm_t)c->comm);
+        c->comm = nullptr;
+    }
     Dev &d = c->d;
     void *ptrs[] = {d.pixel, d.g[0], d.g[1], d.g[2], d.g[3], d.g[4], d.g[5], d.g[6], d.g[7], d.g[8], d.g[9], d.g[10],
                     d.g[11], d.g[12], d.expo, d.vpl, d.ut_i32, d.ut_lum, d.ut_I, d.rows, d.rows_alt, d.keys,
@@ -89,7 +94,7 @@ void free_all(lmc_ctx *c)
                     d.newcells, d.newpos, d.U, d.V, d.Lam, d.Pi, d.Xold, d.S, d.flags, d.iters, d.resid,
                     d.direct_rgb, d.counters, d.img, d.rows_rgb, d.vpl_soa, d.r_perm, d.r_len, d.c_perm, d.c_len,
                     d.r_goff, d.c_goff, d.c_nsolo, d.adm_order, d.r_ent, d.c_ent, d.norm, d.r_grp, d.c_grp,
-                    d.r_slot, d.c_slot, d.ngrp, d.ctot, d.slot_st, d.ord_tmp, d.ord_cub, d.rank_pix};
+                    d.r_slot, d.c_slot, d.ngrp, d.ctot, d.slot_st, d.ord_tmp, d.ord_cub, d.rank_pix, d.all4};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (c->h_stage) cudaFreeHost(c->h_stage);
@@ -269,55 +274,122 @@ lmc_status build_upper(lmc_ctx *c, const HostTree &t)
 // ------------------------------------------------------------------------------------------
 // slicing structure: sizes depend only on (M, target): left child takes ceil(n/2)
 // ------------------------------------------------------------------------------------------
-lmc_status build_levels(lmc_ctx *c)
+// ------------------------------------------------------------------------------------------
+// slicing tree shape (sizes depend only on (M, target): the left child takes ceil(n/2)) and the
+// ranks' shares of it.  P = 2^k ranks and every node above depth k internal: rank r
+// owns the r-th depth-k subtree (slicing levels >= k then run on that rank only); otherwise the
+// slice index range [S r / P, S (r + 1) / P) of a replicated slicing.  Returns k, or -1.
+// ------------------------------------------------------------------------------------------
+struct TNode { int32_t start, len, depth; bool leaf; };
+
+static std::vector<TNode> slicing_tree(int64_t M, int32_t target)
 {
-    struct Node { int32_t start, len, depth; bool leaf; };
-    std::vector<Node> all;
+    std::vector<TNode> all;
     std::function<void(int32_t, int32_t, int32_t)> rec = [&](int32_t start, int32_t len, int32_t depth) {
-        bool leaf = len <= c->cfg.slice_target;
+        bool leaf = len <= target;
         all.push_back({start, len, depth, leaf});
         if (leaf) return;
         int32_t nl = (len + 1) / 2;
         rec(start, nl, depth + 1);
         rec(start + nl, len - nl, depth + 1);
     };
-    c->h_slice_off.assign(1, 0);
-    c->levels.clear();
-    if (c->M > 0) rec(0, (int32_t)c->M, 0);
-    int32_t maxd = 0;
-    for (auto &n : all) maxd = std::max(maxd, n.depth);
-    std::vector<Node> leaves;
+    if (M > 0) rec(0, (int32_t)M, 0);
+    return all;
+}
+
+static std::vector<int32_t> leaf_offsets(const std::vector<TNode> &all)
+{
+    std::vector<TNode> leaves;
     for (auto &n : all)
         if (n.leaf) leaves.push_back(n);
-    std::sort(leaves.begin(), leaves.end(), [](const Node &a, const Node &b) { return a.start < b.start; });
-    for (auto &n : leaves) c->h_slice_off.push_back(n.start + n.len);
-    c->S = (int32_t)leaves.size();
-    // tilings per depth: nodes at depth d + leaves at depth < d
+    std::sort(leaves.begin(), leaves.end(), [](const TNode &a, const TNode &b) { return a.start < b.start; });
+    std::vector<int32_t> off(1, 0);
+    for (auto &n : leaves) off.push_back(n.start + n.len);
+    return off;
+}
+
+static int plan_partition(const std::vector<TNode> &all, const std::vector<int32_t> &slice_off, int64_t M, int world,
+                          std::vector<int32_t> &part_slice, std::vector<int64_t> &part_row)
+{
+    const int32_t S = (int32_t)slice_off.size() - 1;
+    int k = -1;
+    std::vector<int32_t> sub_lo;
+    if (world > 1 && (world & (world - 1)) == 0) {
+        int kk = 0;
+        while ((1 << kk) < world) ++kk;
+        std::vector<TNode> at;
+        bool ok = true;
+        for (auto &n : all) {
+            if (n.depth == kk) at.push_back(n);
+            if (n.depth < kk && n.leaf) ok = false;
+        }
+        if (ok && (int)at.size() == world) {
+            std::sort(at.begin(), at.end(), [](const TNode &a, const TNode &b) { return a.start < b.start; });
+            k = kk;
+            for (auto &n : at) sub_lo.push_back(n.start);
+        }
+    }
+    part_slice.assign(world + 1, 0);
+    part_row.assign(world + 1, 0);
+    for (int r = 0; r <= world; ++r) {
+        if (k >= 0) {
+            const int64_t row = r < world ? sub_lo[r] : M;
+            part_row[r] = row;
+            part_slice[r] = r < world ? (int32_t)(std::lower_bound(slice_off.begin(), slice_off.end() - 1, (int32_t)row) -
+                                                  slice_off.begin())
+                                      : S;
+        } else {
+            const int32_t s = (int32_t)((int64_t)S * r / world);
+            part_slice[r] = s;
+            part_row[r] = slice_off[s];
+        }
+    }
+    return k;
+}
+
+lmc_status build_levels(lmc_ctx *c)
+{
+    typedef TNode Node;
+    std::vector<Node> all = slicing_tree(c->M, c->cfg.slice_target);
+    c->levels.clear();
+    int32_t maxd = 0;
+    for (auto &n : all) maxd = std::max(maxd, n.depth);
+    c->h_slice_off = leaf_offsets(all);
+    c->S = (int32_t)c->h_slice_off.size() - 1;
+    // ---- the ranks' shares, see plan_partition
+    int k = plan_partition(all, c->h_slice_off, c->M, c->cfg.world, c->h_part_slice, c->h_part_row);
+    c->sub_k = k;
+    const int64_t sub_a = c->h_part_row[c->cfg.rank], sub_b = c->h_part_row[c->cfg.rank + 1];
+    // tilings per depth: nodes at depth d + leaves at depth < d; from depth k on only this rank's
+    // subtree, positions relative to the level's first row
     std::vector<int32_t> beg, end, slot, work;
-    auto tiling = [&](int d, std::vector<Node> &out) {
+    auto tiling = [&](int d, int64_t lo, int64_t hi, std::vector<Node> &out) {
         out.clear();
         for (auto &n : all)
-            if (n.depth == d || (n.leaf && n.depth < d)) out.push_back(n);
+            if ((n.depth == d || (n.leaf && n.depth < d)) && n.start >= lo && n.start < hi) out.push_back(n);
         std::sort(out.begin(), out.end(), [](const Node &a, const Node &b) { return a.start < b.start; });
     };
     int max_tiles = 1;
-    std::vector<Node> cur, nxt;
+    std::vector<Node> cur;
     for (int d = 0; d < maxd; ++d) {
-        tiling(d, cur);
-        tiling(d + 1, nxt);
+        const bool sub = k >= 0 && d >= k;
+        const int64_t lo = sub ? sub_a : 0, hi = sub ? sub_b : c->M;
+        tiling(d, lo, hi, cur);
         lmc_ctx::Level L;
+        L.lo = lo;
+        L.n = hi - lo;
         L.tile_off = (int32_t)beg.size();
         L.tile_n = (int32_t)cur.size();
         int ns = 0;
         L.work_off = (int32_t)(work.size() / 3);
         for (auto &n : cur) {
-            beg.push_back(n.start);
-            end.push_back(n.start + n.len);
+            beg.push_back(n.start - (int32_t)lo);
+            end.push_back(n.start + n.len - (int32_t)lo);
             if (n.depth == d && !n.leaf) {
                 slot.push_back(ns);
                 for (int32_t o = 0; o < n.len; o += 4096) {
                     work.push_back(ns);
-                    work.push_back(n.start + o);
+                    work.push_back(n.start - (int32_t)lo + o);
                     work.push_back(std::min<int32_t>(4096, n.len - o));
                 }
                 ++ns;
@@ -327,15 +399,8 @@ lmc_status build_levels(lmc_ctx *c)
         }
         L.work_n = (int32_t)(work.size() / 3) - L.work_off;
         L.nslots = ns;
-        L.next_tile_off = (int32_t)beg.size();
-        L.next_tile_n = (int32_t)nxt.size();
-        for (auto &n : nxt) {
-            beg.push_back(n.start);
-            end.push_back(n.start + n.len);
-            slot.push_back(-1);
-        }
-        max_tiles = std::max(max_tiles, (int)std::max(cur.size(), nxt.size()));
-        c->levels.push_back(L);
+        max_tiles = std::max(max_tiles, (int)cur.size());
+        if (L.n > 0 && ns > 0) c->levels.push_back(L);
     }
     c->max_tiles = max_tiles;
     Dev &d = c->d;
@@ -400,6 +465,7 @@ const char *lmc_status_str(lmc_status s)
     case LMC_ENOMEM: return "LMC_ENOMEM";
     case LMC_ECUDA: return "LMC_ECUDA";
     case LMC_EOVERFLOW: return "LMC_EOVERFLOW";
+    case LMC_ENCCL: return "LMC_ENCCL";
     }
     return "LMC_UNKNOWN";
 }
@@ -484,8 +550,8 @@ static lmc_status create_impl(lmc_ctx *c, const lmc_gbuffer *g, const lmc_vpls *
     // slicing structure and this rank's share
     lmc_status st = build_levels(c);
     if (st != LMC_OK) return st;
-    c->s0 = (int32_t)((int64_t)c->S * cfg.rank / cfg.world);
-    c->s1 = (int32_t)((int64_t)c->S * (cfg.rank + 1) / cfg.world);
+    c->s0 = c->h_part_slice[cfg.rank];
+    c->s1 = c->h_part_slice[cfg.rank + 1];
     c->SL = c->s1 - c->s0;
     c->row0 = c->h_slice_off[c->s0];
     c->ML = c->h_slice_off[c->s1] - c->row0;
@@ -637,6 +703,22 @@ static lmc_status create_impl(lmc_ctx *c, const lmc_gbuffer *g, const lmc_vpls *
                     c->q, c->mmax, (long long)G, need, maxsm);
     for (auto &e : c->ev) CK(cudaEventCreate(&e), "events");
     c->ev_ok = true;
+    // NCCL communicator of the image gather (world > 1 with an id from lmc_nccl_unique_id)
+    bool has_id = false;
+    for (int k = 0; k < 128; ++k) has_id = has_id || cfg.nccl_id[k] != 0;
+    if (cfg.world > 1 && has_id) {
+        ncclUniqueId id;
+        static_assert(sizeof(id.internal) == 128, "ncclUniqueId is 128 bytes");
+        memcpy(id.internal, cfg.nccl_id, 128);
+        ncclComm_t comm = nullptr;
+        ncclResult_t r = ncclCommInitRank(&comm, cfg.world, id, cfg.rank);
+        if (r != ncclSuccess) {
+            c->sticky = LMC_ENCCL;
+            return fail(c, LMC_ENCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+        }
+        c->comm = comm;
+        CK(dalloc(&d.all4, (size_t)std::max<int64_t>(cfg.rank == 0 ? c->M : c->ML, 1)), "alloc gather");
+    }
     return lmc_upload_inputs(c, g, v, t);
 }
 
@@ -793,11 +875,71 @@ lmc_status lmc_complete(lmc_ctx *c)
     return LMC_OK;
 }
 
+// world > 1: every rank packs its rows as (r, g, b, pixel index) float4s; rank 0 receives every
+// other rank's tile at that rank's row offset and scatters all of them into the image -- one
+// NCCL group of P - 1 send / receive pairs, no all-gather
+static lmc_status resolve_gather(lmc_ctx *c, float *image, int32_t image_memory)
+{
+    const int world = c->cfg.world, rank = c->cfg.rank;
+    ncclComm_t comm = (ncclComm_t)c->comm;
+    const size_t f4 = sizeof(float4) / sizeof(float);
+    if (rank == 0) {
+        if (!image) return fail(c, LMC_EINVAL, "null image on rank 0");
+        if (image_memory != LMC_MEM_DEVICE && image_memory != LMC_MEM_HOST) return fail(c, LMC_EINVAL, "bad image_memory");
+        CK(run_resolve(c, nullptr, nullptr, c->d.all4), "resolve");   // rank 0's rows come first
+        ncclResult_t r = ncclGroupStart();
+        for (int p = 1; p < world && r == ncclSuccess; ++p) {
+            const int64_t r0 = c->h_part_row[p], r1 = c->h_part_row[p + 1];
+            if (r1 > r0) r = ncclRecv(c->d.all4 + r0, (size_t)(f4 * (r1 - r0)), ncclFloat, p, comm, c->stream);
+        }
+        ncclResult_t r2 = ncclGroupEnd();
+        if (r != ncclSuccess || r2 != ncclSuccess) {
+            c->sticky = LMC_ENCCL;
+            return fail(c, LMC_ENCCL, "image gather: %s", ncclGetErrorString(r != ncclSuccess ? r : r2));
+        }
+        c->launches += (c->SL > 0 ? 1 : 0) + (c->M > 0 ? 1 : 0);
+        if (image_memory == LMC_MEM_DEVICE) {
+            CK(run_scatter4(c, c->d.all4, c->M, image), "scatter");
+            ev_rec(c, 6);
+            return LMC_OK;
+        }
+        // host image: the packed rows come down and are scattered here (other pixels untouched)
+        ev_rec(c, 6);
+        std::vector<float4> h((size_t)c->M);
+        CK(cudaMemcpyAsync(h.data(), c->d.all4, sizeof(float4) * (size_t)c->M, cudaMemcpyDeviceToHost, c->stream),
+           "image download");
+        CK(cudaStreamSynchronize(c->stream), "sync");
+        const int64_t npix = (int64_t)c->W * c->H;
+        for (const float4 &v : h) {
+            int32_t p;
+            memcpy(&p, &v.w, 4);
+            if (p < 0 || p >= npix) continue;
+            image[3 * (int64_t)p] = v.x;
+            image[3 * (int64_t)p + 1] = v.y;
+            image[3 * (int64_t)p + 2] = v.z;
+        }
+        return LMC_OK;
+    }
+    CK(run_resolve(c, nullptr, nullptr, c->d.all4), "resolve");
+    c->launches += c->SL > 0 ? 1 : 0;
+    ev_rec(c, 6);
+    if (c->ML > 0) {
+        ncclResult_t r = ncclSend(c->d.all4, (size_t)(f4 * c->ML), ncclFloat, 0, comm, c->stream);
+        if (r != ncclSuccess) {
+            c->sticky = LMC_ENCCL;
+            return fail(c, LMC_ENCCL, "image gather: %s", ncclGetErrorString(r));
+        }
+    }
+    if (image_memory == LMC_MEM_HOST) CK(cudaStreamSynchronize(c->stream), "sync");
+    return LMC_OK;
+}
+
 lmc_status lmc_resolve_image(lmc_ctx *c, float *image, int32_t image_memory)
 {
     lmc_status s = check_stage(c, 5);
     if (s != LMC_OK) return s;
-    if (!image) return fail(c, LMC_EINVAL, "null image");
+    if (!image && !(c->comm && c->cfg.rank != 0)) return fail(c, LMC_EINVAL, "null image");
+    if (c->comm) return resolve_gather(c, image, image_memory);
     c->launches += c->SL > 0 ? 1 : 0;
     if (image_memory == LMC_MEM_DEVICE) {
         CK(run_resolve(c, image, nullptr), "resolve");
@@ -833,24 +975,24 @@ lmc_status lmc_resolve_image(lmc_ctx *c, float *image, int32_t image_memory)
     return LMC_OK;
 }
 
-lmc_status lmc_resolve_rows(lmc_ctx *c, float *rows_rgb)
+lmc_status lmc_resolve_rows(lmc_ctx *c, float *tile)
 {
     lmc_status s = check_stage(c, 5);
     if (s != LMC_OK) return s;
-    if (!rows_rgb) return fail(c, LMC_EINVAL, "null rows_rgb");
-    CK(run_resolve(c, nullptr, rows_rgb), "resolve");
+    if (!tile) return fail(c, LMC_EINVAL, "null tile");
+    CK(run_resolve(c, nullptr, nullptr, reinterpret_cast<float4 *>(tile)), "resolve");
     c->launches += c->SL > 0 ? 1 : 0;
     ev_rec(c, 6);
     return LMC_OK;
 }
 
-lmc_status lmc_scatter_rows(lmc_ctx *c, const float *all_rows, float *image)
+lmc_status lmc_scatter_rows(lmc_ctx *c, const float *tiles, int64_t n_rows, float *image)
 {
-    lmc_status s = check_stage(c, 1);
+    lmc_status s = check_stage(c, 0);
     if (s != LMC_OK) return s;
-    if (!all_rows || !image) return fail(c, LMC_EINVAL, "null buffer");
-    CK(run_scatter(c, all_rows, image), "scatter");
-    c->launches += c->M > 0 ? 1 : 0;
+    if (n_rows < 0 || (n_rows > 0 && (!tiles || !image))) return fail(c, LMC_EINVAL, "null buffer");
+    CK(run_scatter4(c, reinterpret_cast<const float4 *>(tiles), n_rows, image), "scatter");
+    c->launches += n_rows > 0 ? 1 : 0;
     return LMC_OK;
 }
 
@@ -1003,6 +1145,37 @@ lmc_status lmc_get_factors(lmc_ctx *c, int32_t slice, float *U, float *V, int32_
         for (int j = 0; j < nn; ++j)
             for (int a = 0; a < c->q; ++a) V[(size_t)a * nn + j] = vt[(size_t)j * c->q + a];
     }
+    return LMC_OK;
+}
+
+lmc_status lmc_nccl_unique_id(uint8_t out[128])
+{
+    if (!out) return LMC_EINVAL;
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) return LMC_ENCCL;
+    memcpy(out, id.internal, 128);
+    return LMC_OK;
+}
+
+lmc_status lmc_plan_partition(int64_t rows, int32_t slice_target, int32_t world, int32_t *slice_first,
+                              int64_t *row_first, int64_t *n_slices)
+{
+    if (rows < 0 || slice_target < 1 || world < 1) return LMC_EINVAL;
+    std::vector<TNode> all = slicing_tree(rows, slice_target);
+    std::vector<int32_t> off = leaf_offsets(all), ps;
+    std::vector<int64_t> pr;
+    plan_partition(all, off, rows, world, ps, pr);
+    if (slice_first) memcpy(slice_first, ps.data(), ps.size() * sizeof(int32_t));
+    if (row_first) memcpy(row_first, pr.data(), pr.size() * sizeof(int64_t));
+    if (n_slices) *n_slices = (int64_t)off.size() - 1;
+    return LMC_OK;
+}
+
+lmc_status lmc_get_partition(lmc_ctx *c, int32_t *slice_first, int64_t *row_first)
+{
+    if (!c) return LMC_EINVAL;
+    if (slice_first) memcpy(slice_first, c->h_part_slice.data(), c->h_part_slice.size() * sizeof(int32_t));
+    if (row_first) memcpy(row_first, c->h_part_row.data(), c->h_part_row.size() * sizeof(int64_t));
     return LMC_OK;
 }
 

@@ -114,6 +114,8 @@ struct Dev {
     void *ord_cub;                     // CUB radix-sort temp of the launch order
     size_t ord_cub_bytes;
     int32_t *rank_pix;                 // [ML] image index of this rank's rows (host-buffer resolve)
+    float4 *all4;                      // world > 1 with NCCL: [ML] this rank's packed (r, g, b, pixel) rows;
+                                       // rank 0: [M], every rank's tile at its row offset
     unsigned long long *r_ent;         // [SL][scap] (M^ bits << 32) | (column-layout index << 10) | column
     uint16_t *c_ent;                   // [SL][scap] row of the column-layout entry
     float4 *norm;                      // [SL] sigma, 1/sigma, sum M^, sum M^^2
@@ -160,7 +162,10 @@ struct lmc_ctx {
     int32_t adm2_Tr = 64, adm2_Tc = 64;   // segment length caps (rows, columns)
     bool use_adm2 = false;         // complete2.cu kernels (q <= 16) instead of complete.cu
     // slicing level structure
-    struct Level { int32_t tile_off, tile_n, work_off, work_n, next_tile_off, next_tile_n, nslots; };
+    struct Level { int64_t lo, n; int32_t tile_off, tile_n, work_off, work_n, nslots; };   // rows [lo, lo + n); tiles relative to lo
+    int32_t sub_k = -1;            // P = 2^k ranks: slicing levels >= k run in this rank's subtree only
+    std::vector<int32_t> h_part_slice;   // [world + 1] first slice of every rank
+    std::vector<int64_t> h_part_row;     // [world + 1] first row of every rank
     std::vector<Level> levels;
     int32_t max_tiles = 0;
     // scene + upper tree
@@ -180,6 +185,7 @@ struct lmc_ctx {
     float *h_stage = nullptr;
     int32_t *h_pix = nullptr;      // pinned [ML] pixel ids of the host-buffer resolve
     int64_t launches = 0;          // kernels (and CUB dispatches, 1 each) issued by stage calls
+    void *comm = nullptr;          // ncclComm_t of the image gather (world > 1 with an NCCL id)
 };
 
 namespace lmc {
@@ -200,7 +206,8 @@ cudaError_t upload_scene(int slot, const SceneConst &sc);
 // complete.cu (fp32 completion + resolve)
 cudaError_t run_layout(lmc_ctx *c);
 cudaError_t run_adm(lmc_ctx *c, int nmax);
-cudaError_t run_resolve(lmc_ctx *c, float *image, float *rows_rgb);
+cudaError_t run_resolve(lmc_ctx *c, float *image, float *rows_rgb, float4 *tile4 = nullptr);
+cudaError_t run_scatter4(lmc_ctx *c, const float4 *all4, int64_t n, float *image);
 cudaError_t run_scatter(lmc_ctx *c, const float *all_rows, float *image);
 cudaError_t run_rank_pixels(lmc_ctx *c, int32_t *out);
 cudaError_t run_check_pixels(lmc_ctx *c, unsigned long long *flag);

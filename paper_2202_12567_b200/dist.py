@@ -1,43 +1,39 @@
-"""Multi-GPU plumbing for the slice-sharded frame (DESIGN.md §8).
+"""Multi-GPU plumbing for the slice-sharded frame (DESIGN.md §8, SURVEY §8(e)).
 
-Slices are independent after slicing: rank r of P owns slices
-[S*r/P, S*(r+1)/P) (lmc_config.rank/world), resolves its pixels as a packed tile in slice-row
-order (lmc_resolve_rows), and the tiles are gathered with one collective; rank 0 scatters the
-concatenation into the image (lmc_scatter_rows).  torch.distributed is the transport (NCCL over
-NVLink on GPUs, gloo in the CPU tests).
+Slices are independent after slicing.  With P = 2^k ranks, rank r owns the
+r-th depth-k subtree of the slicing (every rank slices the top k levels of the whole G-buffer,
+then only inside its subtree); other P split the slice index range.  The library reports the
+shares (Frame.partition()).  The production image assembly is inside the library: the ranks pass
+an NCCL id (lmc_nccl_unique_id on rank 0, broadcast with torch.distributed) and
+lmc_resolve_image gathers every rank's packed rows to rank 0 over NVLink (one NCCL group of
+send / receive pairs).  This module is the alternative transport through torch.distributed (gloo
+in the CPU tests and the single-GPU multi-rank test): each rank packs its rows (lmc_resolve_rows,
+4 floats per row: r, g, b, pixel index), rank 0 gathers them and scatters (lmc_scatter_rows).
 """
 from __future__ import annotations
 
 
-def slice_range(S: int, rank: int, world: int):
-    """slices of a rank: the same integer split as lmc_create (s0 = S*rank/world)"""
-    return (S * rank) // world, (S * (rank + 1)) // world
+def row_counts(row_first):
+    """rows per rank from the partition's row offsets (world + 1 entries, identical on every rank)"""
+    return [int(row_first[r + 1]) - int(row_first[r]) for r in range(len(row_first) - 1)]
 
 
-def row_counts(slice_off, world: int):
-    """rows per rank, in rank order, from the slice offsets (identical on every rank)"""
-    S = len(slice_off) - 1
-    out = []
-    for r in range(world):
-        s0, s1 = slice_range(S, r, world)
-        out.append(int(slice_off[s1]) - int(slice_off[s0]))
-    return out
-
-
-def gather_rows(tile, counts, group=None):
-    """All-gather the per-rank packed tiles (rows x 3 floats, slice-row order) into the
-    slice-ordered array of all rows.  Tiles are padded to the largest rank's size so one
-    equal-size collective moves them; returns a tensor of sum(counts) x 3 on every rank."""
+def gather_rows(tile, counts, group=None, dst=0):
+    """Gather the per-rank packed tiles (rows x 4 floats) to rank `dst` (padded to the largest tile
+    so that one equal-size collective moves them); returns the concatenation (sum(counts) x 4) on
+    `dst` and None elsewhere."""
     import torch
     import torch.distributed as dist
     world = len(counts)
     rank = dist.get_rank(group)
     mx = max(counts)
-    pad = torch.zeros(mx * 3, dtype=tile.dtype, device=tile.device)
-    pad[: counts[rank] * 3] = tile.reshape(-1)[: counts[rank] * 3]
+    pad = torch.zeros(mx * 4, dtype=tile.dtype, device=tile.device)
+    pad[: counts[rank] * 4] = tile.reshape(-1)[: counts[rank] * 4]
     dev = pad.device
-    if pad.is_cuda and dist.get_backend(group) == "gloo":   # gloo moves host tensors (CPU tests)
+    if pad.is_cuda and dist.get_backend(group) == "gloo":   # gloo moves host tensors
         pad = pad.cpu()
-    parts = [torch.empty_like(pad) for _ in range(world)]
-    dist.all_gather(parts, pad, group=group)
-    return torch.cat([parts[r][: counts[r] * 3] for r in range(world)]).view(-1, 3).to(dev)
+    parts = [torch.empty_like(pad) for _ in range(world)] if rank == dst else None
+    dist.gather(pad, parts, dst=dst, group=group)
+    if rank != dst:
+        return None
+    return torch.cat([parts[r][: counts[r] * 4] for r in range(world)]).view(-1, 4).to(dev)

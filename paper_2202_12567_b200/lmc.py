@@ -15,7 +15,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 # LMC_LIB: alternative build of the same library (diagnostic builds); default in-tree
 LIB_PATH = os.environ.get("LMC_LIB") or os.path.join(_HERE, "liblmc.so")
 
-LMC_OK, LMC_EINVAL, LMC_ESTATE, LMC_ENOMEM, LMC_ECUDA, LMC_EOVERFLOW = range(6)
+LMC_OK, LMC_EINVAL, LMC_ESTATE, LMC_ENOMEM, LMC_ECUDA, LMC_EOVERFLOW, LMC_ENCCL = range(7)
 SOLVER_ADM, SOLVER_MALS = 0, 1
 MEM_DEVICE, MEM_HOST = 0, 1
 SLICE_DIRECT, SLICE_DIVERGED, SLICE_ZERO = 1, 2, 4
@@ -49,7 +49,8 @@ class Config(C.Structure):
                 ("p1_nmax", C.c_int32), ("p1_nmin", C.c_int32), ("coarsen_tau", C.c_double), ("rate", C.c_double),
                 ("rank_q", C.c_int32), ("solver", C.c_int32), ("max_iter", C.c_int32), ("tol", C.c_double),
                 ("alpha", C.c_double), ("beta", C.c_double), ("gamma", C.c_double), ("lambda_", C.c_double),
-                ("rank", C.c_int32), ("world", C.c_int32), ("input_memory", C.c_int32), ("stream", _P)]
+                ("rank", C.c_int32), ("world", C.c_int32), ("input_memory", C.c_int32), ("stream", _P),
+                ("nccl_id", C.c_uint8 * 128)]
 
 
 class Stats(C.Structure):
@@ -68,7 +69,7 @@ EXPORTS = ["lmc_create", "lmc_upload_inputs", "lmc_build_slices", "lmc_sample_pa
            "lmc_sample_pass2", "lmc_complete", "lmc_resolve_image", "lmc_resolve_rows", "lmc_scatter_rows",
            "lmc_destroy", "lmc_last_error", "lmc_status_str", "lmc_get_slices", "lmc_get_pass1", "lmc_get_coarsen",
            "lmc_get_cut", "lmc_get_samples", "lmc_get_factors", "lmc_get_stats", "lmc_set_timing",
-           "lmc_eval_entries"]
+           "lmc_eval_entries", "lmc_nccl_unique_id", "lmc_get_partition", "lmc_plan_partition"]
 
 
 def _load():
@@ -85,7 +86,10 @@ def _load():
         getattr(L, f).restype = ST
     L.lmc_resolve_image.argtypes = [_P, _P, C.c_int32]
     L.lmc_resolve_rows.argtypes = [_P, _P]
-    L.lmc_scatter_rows.argtypes = [_P, _P, _P]
+    L.lmc_scatter_rows.argtypes = [_P, _P, C.c_int64, _P]
+    L.lmc_nccl_unique_id.argtypes = [_P]
+    L.lmc_get_partition.argtypes = [_P, _P, _P]
+    L.lmc_plan_partition.argtypes = [C.c_int64, C.c_int32, C.c_int32, _P, _P, _P]
     L.lmc_destroy.argtypes = [_P]
     L.lmc_destroy.restype = None
     L.lmc_last_error.argtypes = [_P]
@@ -127,7 +131,8 @@ class Frame:
     lmc_create are device tensors (MEM_DEVICE, via torch) or pinned host arrays (MEM_HOST).
     """
 
-    def __init__(self, inputs, memory=MEM_DEVICE, rank=0, world=1, stream=None, device="cuda", **override):
+    def __init__(self, inputs, memory=MEM_DEVICE, rank=0, world=1, stream=None, device="cuda", nccl_id=None,
+                 **override):
         import torch
         self.x = inputs
         self.memory = memory
@@ -169,6 +174,8 @@ class Frame:
                           prm["tau"], prm["rate"], prm["rank_q"], prm["solver"], prm["max_iter"], prm["tol"],
                           prm["alpha"], prm["beta"], prm["gamma"], prm["lam"], rank, world, memory,
                           _P(stream.cuda_stream))
+        if nccl_id is not None:
+            self.cfg.nccl_id = (C.c_uint8 * 128)(*bytes(nccl_id))
         h = _P()
         st = lib.lmc_create(C.byref(self.gb), C.byref(self.vp), C.byref(self.tr), C.byref(self.sc),
                             C.byref(self.cfg), C.byref(h))
@@ -215,11 +222,22 @@ class Frame:
     def resolve_image(self, image, memory=MEM_DEVICE):
         self._ck(lib.lmc_resolve_image(self.h, _ptr(image), memory), "resolve_image")
 
-    def resolve_rows(self, rows_rgb):
-        self._ck(lib.lmc_resolve_rows(self.h, _ptr(rows_rgb)), "resolve_rows")
+    def resolve_rows(self, tile):
+        """this rank's rows packed as (r, g, b, pixel bits) float32 x 4 into a device tensor"""
+        self._ck(lib.lmc_resolve_rows(self.h, _ptr(tile)), "resolve_rows")
 
-    def scatter_rows(self, all_rows, image):
-        self._ck(lib.lmc_scatter_rows(self.h, _ptr(all_rows), _ptr(image)), "scatter_rows")
+    def scatter_rows(self, tiles, image):
+        """packed rows (n x 4 float32, any order) into a device image"""
+        n = tiles.numel() // 4
+        self._ck(lib.lmc_scatter_rows(self.h, _ptr(tiles), n, _ptr(image)), "scatter_rows")
+
+    def partition(self):
+        """(slice_first, row_first): every rank's first slice / slice-ordered row, world + 1 entries"""
+        w = int(self.cfg.world)
+        s = np.zeros(w + 1, np.int32)
+        r = np.zeros(w + 1, np.int64)
+        self._ck(lib.lmc_get_partition(self.h, _ptr(s), _ptr(r)), "get_partition")
+        return s, r
 
     def run(self, image, memory=MEM_DEVICE):
         self.build_slices()
@@ -306,3 +324,23 @@ class Frame:
         out = np.zeros(rows.size)
         self._ck(lib.lmc_eval_entries(self.h, rows.size, _ptr(rows), _ptr(vpls), _ptr(out)), "eval_entries")
         return out
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte ncclUniqueId for Frame(nccl_id=...) (rank 0 creates it, the caller broadcasts it)"""
+    buf = (C.c_uint8 * 128)()
+    st = lib.lmc_nccl_unique_id(C.cast(buf, _P))
+    if st != LMC_OK:
+        raise LmcError(f"lmc_nccl_unique_id: {lib.lmc_status_str(st).decode()}")
+    return bytes(buf)
+
+
+def plan_partition(rows: int, slice_target: int, world: int):
+    """(slice_first, row_first, n_slices) of the ranks' shares -- host planning only, no GPU needed"""
+    s = np.zeros(world + 1, np.int32)
+    r = np.zeros(world + 1, np.int64)
+    n = np.zeros(1, np.int64)
+    st = lib.lmc_plan_partition(rows, slice_target, world, _ptr(s), _ptr(r), _ptr(n))
+    if st != LMC_OK:
+        raise LmcError(f"lmc_plan_partition: {lib.lmc_status_str(st).decode()}")
+    return s, r, int(n[0])

@@ -1,9 +1,11 @@
-"""The slice-sharded multi-rank frame on the GPU: world-size 2 and 3, every rank on
-GPU 0 with the gloo transport (one GPU is available to the tests; the production path is NCCL
-with one rank per GPU).  Each rank runs the CUDA path on its slice range (lmc_config.rank/world),
-packs its rows (lmc_resolve_rows), the tiles are all-gathered and rank 0 scatters them
-(lmc_scatter_rows): the image must equal the single-rank image bit for bit, since a slice's
-computation does not depend on which rank runs it."""
+"""The slice-sharded multi-rank frame on the GPU: world-size 2 (a depth-1 subtree
+per rank: the ranks slice only the top level of the whole G-buffer, then their own subtree) and 3
+(slice index ranges), every rank on GPU 0 with the gloo transport (one GPU is available to the
+tests; the production path gathers with NCCL inside lmc_resolve_image, one rank per GPU).  Each
+rank runs the CUDA path on its share (lmc_get_partition), packs its rows (lmc_resolve_rows), the
+tiles are gathered to rank 0 and scattered (lmc_scatter_rows): the image must equal the
+single-rank image bit for bit, and each rank's slicing must equal the single-rank slicing on its
+rows, since a slice's computation does not depend on which rank runs it."""
 import os
 import socket
 
@@ -41,22 +43,24 @@ def _worker(rank, world, port, name, q):
     x = scenegen.make_inputs(name)
     fr = lmc.Frame(x, rank=rank, world=world)
     fr.build_slices()
-    off, _ = fr.slices()
-    counts = pdist.row_counts(off, world)
+    sf, rf = fr.partition()
+    counts = pdist.row_counts(rf)
     st = fr.stats()
-    assert st["rows"] == counts[rank]
+    assert st["rows"] == counts[rank] and st["slice_begin"] == sf[rank] and st["slice_end"] == sf[rank + 1]
+    off, rows = fr.slices()
     fr.sample_pass1()
     fr.coarsen_cut()
     fr.sample_pass2()
     fr.complete()
-    tile = torch.zeros(counts[rank] * 3, device="cuda")
+    tile = torch.zeros(counts[rank] * 4, device="cuda")
     fr.resolve_rows(tile)
     allrows = pdist.gather_rows(tile, counts)
+    q.put(("rows", rank, int(rf[rank]), int(rf[rank + 1]), rows[rf[rank]:rf[rank + 1]].copy()))
     if rank == 0:
         img = torch.zeros(x.height * x.width * 3, device="cuda")
         fr.scatter_rows(allrows, img)
         torch.cuda.synchronize()
-        q.put(img.cpu().numpy())
+        q.put(("img", img.cpu().numpy()))
     dist.barrier()
     fr.close()
     dist.destroy_process_group()
@@ -72,16 +76,21 @@ def test_sharded_frame_equals_single_rank(world):
     procs = [ctx.Process(target=_worker, args=(r, world, port, name, q)) for r in range(world)]
     for p in procs:
         p.start()
-    got = q.get(timeout=600)
+    items = [q.get(timeout=600) for _ in range(world + 1)]
     for p in procs:
         p.join(timeout=300)
         assert p.exitcode == 0
+    got = [it[1] for it in items if it[0] == "img"][0]
+    parts = [it for it in items if it[0] == "rows"]
     x = scenegen.make_inputs(name)
     fr = lmc.Frame(x)
     img = torch.zeros(x.height * x.width * 3, device="cuda")
     fr.run(img)
     torch.cuda.synchronize()
     ref = img.cpu().numpy()
+    _, rows1 = fr.slices()
     fr.close()
+    for _, r, a, b, rws in parts:   # each rank's slicing equals the single-rank slicing on its rows
+        assert np.array_equal(rws, rows1[a:b]), f"rank {r}: slicing differs"
     assert np.array_equal(got, ref)
     assert np.count_nonzero(ref) > 0.5 * ref.size
