@@ -111,6 +111,12 @@ typedef struct {
     uint8_t nccl_id[128];   /* world > 1: the ncclUniqueId from lmc_nccl_unique_id() on rank 0, broadcast
                                to every rank by the caller; all zero = no NCCL communicator (then the
                                image is assembled with lmc_resolve_rows / lmc_scatter_rows) */
+    /* SURVEY §8(f3) variants, 0 = the paper's method:
+     *   row_importance 1: pass-2 rows drawn by f(i) = max - min of the row's carried observations
+     *                     (integer weights as for g(j); P:145 sets f = 1; DESIGN R36)
+     *   cost_mode 1:      Eq. (1) sensitivity, cost(L_f) = (eps(L_f) + cost(L_b)) + cost(L_a)
+     *   resolve_mode 1:   Z-mode image, tint (<U_i, V w^k> + sum_{j in Omega_i} (M~_ij - <U_i, V_j>) w^k_j) */
+    int32_t row_importance, cost_mode, resolve_mode;
 } lmc_config;
 
 typedef struct {

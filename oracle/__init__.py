@@ -54,6 +54,7 @@ class _Inputs(C.Structure):
         ("q", C.c_int32), ("solver", C.c_int32), ("K", C.c_int32),
         ("tol", C.c_double), ("alpha", C.c_double), ("beta", C.c_double), ("gamma", C.c_double), ("lam", C.c_double),
         ("order_seed", C.c_uint64),
+        ("row_importance", C.c_int32), ("cost_mode", C.c_int32), ("resolve_mode", C.c_int32),
     ]
 
 
@@ -115,6 +116,8 @@ def lib():
             L.orc_pdf_weights.argtypes = [C.c_int32, P, P, P]
             L.orc_cdf_pick.argtypes = [C.c_int32, P, C.c_uint64]
             L.orc_cdf_pick.restype = C.c_int32
+            L.orc_pass2_draw_f.argtypes = [C.c_uint64, C.c_int32, C.c_uint32, C.c_uint64, P, C.c_int32, C.c_uint64, P,
+                                           C.c_int32, P, P]
             L.orc_pass2_draws.argtypes = [C.c_uint64, C.c_int32, C.c_uint32, C.c_int64, P, C.c_int32, C.c_int32, P, P]
             _lib = L
     return _lib
@@ -173,6 +176,9 @@ class Oracle:
         s.q, s.solver, s.K = prm["rank_q"], prm["solver"], prm["max_iter"]
         s.tol, s.alpha, s.beta, s.gamma, s.lam = prm["tol"], prm["alpha"], prm["beta"], prm["gamma"], prm["lam"]
         s.order_seed = prm.get("order_seed", 0)
+        s.row_importance = prm.get("row_importance", 0)
+        s.cost_mode = prm.get("cost_mode", 0)
+        s.resolve_mode = prm.get("resolve_mode", 0)
         self._keep = keep
         self.s = s
         self._slices = None
@@ -351,3 +357,14 @@ def pass2_draws(w, m, count, seed=12567, slice_id=0, t0=0):
     cols = np.zeros(count, np.int32)
     lib().orc_pass2_draws(seed, slice_id, t0, count, _p(w), w.size, m, _p(rows), _p(cols))
     return rows, cols
+
+
+def pass2_draw_f(t, w, wr, seed=12567, slice_id=0):
+    """one pass-2 draw with row importance (column CDF from w, row CDF from wr) -> (row, col)"""
+    cdf = np.cumsum(np.asarray(w, np.uint64)).astype(np.uint64)
+    rcdf = np.cumsum(np.asarray(wr, np.uint64)).astype(np.uint64)
+    r = np.zeros(1, np.int32)
+    c = np.zeros(1, np.int32)
+    lib().orc_pass2_draw_f(seed, slice_id, t, int(cdf[-1]), _p(cdf), cdf.size, int(rcdf[-1]), _p(rcdf), rcdf.size,
+                           _p(r), _p(c))
+    return int(r[0]), int(c[0])

@@ -507,8 +507,10 @@ static void coarsen(slice_ctx *c, orc_slice_result *res, const int32_t *parent)
             dv_push(&pva, Ta);
             dv_push(&pvb, Tb);
         }
-        /* Eq. (1): cost(L_f) = eps(L_f) + cost(L_b) (R9) */
+        /* Eq. (1): cost(L_f) = eps(L_f) + cost(L_b) (R9); the sensitivity variant also adds
+         * the accumulated error of L_a (cost_mode 1): (eps + cost(L_b)) + cost(L_a) */
         double cf = eps + cost[b];
+        if (in->cost_mode) cf = cf + cost[a];
         int do_merge = cf < in->tau; /* P:116 "less than a prespecified error bound" (R11) */
         zidx[f] = (int32_t)pnode.n;
         iv_push(&pnode, f);
@@ -637,6 +639,20 @@ void orc_pass2_draw(uint64_t seed, int32_t slice, uint32_t t, uint64_t W, const 
     *row = (int32_t)randint(u[1], (uint32_t)m);
 }
 
+/* Draw t with an image-space row importance f(i) (P:145 sets f(i) = 1, P:246 names
+ * image-space guidance as future work): the row is CDF_r^-1((u1 W_r) >> 32) over integer row
+ * weights built like the column weights (R14) from the rows' carried observations (reading R36). */
+void orc_pass2_draw_f(uint64_t seed, int32_t slice, uint32_t t, uint64_t W, const uint64_t *cdf, int32_t n, uint64_t Wr,
+                      const uint64_t *rcdf, int32_t m, int32_t *row, int32_t *col)
+{
+    uint32_t u[4];
+    philox_draw(seed, t, 0u, (uint32_t)slice, TAG_P2, u);
+    uint64_t x = ((uint64_t)u[0] * W) >> 32;
+    *col = orc_cdf_pick(n, cdf, x);
+    uint64_t y = ((uint64_t)u[1] * Wr) >> 32;
+    *row = orc_cdf_pick(m, rcdf, y);
+}
+
 /* draws t0 .. t0+count-1 of pass 2 without the observed-cell test (statistical pins) */
 void orc_pass2_draws(uint64_t seed, int32_t slice, uint32_t t0, int64_t count, const uint32_t *w, int32_t n, int32_t m,
                      int32_t *rows, int32_t *cols)
@@ -694,6 +710,27 @@ static void pass2(slice_ctx *c, orc_slice_result *res)
     orc_light_importance(n, no, ocol, oval, g, gcnt);
     /* pixel importance f(i) = 1; pdf(i,j) ∝ f(i) g(j) (Eq. 2) as integer weights (R14) */
     orc_pdf_weights(n, g, gcnt, w);
+    /* variant (reading R36): f(i) = max - min of row i's carried observations, row
+     * weights by the same rule, rows drawn from their CDF */
+    uint64_t *rcdf = NULL, Wr = 0;
+    if (in->row_importance) {
+        int32_t *orow = malloc((size_t)(no > 0 ? no : 1) * sizeof(int32_t));
+        int64_t kk = 0;
+        for (int32_t cc = 0; cc < n; ++cc)
+            for (int32_t i = 0; i < m; ++i)
+                if (obs[(size_t)i * (size_t)n + (size_t)cc]) orow[kk++] = i;
+        double *fr = calloc((size_t)(m > 0 ? m : 1), sizeof(double));
+        int32_t *fcnt = calloc((size_t)(m > 0 ? m : 1), sizeof(int32_t));
+        uint32_t *wr = malloc((size_t)(m > 0 ? m : 1) * sizeof(uint32_t));
+        orc_light_importance(m, no, orow, oval, fr, fcnt);
+        orc_pdf_weights(m, fr, fcnt, wr);
+        rcdf = malloc((size_t)(m > 0 ? m : 1) * sizeof(uint64_t));
+        for (int32_t i = 0; i < m; ++i) { Wr += wr[i]; rcdf[i] = Wr; }
+        free(orow);
+        free(fr);
+        free(fcnt);
+        free(wr);
+    }
     free(ocol);
     free(oval);
     free(gcnt);
@@ -706,7 +743,8 @@ static void pass2(slice_ctx *c, orc_slice_result *res)
     int64_t n_new = 0, t = 0;
     for (t = 0; t < 64 * N && n_obs < N; ++t) {
         int32_t i, cc;
-        orc_pass2_draw(in->seed, c->s, (uint32_t)t, W, cdf, n, m, &i, &cc);
+        if (rcdf) orc_pass2_draw_f(in->seed, c->s, (uint32_t)t, W, cdf, n, Wr, rcdf, m, &i, &cc);
+        else orc_pass2_draw(in->seed, c->s, (uint32_t)t, W, cdf, n, m, &i, &cc);
         size_t at = (size_t)i * (size_t)n + (size_t)cc;
         if (!obs[at]) {
             obs[at] = 1;
@@ -719,6 +757,7 @@ static void pass2(slice_ctx *c, orc_slice_result *res)
     }
     res->n_draws = t;
     res->n_new = n_new;
+    free(rcdf);
     /* forced sample for every still-empty column (R17) */
     int64_t n_forced = 0;
     for (int32_t cc = 0; cc < n; ++cc) {
@@ -1033,6 +1072,9 @@ static void resolve(const orc_inputs *in, orc_slice_result *res)
         w[2 * n + c] = lI != 0.0 ? (double)in->tib[f] / lI : 0.0;
     }
     if (res->flags & ORC_FLAG_ZERO) { free(w); return; }
+    int64_t *rowptr = calloc((size_t)m + 1, sizeof(int64_t));   /* CSR row pointers of Omega */
+    for (int64_t e = 0; e < res->nnz; ++e) rowptr[res->om_row[e] + 1]++;
+    for (int32_t i = 0; i < m; ++i) rowptr[i + 1] += rowptr[i];
     for (int32_t i = 0; i < m; ++i) {
         int32_t p = res->rows[i];
         double lr = lum_rho(in, p);
@@ -1048,10 +1090,21 @@ static void resolve(const orc_inputs *in, orc_slice_result *res)
                     for (int32_t c = 0; c < n; ++c) t += res->V[(size_t)a * n + c] * w[k * n + c];
                     s += res->U[(size_t)i * q + a] * t;
                 }
+                if (in->resolve_mode) {
+                    /* Z-mode (A24): the observed entries enter as themselves,
+                     * + sum_{j in Omega_i} (M~_ij - <U_i, V_j>) w^k_j (row i's samples in CSR order) */
+                    for (int64_t e = rowptr[i]; e < rowptr[i + 1]; ++e) {
+                        int32_t c = res->om_col[e];
+                        double uv = 0.0;
+                        for (int a = 0; a < q; ++a) uv += res->U[(size_t)i * q + a] * res->V[(size_t)a * n + c];
+                        s += (res->om_val[e] - uv) * w[k * n + c];
+                    }
+                }
             }
             res->rgb[(size_t)i * 3 + k] = tint[k] * s;
         }
     }
+    free(rowptr);
     free(w);
 }
 

@@ -46,6 +46,10 @@ typedef struct {
     int32_t q, solver, K;
     double tol, alpha, beta, gamma, lam;
     uint64_t order_seed; /* 0: FIFO candidate order; else a seeded shuffle (order-independence pin) */
+    /* SURVEY §8(f3) variants (0 = the paper's method) */
+    int32_t row_importance; /* 1: rows drawn by f(i) = max - min of their carried observations (R36) */
+    int32_t cost_mode;      /* 1: cost(L_f) = (eps + cost(L_b)) + cost(L_a) (Eq. (1) sensitivity) */
+    int32_t resolve_mode;   /* 1: Z-mode image (factored + the observed entries' residuals, A24) */
 } orc_inputs;
 
 enum { ORC_FLAG_DIRECT = 1, ORC_FLAG_DIVERGED = 2, ORC_FLAG_ZERO = 4 };
@@ -98,6 +102,8 @@ void orc_pdf_weights(int32_t n, const double *g, const int32_t *cnt, uint32_t *w
 int32_t orc_cdf_pick(int32_t n, const uint64_t *cdf, uint64_t x);
 void orc_pass2_draw(uint64_t seed, int32_t slice, uint32_t t, uint64_t W, const uint64_t *cdf, int32_t n, int32_t m,
                     int32_t *row, int32_t *col);
+void orc_pass2_draw_f(uint64_t seed, int32_t slice, uint32_t t, uint64_t W, const uint64_t *cdf, int32_t n, uint64_t Wr,
+                      const uint64_t *rcdf, int32_t m, int32_t *row, int32_t *col);
 void orc_pass2_draws(uint64_t seed, int32_t slice, uint32_t t0, int64_t count, const uint32_t *w, int32_t n, int32_t m,
                      int32_t *rows, int32_t *cols);
 /* Per-slice pipeline: coarsening, sampling, completion (App. A),

@@ -1092,6 +1092,12 @@ struct RArgs {
     const float4 *prow;
     float *image, *rows_rgb;
     float4 *tile4;   // optional packed (r, g, b, pixel index bits) per row of this rank (image gather)
+    // Z-mode (resolve_mode 1): the slice's Omega in CSR order
+    int32_t resolve_mode, mmax;
+    int64_t ncap;
+    const int32_t *rowptr;
+    const uint16_t *col;
+    const float *val;
 };
 
 __global__ void __launch_bounds__(256) k_resolve(RArgs A)
@@ -1141,6 +1147,26 @@ __global__ void __launch_bounds__(256) k_resolve(RArgs A)
                 d1 = fmaf(ua, t[q + a], d1);
                 d2 = fmaf(ua, t[2 * q + a], d2);
             }
+            if (A.resolve_mode) {
+                // Z-mode: + sum over row i's samples of (M~_ij - <U_i, V_j>) w^k_j (A24)
+                const int32_t *rp = A.rowptr + (int64_t)ls * (A.mmax + 1);
+                const int64_t ob = (int64_t)ls * A.ncap;
+                for (int e = rp[i]; e < rp[i + 1]; ++e) {
+                    const int j = A.col[ob + e];
+                    const float *vj = V + (int64_t)j * q;
+                    float uv = 0.f;
+                    for (int a = 0; a < q; ++a) uv = fmaf(u[a], vj[a], uv);
+                    const float r = A.val[ob + e] - uv;
+                    const int un = A.cut_cols[cb + j];
+                    const float i0 = A.I[3 * un], i1 = A.I[3 * un + 1], i2 = A.I[3 * un + 2];
+                    const float lj = (0.2126f * i0 + 0.7152f * i1) + 0.0722f * i2;
+                    if (lj != 0.f) {
+                        d0 = fmaf(r, i0 / lj, d0);
+                        d1 = fmaf(r, i1 / lj, d1);
+                        d2 = fmaf(r, i2 / lj, d2);
+                    }
+                }
+            }
             const float4 C = A.prow[4 * li + 2], D = A.prow[4 * li + 3];
             const float lr = (0.2126f * C.z + 0.7152f * C.w) + 0.0722f * D.x;
             const float ir = lr != 0.f ? 1.0f / lr : 0.f;
@@ -1188,6 +1214,12 @@ cudaError_t run_resolve(lmc_ctx *c, float *image, float *rows_rgb, float4 *tile4
     A.image = image;
     A.rows_rgb = rows_rgb;
     A.tile4 = tile4;
+    A.resolve_mode = c->cfg.resolve_mode;
+    A.mmax = c->mmax;
+    A.ncap = c->ncap;
+    A.rowptr = c->d.rowptr;
+    A.col = c->d.col;
+    A.val = c->d.val;
     k_resolve<<<c->SL, 256, 0, c->stream>>>(A);
     return cudaGetLastError();
 }

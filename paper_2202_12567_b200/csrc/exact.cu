@@ -840,7 +840,7 @@ __global__ void __launch_bounds__(CO_THREADS, CO_MINB) k_coarsen(
     const double *__restrict__ p1_Ta, const double *__restrict__ p1_Tb, const int32_t *__restrict__ p1_cnt,
     uint16_t *pool_rows, double *pool_Ta, double *pool_Tb, int32_t *pool_used, int64_t pool_cap, uint8_t *cs_flags,
     double *cs_eps, double *cs_cost, int32_t *cs_zoff, int32_t *cs_zlen, int32_t *cut_n, int32_t *cut_cols,
-    int32_t *src_off, int32_t *src_len, int32_t *src_side, int G, unsigned long long *counters)
+    int32_t *src_off, int32_t *src_len, int32_t *src_side, int G, unsigned long long *counters, int cost_mode)
 {
     extern __shared__ __align__(16) unsigned char smem[];
     const int U = up.U;
@@ -957,8 +957,10 @@ __global__ void __launch_bounds__(CO_THREADS, CO_MINB) k_coarsen(
                 evals += (lane == 0) ? 2ull * total : 0ull;
             }
             eps = warp_max_d(eps);
-            // Eq. (1): cost(L_f) = eps(L_f) + cost(L_b); merge iff below the bound
-            const double cf = eps + sh_cost[b];
+            // Eq. (1): cost(L_f) = eps(L_f) + cost(L_b); merge iff below the bound.
+            // cost_mode 1 (SURVEY f3 sensitivity): (eps + cost(L_b)) + cost(L_a)
+            double cf = eps + sh_cost[b];
+            if (cost_mode) cf = cf + sh_cost[a];
             if (lane == 0) {
                 sh_eps[f] = eps;
                 sh_cost[f] = cf;
@@ -1044,7 +1046,8 @@ cudaError_t run_coarsen(lmc_ctx *c)
         c->scene_slot, c->up, c->d.slice_off, c->s0, c->h_slice_off[c->s0], c->d.prow, c->d.vpl, c->cfg.seed, c->nmax,
         c->cfg.coarsen_tau, c->d.p1_rows, c->d.p1_Ta, c->d.p1_Tb, c->d.p1_cnt, c->d.pool_rows, c->d.pool_Ta,
         c->d.pool_Tb, c->d.pool_used, c->pool_cap, c->d.cs_flags, c->d.cs_eps, c->d.cs_cost, c->d.cs_zoff,
-        c->d.cs_zlen, c->d.cut_n, c->d.cut_cols, c->d.src_off, c->d.src_len, c->d.src_side, c->G, c->d.counters);
+        c->d.cs_zlen, c->d.cut_n, c->d.cut_cols, c->d.src_off, c->d.src_len, c->d.src_side, c->G, c->d.counters,
+        c->cfg.cost_mode);
     return cudaGetLastError();
 }
 
@@ -1085,7 +1088,19 @@ struct P2Args {
     uint32_t *newcells;
     int32_t *newpos;
     unsigned long long *counters;
+    int row_importance;            // rows drawn by f(i) = max - min of their carried entries
 };
+
+// smallest i with rcdf[i] > y (R29)
+__device__ __forceinline__ int row_pick(const unsigned long long *rcdf, int m, unsigned long long y)
+{
+    int lo = 0, hi = m - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (rcdf[mid] > y) hi = mid; else lo = mid + 1;
+    }
+    return lo;
+}
 
 __device__ __forceinline__ int csr_pos(const uint32_t *bm, const uint16_t *P, const int32_t *rp, int W, int i, int c)
 {
@@ -1112,6 +1127,10 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2(P2Args A)
     unsigned long long *cdf = (unsigned long long *)phase;              // G (also holds g as double)
     uint32_t *hkey = (uint32_t *)(cdf + A.G);                           // P2_HSLOTS
     uint32_t *hmin = hkey + P2_HSLOTS;                                  // P2_HSLOTS
+    // row importance (A.row_importance): per row max (bits, then the row CDF), min (bits), count
+    unsigned long long *rcdf = (unsigned long long *)(hmin + P2_HSLOTS);   // mmax
+    unsigned long long *rlo = rcdf + A.mmax;                            // mmax
+    int32_t *rcnt = (int32_t *)(rlo + A.mmax);                          // mmax
     __shared__ typename ScanI::TempStorage scani_tmp;
     __shared__ typename ScanU::TempStorage scanu_tmp;
     // phase B
@@ -1125,6 +1144,8 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2(P2Args A)
 
     for (int k = tid; k < m * W; k += P2_THREADS) bm[k] = 0u;
     for (int c = tid; c < n; c += P2_THREADS) colcnt[c] = 0;
+    if (A.row_importance)
+        for (int i = tid; i < m; i += P2_THREADS) { rcdf[i] = 0ull; rlo[i] = 0x7FF0000000000000ull; rcnt[i] = 0; }
     __syncthreads();
     // carried observations (R13) and light importance g(c) = max C_c - min C_c.
     // The carried entries of all columns form one flat list (prefix of the per-column counts), so
@@ -1162,6 +1183,11 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2(P2Args A)
             atomicMax(&chi[c], vb);
             atomicMin(&clo[c], vb);
             atomicOr(&bm[i * W + (c >> 5)], 1u << (c & 31));
+            if (A.row_importance) {
+                atomicMax(&rcdf[i], vb);
+                atomicMin(&rlo[i], vb);
+                atomicAdd(&rcnt[i], 1);
+            }
         }
         __syncthreads();
         if (tid < n) {
@@ -1223,6 +1249,56 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2(P2Args A)
     if (tid < n) cdf[tid] = incl;
     __syncthreads();
     const unsigned long long Wsum = n > 0 ? cdf[n - 1] : 0ull;
+    // row weights by the rule of the column weights (R14) on f(i) = max - min of row i's carried
+    // entries, and the row CDF (DESIGN R36); m <= 1024 = one row per thread
+    unsigned long long Wr = 0ull;
+    if (A.row_importance) {
+        double fi = -1.0;
+        if (tid < m && rcnt[tid] > 0)
+            fi = __longlong_as_double((long long)rcdf[tid]) - __longlong_as_double((long long)rlo[tid]);
+        double fm = warp_max_d(fmax(fi, 0.0));
+        if (lane == 0) sh_dred[w] = fm;
+        __syncthreads();
+        if (tid == 0) {
+            double v = 0.0;
+            for (int k = 0; k < 32; ++k) v = fmax(v, sh_dred[k]);
+            sh_dred[0] = v;
+        }
+        __syncthreads();
+        const double Fm = sh_dred[0];
+        const int robs = fi >= 0.0;
+        unsigned long long wr = 0ull;
+        if (tid < m) {
+            if (Fm > 0.0) {
+                if (robs) {
+                    double xx = floor(1048575.0 * (fi / Fm));
+                    uint32_t ww = 1u + (uint32_t)xx;
+                    wr = ww > 65536u ? ww : 65536u;
+                }
+            } else {
+                wr = 1ull;
+            }
+        }
+        unsigned long long sw = robs ? wr : 0ull;
+        for (int o = 16; o > 0; o >>= 1) sw += __shfl_xor_sync(FULL_MASK, sw, o);
+        int no = robs;
+        for (int o = 16; o > 0; o >>= 1) no += __shfl_xor_sync(FULL_MASK, no, o);
+        __syncthreads();
+        if (lane == 0) { sh_ured[w] = sw; sh_ired[w] = no; }
+        __syncthreads();
+        if (tid < m && Fm > 0.0 && !robs) {
+            unsigned long long s2 = 0ull;
+            int n2 = 0;
+            for (int k = 0; k < 32; ++k) { s2 += sh_ured[k]; n2 += sh_ired[k]; }
+            wr = n2 ? (unsigned long long)(uint32_t)(s2 / (unsigned long long)n2) : 524288ull;
+        }
+        unsigned long long rincl;
+        ScanU(scanu_tmp).InclusiveSum(wr, rincl);
+        __syncthreads();
+        if (tid < m) rcdf[tid] = rincl;
+        __syncthreads();
+        Wr = m > 0 ? rcdf[m - 1] : 0ull;
+    }
     const int64_t N = (int64_t)ceil(((double)((int64_t)m * (int64_t)n)) * A.rate);
     const int64_t cap = 64 * N;
     if (tid == 0) { sh_count = sh_obs; sh_nnew = 0; sh_draws = 0; sh_bacc = 0; }
@@ -1252,7 +1328,8 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2(P2Args A)
                         if (cdf[mid] > x) hi = mid; else lo = mid + 1;
                     }
                     cc = lo;
-                    const int i = (int)randint_u(uu.y, (uint32_t)m);
+                    const int i = A.row_importance ? row_pick(rcdf, m, ((unsigned long long)uu.y * Wr) >> 32)
+                                                   : (int)randint_u(uu.y, (uint32_t)m);
                     cell = (i << 11) | cc;
                     const uint32_t bit = 1u << (cc & 31);
                     isnew = !(atomicOr(&bm[i * W + (cc >> 5)], bit) & bit);
@@ -1285,7 +1362,7 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2(P2Args A)
                 if (cdf[mid] > x) hi = mid; else lo = mid + 1;
             }
             cc = lo;
-            int i = (int)randint_u(u.y, (uint32_t)m);
+            int i = A.row_importance ? row_pick(rcdf, m, ((unsigned long long)u.y * Wr) >> 32) : (int)randint_u(u.y, (uint32_t)m);
             cell = (i << 11) | cc;   // i < 1024, cc < 2048
             if (!(bm[i * W + (cc >> 5)] & (1u << (cc & 31)))) key = (uint32_t)cell;
         }
@@ -1511,7 +1588,7 @@ __global__ void __launch_bounds__(EV_WARPS * 32, EV_MINB) k_eval_new(int slot, U
 
 static size_t pass2_smem(int mmax, int G)
 {
-    size_t phaseA = (size_t)G * 8 + (size_t)P2_HSLOTS * 4 * 2;
+    size_t phaseA = (size_t)G * 8 + (size_t)P2_HSLOTS * 4 * 2 + (size_t)mmax * 20;   // + row importance
     size_t phaseB = ((((size_t)mmax * 33 + 7) & ~(size_t)7) * 2) + ((size_t)mmax + 1) * 4;
     size_t base = (size_t)mmax * 32 * 4 + (size_t)G * 4;
     return base + (phaseA > phaseB ? phaseA : phaseB) + 64;
@@ -1554,6 +1631,7 @@ cudaError_t run_pass2(lmc_ctx *c)
     A.newcells = c->d.newcells;
     A.newpos = c->d.newpos;
     A.counters = c->d.counters;
+    A.row_importance = c->cfg.row_importance;
     size_t sm = pass2_smem(c->mmax, c->G);
     cudaError_t e = cudaFuncSetAttribute(k_pass2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;

@@ -50,7 +50,8 @@ class Config(C.Structure):
                 ("rank_q", C.c_int32), ("solver", C.c_int32), ("max_iter", C.c_int32), ("tol", C.c_double),
                 ("alpha", C.c_double), ("beta", C.c_double), ("gamma", C.c_double), ("lambda_", C.c_double),
                 ("rank", C.c_int32), ("world", C.c_int32), ("input_memory", C.c_int32), ("stream", _P),
-                ("nccl_id", C.c_uint8 * 128)]
+                ("nccl_id", C.c_uint8 * 128), ("row_importance", C.c_int32), ("cost_mode", C.c_int32),
+                ("resolve_mode", C.c_int32)]
 
 
 class Stats(C.Structure):
@@ -176,6 +177,9 @@ class Frame:
                           _P(stream.cuda_stream))
         if nccl_id is not None:
             self.cfg.nccl_id = (C.c_uint8 * 128)(*bytes(nccl_id))
+        self.cfg.row_importance = int(prm.get("row_importance", 0))
+        self.cfg.cost_mode = int(prm.get("cost_mode", 0))
+        self.cfg.resolve_mode = int(prm.get("resolve_mode", 0))
         h = _P()
         st = lib.lmc_create(C.byref(self.gb), C.byref(self.vp), C.byref(self.tr), C.byref(self.sc),
                             C.byref(self.cfg), C.byref(h))

@@ -55,6 +55,11 @@ class Config:
     p1_nmax: int = 32
     p1_nmin: int = 4
     fixture_seed: int = 1
+    # SURVEY §8(f3) variants (0 = the paper's method): rows drawn by image-space importance f(i)
+    # (R36), Eq. (1) sensitivity cost(L_f) = eps + cost(L_b) + cost(L_a), Z-mode image (A24)
+    row_importance: int = 0
+    cost_mode: int = 0
+    resolve_mode: int = 0
 
 
 PRESETS = {
@@ -334,7 +339,8 @@ class Inputs:
         return dict(slice_target=c.slice_target, normal_weight=c.normal_weight, seed=c.seed,
                     p1_nmax=c.p1_nmax, p1_nmin=c.p1_nmin, tau=self.tau, rate=c.rate, rank_q=c.rank_q,
                     solver=c.solver, max_iter=c.max_iter, tol=c.tol, alpha=c.alpha, beta=c.beta,
-                    gamma=c.gamma, lam=c.lam)
+                    gamma=c.gamma, lam=c.lam, row_importance=c.row_importance, cost_mode=c.cost_mode,
+                    resolve_mode=c.resolve_mode)
 
 
 def _gbuffer(sc: Scene, W: int, H: int):

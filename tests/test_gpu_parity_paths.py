@@ -260,3 +260,21 @@ def test_host_image_leaves_background_untouched():
     bg = np.setdiff1d(np.arange(x.height * x.width), pix)
     assert bg.size > 0 and np.all(h[bg] == 7.0)
     fr.close()
+
+
+# ------------------------------------------------------------------------------ SURVEY f3 variants
+
+@pytest.mark.parametrize("name,over", [("t_interior", dict(row_importance=1)), ("c1", dict(row_importance=1)),
+                                       ("t_interior", dict(cost_mode=1)), ("c1", dict(cost_mode=1, tau=3e-4)),
+                                       ("t_interior", dict(resolve_mode=1)), ("t_cornell", dict(resolve_mode=1, rate=1.0)),
+                                       ("t_interior", dict(resolve_mode=1, solver=1)),
+                                       ("t_interior", dict(row_importance=1, cost_mode=1, resolve_mode=1, rank_q=16))])
+def test_sampling_and_resolve_variants(name, over):
+    """image-space row importance f(i) (R36), Eq. (1) sensitivity, Z-mode image (A24): Omega, cuts
+    bit-exact, completion and pixels within the bars, against the oracle's same variant"""
+    x = scenegen.make_inputs(scenegen.preset(name, **over))
+    fr, img = run_frame(x)
+    off, _ = fr.slices()
+    for r in oracle.Oracle(x).run_slices(list(range(off.size - 1)), stage=4):
+        check_slice(x, fr, img, r)
+    fr.close()
