@@ -117,6 +117,10 @@ typedef struct {
      *   cost_mode 1:      Eq. (1) sensitivity, cost(L_f) = (eps(L_f) + cost(L_b)) + cost(L_a)
      *   resolve_mode 1:   Z-mode image, tint (<U_i, V w^k> + sum_{j in Omega_i} (M~_ij - <U_i, V_j>) w^k_j) */
     int32_t row_importance, cost_mode, resolve_mode;
+    /* SURVEY §8(f4) temporal coherence: warm_start 1 starts the ADM of every slice whose rows and
+     * cut equal the previous frame's (and whose previous result was regular) from the previous
+     * frame's factors (U, V / sigma; multipliers 0) for warm_iters iterations (0: max_iter) */
+    int32_t warm_start, warm_iters;
 } lmc_config;
 
 typedef struct {
@@ -134,6 +138,7 @@ typedef struct {
     float ms_solver;           /* last frame, if timed: the completion kernel alone (ADM or MALS) */
     int64_t layout_row_slots, layout_col_slots; /* q <= 16 ADM: padded sample slots of the row / column layouts */
     float ms_eval2;            /* last frame, if timed: the pass-2 entry-evaluation kernel alone */
+    int64_t n_warm;            /* slices of the last frame whose completion started warm (warm_start) */
 } lmc_stats;
 
 typedef struct lmc_ctx lmc_ctx;

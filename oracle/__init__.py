@@ -55,7 +55,13 @@ class _Inputs(C.Structure):
         ("tol", C.c_double), ("alpha", C.c_double), ("beta", C.c_double), ("gamma", C.c_double), ("lam", C.c_double),
         ("order_seed", C.c_uint64),
         ("row_importance", C.c_int32), ("cost_mode", C.c_int32), ("resolve_mode", C.c_int32),
+        ("warm_iters", C.c_int32), ("nwarm", C.c_int32), ("warm", C.c_void_p),
     ]
+
+
+class _Warm(C.Structure):
+    _fields_ = [("slice", C.c_int32), ("m", C.c_int32), ("n", C.c_int32), ("flags", C.c_int32),
+                ("rows", C.c_void_p), ("cut", C.c_void_p), ("U", C.c_void_p), ("V", C.c_void_p)]
 
 
 class _Result(C.Structure):
@@ -79,6 +85,7 @@ class _Result(C.Structure):
         ("obj", C.POINTER(C.c_double)), ("n_obj", C.c_int32),
         ("full", C.POINTER(C.c_double)),
         ("rgb", C.POINTER(C.c_double)),
+        ("warm", C.c_int32),
     ]
 
 
@@ -107,6 +114,9 @@ def lib():
             L.orc_adm.argtypes = [C.c_int32, C.c_int32, C.c_int64, P, P, P, C.c_int32, C.c_int32, C.c_double,
                                   C.c_double, C.c_double, C.c_double, C.c_uint64, C.c_int32, P, P, P, P, P]
             L.orc_adm.restype = C.c_int32
+            L.orc_adm_warm.argtypes = [C.c_int32, C.c_int32, C.c_int64, P, P, P, C.c_int32, C.c_int32, C.c_double,
+                                       C.c_double, C.c_double, C.c_double, P, P, P, P, P, P, P]
+            L.orc_adm_warm.restype = C.c_int32
             L.orc_mals.argtypes = [C.c_int32, C.c_int32, C.c_int64, P, P, P, C.c_int32, C.c_int32, C.c_double,
                                    C.c_uint64, C.c_int32, P, P, P, P]
             L.orc_mals.restype = C.c_int32
@@ -179,6 +189,9 @@ class Oracle:
         s.row_importance = prm.get("row_importance", 0)
         s.cost_mode = prm.get("cost_mode", 0)
         s.resolve_mode = prm.get("resolve_mode", 0)
+        s.warm_iters = prm.get("warm_iters", 0)
+        s.nwarm = 0
+        s.warm = None
         self._keep = keep
         self.s = s
         self._slices = None
@@ -215,6 +228,19 @@ class Oracle:
             n = int(ns[0])
             self._slices = (off[: n + 1].copy(), rows[:m].copy())
         return self._slices
+
+    def set_warm(self, prev_results):
+        """warm start from the results of the previous frame (dicts of run_slices, stage >= 3)"""
+        keep = []
+        arr = (_Warm * max(len(prev_results), 1))()
+        for k, r in enumerate(prev_results):
+            cols = [np.ascontiguousarray(r["rows"], np.int32), np.ascontiguousarray(r["cut_nodes"], np.int32),
+                    np.ascontiguousarray(r["U"], np.float64), np.ascontiguousarray(r["V"], np.float64)]
+            keep += cols
+            arr[k] = _Warm(r["slice"], r["m"], r["n"], r["flags"], *[_p(a).value for a in cols])
+        self._warm_keep = (keep, arr)
+        self.s.nwarm = len(prev_results)
+        self.s.warm = C.cast(arr, C.c_void_p)
 
     def run_slices(self, slice_ids, stage: int = 4):
         off, rows = self.slices()
@@ -278,7 +304,7 @@ def _convert(r: _Result, stage: int) -> dict:
                  om_val=_arr(r.om_val, k, np.float64), om_carried=_arr(r.om_carried, k, np.int32),
                  weights=_arr(r.weights, n, np.uint32))
     if stage >= 3:
-        d.update(q=q, iters=r.iters, flags=r.flags, sigma=r.sigma, resid=r.resid,
+        d.update(q=q, iters=r.iters, flags=r.flags, sigma=r.sigma, resid=r.resid, warm=r.warm,
                  U=_arr(r.U, m * q, np.float64).reshape(m, q), V=_arr(r.V, q * n, np.float64).reshape(q, n),
                  obj=_arr(r.obj, r.n_obj, np.float64),
                  full=_arr(r.full, m * n, np.float64).reshape(m, n) if r.full else None)
@@ -368,3 +394,19 @@ def pass2_draw_f(t, w, wr, seed=12567, slice_id=0):
     lib().orc_pass2_draw_f(seed, slice_id, t, int(cdf[-1]), _p(cdf), cdf.size, int(rcdf[-1]), _p(rcdf), rcdf.size,
                            _p(r), _p(c))
     return int(r[0]), int(c[0])
+
+
+def adm_warm(m, n, row, col, val, q, X0, Y0, K=100, tol=0.0, alpha=1.0, beta=1.0, gamma=1.6):
+    row = np.ascontiguousarray(row, np.int32)
+    col = np.ascontiguousarray(col, np.int32)
+    val = np.ascontiguousarray(val, np.float64)
+    X0 = np.ascontiguousarray(X0, np.float64)
+    Y0 = np.ascontiguousarray(Y0, np.float64)
+    U = np.zeros((m, q))
+    V = np.zeros((q, n))
+    it = np.zeros(1, np.int32)
+    res = np.zeros(1)
+    sg = np.zeros(1)
+    flags = lib().orc_adm_warm(m, n, row.size, _p(row), _p(col), _p(val), q, K, tol, alpha, beta, gamma, _p(X0), _p(Y0),
+                               _p(U), _p(V), _p(it), _p(res), _p(sg))
+    return dict(U=U, V=V, iters=int(it[0]), resid=float(res[0]), sigma=float(sg[0]), flags=flags)

@@ -863,9 +863,32 @@ static void init_factors(int32_t m, int32_t n, int32_t q, double c0, uint64_t se
  * ADM nonnegative factorisation (Appendix A; typo readings R18).
  * Literal: Z is kept dense (m x n), every product is formed as written.
  * ---------------------------------------------------------------------------------------- */
+/* ADM of App. A with the initial factors X_0 = Xw, Y_0 = Yw when given (warm start, SURVEY f4:
+ * the previous frame's factors of the same slice), else the Philox initialisation (R20) */
+static int32_t adm_core(int32_t m, int32_t n, int64_t nnz, const int32_t *row, const int32_t *col, const double *val,
+                        int32_t q, int32_t K, double tol, double alpha, double beta, double gamma, uint64_t seed,
+                        int32_t slice, const double *Xw, const double *Yw, double *U, double *V, int32_t *iters,
+                        double *resid, double *sigma);
+
+int32_t orc_adm_warm(int32_t m, int32_t n, int64_t nnz, const int32_t *row, const int32_t *col, const double *val,
+                     int32_t q, int32_t K, double tol, double alpha, double beta, double gamma, const double *X0,
+                     const double *Y0, double *U, double *V, int32_t *iters, double *resid, double *sigma)
+{
+    return adm_core(m, n, nnz, row, col, val, q, K, tol, alpha, beta, gamma, 0, 0, X0, Y0, U, V, iters, resid, sigma);
+}
+
 int32_t orc_adm(int32_t m, int32_t n, int64_t nnz, const int32_t *row, const int32_t *col, const double *val,
                 int32_t q, int32_t K, double tol, double alpha, double beta, double gamma, uint64_t seed,
                 int32_t slice, double *U, double *V, int32_t *iters, double *resid, double *sigma)
+{
+    return adm_core(m, n, nnz, row, col, val, q, K, tol, alpha, beta, gamma, seed, slice, NULL, NULL, U, V, iters, resid,
+                    sigma);
+}
+
+static int32_t adm_core(int32_t m, int32_t n, int64_t nnz, const int32_t *row, const int32_t *col, const double *val,
+                        int32_t q, int32_t K, double tol, double alpha, double beta, double gamma, uint64_t seed,
+                        int32_t slice, const double *Xw, const double *Yw, double *U, double *V, int32_t *iters,
+                        double *resid, double *sigma)
 {
     size_t mq = (size_t)m * q, qn = (size_t)q * n, mn = (size_t)m * n;
     double sg = max_omega(nnz, val); /* R23 */
@@ -888,7 +911,13 @@ int32_t orc_adm(int32_t m, int32_t n, int64_t nnz, const int32_t *row, const int
     double *Z = calloc(mn, sizeof(double)), *W = malloc(mn * sizeof(double));
     double *A = malloc((size_t)q * q * sizeof(double));
     double *rhs = malloc((size_t)(q > 0 ? q : 1) * sizeof(double));
-    init_factors(m, n, q, c0, seed, slice, X, Y);
+    if (Xw && Yw) {
+        /* warm start: the previous frame's U and V (already divided by this frame's sigma) */
+        memcpy(X, Xw, mq * sizeof(double));
+        memcpy(Y, Yw, qn * sizeof(double));
+    } else {
+        init_factors(m, n, q, c0, seed, slice, X, Y);
+    }
     memcpy(U, X, mq * sizeof(double));
     memcpy(V, Y, qn * sizeof(double));
     for (int64_t k = 0; k < nnz; ++k) Z[(size_t)row[k] * n + col[k]] = Mh[k]; /* Z_0 = P_Omega(M) */
@@ -1156,9 +1185,30 @@ static orc_slice_result *run_slice(const orc_inputs *in, const int32_t *parent, 
         if (m <= q || n <= q) { /* R25: rank not below the slice dimensions -> direct */
             res->flags = ORC_FLAG_DIRECT;
         } else if (in->solver == 0) {
-            res->flags = orc_adm(m, n, res->nnz, res->om_row, res->om_col, res->om_val, q, in->K, in->tol,
-                                 in->alpha, in->beta, in->gamma, in->seed, s, res->U, res->V, &res->iters,
-                                 &res->resid, &res->sigma);
+            /* warm start: the same slice of the previous frame with the same rows, the same
+             * cut and a regular ADM result starts from that result's factors, for warm_iters iterations */
+            const orc_warm *wp = NULL;
+            for (int32_t k = 0; k < in->nwarm && !wp; ++k) {
+                const orc_warm *e = &in->warm[k];
+                if (e->slice == s && e->m == m && e->n == n && e->flags == 0 &&
+                    !memcmp(e->rows, rows, (size_t)m * sizeof(int32_t)) &&
+                    !memcmp(e->cut, res->cut_nodes, (size_t)n * sizeof(int32_t)))
+                    wp = e;
+            }
+            if (wp) {
+                double sg = max_omega(res->nnz, res->om_val);
+                double *Yw = malloc((size_t)q * n * sizeof(double) + 8);
+                for (size_t k = 0; k < (size_t)q * n; ++k) Yw[k] = sg > 0.0 ? wp->V[k] / sg : 0.0;
+                res->flags = adm_core(m, n, res->nnz, res->om_row, res->om_col, res->om_val, q,
+                                      in->warm_iters > 0 ? in->warm_iters : in->K, in->tol, in->alpha, in->beta, in->gamma,
+                                      in->seed, s, wp->U, Yw, res->U, res->V, &res->iters, &res->resid, &res->sigma);
+                res->warm = 1;
+                free(Yw);
+            } else {
+                res->flags = orc_adm(m, n, res->nnz, res->om_row, res->om_col, res->om_val, q, in->K, in->tol,
+                                     in->alpha, in->beta, in->gamma, in->seed, s, res->U, res->V, &res->iters,
+                                     &res->resid, &res->sigma);
+            }
         } else {
             res->obj = malloc((size_t)2 * (size_t)(in->K > 0 ? in->K : 1) * sizeof(double));
             res->n_obj = 2 * in->K;

@@ -19,6 +19,14 @@
 extern "C" {
 #endif
 
+/* one slice of the previous frame (warm start) */
+typedef struct {
+    int32_t slice, m, n, flags;
+    const int32_t *rows;          /* m G-buffer rows */
+    const int32_t *cut;           /* n cut nodes */
+    const double *U, *V;          /* m*q, q*n (V times that frame's sigma) */
+} orc_warm;
+
 typedef struct {
     /* G-buffer rows (valid pixels), float32 promoted exactly to double */
     int64_t m;
@@ -50,6 +58,10 @@ typedef struct {
     int32_t row_importance; /* 1: rows drawn by f(i) = max - min of their carried observations (R36) */
     int32_t cost_mode;      /* 1: cost(L_f) = (eps + cost(L_b)) + cost(L_a) (Eq. (1) sensitivity) */
     int32_t resolve_mode;   /* 1: Z-mode image (factored + the observed entries' residuals, A24) */
+    /* warm start: ADM slices found in warm[] (same slice, rows and cut, regular
+     * result) start from those factors and run warm_iters iterations (0: K) */
+    int32_t warm_iters, nwarm;
+    const orc_warm *warm;
 } orc_inputs;
 
 enum { ORC_FLAG_DIRECT = 1, ORC_FLAG_DIVERGED = 2, ORC_FLAG_ZERO = 4 };
@@ -80,6 +92,7 @@ typedef struct {
     double *full;                 /* m*n full M~ for direct slices, else NULL */
     /* resolve */
     double *rgb;                  /* m*3 */
+    int32_t warm;                 /* 1: the completion started from the previous frame's factors */
 } orc_slice_result;
 
 /* P:? — Philox4x32-10 (Salmon et al. SC'11), R-readings O3 */
@@ -116,6 +129,10 @@ void orc_free_result(orc_slice_result *r);
 int32_t orc_adm(int32_t m, int32_t n, int64_t nnz, const int32_t *row, const int32_t *col, const double *val,
                 int32_t q, int32_t K, double tol, double alpha, double beta, double gamma, uint64_t seed,
                 int32_t slice, double *U, double *V, int32_t *iters, double *resid, double *sigma);
+/* ADM started from given factors X0 (m*q), Y0 (q*n, in units of val / sigma) -- warm start */
+int32_t orc_adm_warm(int32_t m, int32_t n, int64_t nnz, const int32_t *row, const int32_t *col, const double *val,
+                     int32_t q, int32_t K, double tol, double alpha, double beta, double gamma, const double *X0,
+                     const double *Y0, double *U, double *V, int32_t *iters, double *resid, double *sigma);
 /* Masked ALS (BASELINE north_star) on an explicit sample set. obj: 2K objective values (may be NULL). */
 int32_t orc_mals(int32_t m, int32_t n, int64_t nnz, const int32_t *row, const int32_t *col, const double *val,
                  int32_t q, int32_t K, double lam, uint64_t seed, int32_t slice, double *X, double *Y,

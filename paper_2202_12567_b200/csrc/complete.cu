@@ -333,6 +333,8 @@ struct CArgs {
     const int32_t *order;       // CTA -> slice, or null for CTA = slice
     unsigned long long *prof;   // optional phase clocks (LMC_ADM_PROF=1), else null
     int32_t force_nf;           // test hook (LMC_TEST_NONFINITE_SLICE): this slice's residual is made NaN
+    const int32_t *warm_ok;     // warm start: per slice, start from the previous U, V / sigma
+    int32_t warm_iters;
 };
 
 // Per-rank kernel shape.  q <= 16: 32 warps, a 2 KB ring per warp, 128-entry column chunks.
@@ -699,16 +701,18 @@ __global__ void __launch_bounds__(Cfg<Q>::NT, 1) k_adm(CArgs A)
     const float nrmM2 = nm.w;
     // R20: X_0, Y_0 Philox-uniform with E[X_0 Y_0] = mean_Omega M^
     const float c0 = 2.0f * sqrtf((nm.z / (float)A.nnz[ls]) / (float)Q);
+    const bool warm = A.warm_ok && A.warm_ok[ls];   // the previous frame's U and V / sigma
+    const int Keff = warm && A.warm_iters > 0 ? A.warm_iters : A.K;
     for (int e = tid; e < m * Q; e += NT) {
         const int i = e / Q, l = e % Q;
-        const float x = c0 * unif_f(philox4((uint32_t)i, (uint32_t)l, (uint32_t)s, TAG_X0, A.seed).x);
+        const float x = warm ? Ug[e] : c0 * unif_f(philox4((uint32_t)i, (uint32_t)l, (uint32_t)s, TAG_X0, A.seed).x);
         X[e] = x;
         Ug[e] = x;
         Lg[e] = 0.f;
     }
     for (int e = tid; e < n * Q; e += NT) {
         const int j = e / Q, l = e % Q;
-        const float y = c0 * unif_f(philox4((uint32_t)l, (uint32_t)j, (uint32_t)s, TAG_Y0, A.seed).x);
+        const float y = warm ? Vg[e] * nm.y : c0 * unif_f(philox4((uint32_t)l, (uint32_t)j, (uint32_t)s, TAG_Y0, A.seed).x);
         Y[e] = y;
         Vg[e] = y;
         Pg[e] = 0.f;
@@ -730,7 +734,7 @@ __global__ void __launch_bounds__(Cfg<Q>::NT, 1) k_adm(CArgs A)
     const int nsolo = A.c_nsolo[ls];
     const int ngr = (m + R - 1) / R, ngc = nsolo + (n - nsolo + R - 1) / R;
     int it = 0;
-    for (; it < A.K; ++it) {
+    for (; it < Keff; ++it) {
         const float fd = (it == 0) ? 0.f : 1.f;   // Z_0 = P_Omega(M^): no X_0 Y_0 part in step 0
         // ---- row phase: s_ij = M^_ij - x_i.y_j on Omega_i, r_i = sum_j s_ij y_j, X/U/Lambda update
         for (int g = next_group(&sh_ctr[0], lane); g < ngr; g = next_group(&sh_ctr[0], lane)) {
@@ -1051,6 +1055,8 @@ cudaError_t run_adm(lmc_ctx *c, int nmax)
     A.order = c->adm_ordered ? c->d.adm_order : nullptr;
     const char *fe = getenv("LMC_TEST_NONFINITE_SLICE");
     A.force_nf = fe ? atoi(fe) : -1;
+    A.warm_ok = c->cfg.warm_start ? c->d.warm_ok : nullptr;
+    A.warm_iters = c->cfg.warm_iters;
     // LMC_ADM_PROF=1: per-phase clock64 totals (diagnostic only; synchronises and prints to stderr)
     const char *pe = getenv("LMC_ADM_PROF");
     const bool prof = pe && pe[0] == '1' && c->q == 16;   // instrumented build for q = 16 only
@@ -1340,4 +1346,62 @@ cudaError_t run_launch_order(lmc_ctx *c, int ntail)
     return cudaGetLastError();
 }
 
+}  // namespace lmc
+
+namespace lmc {
+// ------------------------------------------------------------------------------------------
+// Warm start: a slice starts from the previous frame's factors iff its rows and its
+// cut equal the previous frame's and the previous result was a regular completion (flags 0)
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_warm_check(const int32_t *__restrict__ slice_off, int32_t s0, int64_t lbase,
+                                                    int64_t row0, const int32_t *__restrict__ rows,
+                                                    const int32_t *__restrict__ cut_n, const int32_t *__restrict__ cut_cols,
+                                                    const int32_t *__restrict__ prev_rows, const int32_t *__restrict__ prev_n,
+                                                    const int32_t *__restrict__ prev_cut, const int32_t *__restrict__ prev_flags,
+                                                    int G, int have_prev, int32_t *warm_ok)
+{
+    const int ls = blockIdx.x, s = s0 + ls;
+    const int64_t lr0 = slice_off[s] - lbase;
+    const int m = slice_off[s + 1] - slice_off[s], n = cut_n[ls];
+    int same = have_prev && prev_flags[ls] == 0 && prev_n[ls] == n;
+    if (same) {
+        for (int k = threadIdx.x; k < m; k += blockDim.x)
+            if (rows[row0 + lr0 + k] != prev_rows[lr0 + k]) same = 0;
+        for (int k = threadIdx.x; k < n; k += blockDim.x)
+            if (cut_cols[(int64_t)ls * G + k] != prev_cut[(int64_t)ls * G + k]) same = 0;
+    }
+    same = __syncthreads_and(same);
+    if (threadIdx.x == 0) warm_ok[ls] = same;
+}
+
+__global__ void k_warm_save(int SL, int G, int64_t ML, int64_t row0, const int32_t *__restrict__ rows,
+                            const int32_t *__restrict__ cut_n, const int32_t *__restrict__ cut_cols,
+                            const int32_t *__restrict__ flags, int32_t *prev_rows, int32_t *prev_n, int32_t *prev_cut,
+                            int32_t *prev_flags)
+{
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < ML) prev_rows[k] = rows[row0 + k];
+    if (k < (int64_t)SL * G) prev_cut[k] = cut_cols[k];
+    if (k < SL) { prev_n[k] = cut_n[k]; prev_flags[k] = flags[k]; }
+}
+
+cudaError_t run_warm_check(lmc_ctx *c)
+{
+    if (c->SL == 0) return cudaSuccess;
+    k_warm_check<<<c->SL, 256, 0, c->stream>>>(c->d.slice_off, c->s0, c->h_slice_off[c->s0], c->row0, c->d.rows, c->d.cut_n,
+                                               c->d.cut_cols, c->d.prev_rows, c->d.prev_n, c->d.prev_cut, c->d.prev_flags,
+                                               c->G, c->have_prev ? 1 : 0, c->d.warm_ok);
+    return cudaGetLastError();
+}
+
+cudaError_t run_warm_save(lmc_ctx *c)
+{
+    if (c->SL == 0) return cudaSuccess;
+    const int64_t n = std::max<int64_t>(std::max<int64_t>(c->ML, (int64_t)c->SL * c->G), c->SL);
+    k_warm_save<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(c->SL, c->G, c->ML, c->row0, c->d.rows, c->d.cut_n,
+                                                                   c->d.cut_cols, c->d.flags, c->d.prev_rows, c->d.prev_n,
+                                                                   c->d.prev_cut, c->d.prev_flags);
+    c->have_prev = true;
+    return cudaGetLastError();
+}
 }  // namespace lmc

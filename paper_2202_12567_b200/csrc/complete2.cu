@@ -310,6 +310,8 @@ struct C2Args {
     const int32_t *order;
     unsigned long long *prof;   // optional phase clocks (LMC_ADM_PROF=1)
     int32_t force_nf;           // test hook (LMC_TEST_NONFINITE_SLICE): this slice's residual is made NaN
+    const int32_t *warm_ok;     // warm start: per slice, start from the previous U, V / sigma
+    int32_t warm_iters;
     int32_t dbg;                // diagnostic timing switches (LMC_ADM2_DBG, wrong results): 1 no Grams after it 1, 2 no epilogue matvecs, 4 no S stores
 };
 
@@ -698,14 +700,18 @@ __global__ void __launch_bounds__(K2<Q>::NT, 1) k_adm2(C2Args A)
     // R20: X_0, Y_0 Philox-uniform with E[X_0 Y_0] = mean_Omega M^ (every copy of a row slot)
     const float c0 = 2.0f * sqrtf((nm.z / (float)A.nnz[ls]) / (float)Q);
     constexpr int CP = 16 / Q;   // copies per row slot
+    const bool warm = A.warm_ok && A.warm_ok[ls];   // the previous frame's U and V / sigma
+    const int Keff = warm && A.warm_iters > 0 ? A.warm_iters : A.K;
     for (int e = tid; e < (m + 2) * 16; e += NT) {
         const int i = e >> 4, ph = e & 15, l = ph % Q;   // physical float ph of slot i holds element l
-        const float x = i < m ? c0 * unif_f(philox4((uint32_t)i, (uint32_t)l, (uint32_t)s, TAG_X0, A.seed).x) : 0.f;
+        const float x = i >= m ? 0.f : warm ? Ug[i * Q + l]
+                                            : c0 * unif_f(philox4((uint32_t)i, (uint32_t)l, (uint32_t)s, TAG_X0, A.seed).x);
         reinterpret_cast<float *>(Xb + i * RB)[ph] = x;
     }
     for (int e = tid; e < (n + 2) * 16; e += NT) {
         const int j = e >> 4, ph = e & 15, l = ph % Q;
-        const float y = j < n ? c0 * unif_f(philox4((uint32_t)l, (uint32_t)j, (uint32_t)s, TAG_Y0, A.seed).x) : 0.f;
+        const float y = j >= n ? 0.f : warm ? Vg[j * Q + l] * nm.y
+                                            : c0 * unif_f(philox4((uint32_t)l, (uint32_t)j, (uint32_t)s, TAG_Y0, A.seed).x);
         reinterpret_cast<float *>(Yb + j * RB)[ph] = y;
     }
     (void)CP;
@@ -738,7 +744,7 @@ __global__ void __launch_bounds__(K2<Q>::NT, 1) k_adm2(C2Args A)
     const float nrmM2 = nm.w;
     if (PROF) { PCLK(pt1); pacc[0] += pt1 - pt0; pt0 = pt1; }
     int it = 0;
-    for (; it < A.K; ++it) {
+    for (; it < Keff; ++it) {
         const float fd = (it == 0) ? 0.f : 1.f;   // Z_0 = P_Omega(M^): no X_0 Y_0 part in step 0
         // ---- row phase: s_ij = M^_ij - x_i.y_j, r_i = sum_j s_ij y_j, X / U / Lambda update
         // B = (Y Y^T + aI)^{-1} of the previous iteration is produced by warp 0 while the other warps
@@ -918,7 +924,7 @@ __global__ void __launch_bounds__(K2<Q>::NT, 1) k_adm2(C2Args A)
             if (!(ss == ss) || isinf(ss) || sqrtf(ss / nrmM2) < A.tol) { ++it; break; }
         }
         // ---- (Y Y^T + aI)^{-1} for the next row phase: Gram warps + warp 0, barriers 3, 4 ------
-        if (it + 1 < A.K) {
+        if (it + 1 < Keff) {
             const bool skipy = (A.dbg & 1) && it > 1;
             if (!skipy) gram_all<Q>(Yb, nullptr, n, part, false);
             __syncthreads();
@@ -1081,6 +1087,8 @@ cudaError_t run_adm2(lmc_ctx *c)
     A.dbg = dbe ? atoi(dbe) : 0;
     const char *fe = getenv("LMC_TEST_NONFINITE_SLICE");
     A.force_nf = fe ? atoi(fe) : -1;
+    A.warm_ok = c->cfg.warm_start ? c->d.warm_ok : nullptr;
+    A.warm_iters = c->cfg.warm_iters;
     if (prof) {
         if (cudaMalloc(&A.prof, 8 * sizeof(unsigned long long)) != cudaSuccess) return cudaErrorMemoryAllocation;
         cudaMemsetAsync(A.prof, 0, 8 * sizeof(unsigned long long), c->stream);

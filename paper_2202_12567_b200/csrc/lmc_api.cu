@@ -94,7 +94,7 @@ void free_all(lmc_ctx *c)
                     d.newcells, d.newpos, d.U, d.V, d.Lam, d.Pi, d.Xold, d.S, d.flags, d.iters, d.resid,
                     d.direct_rgb, d.counters, d.img, d.rows_rgb, d.vpl_soa, d.r_perm, d.r_len, d.c_perm, d.c_len,
                     d.r_goff, d.c_goff, d.c_nsolo, d.adm_order, d.r_ent, d.c_ent, d.norm, d.r_grp, d.c_grp,
-                    d.r_slot, d.c_slot, d.ngrp, d.ctot, d.slot_st, d.ord_tmp, d.ord_cub, d.rank_pix, d.all4};
+                    d.r_slot, d.c_slot, d.ngrp, d.ctot, d.slot_st, d.ord_tmp, d.ord_cub, d.rank_pix, d.all4, d.prev_cut, d.prev_n, d.prev_flags, d.prev_rows, d.warm_ok};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (c->h_stage) cudaFreeHost(c->h_stage);
@@ -666,6 +666,15 @@ static lmc_status create_impl(lmc_ctx *c, const lmc_gbuffer *g, const lmc_vpls *
     CK(launch_order_bytes((int32_t)std::max<int64_t>(SL, 1), &d.ord_cub_bytes), "cub sizing");
     CK(cudaMalloc(&d.ord_cub, std::max<size_t>(d.ord_cub_bytes, 16)), "alloc cub");
     CK(dalloc(&d.rank_pix, ML), "alloc resolve");
+    if (cfg.warm_start) {
+        if (cfg.warm_iters < 0) return fail(c, LMC_EINVAL, "warm_iters must be >= 0");
+        CK(dalloc(&d.prev_cut, SL * G), "alloc warm start");
+        CK(dalloc(&d.prev_n, SL), "alloc warm start");
+        CK(dalloc(&d.prev_flags, SL), "alloc warm start");
+        CK(dalloc(&d.prev_rows, ML), "alloc warm start");
+        CK(dalloc(&d.warm_ok, SL), "alloc warm start");
+        CK(cudaMemsetAsync(d.warm_ok, 0, sizeof(int32_t) * (size_t)std::max<int64_t>(SL, 1), c->stream), "memset");
+    }
     CK(cudaMallocHost(&c->h_pix, sizeof(int32_t) * (size_t)std::max<int64_t>(ML, 1)), "alloc staging");
     CK(dalloc(&d.r_ent, SL * c->scap), "alloc layout");
     CK(dalloc(&d.c_ent, SL * c->scap), "alloc layout");
@@ -852,6 +861,7 @@ lmc_status lmc_complete(lmc_ctx *c)
         CK(run_mals(c), "completion (MALS)");
         ev_rec(c, 9);
     } else if (c->use_adm2) {
+        if (c->cfg.warm_start) { CK(run_warm_check(c), "warm start"); c->launches += c->SL > 0 ? 1 : 0; }
         CK(run_layout2(c), "Omega layout");
         CK(completion_order(c), "completion order");
         ev_rec(c, 8);
@@ -859,6 +869,7 @@ lmc_status lmc_complete(lmc_ctx *c)
         ev_rec(c, 9);
         c->launches += c->SL > 0 ? 2 : 0;
     } else {
+        if (c->cfg.warm_start) { CK(run_warm_check(c), "warm start"); c->launches += c->SL > 0 ? 1 : 0; }
         CK(run_layout(c), "Omega layout");
         // shared memory of the ADM kernel is sized by the cut bound G (validated at lmc_create), so
         // nothing of this frame has to be read back: the call only enqueues
@@ -870,6 +881,10 @@ lmc_status lmc_complete(lmc_ctx *c)
     }
     CK(run_direct(c), "direct slices");
     c->launches += c->SL > 0 ? 2 : 0;
+    if (c->cfg.warm_start && c->cfg.solver == LMC_SOLVER_ADM) {
+        CK(run_warm_save(c), "warm start");   // this frame's cut, rows and flags for the next frame
+        c->launches += c->SL > 0 ? 1 : 0;
+    }
     ev_rec(c, 5);
     c->state = 5;
     return LMC_OK;
@@ -1216,6 +1231,11 @@ lmc_status lmc_get_stats(lmc_ctx *c, lmc_stats *st)
         std::vector<int32_t> nz(c->SL);
         CK(d2h(nz.data(), c->d.nnz, (size_t)c->SL), "stats");
         for (int v : nz) st->sum_samples += v;
+    }
+    if (c->state >= 5 && c->cfg.warm_start && c->d.warm_ok) {
+        std::vector<int32_t> wk(c->SL);
+        CK(d2h(wk.data(), c->d.warm_ok, (size_t)c->SL), "stats");
+        for (int v : wk) st->n_warm += v;
     }
     if (c->state >= 5) {
         std::vector<int32_t> fl(c->SL);

@@ -114,6 +114,8 @@ struct Dev {
     void *ord_cub;                     // CUB radix-sort temp of the launch order
     size_t ord_cub_bytes;
     int32_t *rank_pix;                 // [ML] image index of this rank's rows (host-buffer resolve)
+    // warm start: the previous frame's cut, rows and flags of this rank's slices
+    int32_t *prev_cut, *prev_n, *prev_flags, *prev_rows, *warm_ok;   // [SL][G], [SL], [SL], [ML], [SL]
     float4 *all4;                      // world > 1 with NCCL: [ML] this rank's packed (r, g, b, pixel) rows;
                                        // rank 0: [M], every rank's tile at its row offset
     unsigned long long *r_ent;         // [SL][scap] (M^ bits << 32) | (column-layout index << 10) | column
@@ -186,6 +188,7 @@ struct lmc_ctx {
     int32_t *h_pix = nullptr;      // pinned [ML] pixel ids of the host-buffer resolve
     int64_t launches = 0;          // kernels (and CUB dispatches, 1 each) issued by stage calls
     void *comm = nullptr;          // ncclComm_t of the image gather (world > 1 with an NCCL id)
+    bool have_prev = false;        // warm start: a previous frame's completion exists
 };
 
 namespace lmc {
@@ -213,6 +216,8 @@ cudaError_t run_rank_pixels(lmc_ctx *c, int32_t *out);
 cudaError_t run_check_pixels(lmc_ctx *c, unsigned long long *flag);
 cudaError_t launch_order_bytes(int32_t SL, size_t *bytes);
 cudaError_t run_launch_order(lmc_ctx *c, int ntail);
+cudaError_t run_warm_check(lmc_ctx *c);
+cudaError_t run_warm_save(lmc_ctx *c);
 size_t adm_smem_bytes(int q, int mmax, int nmax);
 // complete2.cu (lane-per-segment ADM, q <= 16)
 cudaError_t run_layout2(lmc_ctx *c);

@@ -51,7 +51,7 @@ class Config(C.Structure):
                 ("alpha", C.c_double), ("beta", C.c_double), ("gamma", C.c_double), ("lambda_", C.c_double),
                 ("rank", C.c_int32), ("world", C.c_int32), ("input_memory", C.c_int32), ("stream", _P),
                 ("nccl_id", C.c_uint8 * 128), ("row_importance", C.c_int32), ("cost_mode", C.c_int32),
-                ("resolve_mode", C.c_int32)]
+                ("resolve_mode", C.c_int32), ("warm_start", C.c_int32), ("warm_iters", C.c_int32)]
 
 
 class Stats(C.Structure):
@@ -60,7 +60,7 @@ class Stats(C.Structure):
                                          "n_zero", "n_diverged", "pool_used_max", "pool_cap", "launches")] + \
               [(k, C.c_float) for k in ("ms_slices", "ms_pass1", "ms_coarsen", "ms_pass2", "ms_complete",
                                         "ms_resolve", "ms_solver")] + \
-              [(k, C.c_int64) for k in ("layout_row_slots", "layout_col_slots")] + [("ms_eval2", C.c_float)]
+              [(k, C.c_int64) for k in ("layout_row_slots", "layout_col_slots")] + [("ms_eval2", C.c_float), ("n_warm", C.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -180,6 +180,8 @@ class Frame:
         self.cfg.row_importance = int(prm.get("row_importance", 0))
         self.cfg.cost_mode = int(prm.get("cost_mode", 0))
         self.cfg.resolve_mode = int(prm.get("resolve_mode", 0))
+        self.cfg.warm_start = int(prm.get("warm_start", 0))
+        self.cfg.warm_iters = int(prm.get("warm_iters", 0))
         h = _P()
         st = lib.lmc_create(C.byref(self.gb), C.byref(self.vp), C.byref(self.tr), C.byref(self.sc),
                             C.byref(self.cfg), C.byref(h))
@@ -205,7 +207,18 @@ class Frame:
             raise LmcError(f"{what}: {lib.lmc_status_str(st).decode()}: {msg}")
 
     # -- the seven calls -------------------------------------------------------------------------
-    def upload_inputs(self):
+    def upload_inputs(self, inputs=None):
+        """re-upload the per-frame inputs (G-buffer, VPLs) -- of `inputs` (same sizes) if given; the light
+        tree and global cut stay those of lmc_create"""
+        if inputs is not None:
+            g, v = inputs.gbuf, inputs.vpls
+            arr = self.arr
+            self.gb = Gbuffer(inputs.width, inputs.height, g["px"].shape[0], arr(g["pixel"], np.int32),
+                              *[arr(g[k], np.float32) for k in ("px", "py", "pz", "nx", "ny", "nz", "vx", "vy", "vz",
+                                                                "rho_r", "rho_g", "rho_b", "spec")],
+                              arr(g["exponent"], np.int32))
+            self.vp = Vpls(v["px"].shape[0], *[arr(v[k], np.float32) for k in ("px", "py", "pz", "nx", "ny", "nz",
+                                                                               "ir", "ig", "ib")])
         self._ck(lib.lmc_upload_inputs(self.h, C.byref(self.gb), C.byref(self.vp), C.byref(self.tr)), "upload_inputs")
 
     def build_slices(self):

@@ -278,3 +278,42 @@ def test_sampling_and_resolve_variants(name, over):
     for r in oracle.Oracle(x).run_slices(list(range(off.size - 1)), stage=4):
         check_slice(x, fr, img, r)
     fr.close()
+
+
+# ------------------------------------------------------------------------------ SURVEY f4 warm start
+
+@pytest.mark.parametrize("q", [8, 16])
+def test_warm_start_frame_sequence(q):
+    """frame 2 starts every slice whose rows and cut are unchanged from frame 1's factors (its VPLs
+    near the ceiling moved, so some cuts change and those slices start cold); both frames against
+    the oracle's same sequence"""
+    import dataclasses
+    x1 = scenegen.make_inputs(scenegen.preset("t_interior", rank_q=q, warm_start=1, warm_iters=25))
+    v2 = dict(x1.vpls)
+    move = v2["py"] > np.quantile(v2["py"], 0.7)
+    v2["px"] = np.where(move, v2["px"] + 0.05, v2["px"]).astype(np.float32)
+    x2 = dataclasses.replace(x1, vpls=v2)
+    fr, img1 = run_frame(x1)
+    o1 = oracle.Oracle(x1)
+    off, _ = fr.slices()
+    ids = list(range(off.size - 1))
+    r1 = o1.run_slices(ids, stage=4)
+    for r in r1:
+        check_slice(x1, fr, img1, r)
+    assert fr.stats()["n_warm"] == 0
+    fr.upload_inputs(x2)
+    img = torch.zeros(x2.height * x2.width * 3, device="cuda")
+    fr.run(img)
+    torch.cuda.synchronize()
+    img2 = img.view(-1, 3).cpu().numpy().astype(np.float64)
+    o2 = oracle.Oracle(x2)
+    o2.set_warm(r1)
+    r2 = o2.run_slices(ids, stage=4)
+    nwarm = sum(r["warm"] for r in r2)
+    assert 0 < nwarm < len(r2), "some slices start warm, some cold"
+    assert fr.stats()["n_warm"] == nwarm
+    for r in r2:
+        check_slice(x2, fr, img2, r)
+        if r["warm"]:
+            assert fr.factors(r["slice"])["iters"] == 25
+    fr.close()

@@ -92,3 +92,46 @@ def test_z_mode_adds_the_observed_residuals():
         lr = (0.2126 * rho[:, 0] + 0.7152 * rho[:, 1]) + 0.0722 * rho[:, 2]
         extra = (rho / lr[:, None]) * (M @ wk)
         np.testing.assert_allclose(b["rgb"] - a["rgb"], extra, rtol=1e-9, atol=1e-12 * np.abs(a["rgb"]).max())
+
+
+# ------------------------------------------------------------------------------ warm start
+
+def test_exact_nonnegative_factors_are_an_adm_fixed_point():
+    # fully observed M = X* Y* >= 0: Z = M, U = X*, Lambda = 0 give X_1 = (M Y*^T + a X*)(Y* Y*^T + a I)^-1 = X*
+    # and then Y_1 = Y*, so a warm start from the exact factors stays there (App. A updates)
+    rng = np.random.default_rng(8)
+    m, n, q = 60, 40, 4
+    Xs = rng.uniform(0.1, 1.0, (m, q))
+    Ys = rng.uniform(0.1, 1.0, (q, n))
+    M = Xs @ Ys
+    row, col = np.nonzero(np.ones((m, n)))
+    val = M[row, col]
+    sg = val.max()
+    w = oracle.adm_warm(m, n, row, col, val, q, Xs, Ys / sg, K=50)
+    assert w["iters"] == 50
+    np.testing.assert_allclose(w["U"] @ w["V"], M, rtol=1e-11, atol=1e-12)
+    c = oracle.adm(m, n, row, col, val, q, K=50)          # the cold start is not there after 50 steps
+    assert np.linalg.norm(c["U"] @ c["V"] - M) / np.linalg.norm(M) > 1e-6
+
+
+def test_warm_start_frame_sequence():
+    x = scenegen.make_inputs(scenegen.preset("t_interior", warm_start=1, warm_iters=20))
+    o = oracle.Oracle(x)
+    off, _ = o.slices()
+    ids = list(range(off.size - 1))
+    f1 = o.run_slices(ids, stage=4)
+    assert not any(r["warm"] for r in f1)
+    o.set_warm(f1)
+    f2 = o.run_slices(ids, stage=4)       # same inputs: every regular ADM slice starts warm
+    for a, b in zip(f1, f2):
+        assert np.array_equal(a["cut_nodes"], b["cut_nodes"])
+        if a["flags"] == 0:
+            assert b["warm"] == 1 and b["iters"] == 20
+            # the multipliers restart at 0, so ADM leaves the previous point but stays near its fit
+            assert b["resid"] < 2.0 * a["resid"] and not np.array_equal(a["U"], b["U"])
+        else:
+            assert b["warm"] == 0
+    # a changed row set (other slice id) never matches: cold start
+    o2 = oracle.Oracle(x)
+    o2.set_warm([dict(f1[0], slice=1)])
+    assert o2.run_slices([1], stage=3)[0]["warm"] == 0
