@@ -284,15 +284,16 @@ def test_sampling_and_resolve_variants(name, over):
 
 @pytest.mark.parametrize("q", [8, 16])
 def test_warm_start_frame_sequence(q):
-    """frame 2 starts every slice whose rows and cut are unchanged from frame 1's factors (its VPLs
-    near the ceiling moved, so some cuts change and those slices start cold); both frames against
-    the oracle's same sequence"""
+    """frame 2 starts every slice whose rows and cut are unchanged from frame 1's factors (the albedo of
+    the pixels of the left 40% of the room dropped, so the cuts of the slices there change and those
+    start cold); both frames against the oracle's same sequence"""
     import dataclasses
     x1 = scenegen.make_inputs(scenegen.preset("t_interior", rank_q=q, warm_start=1, warm_iters=25))
-    v2 = dict(x1.vpls)
-    move = v2["py"] > np.quantile(v2["py"], 0.7)
-    v2["px"] = np.where(move, v2["px"] + 0.05, v2["px"]).astype(np.float32)
-    x2 = dataclasses.replace(x1, vpls=v2)
+    g2 = dict(x1.gbuf)
+    sel = g2["px"] < np.quantile(g2["px"], 0.4)
+    for k in ("rho_r", "rho_g", "rho_b"):
+        g2[k] = np.where(sel, g2[k] * 0.3, g2[k]).astype(np.float32)
+    x2 = dataclasses.replace(x1, gbuf=g2)
     fr, img1 = run_frame(x1)
     o1 = oracle.Oracle(x1)
     off, _ = fr.slices()
