@@ -121,6 +121,10 @@ typedef struct {
      * cut equal the previous frame's (and whose previous result was regular) from the previous
      * frame's factors (U, V / sigma; multipliers 0) for warm_iters iterations (0: max_iter) */
     int32_t warm_start, warm_iters;
+    /* SURVEY §8(f2) count-target coarsening (DESIGN R37): > 0 merges, per slice, the least-cost
+     * pair of sibling cut nodes (ties: smallest node id) until the cut has coarsen_target nodes
+     * (coarsen_tau unused); 0 = the threshold rule */
+    int32_t coarsen_target;
 } lmc_config;
 
 typedef struct {
@@ -188,6 +192,10 @@ lmc_status lmc_complete(lmc_ctx *ctx);
  * ncclSend theirs; one NCCL group) and writes every pixel of the frame; image_rgb is ignored on
  * ranks != 0 (may be NULL there).  world > 1 without a communicator: this rank's pixels only. */
 lmc_status lmc_resolve_image(lmc_ctx *ctx, float *image_rgb, int32_t image_memory);
+
+/* sizeof of the ABI structs (0 gbuffer, 1 vpls, 2 light tree, 3 scene, 4 config, 5 stats; -1 otherwise):
+ * lets a binding check its struct layouts against the library */
+int64_t lmc_sizeof_struct(int32_t which);
 
 /* ncclGetUniqueId for lmc_config.nccl_id (call on rank 0 only; LMC_ENCCL on failure) */
 lmc_status lmc_nccl_unique_id(uint8_t out[128]);

@@ -55,7 +55,7 @@ class _Inputs(C.Structure):
         ("tol", C.c_double), ("alpha", C.c_double), ("beta", C.c_double), ("gamma", C.c_double), ("lam", C.c_double),
         ("order_seed", C.c_uint64),
         ("row_importance", C.c_int32), ("cost_mode", C.c_int32), ("resolve_mode", C.c_int32),
-        ("warm_iters", C.c_int32), ("nwarm", C.c_int32), ("warm", C.c_void_p),
+        ("warm_iters", C.c_int32), ("nwarm", C.c_int32), ("coarsen_target", C.c_int32), ("warm", C.c_void_p),
     ]
 
 
@@ -190,6 +190,7 @@ class Oracle:
         s.cost_mode = prm.get("cost_mode", 0)
         s.resolve_mode = prm.get("resolve_mode", 0)
         s.warm_iters = prm.get("warm_iters", 0)
+        s.coarsen_target = prm.get("coarsen_target", 0)
         s.nwarm = 0
         s.warm = None
         self._keep = keep

@@ -221,6 +221,10 @@ double orc_entry_T(const orc_inputs *in, int64_t p, int64_t v)
     return phi * G;
 }
 
+/* struct sizes for the binding's layout check */
+int64_t orc_sizeof_inputs(void) { return (int64_t)sizeof(orc_inputs); }
+int64_t orc_sizeof_result(void) { return (int64_t)sizeof(orc_slice_result); }
+
 /* T for n (row, vpl) pairs, one orc_entry_T call each (test convenience, no new arithmetic) */
 void orc_entry_T_many(const orc_inputs *in, int64_t n, const int32_t *rows, const int32_t *vpls, double *out)
 {
@@ -451,6 +455,12 @@ static void coarsen(slice_ctx *c, orc_slice_result *res, const int32_t *parent)
     int32_t *fresh = malloc((size_t)(c->m + 1) * sizeof(int32_t));
     uint64_t rs = in->order_seed;
     int64_t head = 0;
+    /* count-target mode (reading R37): candidates are evaluated when they appear, merges
+     * follow the least cost (ties: smallest node id) until the cut has coarsen_target nodes */
+    const int count_mode = in->coarsen_target > 0;
+    int64_t cut_size = in->ncut;
+    ivec cands = {0};
+    for (;;) {
     while (head < work.n) {
         int32_t f;
         if (in->order_seed) { /* order-independence pin: process a random pending candidate */
@@ -511,19 +521,21 @@ static void coarsen(slice_ctx *c, orc_slice_result *res, const int32_t *parent)
          * the accumulated error of L_a (cost_mode 1): (eps + cost(L_b)) + cost(L_a) */
         double cf = eps + cost[b];
         if (in->cost_mode) cf = cf + cost[a];
-        int do_merge = cf < in->tau; /* P:116 "less than a prespecified error bound" (R11) */
+        int do_merge = !count_mode && cf < in->tau; /* P:116 "less than a prespecified error bound" (R11) */
         zidx[f] = (int32_t)pnode.n;
         iv_push(&pnode, f);
         iv_push(&pmerged, do_merge);
         dv_push(&peps, eps);
         dv_push(&pcost, cf);
         iv_push(&zoff, (int32_t)zrows.n);
+        cost[f] = cf;
+        if (count_mode) iv_push(&cands, f);
         if (do_merge) {
             in_cut[l] = 0;
             in_cut[r] = 0;
             in_cut[f] = 1;
             merged[f] = 1;
-            cost[f] = cf;
+            cut_size--;
             int32_t p = parent[f];
             if (p >= 0) {
                 int32_t sib = in->left[p] == f ? in->right[p] : in->left[p];
@@ -531,6 +543,31 @@ static void coarsen(slice_ctx *c, orc_slice_result *res, const int32_t *parent)
             }
         }
     }
+    if (!count_mode || cut_size <= in->coarsen_target) break;
+    /* the least-cost pair of sibling cut nodes */
+    int64_t bk = -1;
+    for (int64_t k = 0; k < cands.n; ++k) {
+        int32_t g = cands.a[k];
+        if (merged[g]) continue;
+        if (bk < 0 || cost[g] < cost[cands.a[bk]] || (cost[g] == cost[cands.a[bk]] && g < cands.a[bk])) bk = k;
+    }
+    if (bk < 0) break;
+    {
+        int32_t f = cands.a[bk];
+        in_cut[in->left[f]] = 0;
+        in_cut[in->right[f]] = 0;
+        in_cut[f] = 1;
+        merged[f] = 1;
+        pmerged.a[zidx[f]] = 1;
+        cut_size--;
+        int32_t p = parent[f];
+        if (p >= 0) {
+            int32_t sib = in->left[p] == f ? in->right[p] : in->left[p];
+            if (in_cut[sib]) iv_push(&work, p);
+        }
+    }
+    }
+    free(cands.a);
     /* final cut, sorted by node id = column order (R29) */
     int32_t n = 0;
     ivec cutv = {0};

@@ -61,6 +61,9 @@ typedef struct {
     /* warm start: ADM slices found in warm[] (same slice, rows and cut, regular
      * result) start from those factors and run warm_iters iterations (0: K) */
     int32_t warm_iters, nwarm;
+    /* SURVEY §8(f2) count-target coarsening (R37): > 0 merges the least-cost sibling pair
+     * until the cut has this many nodes (tau unused); 0 = the threshold rule */
+    int32_t coarsen_target;
     const orc_warm *warm;
 } orc_inputs;
 
@@ -95,6 +98,8 @@ typedef struct {
     int32_t warm;                 /* 1: the completion started from the previous frame's factors */
 } orc_slice_result;
 
+int64_t orc_sizeof_inputs(void);
+int64_t orc_sizeof_result(void);
 /* P:? — Philox4x32-10 (Salmon et al. SC'11), R-readings O3 */
 void orc_philox(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
 /* Floyd sampling of n distinct rows of [0,m) keyed by (a, slice); writes sorted rows, returns count */

@@ -840,7 +840,8 @@ __global__ void __launch_bounds__(CO_THREADS, CO_MINB) k_coarsen(
     const double *__restrict__ p1_Ta, const double *__restrict__ p1_Tb, const int32_t *__restrict__ p1_cnt,
     uint16_t *pool_rows, double *pool_Ta, double *pool_Tb, int32_t *pool_used, int64_t pool_cap, uint8_t *cs_flags,
     double *cs_eps, double *cs_cost, int32_t *cs_zoff, int32_t *cs_zlen, int32_t *cut_n, int32_t *cut_cols,
-    int32_t *src_off, int32_t *src_len, int32_t *src_side, int G, unsigned long long *counters, int cost_mode)
+    int32_t *src_off, int32_t *src_len, int32_t *src_side, int G, unsigned long long *counters, int cost_mode,
+    int count_target)
 {
     extern __shared__ __align__(16) unsigned char smem[];
     const int U = up.U;
@@ -870,113 +871,178 @@ __global__ void __launch_bounds__(CO_THREADS, CO_MINB) k_coarsen(
     unsigned long long evals = 0;
     bool overflow = false;
     uint32_t *bm = sh_bm + w * 32;
-    for (int h = 1; h <= up.H; ++h) {
-        for (int idx = up.hoff[h] + w; idx < up.hoff[h + 1]; idx += CO_WARPS) {
-            const int f = up.hlist[idx];
-            const int l = up.left[f], r = up.right[f];
-            if (!((sh_flag[l] & F_INCUT) && (sh_flag[r] & F_INCUT))) continue;   // not a candidate
-            const int a = (up.rep[l] == up.rep[f]) ? l : r;
-            const int b = (a == l) ? r : l;
-            const int va = up.rep[a], vb = up.rep[b];
-            const double la = up.lum[a], lb = up.lum[b];
-            const double ratio = la > 0.0 ? lb / la : 0.0;
-            const bool ml = (sh_flag[l] & F_MERGED) != 0, mr = (sh_flag[r] & F_MERGED) != 0;
-            int total, off = 0;
-            double eps = 0.0;
-            if (!ml && !mr) {
-                // base pair: rows and entries from pass 1
-                const int bi = up.base_of[f];
-                const int64_t pi = ((int64_t)ls * up.nB + bi);
-                total = p1_cnt[pi];
-                if (lane == 0) off = atomicAdd(&sh_pool, total);
-                off = __shfl_sync(FULL_MASK, off, 0);
-                if (off + total > pool_cap) { overflow = true; continue; }
-                if (lane < total) {
-                    int i = p1_rows[pi * nmax + lane];
-                    double Ta = p1_Ta[pi * nmax + lane], Tb = p1_Tb[pi * nmax + lane];
-                    pool_rows[pbase + off + lane] = (uint16_t)i;
-                    pool_Ta[pbase + off + lane] = Ta;
-                    pool_Tb[pbase + off + lane] = Tb;
-                    double lr = lum_rho_d(prow, lrow0 + i);
-                    double Va = (lr * la) * Ta, Vb = (lr * lb) * Tb;
-                    eps = la > 0.0 ? fabs(Vb - Va * ratio) : fabs(Vb);
+    // one warp evaluates candidate f (both children in the cut): zeta_f, the entries, eps and
+    // cost; `decide` applies the threshold rule right away
+    auto eval_cand = [&](const int f, const bool decide) {
+        const int l = up.left[f], r = up.right[f];
+        if (!((sh_flag[l] & F_INCUT) && (sh_flag[r] & F_INCUT))) return;   // not a candidate
+        const int a = (up.rep[l] == up.rep[f]) ? l : r;
+        const int b = (a == l) ? r : l;
+        const int va = up.rep[a], vb = up.rep[b];
+        const double la = up.lum[a], lb = up.lum[b];
+        const double ratio = la > 0.0 ? lb / la : 0.0;
+        const bool ml = (sh_flag[l] & F_MERGED) != 0, mr = (sh_flag[r] & F_MERGED) != 0;
+        int total, off = 0;
+        double eps = 0.0;
+        if (!ml && !mr) {
+            // base pair: rows and entries from pass 1
+            const int bi = up.base_of[f];
+            const int64_t pi = ((int64_t)ls * up.nB + bi);
+            total = p1_cnt[pi];
+            if (lane == 0) off = atomicAdd(&sh_pool, total);
+            off = __shfl_sync(FULL_MASK, off, 0);
+            if (off + total > pool_cap) { overflow = true; return; }
+            if (lane < total) {
+                int i = p1_rows[pi * nmax + lane];
+                double Ta = p1_Ta[pi * nmax + lane], Tb = p1_Tb[pi * nmax + lane];
+                pool_rows[pbase + off + lane] = (uint16_t)i;
+                pool_Ta[pbase + off + lane] = Ta;
+                pool_Tb[pbase + off + lane] = Tb;
+                double lr = lum_rho_d(prow, lrow0 + i);
+                double Va = (lr * la) * Ta, Vb = (lr * lb) * Tb;
+                eps = la > 0.0 ? fabs(Vb - Va * ratio) : fabs(Vb);
+            }
+        } else {
+            // zeta_f = zeta_a U zeta_b (both merged) or zeta_h U Floyd(n(o)) (mixed), R10
+            bm[lane] = 0u;
+            __syncwarp();
+            const int h1 = ml ? l : r;
+            {
+                int o1 = sh_zoff[h1], n1 = sh_zlen[h1];
+                for (int k = lane; k < n1; k += 32) {
+                    int i = pool_rows[pbase + o1 + k];
+                    atomicOr(&bm[i >> 5], 1u << (i & 31));
+                }
+            }
+            if (ml && mr) {
+                int o2 = sh_zoff[r], n2 = sh_zlen[r];
+                for (int k = lane; k < n2; k += 32) {
+                    int i = pool_rows[pbase + o2 + k];
+                    atomicOr(&bm[i >> 5], 1u << (i & 31));
                 }
             } else {
-                // zeta_f = zeta_a U zeta_b (both merged) or zeta_h U Floyd(n(o)) (mixed), R10
-                bm[lane] = 0u;
-                __syncwarp();
-                const int h1 = ml ? l : r;
-                {
-                    int o1 = sh_zoff[h1], n1 = sh_zlen[h1];
-                    for (int k = lane; k < n1; k += 32) {
-                        int i = pool_rows[pbase + o1 + k];
-                        atomicOr(&bm[i >> 5], 1u << (i & 31));
-                    }
-                }
-                if (ml && mr) {
-                    int o2 = sh_zoff[r], n2 = sh_zlen[r];
-                    for (int k = lane; k < n2; k += 32) {
-                        int i = pool_rows[pbase + o2 + k];
-                        atomicOr(&bm[i >> 5], 1u << (i & 31));
-                    }
-                } else {
-                    const int o = ml ? r : l;
-                    int n = up.nunc[o] < m ? up.nunc[o] : m;
-                    int i = warp_floyd(m, n, (uint32_t)up.node[f], s, seed, lane);
-                    if (lane < n) atomicOr(&bm[i >> 5], 1u << (i & 31));
-                }
-                __syncwarp();
-                uint32_t word = bm[lane];
-                int cnt = __popc(word), incl = cnt;
-                for (int o = 1; o < 32; o <<= 1) {
-                    int t = __shfl_up_sync(FULL_MASK, incl, o);
-                    if (lane >= o) incl += t;
-                }
-                total = __shfl_sync(FULL_MASK, incl, 31);
-                if (lane == 0) off = atomicAdd(&sh_pool, total);
-                off = __shfl_sync(FULL_MASK, off, 0);
-                if (off + total > pool_cap) { overflow = true; continue; }
-                int pos = off + incl - cnt;
-                while (word) {
-                    int bit = __ffs(word) - 1;
-                    word &= word - 1;
-                    pool_rows[pbase + pos++] = (uint16_t)(lane * 32 + bit);
-                }
-                __syncwarp();
-                for (int k = lane; k < total; k += 32) {
-                    int i = pool_rows[pbase + off + k];
-                    double Ta = entry_T(slot, prow, lrow0 + i, vpl, va);
-                    double Tb = entry_T(slot, prow, lrow0 + i, vpl, vb);
-                    pool_Ta[pbase + off + k] = Ta;
-                    pool_Tb[pbase + off + k] = Tb;
-                    double lr = lum_rho_d(prow, lrow0 + i);
-                    double Va = (lr * la) * Ta, Vb = (lr * lb) * Tb;
-                    double e = la > 0.0 ? fabs(Vb - Va * ratio) : fabs(Vb);
-                    eps = fmax(eps, e);
-                }
-                evals += (lane == 0) ? 2ull * total : 0ull;
-            }
-            eps = warp_max_d(eps);
-            // Eq. (1): cost(L_f) = eps(L_f) + cost(L_b); merge iff below the bound.
-            // cost_mode 1 (SURVEY f3 sensitivity): (eps + cost(L_b)) + cost(L_a)
-            double cf = eps + sh_cost[b];
-            if (cost_mode) cf = cf + sh_cost[a];
-            if (lane == 0) {
-                sh_eps[f] = eps;
-                sh_cost[f] = cf;
-                sh_zoff[f] = off;
-                sh_zlen[f] = total;
-                uint8_t fl = F_PROC;
-                if (cf < tau) {
-                    fl |= F_INCUT | F_MERGED;
-                    sh_flag[l] &= (uint8_t)~F_INCUT;
-                    sh_flag[r] &= (uint8_t)~F_INCUT;
-                }
-                sh_flag[f] = fl;
+                const int o = ml ? r : l;
+                int n = up.nunc[o] < m ? up.nunc[o] : m;
+                int i = warp_floyd(m, n, (uint32_t)up.node[f], s, seed, lane);
+                if (lane < n) atomicOr(&bm[i >> 5], 1u << (i & 31));
             }
             __syncwarp();
+            uint32_t word = bm[lane];
+            int cnt = __popc(word), incl = cnt;
+            for (int o = 1; o < 32; o <<= 1) {
+                int t = __shfl_up_sync(FULL_MASK, incl, o);
+                if (lane >= o) incl += t;
+            }
+            total = __shfl_sync(FULL_MASK, incl, 31);
+            if (lane == 0) off = atomicAdd(&sh_pool, total);
+            off = __shfl_sync(FULL_MASK, off, 0);
+            if (off + total > pool_cap) { overflow = true; return; }
+            int pos = off + incl - cnt;
+            while (word) {
+                int bit = __ffs(word) - 1;
+                word &= word - 1;
+                pool_rows[pbase + pos++] = (uint16_t)(lane * 32 + bit);
+            }
+            __syncwarp();
+            for (int k = lane; k < total; k += 32) {
+                int i = pool_rows[pbase + off + k];
+                double Ta = entry_T(slot, prow, lrow0 + i, vpl, va);
+                double Tb = entry_T(slot, prow, lrow0 + i, vpl, vb);
+                pool_Ta[pbase + off + k] = Ta;
+                pool_Tb[pbase + off + k] = Tb;
+                double lr = lum_rho_d(prow, lrow0 + i);
+                double Va = (lr * la) * Ta, Vb = (lr * lb) * Tb;
+                double e = la > 0.0 ? fabs(Vb - Va * ratio) : fabs(Vb);
+                eps = fmax(eps, e);
+            }
+            evals += (lane == 0) ? 2ull * total : 0ull;
         }
+        eps = warp_max_d(eps);
+        // Eq. (1): cost(L_f) = eps(L_f) + cost(L_b); merge iff below the bound.
+        // cost_mode 1 (SURVEY f3 sensitivity): (eps + cost(L_b)) + cost(L_a)
+        double cf = eps + sh_cost[b];
+        if (cost_mode) cf = cf + sh_cost[a];
+        if (lane == 0) {
+            sh_eps[f] = eps;
+            sh_cost[f] = cf;
+            sh_zoff[f] = off;
+            sh_zlen[f] = total;
+            uint8_t fl = F_PROC;
+            if (decide && cf < tau) {
+                fl |= F_INCUT | F_MERGED;
+                sh_flag[l] &= (uint8_t)~F_INCUT;
+                sh_flag[r] &= (uint8_t)~F_INCUT;
+            }
+            sh_flag[f] = fl;
+        }
+        __syncwarp();
+    };
+    if (count_target <= 0) {
+        // threshold rule: candidates height by height (a node's outcome depends on its subtree only)
+        for (int h = 1; h <= up.H; ++h) {
+            for (int idx = up.hoff[h] + w; idx < up.hoff[h + 1]; idx += CO_WARPS) {
+                const int f = up.hlist[idx];
+                const int l = up.left[f], r = up.right[f];
+                if (!((sh_flag[l] & F_INCUT) && (sh_flag[r] & F_INCUT))) continue;   // not a candidate
+                eval_cand(f, true);
+            }
+            __syncthreads();
+        }
+    } else {
+        // count target (R37): every base pair is evaluated, then the least-cost candidate
+        // (ties: smallest node id) merges until the cut has count_target nodes; a merge may make
+        // the parent a candidate, evaluated before the next choice
+        if (up.H >= 1)
+            for (int idx = up.hoff[1] + w; idx < up.hoff[2]; idx += CO_WARPS) eval_cand(up.hlist[idx], false);
         __syncthreads();
+        __shared__ int sh_best, sh_pend, sh_cut;
+        __shared__ double sh_bc[CO_WARPS];
+        __shared__ int sh_bu[CO_WARPS];
+        if (threadIdx.x == 0) sh_cut = G;
+        __syncthreads();
+        for (;;) {
+            if (sh_cut <= count_target) break;
+            double bc = 0.0;
+            int bu = -1;
+            for (int u = threadIdx.x; u < U; u += CO_THREADS) {
+                const uint8_t fl = sh_flag[u];
+                if (!(fl & F_PROC) || (fl & F_MERGED)) continue;
+                if (!((sh_flag[up.left[u]] & F_INCUT) && (sh_flag[up.right[u]] & F_INCUT))) continue;
+                if (bu < 0 || sh_cost[u] < bc) { bc = sh_cost[u]; bu = u; }   // u ascending: first = smallest id
+            }
+            for (int o = 16; o > 0; o >>= 1) {
+                const double oc = __shfl_xor_sync(FULL_MASK, bc, o);
+                const int ou = __shfl_xor_sync(FULL_MASK, bu, o);
+                if (ou >= 0 && (bu < 0 || oc < bc || (oc == bc && ou < bu))) { bc = oc; bu = ou; }
+            }
+            if (lane == 0) { sh_bc[w] = bc; sh_bu[w] = bu; }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                double c2 = 0.0;
+                int u2 = -1;
+                for (int k = 0; k < CO_WARPS; ++k) {
+                    const int ou = sh_bu[k];
+                    if (ou >= 0 && (u2 < 0 || sh_bc[k] < c2 || (sh_bc[k] == c2 && ou < u2))) { c2 = sh_bc[k]; u2 = ou; }
+                }
+                sh_best = u2;
+                sh_pend = -1;
+                if (u2 >= 0) {
+                    sh_flag[up.left[u2]] &= (uint8_t)~F_INCUT;
+                    sh_flag[up.right[u2]] &= (uint8_t)~F_INCUT;
+                    sh_flag[u2] |= F_INCUT | F_MERGED;
+                    sh_cut -= 1;
+                    const int p = up.parent[u2];
+                    if (p >= 0) {
+                        const int sib = up.left[p] == u2 ? up.right[p] : up.left[p];
+                        if (sh_flag[sib] & F_INCUT) sh_pend = p;
+                    }
+                }
+            }
+            __syncthreads();
+            if (sh_best < 0) break;
+            if (sh_pend >= 0 && w == 0) eval_cand(sh_pend, false);
+            __syncthreads();
+        }
     }
     if (lane == 0 && evals) atomicAdd(&counters[1], evals);
     if (overflow) atomicOr(&counters[3], 1ull);
@@ -1047,7 +1113,7 @@ cudaError_t run_coarsen(lmc_ctx *c)
         c->cfg.coarsen_tau, c->d.p1_rows, c->d.p1_Ta, c->d.p1_Tb, c->d.p1_cnt, c->d.pool_rows, c->d.pool_Ta,
         c->d.pool_Tb, c->d.pool_used, c->pool_cap, c->d.cs_flags, c->d.cs_eps, c->d.cs_cost, c->d.cs_zoff,
         c->d.cs_zlen, c->d.cut_n, c->d.cut_cols, c->d.src_off, c->d.src_len, c->d.src_side, c->G, c->d.counters,
-        c->cfg.cost_mode);
+        c->cfg.cost_mode, c->cfg.coarsen_target);
     return cudaGetLastError();
 }
 

@@ -1163,6 +1163,19 @@ lmc_status lmc_get_factors(lmc_ctx *c, int32_t slice, float *U, float *V, int32_
     return LMC_OK;
 }
 
+int64_t lmc_sizeof_struct(int32_t which)
+{
+    switch (which) {
+    case 0: return (int64_t)sizeof(lmc_gbuffer);
+    case 1: return (int64_t)sizeof(lmc_vpls);
+    case 2: return (int64_t)sizeof(lmc_light_tree);
+    case 3: return (int64_t)sizeof(lmc_scene);
+    case 4: return (int64_t)sizeof(lmc_config);
+    case 5: return (int64_t)sizeof(lmc_stats);
+    }
+    return -1;
+}
+
 lmc_status lmc_nccl_unique_id(uint8_t out[128])
 {
     if (!out) return LMC_EINVAL;

@@ -51,7 +51,8 @@ class Config(C.Structure):
                 ("alpha", C.c_double), ("beta", C.c_double), ("gamma", C.c_double), ("lambda_", C.c_double),
                 ("rank", C.c_int32), ("world", C.c_int32), ("input_memory", C.c_int32), ("stream", _P),
                 ("nccl_id", C.c_uint8 * 128), ("row_importance", C.c_int32), ("cost_mode", C.c_int32),
-                ("resolve_mode", C.c_int32), ("warm_start", C.c_int32), ("warm_iters", C.c_int32)]
+                ("resolve_mode", C.c_int32), ("warm_start", C.c_int32), ("warm_iters", C.c_int32),
+                ("coarsen_target", C.c_int32)]
 
 
 class Stats(C.Structure):
@@ -70,7 +71,7 @@ EXPORTS = ["lmc_create", "lmc_upload_inputs", "lmc_build_slices", "lmc_sample_pa
            "lmc_sample_pass2", "lmc_complete", "lmc_resolve_image", "lmc_resolve_rows", "lmc_scatter_rows",
            "lmc_destroy", "lmc_last_error", "lmc_status_str", "lmc_get_slices", "lmc_get_pass1", "lmc_get_coarsen",
            "lmc_get_cut", "lmc_get_samples", "lmc_get_factors", "lmc_get_stats", "lmc_set_timing",
-           "lmc_eval_entries", "lmc_nccl_unique_id", "lmc_get_partition", "lmc_plan_partition"]
+           "lmc_eval_entries", "lmc_nccl_unique_id", "lmc_get_partition", "lmc_plan_partition", "lmc_sizeof_struct"]
 
 
 def _load():
@@ -90,6 +91,8 @@ def _load():
     L.lmc_scatter_rows.argtypes = [_P, _P, C.c_int64, _P]
     L.lmc_nccl_unique_id.argtypes = [_P]
     L.lmc_get_partition.argtypes = [_P, _P, _P]
+    L.lmc_sizeof_struct.argtypes = [C.c_int32]
+    L.lmc_sizeof_struct.restype = C.c_int64
     L.lmc_plan_partition.argtypes = [C.c_int64, C.c_int32, C.c_int32, _P, _P, _P]
     L.lmc_destroy.argtypes = [_P]
     L.lmc_destroy.restype = None
@@ -182,6 +185,7 @@ class Frame:
         self.cfg.resolve_mode = int(prm.get("resolve_mode", 0))
         self.cfg.warm_start = int(prm.get("warm_start", 0))
         self.cfg.warm_iters = int(prm.get("warm_iters", 0))
+        self.cfg.coarsen_target = int(prm.get("coarsen_target", 0))
         h = _P()
         st = lib.lmc_create(C.byref(self.gb), C.byref(self.vp), C.byref(self.tr), C.byref(self.sc),
                             C.byref(self.cfg), C.byref(h))

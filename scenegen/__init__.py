@@ -63,6 +63,8 @@ class Config:
     # warm start of the completion from the previous frame's factors
     warm_start: int = 0
     warm_iters: int = 0
+    # count-target coarsening, 0 = threshold rule
+    coarsen_target: int = 0
 
 
 PRESETS = {
@@ -343,7 +345,8 @@ class Inputs:
                     p1_nmax=c.p1_nmax, p1_nmin=c.p1_nmin, tau=self.tau, rate=c.rate, rank_q=c.rank_q,
                     solver=c.solver, max_iter=c.max_iter, tol=c.tol, alpha=c.alpha, beta=c.beta,
                     gamma=c.gamma, lam=c.lam, row_importance=c.row_importance, cost_mode=c.cost_mode,
-                    resolve_mode=c.resolve_mode, warm_start=c.warm_start, warm_iters=c.warm_iters)
+                    resolve_mode=c.resolve_mode, warm_start=c.warm_start, warm_iters=c.warm_iters,
+                    coarsen_target=c.coarsen_target)
 
 
 def _gbuffer(sc: Scene, W: int, H: int):

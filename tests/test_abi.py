@@ -34,3 +34,18 @@ def test_status_strings_without_gpu():
     assert lmc.lib.lmc_status_str(5) == b"LMC_EOVERFLOW"
     # a NULL config is rejected before any CUDA call
     assert lmc.lib.lmc_create(None, None, None, None, None, None) == lmc.LMC_EINVAL
+
+
+def test_struct_layouts_match_the_library():
+    from paper_2202_12567_b200 import lmc
+    for k, cls in enumerate((lmc.Gbuffer, lmc.Vpls, lmc.LightTree, lmc.Scene, lmc.Config, lmc.Stats)):
+        assert ctypes.sizeof(cls) == lmc.lib.lmc_sizeof_struct(k), cls.__name__
+
+
+def test_oracle_struct_layouts_match():
+    import oracle
+    L = oracle.lib()
+    L.orc_sizeof_inputs.restype = ctypes.c_int64
+    L.orc_sizeof_result.restype = ctypes.c_int64
+    assert ctypes.sizeof(oracle._Inputs) == L.orc_sizeof_inputs()
+    assert ctypes.sizeof(oracle._Result) == L.orc_sizeof_result()

@@ -318,3 +318,22 @@ def test_warm_start_frame_sequence(q):
         if r["warm"]:
             assert fr.factors(r["slice"])["iters"] == 25
     fr.close()
+
+
+# ------------------------------------------------------------------------------ SURVEY f2 count target
+
+@pytest.mark.parametrize("name,over", [("t_interior", dict(coarsen_target=60)), ("c1", dict(coarsen_target=100)),
+                                       ("t_interior", dict(coarsen_target=25, rank_q=16)),
+                                       ("t_cornell", dict(coarsen_target=10 ** 6))])
+def test_count_target_coarsening(name, over):
+    """least-cost-first coarsening to a cut size (R37): processed candidates, merge decisions,
+    eps, cost, cuts and everything downstream bit-exact / within the bars against the oracle"""
+    x = scenegen.make_inputs(scenegen.preset(name, **over))
+    fr, img = run_frame(x)
+    off, _ = fr.slices()
+    res = oracle.Oracle(x).run_slices(list(range(off.size - 1)), stage=4)
+    for r in res:
+        check_slice(x, fr, img, r)
+    if over["coarsen_target"] < 10 ** 6:
+        assert any(r["n"] == over["coarsen_target"] for r in res)
+    fr.close()

@@ -135,3 +135,35 @@ def test_warm_start_frame_sequence():
     o2 = oracle.Oracle(x)
     o2.set_warm([dict(f1[0], slice=1)])
     assert o2.run_slices([1], stage=3)[0]["warm"] == 0
+
+
+# ------------------------------------------------------------------------------ count target
+
+@pytest.mark.parametrize("tau", [3e-6, 1e-5, 4e-5])
+def test_count_target_reproduces_the_threshold_cut(tau):
+    # least-cost-first merging stopped at the size of the threshold cut merges the
+    # same nodes: while a candidate of cost < tau is open the least cost is below tau, and the
+    # threshold rule merges exactly the candidates below tau (costs depend on subtrees only)
+    base = scenegen.make_inputs(scenegen.preset("t_interior", tau=tau))
+    thr = oracle.Oracle(base).run_slices([0, 2, 5], stage=1)
+    for r in thr:
+        K = r["n"]
+        x = scenegen.make_inputs(scenegen.preset("t_interior", tau=tau, coarsen_target=K))
+        c = oracle.Oracle(x).run_slices([r["slice"]], stage=1)[0]
+        assert np.array_equal(c["cut_nodes"], r["cut_nodes"])
+        mc = {f: k for k, f in enumerate(c["proc_node"])}
+        for k, f in enumerate(r["proc_node"]):
+            if r["proc_merged"][k]:
+                assert c["proc_merged"][mc[f]] == 1 and c["proc_cost"][mc[f]] == r["proc_cost"][k]
+
+
+def test_count_target_sizes_and_order():
+    x = scenegen.make_inputs(scenegen.preset("t_interior", coarsen_target=40))
+    t = x.tree
+    g = t["global_cut"].size
+    for r in oracle.Oracle(x).run_slices(range(8), stage=1):
+        assert r["n"] == 40 or r["proc_merged"].sum() == len(r["proc_node"])   # reached, or nothing left
+        assert g - r["proc_merged"].sum() == r["n"]
+    big = scenegen.make_inputs(scenegen.preset("t_interior", coarsen_target=10 ** 6))
+    for r in oracle.Oracle(big).run_slices([0, 1], stage=1):
+        assert r["proc_merged"].sum() == 0 and r["n"] == g
