@@ -193,6 +193,19 @@ lmc_status lmc_complete(lmc_ctx *ctx);
  * ranks != 0 (may be NULL there).  world > 1 without a communicator: this rank's pixels only. */
 lmc_status lmc_resolve_image(lmc_ctx *ctx, float *image_rgb, int32_t image_memory);
 
+/* Step 1 on the GPU (DESIGN R38): the light tree of v and its conservative
+ * global cut.  Tree: median split on the axis of the largest bounding-box extent, (coordinate, VPL
+ * index) order, left child ceil(n/2), breadth-first node ids; I_f = I_l + I_r (fp64, returned as
+ * float32), rep(f) = rep of the brighter child (ties: left).  Cut: the internal nodes of largest
+ * bound lum(I_f) |bbox diagonal| (ties: smaller id) split until the cut has cut_max nodes
+ * (fewer if the tree has fewer leaves).  Inputs v and the outputs (2 count - 1 node arrays, a cut
+ * array of cut_max ids in ascending order, any output may be NULL) are device or host memory per
+ * `memory`; runs on `stream` (cudaStream_t) and synchronises it; *cut_size = |cut|.
+ * LMC_EINVAL bad sizes / null inputs, LMC_ENOMEM, LMC_ECUDA. */
+lmc_status lmc_build_light_tree(const lmc_vpls *v, int32_t cut_max, int32_t memory, void *stream, int32_t *left,
+                                int32_t *right, int32_t *rep, float *ir, float *ig, float *ib, int32_t *global_cut,
+                                int64_t *cut_size);
+
 /* sizeof of the ABI structs (0 gbuffer, 1 vpls, 2 light tree, 3 scene, 4 config, 5 stats; -1 otherwise):
  * lets a binding check its struct layouts against the library */
 int64_t lmc_sizeof_struct(int32_t which);

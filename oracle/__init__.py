@@ -122,6 +122,8 @@ def lib():
             L.orc_mals.restype = C.c_int32
             L.orc_fullcut_slice.argtypes = [C.POINTER(_Inputs), P, C.c_int32, P, C.c_int32, P]
             L.orc_bruteforce_rows.argtypes = [C.POINTER(_Inputs), P, C.c_int32, P]
+            L.orc_build_light_tree.argtypes = [C.c_int64, P, P, P, P, P, P, C.c_int32, P, P, P, P, P, P, P, P]
+            L.orc_build_light_tree.restype = C.c_int32
             L.orc_light_importance.argtypes = [C.c_int32, C.c_int64, P, P, P, P]
             L.orc_pdf_weights.argtypes = [C.c_int32, P, P, P]
             L.orc_cdf_pick.argtypes = [C.c_int32, P, C.c_uint64]
@@ -411,3 +413,18 @@ def adm_warm(m, n, row, col, val, q, X0, Y0, K=100, tol=0.0, alpha=1.0, beta=1.0
     flags = lib().orc_adm_warm(m, n, row.size, _p(row), _p(col), _p(val), q, K, tol, alpha, beta, gamma, _p(X0), _p(Y0),
                                _p(U), _p(V), _p(it), _p(res), _p(sg))
     return dict(U=U, V=V, iters=int(it[0]), resid=float(res[0]), sigma=float(sg[0]), flags=flags)
+
+
+def build_light_tree(vpls, cut_max):
+    """light tree + global cut (R38) from VPL SoA arrays -> dict like scenegen's tree"""
+    v = {k: np.ascontiguousarray(vpls[k], np.float32) for k in ("px", "py", "pz", "ir", "ig", "ib")}
+    nv = v["px"].size
+    nn = 2 * nv - 1
+    left, right, rep = (np.zeros(nn, np.int32) for _ in range(3))
+    ir, ig, ib = (np.zeros(nn, np.float32) for _ in range(3))
+    cut = np.zeros(max(nn, 1), np.int32)
+    nc = np.zeros(1, np.int64)
+    st = lib().orc_build_light_tree(nv, *[_p(v[k]) for k in ("px", "py", "pz", "ir", "ig", "ib")], cut_max, _p(left),
+                                    _p(right), _p(rep), _p(ir), _p(ig), _p(ib), _p(cut), _p(nc))
+    assert st == 0
+    return dict(left=left, right=right, rep=rep, ir=ir, ig=ig, ib=ib, global_cut=cut[: int(nc[0])].copy(), root=0)

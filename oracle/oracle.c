@@ -1328,3 +1328,125 @@ void orc_bruteforce_rows(const orc_inputs *in, const int32_t *rows, int32_t nrow
         out[3 * i + 2] = acc[2];
     }
 }
+
+/* ------------------------------------------------------------------------------------------
+ * Light tree and conservative global lightcut (step 1, reading R38).
+ * Binary tree by median split: a node's VPLs split on the axis of largest bounding-box extent
+ * (first maximum), ordered by (coordinate, VPL index), the left child taking ceil(n/2); node ids
+ * breadth-first (children of a level's internal nodes in level order, left then right).  I_f =
+ * I_l + I_r (fp64), rep(f) = rep of the brighter child (lum, ties: left).  Global cut: the
+ * internal nodes with the largest bounds lum(I_f) * |bbox diagonal| (ties: smaller id) are split
+ * while the cut has fewer than cut_max nodes -- a lightcut-style greedy refinement, which with
+ * bounds non-increasing down the tree is the same as a threshold on the bound (split test per node).
+ * ---------------------------------------------------------------------------------------- */
+static const float *lt_pos[3];
+static int lt_axis;
+static int cmp_vpl_axis(const void *a, const void *b)
+{
+    int32_t i = *(const int32_t *)a, j = *(const int32_t *)b;
+    double ki = lt_pos[lt_axis][i], kj = lt_pos[lt_axis][j];
+    if (ki < kj) return -1;
+    if (ki > kj) return 1;
+    return (i > j) - (i < j);
+}
+
+int32_t orc_build_light_tree(int64_t nv, const float *px, const float *py, const float *pz, const float *ir,
+                             const float *ig, const float *ib, int32_t cut_max, int32_t *left, int32_t *right,
+                             int32_t *rep, float *tir, float *tig, float *tib, int32_t *cut, int64_t *ncut)
+{
+    if (nv < 1 || cut_max < 1) return -1;
+    int64_t nn = 2 * nv - 1;
+    int32_t *idx = malloc((size_t)nv * sizeof(int32_t));
+    for (int64_t k = 0; k < nv; ++k) idx[k] = (int32_t)k;
+    int32_t *segn = malloc((size_t)nn * sizeof(int32_t)), *segs = malloc((size_t)nn * sizeof(int32_t)),
+            *segl = malloc((size_t)nn * sizeof(int32_t)), *level_of = malloc((size_t)nn * sizeof(int32_t));
+    double *blo = malloc((size_t)nn * 3 * sizeof(double)), *bhi = malloc((size_t)nn * 3 * sizeof(double));
+    double *I = calloc((size_t)nn * 3, sizeof(double));
+    for (int64_t f = 0; f < nn; ++f) { left[f] = -1; right[f] = -1; rep[f] = -1; }
+    const float *pos[3] = {px, py, pz};
+    /* level by level: segments (node, start, len) in breadth-first order */
+    int64_t q0 = 0, q1 = 1, next_id = 1;
+    segn[0] = 0; segs[0] = 0; segl[0] = (int32_t)nv; level_of[0] = 0;
+    int32_t depth = 0;
+    while (q0 < q1) {
+        int64_t qe = q1;
+        for (int64_t k = q0; k < qe; ++k) {
+            int32_t f = segn[k], s = segs[k], n = segl[k];
+            for (int a = 0; a < 3; ++a) { blo[3 * f + a] = INFINITY; bhi[3 * f + a] = -INFINITY; }
+            for (int32_t t = s; t < s + n; ++t)
+                for (int a = 0; a < 3; ++a) {
+                    double v = pos[a][idx[t]];
+                    if (v < blo[3 * f + a]) blo[3 * f + a] = v;
+                    if (v > bhi[3 * f + a]) bhi[3 * f + a] = v;
+                }
+            if (n == 1) { rep[f] = idx[s]; continue; }
+            int ax = 0;
+            double best = bhi[3 * f] - blo[3 * f];
+            for (int a = 1; a < 3; ++a)
+                if (bhi[3 * f + a] - blo[3 * f + a] > best) { best = bhi[3 * f + a] - blo[3 * f + a]; ax = a; }
+            lt_pos[0] = px; lt_pos[1] = py; lt_pos[2] = pz; lt_axis = ax;
+            qsort(idx + s, (size_t)n, sizeof(int32_t), cmp_vpl_axis);
+        }
+        for (int64_t k = q0; k < qe; ++k) {   /* children ids in level order */
+            int32_t f = segn[k], s = segs[k], n = segl[k];
+            if (n == 1) continue;
+            int32_t nl = (n + 1) / 2;
+            left[f] = (int32_t)next_id;
+            right[f] = (int32_t)(next_id + 1);
+            segn[q1] = left[f]; segs[q1] = s; segl[q1] = nl; level_of[q1] = depth + 1; q1++;
+            segn[q1] = right[f]; segs[q1] = s + nl; segl[q1] = n - nl; level_of[q1] = depth + 1; q1++;
+            next_id += 2;
+        }
+        q0 = qe;
+        depth++;
+    }
+    /* intensities and representatives bottom-up (reverse breadth-first order) */
+    for (int64_t k = q1 - 1; k >= 0; --k) {
+        int32_t f = segn[k];
+        if (left[f] < 0) {
+            int32_t v = rep[f];
+            I[3 * f] = ir[v]; I[3 * f + 1] = ig[v]; I[3 * f + 2] = ib[v];
+        } else {
+            int32_t l = left[f], r = right[f];
+            for (int c = 0; c < 3; ++c) I[3 * f + c] = I[3 * l + c] + I[3 * r + c];
+            double ll = (0.2126 * I[3 * l] + 0.7152 * I[3 * l + 1]) + 0.0722 * I[3 * l + 2];
+            double lr = (0.2126 * I[3 * r] + 0.7152 * I[3 * r + 1]) + 0.0722 * I[3 * r + 2];
+            rep[f] = ll >= lr ? rep[l] : rep[r];
+        }
+    }
+    for (int64_t f = 0; f < nn; ++f) { tir[f] = (float)I[3 * f]; tig[f] = (float)I[3 * f + 1]; tib[f] = (float)I[3 * f + 2]; }
+    /* global cut: split the internal nodes by (bound desc, id asc) while the cut is short of cut_max */
+    int64_t nint = 0;
+    int32_t *ord = malloc((size_t)nn * sizeof(int32_t));
+    double *bnd = malloc((size_t)nn * sizeof(double));
+    for (int64_t f = 0; f < nn; ++f) {
+        double dx = bhi[3 * f] - blo[3 * f], dy = bhi[3 * f + 1] - blo[3 * f + 1], dz = bhi[3 * f + 2] - blo[3 * f + 2];
+        double lf = (0.2126 * I[3 * f] + 0.7152 * I[3 * f + 1]) + 0.0722 * I[3 * f + 2];
+        bnd[f] = lf * sqrt((dx * dx + dy * dy) + dz * dz);
+        if (left[f] >= 0) ord[nint++] = (int32_t)f;
+    }
+    /* insertion into order by (bound desc, id asc): plain selection of the next largest, nsplit times */
+    int64_t nsplit = cut_max - 1 < nint ? cut_max - 1 : nint;
+    uint8_t *split = calloc((size_t)nn, 1);
+    for (int64_t k = 0; k < nsplit; ++k) {
+        int64_t bk = k;
+        for (int64_t t = k + 1; t < nint; ++t)
+            if (bnd[ord[t]] > bnd[ord[bk]] || (bnd[ord[t]] == bnd[ord[bk]] && ord[t] < ord[bk])) bk = t;
+        int32_t tmp = ord[k]; ord[k] = ord[bk]; ord[bk] = tmp;
+        split[ord[k]] = 1;
+    }
+    int64_t nc = 0;
+    for (int64_t f = 0; f < nn; ++f) {
+        if (split[f]) continue;
+        /* parent split (or the root itself) */
+        int is_child_of_split = (f == 0);
+        if (!is_child_of_split)
+            for (int64_t k = 0; k < nsplit && !is_child_of_split; ++k)
+                is_child_of_split = left[ord[k]] == f || right[ord[k]] == f;
+        if (is_child_of_split) cut[nc++] = (int32_t)f;
+    }
+    *ncut = nc;
+    free(idx); free(segn); free(segs); free(segl); free(level_of); free(blo); free(bhi); free(I);
+    free(ord); free(bnd); free(split);
+    return 0;
+}

@@ -148,6 +148,12 @@ void orc_fullcut_slice(const orc_inputs *in, const int32_t *rows, int32_t m, con
 /* brute force over all VPLs for the given rows, out nrows*3 */
 void orc_bruteforce_rows(const orc_inputs *in, const int32_t *rows, int32_t nrows, double *out);
 
+/* Light tree + conservative global lightcut (reading R38): arrays of 2 nv - 1
+ * nodes, cut (<= cut_max nodes, ascending id); returns 0 */
+int32_t orc_build_light_tree(int64_t nv, const float *px, const float *py, const float *pz, const float *ir,
+                             const float *ig, const float *ib, int32_t cut_max, int32_t *left, int32_t *right,
+                             int32_t *rep, float *tir, float *tig, float *tib, int32_t *cut, int64_t *ncut);
+
 #ifdef __cplusplus
 }
 #endif

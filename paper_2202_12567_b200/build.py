@@ -1,6 +1,7 @@
 """Build liblmc.so (the C-ABI library) in-tree for sm_100a with nvcc.
 
-exact.cu is compiled with -fmad=false (decision precision: no FMA contraction, R30);
+exact.cu and lighttree.cu are compiled with -fmad=false (decision precision: no FMA contraction,
+DESIGN.md R30);
 complete.cu and lmc_api.cu with the default contraction.
 """
 import os
@@ -15,7 +16,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC,-ffp-contract=off",
           "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-Xptxas", "-v"]
-UNITS = [("exact.cu", ["-fmad=false"]), ("complete.cu", []), ("complete2.cu", []), ("mals.cu", []), ("lmc_api.cu", [])]
+UNITS = [("exact.cu", ["-fmad=false"]), ("complete.cu", []), ("complete2.cu", []), ("mals.cu", []), ("lighttree.cu", ["-fmad=false"]), ("lmc_api.cu", [])]
 
 
 def _stale(obj, deps):

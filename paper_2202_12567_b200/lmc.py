@@ -71,7 +71,8 @@ EXPORTS = ["lmc_create", "lmc_upload_inputs", "lmc_build_slices", "lmc_sample_pa
            "lmc_sample_pass2", "lmc_complete", "lmc_resolve_image", "lmc_resolve_rows", "lmc_scatter_rows",
            "lmc_destroy", "lmc_last_error", "lmc_status_str", "lmc_get_slices", "lmc_get_pass1", "lmc_get_coarsen",
            "lmc_get_cut", "lmc_get_samples", "lmc_get_factors", "lmc_get_stats", "lmc_set_timing",
-           "lmc_eval_entries", "lmc_nccl_unique_id", "lmc_get_partition", "lmc_plan_partition", "lmc_sizeof_struct"]
+           "lmc_eval_entries", "lmc_nccl_unique_id", "lmc_get_partition", "lmc_plan_partition", "lmc_sizeof_struct",
+           "lmc_build_light_tree"]
 
 
 def _load():
@@ -91,6 +92,7 @@ def _load():
     L.lmc_scatter_rows.argtypes = [_P, _P, C.c_int64, _P]
     L.lmc_nccl_unique_id.argtypes = [_P]
     L.lmc_get_partition.argtypes = [_P, _P, _P]
+    L.lmc_build_light_tree.argtypes = [C.POINTER(Vpls), C.c_int32, C.c_int32, _P, _P, _P, _P, _P, _P, _P, _P, _P]
     L.lmc_sizeof_struct.argtypes = [C.c_int32]
     L.lmc_sizeof_struct.restype = C.c_int64
     L.lmc_plan_partition.argtypes = [C.c_int64, C.c_int32, C.c_int32, _P, _P, _P]
@@ -365,3 +367,27 @@ def plan_partition(rows: int, slice_target: int, world: int):
     if st != LMC_OK:
         raise LmcError(f"lmc_plan_partition: {lib.lmc_status_str(st).decode()}")
     return s, r, int(n[0])
+
+
+def build_light_tree(vpls, cut_max: int, device="cuda"):
+    """Step 1 on the GPU (lmc_build_light_tree): light tree + global cut of the VPL SoA arrays, returned
+    as numpy arrays (dict like scenegen's tree)"""
+    import torch
+    t = {k: torch.from_numpy(np.ascontiguousarray(vpls[k], np.float32)).to(device)
+         for k in ("px", "py", "pz", "nx", "ny", "nz", "ir", "ig", "ib")}
+    nv = t["px"].numel()
+    nn = 2 * nv - 1
+    out = {k: torch.zeros(nn, dtype=torch.int32, device=device) for k in ("left", "right", "rep")}
+    out.update({k: torch.zeros(nn, dtype=torch.float32, device=device) for k in ("ir", "ig", "ib")})
+    cut = torch.zeros(max(cut_max, 1), dtype=torch.int32, device=device)
+    v = Vpls(nv, *[_P(t[k].data_ptr()) for k in ("px", "py", "pz", "nx", "ny", "nz", "ir", "ig", "ib")])
+    n = np.zeros(1, np.int64)
+    st = lib.lmc_build_light_tree(C.byref(v), cut_max, MEM_DEVICE, _P(torch.cuda.current_stream().cuda_stream),
+                                  *[_P(out[k].data_ptr()) for k in ("left", "right", "rep", "ir", "ig", "ib")],
+                                  _P(cut.data_ptr()), _ptr(n))
+    if st != LMC_OK:
+        raise LmcError(f"lmc_build_light_tree: {lib.lmc_status_str(st).decode()}")
+    res = {k: a.cpu().numpy() for k, a in out.items()}
+    res["global_cut"] = cut[: int(n[0])].cpu().numpy()
+    res["root"] = 0
+    return res

@@ -337,3 +337,29 @@ def test_count_target_coarsening(name, over):
     if over["coarsen_target"] < 10 ** 6:
         assert any(r["n"] == over["coarsen_target"] for r in res)
     fr.close()
+
+
+# ------------------------------------------------------------------------------ SURVEY f2 step 1 on the GPU
+
+@pytest.mark.parametrize("name", ["c1", "t_interior", "t_cornell", "c2"])
+def test_light_tree_and_global_cut_bit_exact(name):
+    """lmc_build_light_tree (median-split tree, breadth-first ids, fp64 sums, greedy bound cut; R38)
+    equals the oracle's build node for node"""
+    x = scenegen.make_inputs(name)
+    got = lmc.build_light_tree(x.vpls, x.cfg.cut_max)
+    ref = oracle.build_light_tree(x.vpls, x.cfg.cut_max)
+    for k in ("left", "right", "rep", "ir", "ig", "ib", "global_cut"):
+        assert np.array_equal(got[k], ref[k]), k
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["c3", "c4"])
+def test_light_tree_full_size(name):
+    x = scenegen.make_inputs(name)
+    got = lmc.build_light_tree(x.vpls, x.cfg.cut_max)
+    ref = oracle.build_light_tree(x.vpls, x.cfg.cut_max)
+    for k in ("left", "right", "rep", "ir", "ig", "ib", "global_cut"):
+        assert np.array_equal(got[k], ref[k]), k
+    # the frame runs on the GPU-built tree exactly as on the fixture's
+    for k in ("left", "right", "rep", "global_cut"):
+        assert np.array_equal(got[k], x.tree[k]), k

@@ -247,3 +247,36 @@ def test_pass2_importance_follows_weights():
         rho, _ = stats.spearmanr(r["weights"], newcnt)
         rhos.append(rho)
     assert np.mean(rhos) > 0.3
+
+
+# ---------------------------------------------------------------------------------------- step 1
+
+@pytest.mark.parametrize("name", ["c1", "t_cornell", "t_interior", "c2"])
+def test_light_tree_oracle_equals_the_fixture(inputs_cache, name):
+    """the oracle's light tree + global cut (R38) is the scene generator's tree, built by an
+    independent numpy implementation (level-synchronous lexsort, heap-driven greedy cut)"""
+    x = inputs_cache(name)
+    t = oracle.build_light_tree(x.vpls, x.cfg.cut_max)
+    for k in ("left", "right", "rep", "ir", "ig", "ib", "global_cut"):
+        assert np.array_equal(t[k], x.tree[k]), k
+
+
+def test_light_tree_invariants():
+    rng = np.random.default_rng(21)
+    nv = 777
+    v = {k: rng.uniform(0, 1, nv).astype(np.float32) for k in ("px", "py", "pz", "ir", "ig", "ib")}
+    v["px"][::7] = v["px"][3]                      # coordinate ties (broken by VPL index)
+    for cut_max in (1, 2, 50, 776, 777, 5000):
+        t = oracle.build_light_tree(v, cut_max)
+        left, right = t["left"], t["right"]
+        nn = 2 * nv - 1
+        assert left.size == nn and np.sum(left < 0) == nv
+        for f in np.flatnonzero(left >= 0):
+            l, r = left[f], right[f]
+            assert t["rep"][f] in (t["rep"][l], t["rep"][r])
+            for k in ("ir", "ig", "ib"):
+                assert t[k][f] == np.float32(np.float64(t[k][l]) + np.float64(t[k][r])) or \
+                    abs(t[k][f] - (t[k][l] + t[k][r])) <= 1e-6 * t[k][f]
+        assert sorted(t["rep"][left < 0]) == list(range(nv))
+        assert _cover_check(t, t["global_cut"])
+        assert t["global_cut"].size == min(cut_max, nv)
