@@ -30,6 +30,17 @@ __device__ __forceinline__ uint32_t ord_f(float v)
 }
 __device__ __forceinline__ float unord_f(uint32_t u) { return __uint_as_float((u & 0x80000000u) ? (u & 0x7fffffffu) : ~u); }
 
+// internal segment of the level holding position `pos` (segments sorted by start), or -1 (a leaf)
+__device__ __forceinline__ int seg_of(const int32_t *__restrict__ seg, int nseg, int64_t pos)
+{
+    int lo = 0, hi = nseg - 1;
+    while (lo < hi) {   // last segment with start <= pos
+        const int mid = (lo + hi + 1) >> 1;
+        if (seg[3 * mid + 1] <= pos) lo = mid; else hi = mid - 1;
+    }
+    return pos < (int64_t)seg[3 * lo + 1] + seg[3 * lo + 2] && pos >= seg[3 * lo + 1] ? lo : -1;
+}
+
 // bounding boxes of the level's segments: a CTA per (segment, chunk) work item, block min/max, one
 // atomic per chunk on the ordered encodings
 __global__ void __launch_bounds__(256) k_lt_bbox(const int32_t *__restrict__ work, const int32_t *__restrict__ idx,
@@ -73,12 +84,12 @@ __global__ void k_lt_bbox_init(int64_t n, uint32_t *bb)
 // sort keys of the level's internal segments: (coordinate on the longest axis, VPL index)
 __global__ void k_lt_keys(const int32_t *__restrict__ seg /* [s][3] node, start, len */, int nseg,
                           const int32_t *__restrict__ idx, const float *__restrict__ px, const float *__restrict__ py,
-                          const float *__restrict__ pz, const uint32_t *__restrict__ bb, const int32_t *__restrict__ pos_seg,
-                          int64_t base, int64_t n, unsigned long long *keys)
+                          const float *__restrict__ pz, const uint32_t *__restrict__ bb, int64_t base, int64_t n,
+                          unsigned long long *keys)
 {
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
-    const int s = pos_seg[k];
+    const int s = seg_of(seg, nseg, base + k);
     if (s < 0) return;   // a leaf of this level between two sorted segments
     const int node = seg[3 * s];
     double best = -1.0;
@@ -93,11 +104,11 @@ __global__ void k_lt_keys(const int32_t *__restrict__ seg /* [s][3] node, start,
     keys[k] = ((unsigned long long)ord_f(c) << 32) | (uint32_t)v;
 }
 
-__global__ void k_lt_unkey(const unsigned long long *__restrict__ keys, const int32_t *__restrict__ pos_seg, int64_t n,
-                           int32_t *idx_out)
+__global__ void k_lt_unkey(const unsigned long long *__restrict__ keys, const int32_t *__restrict__ seg, int nseg,
+                           int64_t base, int64_t n, int32_t *idx_out)
 {
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k < n && pos_seg[k] >= 0) idx_out[k] = (int32_t)(uint32_t)keys[k];
+    if (k < n && seg_of(seg, nseg, base + k) >= 0) idx_out[k] = (int32_t)(uint32_t)keys[k];
 }
 
 // bottom-up intensities / representatives of one level's nodes
@@ -212,7 +223,7 @@ extern "C" lmc_status lmc_build_light_tree(const lmc_vpls *v, int32_t cut_max, i
     // per level: internal segments (sort ranges) and bbox work chunks
     struct LvlDev { int64_t base, n; int nint; size_t seg_off, work_off; int nwork; };
     std::vector<LvlDev> lv;
-    std::vector<int32_t> iseg, work, beg, end, pos_seg_all;
+    std::vector<int32_t> iseg, work;
     std::vector<int64_t> pos_off;
     for (auto &L : levels) {
         LvlDev d;
@@ -235,23 +246,10 @@ extern "C" lmc_status lmc_build_light_tree(const lmc_vpls *v, int32_t cut_max, i
         d.n = lo < 0 ? 0 : hi - lo;
         lv.push_back(d);
     }
-    // position -> internal segment of the level over the span [base, base + n) of its internal
-    // segments (-1 on the leaves that sit between them)
-    std::vector<int32_t> pos_seg;
-    std::vector<size_t> pos_seg_off;
-    for (auto &d : lv) {
-        pos_seg_off.push_back(pos_seg.size());
-        const size_t o = pos_seg.size();
-        pos_seg.resize(o + (size_t)d.n, -1);
-        for (int k = 0; k < d.nint; ++k) {
-            const int32_t st0 = iseg[3 * (d.seg_off + k) + 1], n = iseg[3 * (d.seg_off + k) + 2];
-            for (int32_t t = 0; t < n; ++t) pos_seg[o + (size_t)(st0 - d.base) + t] = k;
-        }
-    }
     // ---- device buffers
     lmc_status ret = LMC_OK;
     cudaError_t e = cudaSuccess;
-    int32_t *d_idx = nullptr, *d_idx2 = nullptr, *d_iseg = nullptr, *d_work = nullptr, *d_pos = nullptr, *d_beg = nullptr,
+    int32_t *d_idx = nullptr, *d_idx2 = nullptr, *d_iseg = nullptr, *d_work = nullptr, *d_beg = nullptr,
             *d_end = nullptr, *d_left = nullptr, *d_right = nullptr, *d_parent = nullptr, *d_leaf = nullptr,
             *d_nodes = nullptr, *d_rep = nullptr, *d_id = nullptr, *d_id2 = nullptr, *d_flag = nullptr, *d_pre = nullptr,
             *d_cut = nullptr;
@@ -268,7 +266,6 @@ extern "C" lmc_status lmc_build_light_tree(const lmc_vpls *v, int32_t cut_max, i
     ck(dmal(&d_idx2, nv));
     ck(dmal(&d_iseg, iseg.size()));
     ck(dmal(&d_work, work.size()));
-    ck(dmal(&d_pos, pos_seg.size()));
     ck(dmal(&d_left, nn));
     ck(dmal(&d_right, nn));
     ck(dmal(&d_parent, nn));
@@ -303,7 +300,6 @@ extern "C" lmc_status lmc_build_light_tree(const lmc_vpls *v, int32_t cut_max, i
         ck(cudaMemcpyAsync(d_idx, iota.data(), nv * 4, cudaMemcpyHostToDevice, st));
         ck(cudaMemcpyAsync(d_iseg, iseg.data(), iseg.size() * 4, cudaMemcpyHostToDevice, st));
         ck(cudaMemcpyAsync(d_work, work.data(), work.size() * 4, cudaMemcpyHostToDevice, st));
-        ck(cudaMemcpyAsync(d_pos, pos_seg.data(), pos_seg.size() * 4, cudaMemcpyHostToDevice, st));
         ck(cudaMemcpyAsync(d_left, left.data(), nn * 4, cudaMemcpyHostToDevice, st));
         ck(cudaMemcpyAsync(d_right, right.data(), nn * 4, cudaMemcpyHostToDevice, st));
         ck(cudaMemcpyAsync(d_parent, parent.data(), nn * 4, cudaMemcpyHostToDevice, st));
@@ -337,11 +333,11 @@ extern "C" lmc_status lmc_build_light_tree(const lmc_vpls *v, int32_t cut_max, i
             if (d.nint == 0) continue;
             const unsigned nb = (unsigned)((d.n + 255) / 256);
             k_lt_keys<<<nb, 256, 0, st>>>(d_iseg + 3 * d.seg_off, d.nint, d_idx, d_pos3[0], d_pos3[1], d_pos3[2], d_bb,
-                                          d_pos + pos_seg_off[li], d.base, d.n, d_key);
+                                          d.base, d.n, d_key);
             size_t bytes = tmp_bytes;
             ck(cub::DeviceSegmentedSort::SortKeys(d_tmp, bytes, d_key, d_key2, (int)d.n, d.nint, d_beg + boff,
                                                   d_end + boff, st));
-            k_lt_unkey<<<nb, 256, 0, st>>>(d_key2, d_pos + pos_seg_off[li], d.n, d_idx + d.base);
+            k_lt_unkey<<<nb, 256, 0, st>>>(d_key2, d_iseg + 3 * d.seg_off, d.nint, d.base, d.n, d_idx + d.base);
             boff += d.nint;
             ck(cudaGetLastError());
         }
@@ -381,7 +377,7 @@ extern "C" lmc_status lmc_build_light_tree(const lmc_vpls *v, int32_t cut_max, i
     }
     if (e == cudaErrorMemoryAllocation) ret = LMC_ENOMEM;
     else if (e != cudaSuccess) ret = LMC_ECUDA;
-    void *all[] = {d_idx, d_idx2, d_iseg, d_work, d_pos, d_beg, d_end, d_left, d_right, d_parent, d_leaf, d_nodes, d_rep,
+    void *all[] = {d_idx, d_idx2, d_iseg, d_work, d_beg, d_end, d_left, d_right, d_parent, d_leaf, d_nodes, d_rep,
                    d_id, d_id2, d_flag, d_pre, d_cut, d_bb, d_I, d_key, d_key2, d_split, d_tmp,
                    d_pos3[0], d_pos3[1], d_pos3[2], d_I3[0], d_I3[1], d_I3[2], d_io[0], d_io[1], d_io[2]};
     for (void *p : all)
