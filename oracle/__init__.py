@@ -56,6 +56,7 @@ class _Inputs(C.Structure):
         ("order_seed", C.c_uint64),
         ("row_importance", C.c_int32), ("cost_mode", C.c_int32), ("resolve_mode", C.c_int32),
         ("warm_iters", C.c_int32), ("nwarm", C.c_int32), ("coarsen_target", C.c_int32), ("warm", C.c_void_p),
+        ("ntri", C.c_int64), ("tri", C.c_void_p),
     ]
 
 
@@ -179,6 +180,9 @@ class Oracle:
         s.sph = arr(pr["sph"], np.float32)
         s.box = arr(pr["box"], np.float32)
         s.rect = arr(pr["rect"], np.float32)
+        tri = pr.get("tri", np.zeros((0, 9), np.float32))
+        s.ntri = tri.shape[0]
+        s.tri = arr(tri, np.float32)
         s.clamp_dist, s.shadow_eps, s.diag = x.clamp_dist, x.shadow_eps, x.diag
         s.wn = prm["normal_weight"]
         s.target = prm["slice_target"]

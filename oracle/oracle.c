@@ -148,6 +148,45 @@ static int seg_hits_rect(const float *rc, const double x[3], const double l[3], 
     return a >= 0.0 && a <= 1.0 && b >= 0.0 && b <= 1.0;
 }
 
+/* Segment vs triangle (v0, v1, v2) — SURVEY §8(f1), reading R39: the Moller-Trumbore test
+ * (Moller & Trumbore 1997) in this exact operation order, written out once here and once in the
+ * CUDA path.  e1 = v1 - v0, e2 = v2 - v0, p = l x e2, det = e1 . p (0: parallel, miss),
+ * s = x - v0, u = (s . p) / det in [0, 1], qv = s x e1, v = (l . qv) / det >= 0, u + v <= 1,
+ * t = (e2 . qv) / det in (tmin, tmax).  Each "/ det" is a multiplication by inv = 1 / det. */
+static void cross3(const double a[3], const double b[3], double c[3])
+{
+    c[0] = a[1] * b[2] - a[2] * b[1];
+    c[1] = a[2] * b[0] - a[0] * b[2];
+    c[2] = a[0] * b[1] - a[1] * b[0];
+    FL(9);
+}
+
+static int seg_hits_tri(const float *tr, const double x[3], const double l[3], double tmin, double tmax)
+{
+    double v0[3] = {tr[0], tr[1], tr[2]};
+    double e1[3] = {(double)tr[3] - v0[0], (double)tr[4] - v0[1], (double)tr[5] - v0[2]};
+    double e2[3] = {(double)tr[6] - v0[0], (double)tr[7] - v0[1], (double)tr[8] - v0[2]};
+    FL(6);
+    double p[3];
+    cross3(l, e2, p);
+    double det = dot3(e1, p);
+    if (det == 0.0) return 0;
+    double inv = 1.0 / det;
+    double sv[3] = {x[0] - v0[0], x[1] - v0[1], x[2] - v0[2]};
+    FL(4);
+    double u = dot3(sv, p) * inv;
+    FL(1);
+    if (u < 0.0 || u > 1.0) return 0;
+    double qv[3];
+    cross3(sv, e1, qv);
+    double v = dot3(l, qv) * inv;
+    FL(2);
+    if (v < 0.0 || u + v > 1.0) return 0;
+    double t = dot3(e2, qv) * inv;
+    FL(1);
+    return t > tmin && t < tmax;
+}
+
 /* V(x, y): 1 iff no occluder is hit with t in (eps, dist - eps) along the segment. */
 static int visible_dir(const orc_inputs *in, const double x[3], const double l[3], double dist)
 {
@@ -159,6 +198,8 @@ static int visible_dir(const orc_inputs *in, const double x[3], const double l[3
         if (seg_hits_box(in->box + 6 * k, x, l, tmin, tmax)) return 0;
     for (int k = 0; k < in->nrect; ++k)
         if (seg_hits_rect(in->rect + 12 * k, x, l, tmin, tmax)) return 0;
+    for (int64_t k = 0; k < in->ntri; ++k)   /* brute force: every triangle (no BVH) */
+        if (seg_hits_tri(in->tri + 9 * k, x, l, tmin, tmax)) return 0;
     return 1;
 }
 

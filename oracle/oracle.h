@@ -65,6 +65,9 @@ typedef struct {
      * until the cut has this many nodes (tau unused); 0 = the threshold rule */
     int32_t coarsen_target;
     const orc_warm *warm;
+    /* SURVEY §8(f1) triangle occluders, tri[9*k] = (v0, v1, v2), tested by brute force (R39) */
+    int64_t ntri;
+    const float *tri;
 } orc_inputs;
 
 enum { ORC_FLAG_DIRECT = 1, ORC_FLAG_DIVERGED = 2, ORC_FLAG_ZERO = 4 };

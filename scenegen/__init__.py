@@ -34,7 +34,7 @@ __all__ = ["Config", "PRESETS", "Inputs", "make_inputs", "preset"]
 @dataclasses.dataclass
 class Config:
     name: str
-    scene: str            # "cornell" | "interior"
+    scene: str            # "cornell" | "interior" | "mesh" (interior + triangle meshes)
     width: int
     height: int
     n_vpls: int
@@ -65,6 +65,8 @@ class Config:
     warm_iters: int = 0
     # count-target coarsening, 0 = threshold rule
     coarsen_target: int = 0
+    # tessellation level of the triangle meshes of the "mesh" scene
+    mesh_level: int = 0
 
 
 PRESETS = {
@@ -75,6 +77,9 @@ PRESETS = {
     # small variants used by parity tests (a few slices, ragged sizes)
     "t_cornell": Config("t_cornell", "cornell", 40, 37, 2048, 128, 200, 8, 0.10, 1.0e-4),
     "t_interior": Config("t_interior", "interior", 48, 40, 4096, 256, 256, 8, 0.15, 1.0e-3),
+    # the interior plus three triangle meshes (416 / 6656 triangles)
+    "t_mesh": Config("t_mesh", "mesh", 48, 40, 4096, 256, 256, 8, 0.15, 1.0e-3, mesh_level=1),
+    "c_mesh": Config("c_mesh", "mesh", 512, 512, 100_000, 1024, 800, 16, 0.10, 3.0e-6, mesh_level=3),
 }
 
 
@@ -110,6 +115,8 @@ class Scene:
     cam_pos: np.ndarray
     cam_look: np.ndarray
     vfov_deg: float
+    tris: np.ndarray = dataclasses.field(default_factory=lambda: np.zeros((0, 9)))  # (nt, 9) v0, v1, v2
+    tri_mat: np.ndarray = dataclasses.field(default_factory=lambda: np.zeros(0, np.int64))
 
     @property
     def diag(self) -> float:
@@ -215,6 +222,82 @@ def _interior(seed: int = 3) -> Scene:
                  cam_pos=cam, cam_look=np.array([2.0, 1.25, 6.0]), vfov_deg=62.0)
 
 
+def _icosphere(level: int):
+    """Unit icosphere: the icosahedron with every face split in 4, `level` times (20 * 4^level faces)."""
+    t = (1.0 + math.sqrt(5.0)) / 2.0
+    V = [[-1, t, 0], [1, t, 0], [-1, -t, 0], [1, -t, 0], [0, -1, t], [0, 1, t], [0, -1, -t], [0, 1, -t],
+         [t, 0, -1], [t, 0, 1], [-t, 0, -1], [-t, 0, 1]]
+    V = [list(np.array(v, np.float64) / math.sqrt(1.0 + t * t)) for v in V]
+    F = [[0, 11, 5], [0, 5, 1], [0, 1, 7], [0, 7, 10], [0, 10, 11], [1, 5, 9], [5, 11, 4], [11, 10, 2],
+         [10, 7, 6], [7, 1, 8], [3, 9, 4], [3, 4, 2], [3, 2, 6], [3, 6, 8], [3, 8, 9], [4, 9, 5], [2, 4, 11],
+         [6, 2, 10], [8, 6, 7], [9, 8, 1]]
+    for _ in range(level):
+        mid = {}
+
+        def m(a, b):
+            k = (min(a, b), max(a, b))
+            if k not in mid:
+                p = np.array(V[a]) + np.array(V[b])
+                V.append(list(p / np.linalg.norm(p)))
+                mid[k] = len(V) - 1
+            return mid[k]
+
+        F2 = []
+        for a, b, c in F:
+            ab, bc, ca = m(a, b), m(b, c), m(c, a)
+            F2 += [[a, ab, ca], [b, bc, ab], [c, ca, bc], [ab, bc, ca]]
+        F = F2
+    V = np.array(V)
+    F = np.array(F)
+    return np.concatenate([V[F[:, 0]], V[F[:, 1]], V[F[:, 2]]], 1)
+
+
+def _torus(R: float, r: float, nu: int, nv: int):
+    """Torus around the y axis, nu x nv quads, each split in two triangles."""
+    u = np.arange(nu) * (2.0 * math.pi / nu)
+    v = np.arange(nv) * (2.0 * math.pi / nv)
+
+    def P(i, j):
+        a, b = u[i % nu], v[j % nv]
+        return np.array([(R + r * math.cos(b)) * math.cos(a), r * math.sin(b), (R + r * math.cos(b)) * math.sin(a)])
+
+    T = []
+    for i in range(nu):
+        for j in range(nv):
+            p00, p10, p01, p11 = P(i, j), P(i + 1, j), P(i, j + 1), P(i + 1, j + 1)
+            T.append(np.r_[p00, p10, p11])
+            T.append(np.r_[p00, p11, p01])
+    return np.array(T)
+
+
+def _mesh_scene(level: int) -> Scene:
+    """The interior with three triangle meshes (DESIGN.md input recipe): an
+    icosphere, a tilted torus and a bumpy icosphere (radius modulated by a smooth function of the
+    vertex direction), 416 triangles at level 1, 6656 at level 3."""
+    sc = _interior()
+    tris, mats = [], []
+    ico = _icosphere(level) * 0.42 + np.tile([1.0, 0.55, 3.2], 3)
+    tris.append(ico)
+    mats.append(np.full(ico.shape[0], 5 + 1))
+    tor = _torus(0.42, 0.14, 8 << level, 4 << level)
+    ca, sa = math.cos(0.6), math.sin(0.6)
+    rot = np.array([[1.0, 0.0, 0.0], [0.0, ca, -sa], [0.0, sa, ca]])
+    tor = np.concatenate([tor[:, 3 * k:3 * k + 3] @ rot.T + np.array([2.9, 1.3, 3.9]) for k in range(3)], 1)
+    tris.append(tor)
+    mats.append(np.full(tor.shape[0], 5 + 7))
+    bump = _icosphere(level)
+    for k in range(3):
+        d = bump[:, 3 * k:3 * k + 3]
+        rad = 0.34 * (1.0 + 0.15 * np.sin(5.0 * d[:, 0]) * np.cos(4.0 * d[:, 1] + 3.0 * d[:, 2]))
+        bump[:, 3 * k:3 * k + 3] = d * rad[:, None] + np.array([2.1, 1.9, 4.9])
+    tris.append(bump)
+    mats.append(np.full(bump.shape[0], 5 + 3))
+    # the arrays handed to both sides are float32: cast the vertices so the fixture rays see them too
+    sc.tris = np.concatenate(tris).astype(np.float32).astype(np.float64)
+    sc.tri_mat = np.concatenate(mats).astype(np.int64)
+    return sc
+
+
 # ----------------------------------------------------------------------------------------
 # Closest-hit ray casting (fixture-only: camera rays and light paths; never a shadow test)
 # ----------------------------------------------------------------------------------------
@@ -296,9 +379,57 @@ def _closest_hit(sc: Scene, O: np.ndarray, D: np.ndarray, tmin: float):
             nn = nr / np.linalg.norm(nr)
             nrm = np.where((den < 0)[:, None], nn[None, :], -nn[None, :])
             take(t, nrm, sc.rect_mat[k])
+        if sc.tris.shape[0]:
+            _hit_tris(sc, O, D, tmin, take)
     nl = np.linalg.norm(best_n, axis=1, keepdims=True)
     best_n = best_n / np.where(nl > 0, nl, 1.0)
     return best_t, best_n, best_m
+
+
+def _hit_tris(sc: Scene, O, D, tmin, take):
+    """Closest triangle hits (Moller-Trumbore) by clusters of 64 consecutive triangles (spatially
+    coherent by construction): rays that miss a cluster's bounding sphere skip it."""
+    T = sc.tris
+    nt = T.shape[0]
+    n = O.shape[0]
+    for c0 in range(0, nt, 64):
+        Tm = T[c0:c0 + 64]
+        mat = sc.tri_mat[c0:c0 + 64]
+        V = Tm.reshape(-1, 3)
+        c = V.mean(0)
+        rad = np.sqrt(((V - c) ** 2).sum(1).max()) * 1.001
+        oc = O - c
+        b = np.einsum("ij,ij->i", oc, D)
+        cc = np.einsum("ij,ij->i", oc, oc) - rad * rad
+        idx = np.nonzero((b * b - cc >= 0) & (-b + np.sqrt(np.maximum(b * b - cc, 0.0)) > tmin))[0]
+        if idx.size == 0:
+            continue
+        v0, e1, e2 = Tm[:, 0:3], Tm[:, 3:6] - Tm[:, 0:3], Tm[:, 6:9] - Tm[:, 0:3]
+        fn = np.cross(e1, e2)
+        fn /= np.linalg.norm(fn, axis=1, keepdims=True)
+        o = O[idx][:, None, :]
+        d = D[idx][:, None, :]
+        p = np.cross(d, e2[None])
+        det = (e1[None] * p).sum(2)
+        inv = 1.0 / np.where(det == 0, 1.0, det)
+        sv = o - v0[None]
+        u = (sv * p).sum(2) * inv
+        qv = np.cross(sv, e1[None])
+        v = (d * qv).sum(2) * inv
+        t = (e2[None] * qv).sum(2) * inv
+        ok = (det != 0) & (u >= 0) & (u <= 1) & (v >= 0) & (u + v <= 1) & (t > tmin)
+        t = np.where(ok, t, np.inf)
+        j = np.argmin(t, 1)
+        tb = t[np.arange(idx.size), j]
+        nrm = fn[j]
+        nrm = np.where(((nrm * D[idx]).sum(1) > 0)[:, None], -nrm, nrm)
+        tt = np.full(n, np.inf)
+        tt[idx] = tb
+        nn = np.zeros((n, 3))
+        nn[idx] = nrm
+        mm = np.full(n, -1, np.int64)
+        mm[idx] = mat[j]
+        take(tt, nn, mm)
 
 
 def _cosine_dirs(nrm: np.ndarray, u1: np.ndarray, u2: np.ndarray) -> np.ndarray:
@@ -528,14 +659,15 @@ def make_inputs(cfg: Config | str) -> Inputs:
     if isinstance(cfg, str):
         cfg = preset(cfg)
     rng = np.random.default_rng(cfg.fixture_seed)
-    sc = _cornell() if cfg.scene == "cornell" else _interior()
+    sc = _cornell() if cfg.scene == "cornell" else _mesh_scene(cfg.mesh_level) if cfg.scene == "mesh" else _interior()
     g = _gbuffer(sc, cfg.width, cfg.height)
     v = _vpls(sc, cfg.n_vpls, rng)
     t = _light_tree(v, cfg.cut_max)
     f32 = np.float32
     prims = dict(sph=np.ascontiguousarray(sc.spheres, f32).reshape(-1, 4),
                  box=np.ascontiguousarray(sc.boxes, f32).reshape(-1, 6),
-                 rect=np.ascontiguousarray(sc.rects, f32).reshape(-1, 12))
+                 rect=np.ascontiguousarray(sc.rects, f32).reshape(-1, 12),
+                 tri=np.ascontiguousarray(sc.tris, f32).reshape(-1, 9))
     D = sc.diag
     return Inputs(cfg=cfg, scene=sc, width=cfg.width, height=cfg.height, gbuf=g, vpls=v, tree=t,
                   prims=prims, diag=D, clamp_dist=0.01 * D, shadow_eps=1e-4 * D, tau=cfg.tau)

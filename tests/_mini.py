@@ -7,7 +7,7 @@ import scenegen
 
 
 def mini(points, normals, vpl_pos, vpl_nrm, vpl_I, views=None, rho=None, spec=None, expo=None,
-         sph=(), box=(), rect=(), clamp_dist=1e-3, shadow_eps=1e-6, diag=1.0, tree=None, **cfg_over):
+         sph=(), box=(), rect=(), tri=(), clamp_dist=1e-3, shadow_eps=1e-6, diag=1.0, tree=None, **cfg_over):
     P = np.atleast_2d(np.asarray(points, np.float64))
     N = np.atleast_2d(np.asarray(normals, np.float64))
     m = P.shape[0]
@@ -30,7 +30,7 @@ def mini(points, normals, vpl_pos, vpl_nrm, vpl_I, views=None, rho=None, spec=No
     if tree is None:
         tree = scenegen._light_tree(v, LP.shape[0])   # cut = all leaves
     prims = dict(sph=np.asarray(sph, f32).reshape(-1, 4), box=np.asarray(box, f32).reshape(-1, 6),
-                 rect=np.asarray(rect, f32).reshape(-1, 12))
+                 rect=np.asarray(rect, f32).reshape(-1, 12), tri=np.asarray(tri, f32).reshape(-1, 9))
     cfg = dataclasses.replace(scenegen.PRESETS["c1"], width=m, height=1, n_vpls=LP.shape[0], **cfg_over)
     return scenegen.Inputs(cfg=cfg, scene=None, width=m, height=1, gbuf=g, vpls=v, tree=tree, prims=prims,
                            diag=diag, clamp_dist=clamp_dist, shadow_eps=shadow_eps, tau=cfg.tau)

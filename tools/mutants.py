@@ -14,7 +14,7 @@ import tempfile
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SRC = os.path.join(ROOT, "oracle", "oracle.c")
 TESTS = ["tests/test_oracle_pins.py", "tests/test_oracle_sampling.py", "tests/test_oracle_entry.py",
-         "tests/test_oracle_completion.py"]
+         "tests/test_oracle_completion.py", "tests/test_oracle_mesh.py"]
 
 MUTANTS = [
     ("g(j) = max instead of max - min (P:143)", "if (cnt[c]) g[c] = hi[c] - lo[c];", "if (cnt[c]) g[c] = hi[c];"),
@@ -27,6 +27,10 @@ MUTANTS = [
     ("unobserved column weight = floor (R14)", "if (!cnt[c]) w[c] = wu;", "if (!cnt[c]) w[c] = 65536u;"),
     ("Eq. (1) with cost(a) added (P:112)", "double cf = eps + cost[b];", "double cf = eps + cost[b] + cost[a];"),
     ("weight floor 2^12 instead of 2^16 (R14)", "w[c] = wc > 65536u ? wc : 65536u;", "w[c] = wc > 4096u ? wc : 4096u;"),
+    ("triangle: v + u bound dropped (R39)", "if (v < 0.0 || u + v > 1.0) return 0;", "if (v < 0.0 || v > 1.0) return 0;"),
+    ("triangle: tmin ignored (R39)", "return t > tmin && t < tmax;\n}", "return t < tmax;\n}"),
+    ("triangle: cross product sign (R39)", "c[1] = a[2] * b[0] - a[0] * b[2];", "c[1] = a[0] * b[2] - a[2] * b[0];"),
+    ("triangle: e2 taken from v1 (R39)", "double e2[3] = {(double)tr[6] - v0[0]", "double e2[3] = {(double)tr[3] - v0[0]"),
 ]
 
 
