@@ -88,6 +88,13 @@ typedef struct {
     int32_t n_sph, n_box, n_rect;
     const float *sph, *box, *rect;
     double clamp_dist, shadow_eps, diag;
+    /* SURVEY §8(f1) triangle meshes: tri[9*k] = (v0, v1, v2), HOST float32, 0 <= n_tri <= 2^26.
+     * lmc_create builds a BVH over them on the host (median split, <= 4 triangles per leaf) and
+     * keeps nodes + triangles in device memory for the context's lifetime; traversal uses fp32
+     * node boxes widened by 1e-3 D and the exact fp64 Moller-Trumbore test of DESIGN.md R39 at
+     * the leaves, so each visibility decision equals the brute-force test over all triangles. */
+    int32_t n_tri;
+    const float *tri;
 } lmc_scene;
 
 typedef struct {

@@ -47,6 +47,78 @@ __device__ __forceinline__ double powi_d(double base, int e)
     return r;
 }
 
+// Segment vs triangle (R39): Moller-Trumbore in the oracle's operation
+// order — e1 = v1 - v0, e2 = v2 - v0, p = l x e2, det = e1 . p, inv = 1 / det, s = x - v0,
+// u = (s . p) inv, qv = s x e1, v = (l . qv) inv, t = (e2 . qv) inv.
+__device__ __forceinline__ bool tri_hit(const float4 *__restrict__ t4, double x0, double x1, double x2, double l0,
+                                        double l1, double l2, double tmin, double tmax)
+{
+    const float4 A = t4[0], B = t4[1], C = t4[2];
+    const double v00 = A.x, v01 = A.y, v02 = A.z;
+    const double e10 = (double)A.w - v00, e11 = (double)B.x - v01, e12 = (double)B.y - v02;
+    const double e20 = (double)B.z - v00, e21 = (double)B.w - v01, e22 = (double)C.x - v02;
+    const double p0 = l1 * e22 - l2 * e21, p1 = l2 * e20 - l0 * e22, p2 = l0 * e21 - l1 * e20;
+    const double det = dot3d(e10, e11, e12, p0, p1, p2);
+    if (det == 0.0) return false;
+    const double inv = 1.0 / det;
+    const double s0 = x0 - v00, s1 = x1 - v01, s2 = x2 - v02;
+    const double u = dot3d(s0, s1, s2, p0, p1, p2) * inv;
+    if (u < 0.0 || u > 1.0) return false;
+    const double q0 = s1 * e12 - s2 * e11, q1 = s2 * e10 - s0 * e12, q2 = s0 * e11 - s1 * e10;
+    const double v = dot3d(l0, l1, l2, q0, q1, q2) * inv;
+    if (v < 0.0 || u + v > 1.0) return false;
+    const double t = dot3d(e20, e21, e22, q0, q1, q2) * inv;
+    return t > tmin && t < tmax;
+}
+
+constexpr int BVH_STACK = 32;   // > depth of the median-split BVH of 2^26 triangles (lmc_create checks)
+
+// 1 iff some triangle is hit by the open segment.  The BVH is walked with fp32 slab tests of the
+// segment [x, y] (parameter s in [0, 1] over w = y - x) against node boxes widened by the margin
+// (1e-3 D, far above fp32 rounding of the coordinates): a node is skipped only when no point of
+// the segment lies within the margin of its box, so every triangle the exact test could report is
+// reached and the decision equals the brute-force OR over all triangles.
+__device__ bool bvh_hit(const SceneConst *sc, double x0, double x1, double x2, double l0, double l1, double l2,
+                        double tmin, double tmax, float x0f, float x1f, float x2f, float y0f, float y1f, float y2f)
+{
+    const float mg = sc->margin;
+    float w0 = y0f - x0f, w1 = y1f - x1f, w2 = y2f - x2f;
+    // an axis the segment does not move along: a tiny slope keeps the slab test finite and exact in sign
+    if (fabsf(w0) < 1e-20f) w0 = copysignf(1e-20f, w0);
+    if (fabsf(w1) < 1e-20f) w1 = copysignf(1e-20f, w1);
+    if (fabsf(w2) < 1e-20f) w2 = copysignf(1e-20f, w2);
+    const float i0 = 1.f / w0, i1 = 1.f / w1, i2 = 1.f / w2;
+    const float4 *__restrict__ bv = sc->bvh;
+    const float4 *__restrict__ tr = sc->tri4;
+    int stack[BVH_STACK];
+    int sp = 0, node = 0;
+    while (true) {
+        const float4 A = bv[2 * node], B = bv[2 * node + 1];
+        float ta = (A.x - mg - x0f) * i0, tb = (B.x + mg - x0f) * i0;
+        float tn = fminf(ta, tb), tf = fmaxf(ta, tb);
+        ta = (A.y - mg - x1f) * i1;
+        tb = (B.y + mg - x1f) * i1;
+        tn = fmaxf(tn, fminf(ta, tb));
+        tf = fminf(tf, fmaxf(ta, tb));
+        ta = (A.z - mg - x2f) * i2;
+        tb = (B.z + mg - x2f) * i2;
+        tn = fmaxf(tn, fminf(ta, tb));
+        tf = fminf(tf, fmaxf(ta, tb));
+        if (fmaxf(tn, 0.f) <= fminf(tf, 1.f)) {
+            const int first = __float_as_int(A.w), cnt = __float_as_int(B.w);
+            if (cnt == 0) {
+                stack[sp++] = first + 1;
+                node = first;
+                continue;
+            }
+            for (int k = 0; k < cnt; ++k)
+                if (tri_hit(tr + 3 * (first + k), x0, x1, x2, l0, l1, l2, tmin, tmax)) return true;
+        }
+        if (sp == 0) return false;
+        node = stack[--sp];
+    }
+}
+
 // 1 iff the open segment x + t l, t in (eps, dist - eps), misses every occluder.
 // Each primitive is first screened by a conservative fp32 test on the segment [x, y] (y = VPL
 // position) with a margin of 1e-3 D, orders of magnitude above fp32 rounding: a primitive is
@@ -126,6 +198,7 @@ __device__ bool visible_d(int slot, double x0, double x1, double x2, double l0, 
         double b = dot3d(q0, q1, q2, e20, e21, e22) / dot3d(e20, e21, e22, e20, e21, e22);
         if (a >= 0.0 && a <= 1.0 && b >= 0.0 && b <= 1.0) return false;
     }
+    if (sc->ntri > 0 && bvh_hit(sc, x0, x1, x2, l0, l1, l2, tmin, tmax, x0f, x1f, x2f, y0f, y1f, y2f)) return false;
     return true;
 }
 
@@ -296,6 +369,7 @@ __device__ bool visible_w(const SceneConst *sc, double x0, double x1, double x2,
             if (rect_hit(sc->rect + 12 * k, x0, x1, x2, l0, l1, l2, tmin, tmax)) { hit = true; mr = 0u; }
         }
     }
+    if (!hit && sc->ntri > 0) hit = bvh_hit(sc, x0, x1, x2, l0, l1, l2, tmin, tmax, x0f, x1f, x2f, y0f, y1f, y2f);
     return !hit;
 }
 

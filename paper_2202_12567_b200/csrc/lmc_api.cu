@@ -94,7 +94,7 @@ void free_all(lmc_ctx *c)
                     d.newcells, d.newpos, d.U, d.V, d.Lam, d.Pi, d.Xold, d.S, d.flags, d.iters, d.resid,
                     d.direct_rgb, d.counters, d.img, d.rows_rgb, d.vpl_soa, d.r_perm, d.r_len, d.c_perm, d.c_len,
                     d.r_goff, d.c_goff, d.c_nsolo, d.adm_order, d.r_ent, d.c_ent, d.norm, d.r_grp, d.c_grp,
-                    d.r_slot, d.c_slot, d.ngrp, d.ctot, d.slot_st, d.ord_tmp, d.ord_cub, d.rank_pix, d.all4, d.prev_cut, d.prev_n, d.prev_flags, d.prev_rows, d.warm_ok};
+                    d.r_slot, d.c_slot, d.ngrp, d.ctot, d.slot_st, d.ord_tmp, d.ord_cub, d.rank_pix, d.all4, d.prev_cut, d.prev_n, d.prev_flags, d.prev_rows, d.warm_ok, d.bvh, d.tri4};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (c->h_stage) cudaFreeHost(c->h_stage);
@@ -453,6 +453,73 @@ void ev_rec(lmc_ctx *c, int k)
 
 }  // namespace
 
+// Triangle BVH: median split of the triangle centroids on the longest axis of their
+// bounds, ties by triangle index (deterministic), at most 4 triangles per leaf; children of a
+// node are adjacent (first, first + 1).  Node bounds are the exact float32 min / max of the
+// vertices.  Only acceleration: the decision per triangle is the exact fp64 test in exact.cu.
+static void build_tri_bvh(const float *tri, int32_t n, std::vector<float4> &nodes, std::vector<float4> &tris)
+{
+    std::vector<int32_t> idx(n);
+    for (int32_t k = 0; k < n; ++k) idx[k] = k;
+    std::vector<float> cen(3 * (size_t)n);
+    for (int32_t k = 0; k < n; ++k)
+        for (int a = 0; a < 3; ++a) cen[3 * (size_t)k + a] = (tri[9 * (size_t)k + a] + tri[9 * (size_t)k + 3 + a] + tri[9 * (size_t)k + 6 + a]) / 3.0f;
+    struct Job {
+        int32_t node, lo, hi;
+    };
+    nodes.assign(2, make_float4(0, 0, 0, 0));
+    std::vector<Job> stack{{0, 0, n}};
+    while (!stack.empty()) {
+        Job j = stack.back();
+        stack.pop_back();
+        float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+        float clo[3] = {INFINITY, INFINITY, INFINITY}, chi[3] = {-INFINITY, -INFINITY, -INFINITY};
+        for (int32_t i = j.lo; i < j.hi; ++i) {
+            const float *t = tri + 9 * (size_t)idx[i];
+            for (int a = 0; a < 3; ++a) {
+                lo[a] = std::min(lo[a], std::min(t[a], std::min(t[3 + a], t[6 + a])));
+                hi[a] = std::max(hi[a], std::max(t[a], std::max(t[3 + a], t[6 + a])));
+                clo[a] = std::min(clo[a], cen[3 * (size_t)idx[i] + a]);
+                chi[a] = std::max(chi[a], cen[3 * (size_t)idx[i] + a]);
+            }
+        }
+        float4 &A = nodes[2 * (size_t)j.node];
+        float4 &B = nodes[2 * (size_t)j.node + 1];
+        A = make_float4(lo[0], lo[1], lo[2], 0.f);
+        B = make_float4(hi[0], hi[1], hi[2], 0.f);
+        const int32_t cnt = j.hi - j.lo;
+        if (cnt <= 4) {
+            int32_t first = j.lo, c4 = cnt;
+            memcpy(&A.w, &first, 4);
+            memcpy(&B.w, &c4, 4);
+            continue;
+        }
+        int ax = 0;
+        for (int a = 1; a < 3; ++a)
+            if (chi[a] - clo[a] > chi[ax] - clo[ax]) ax = a;
+        const int32_t mid = j.lo + cnt / 2;
+        std::nth_element(idx.begin() + j.lo, idx.begin() + mid, idx.begin() + j.hi, [&](int32_t p, int32_t q) {
+            const float cp = cen[3 * (size_t)p + ax], cq = cen[3 * (size_t)q + ax];
+            return cp < cq || (cp == cq && p < q);
+        });
+        const int32_t child = (int32_t)(nodes.size() / 2);
+        nodes.resize(nodes.size() + 4);
+        float4 &A2 = nodes[2 * (size_t)j.node];   // (re-fetch: resize may move the storage)
+        int32_t zero = 0;
+        memcpy(&A2.w, &child, 4);
+        memcpy(&nodes[2 * (size_t)j.node + 1].w, &zero, 4);
+        stack.push_back({child + 1, mid, j.hi});
+        stack.push_back({child, j.lo, mid});
+    }
+    tris.resize(3 * (size_t)n);
+    for (int32_t i = 0; i < n; ++i) {
+        const float *t = tri + 9 * (size_t)idx[i];
+        tris[3 * (size_t)i + 0] = make_float4(t[0], t[1], t[2], t[3]);
+        tris[3 * (size_t)i + 1] = make_float4(t[4], t[5], t[6], t[7]);
+        tris[3 * (size_t)i + 2] = make_float4(t[8], 0.f, 0.f, 0.f);
+    }
+}
+
 // ==========================================================================================
 extern "C" {
 
@@ -515,6 +582,7 @@ static lmc_status create_impl(lmc_ctx *c, const lmc_gbuffer *g, const lmc_vpls *
         return fail(c, LMC_EINVAL, "at most %d occluders of each kind", MAX_PRIMS);
     if ((sc->n_sph && !sc->sph) || (sc->n_box && !sc->box) || (sc->n_rect && !sc->rect)) return fail(c, LMC_EINVAL, "null occluder array");
     if (!(sc->diag > 0.0)) return fail(c, LMC_EINVAL, "scene diagonal must be > 0");
+    if (sc->n_tri < 0 || sc->n_tri > (1 << 26) || (sc->n_tri && !sc->tri)) return fail(c, LMC_EINVAL, "bad triangle array");
     c->M = g->count;
     c->W = g->width;
     c->H = g->height;
@@ -543,6 +611,20 @@ static lmc_status create_impl(lmc_ctx *c, const lmc_gbuffer *g, const lmc_vpls *
             c->scene.rbox[6 * k + 3 + a] = std::max(std::max(c0, c1), std::max(c2, c3));
         }
         c->scene.rnorm[k] = (float)std::sqrt((double)r[9] * r[9] + (double)r[10] * r[10] + (double)r[11] * r[11]);
+    }
+    if (sc->n_tri > 0) {   // triangle BVH, device-resident for the context's lifetime
+        for (int64_t k = 0; k < 9ll * sc->n_tri; ++k)
+            if (!std::isfinite(sc->tri[k])) return fail(c, LMC_EINVAL, "non-finite triangle vertex");
+        std::vector<float4> nodes, tris;
+        build_tri_bvh(sc->tri, sc->n_tri, nodes, tris);
+        CK(cudaMalloc(&c->d.bvh, nodes.size() * sizeof(float4)), "alloc bvh");
+        CK(cudaMalloc(&c->d.tri4, tris.size() * sizeof(float4)), "alloc triangles");
+        CK(cudaMemcpy(c->d.bvh, nodes.data(), nodes.size() * sizeof(float4), cudaMemcpyHostToDevice), "upload bvh");
+        CK(cudaMemcpy(c->d.tri4, tris.data(), tris.size() * sizeof(float4), cudaMemcpyHostToDevice), "upload triangles");
+        c->scene.bvh = c->d.bvh;
+        c->scene.tri4 = c->d.tri4;
+        c->scene.ntri = sc->n_tri;
+        c->scene.nbvh = (int32_t)(nodes.size() / 2);
     }
     c->scene_slot = acquire_scene_slot();
     if (c->scene_slot < 0) return fail(c, LMC_EINVAL, "more than %d live contexts in this process", SCENE_SLOTS);

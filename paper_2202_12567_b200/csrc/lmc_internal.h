@@ -26,6 +26,12 @@ struct SceneConst {
     double eps;        // shadow_eps
     float margin;      // conservative screening margin (1e-3 D) of the fp32 visibility pre-tests
     float pad3[3];
+    // triangle meshes: BVH nodes, 2 float4 each: (lo3, first child | first triangle),
+    // (hi3, triangle count; 0 = internal node, children at first, first + 1); triangles 3 float4
+    // each: (v0, v1.x) (v1.yz, v2.xy) (v2.z, 0, 0, 0), in leaf order
+    const float4 *bvh;
+    const float4 *tri4;
+    int32_t ntri, nbvh, pad5[2];
     float sph[MAX_PRIMS * 4];
     float box[MAX_PRIMS * 6];
     float rect[MAX_PRIMS * 12];
@@ -58,6 +64,7 @@ struct Dev {
     float *g[13];             // px py pz nx ny nz vx vy vz rho_r rho_g rho_b spec
     int32_t *expo;
     float4 *vpl;              // 2 per VPL: (px,py,pz,nx) (ny,nz,0,0)
+    float4 *bvh, *tri4;       // triangle BVH + triangles (SceneConst.bvh / tri4)
     // upper tree arrays (backing store of Upper)
     int32_t *ut_i32;
     double *ut_lum;

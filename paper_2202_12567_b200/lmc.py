@@ -41,7 +41,8 @@ class LightTree(C.Structure):
 
 class Scene(C.Structure):
     _fields_ = [("n_sph", C.c_int32), ("n_box", C.c_int32), ("n_rect", C.c_int32), ("sph", _P), ("box", _P),
-                ("rect", _P), ("clamp_dist", C.c_double), ("shadow_eps", C.c_double), ("diag", C.c_double)]
+                ("rect", _P), ("clamp_dist", C.c_double), ("shadow_eps", C.c_double), ("diag", C.c_double),
+                ("n_tri", C.c_int32), ("tri", _P)]
 
 
 class Config(C.Structure):
@@ -170,9 +171,11 @@ class Frame:
                             arr(t["rep"], np.int32), arr(t["ir"], np.float32), arr(t["ig"], np.float32),
                             arr(t["ib"], np.float32), t["global_cut"].shape[0], arr(t["global_cut"], np.int32))
         pr = inputs.prims
-        self._prims = [np.ascontiguousarray(pr[k], np.float32) for k in ("sph", "box", "rect")]
-        self.sc = Scene(pr["sph"].shape[0], pr["box"].shape[0], pr["rect"].shape[0], *[_ptr(a) for a in self._prims],
-                        inputs.clamp_dist, inputs.shadow_eps, inputs.diag)
+        tri = pr.get("tri", np.zeros((0, 9), np.float32))
+        self._prims = [np.ascontiguousarray(pr[k], np.float32) for k in ("sph", "box", "rect")] + \
+            [np.ascontiguousarray(tri, np.float32)]
+        self.sc = Scene(pr["sph"].shape[0], pr["box"].shape[0], pr["rect"].shape[0], *[_ptr(a) for a in self._prims[:3]],
+                        inputs.clamp_dist, inputs.shadow_eps, inputs.diag, tri.shape[0], _ptr(self._prims[3]))
         if stream is None:
             stream = torch.cuda.current_stream(device)
         self.stream = stream
