@@ -1563,17 +1563,26 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2(P2Args A)
     }
     const int nnew = sh_nnew;
     const int nnz = sh_obs + nnew;
-    // phase B: CSR row pointers from per-row word prefix counts
-    int rowtot = 0;
-    if (tid < m) {
-        uint16_t run = 0;
-        for (int wi = 0; wi < W; ++wi) {
-            P[tid * (W + 1) + wi] = run;
-            run = (uint16_t)(run + __popc(bm[tid * W + wi]));
+    // phase B: CSR row pointers from per-row word prefix counts.  A warp per row: lane wi takes
+    // bitmap word wi (W <= 32), the word prefix is a warp scan, so the row's column indices are
+    // then written by all lanes at once in ascending order (consecutive lanes, consecutive ranges).
+    for (int i = w; i < m; i += P2_THREADS / 32) {
+        const uint32_t word = lane < W ? bm[i * W + lane] : 0u;
+        const int cnt = __popc(word);
+        int incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(FULL_MASK, incl, o);
+            if (lane >= o) incl += t;
         }
-        P[tid * (W + 1) + W] = run;
-        rowtot = run;
+        if (lane < W) P[i * (W + 1) + lane] = (uint16_t)(incl - cnt);
+        if (lane == 31) {
+            P[i * (W + 1) + W] = (uint16_t)incl;
+            rp[i] = incl;   // row total (the row pointers replace it below)
+        }
     }
+    __syncthreads();
+    const int rowtot = tid < m ? rp[tid] : 0;
     __syncthreads();
     int rpre, rtot;
     ScanI(scani_tmp).ExclusiveSum(rowtot, rpre, rtot);
@@ -1582,14 +1591,14 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2(P2Args A)
     __syncthreads();
     int32_t *grp = A.rowptr + (int64_t)ls * (A.mmax + 1);
     for (int i = tid; i <= m; i += P2_THREADS) grp[i] = rp[i];
-    if (tid < m) {   // column indices, ascending within the row
-        int pos = rp[tid];
-        for (int wi = 0; wi < W; ++wi) {
-            uint32_t word = bm[tid * W + wi];
+    for (int i = w; i < m; i += P2_THREADS / 32) {   // column indices, ascending within the row
+        if (lane < W) {
+            uint32_t word = bm[i * W + lane];
+            int pos = rp[i] + P[i * (W + 1) + lane];
             while (word) {
-                int bit = __ffs(word) - 1;
+                const int bit = __ffs(word) - 1;
                 word &= word - 1;
-                A.col[ob + pos++] = (uint16_t)(wi * 32 + bit);
+                A.col[ob + pos++] = (uint16_t)(lane * 32 + bit);
             }
         }
     }
