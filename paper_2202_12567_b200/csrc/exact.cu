@@ -1783,7 +1783,13 @@ cudaError_t run_pass2(lmc_ctx *c)
     A.row_importance = c->cfg.row_importance;
     size_t sm = pass2_smem(c->mmax, c->G);
     cudaError_t e = cudaFuncSetAttribute(k_pass2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    if (e != cudaSuccess) return e;
+    if (e != cudaSuccess) {
+        cudaFuncAttributes fa;
+        cudaFuncGetAttributes(&fa, k_pass2);
+        fprintf(stderr, "lmc: k_pass2 needs %zu + %zu bytes of shared memory (limit %d)\n", sm, (size_t)fa.sharedSizeBytes,
+                fa.maxDynamicSharedSizeBytes);
+        return e;
+    }
     k_pass2<<<c->SL, P2_THREADS, sm, c->stream>>>(A);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
