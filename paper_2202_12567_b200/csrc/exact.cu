@@ -485,6 +485,16 @@ __device__ __forceinline__ double slice_key(const GView &g, int32_t r, int d, do
     }
 }
 
+// encoded keys of all 6 dimensions of every G-buffer row, once per frame (row-major, 48 bytes per
+// row): the per-level extent and key kernels then gather one record per row
+__global__ void k_keys6(GView g, int64_t M, double diag, double wn, unsigned long long *keys6)
+{
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= 6 * M) return;
+    const int32_t r = (int32_t)(k / 6);
+    keys6[k] = enc_key(slice_key(g, r, (int)(k - 6 * (int64_t)r), diag, wn));
+}
+
 __global__ void k_ext_init(unsigned long long *ext, int n)
 {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -493,17 +503,20 @@ __global__ void k_ext_init(unsigned long long *ext, int n)
 
 // one CTA per work item (slot, start, len): extents of the 6 key dimensions of a chunk
 __global__ void __launch_bounds__(256) k_slice_extent(const int32_t *__restrict__ rows, const int32_t *__restrict__ work,
-                                                      unsigned long long *ext, GView g, double diag, double wn)
+                                                      unsigned long long *ext, const unsigned long long *__restrict__ keys6)
 {
     int slot = work[3 * blockIdx.x], start = work[3 * blockIdx.x + 1], len = work[3 * blockIdx.x + 2];
     unsigned long long mx[6], mn[6];
 #pragma unroll
     for (int d = 0; d < 6; ++d) { mx[d] = 0ull; mn[d] = ~0ull; }
     for (int k = threadIdx.x; k < len; k += blockDim.x) {
-        int r = rows[start + k];
+        const int64_t r = rows[start + k];
+        const ulonglong2 *kr = reinterpret_cast<const ulonglong2 *>(keys6 + 6 * r);
+        const ulonglong2 e01 = kr[0], e23 = kr[1], e45 = kr[2];
+        const unsigned long long ek[6] = {e01.x, e01.y, e23.x, e23.y, e45.x, e45.y};
 #pragma unroll
         for (int d = 0; d < 6; ++d) {
-            unsigned long long e = enc_key(slice_key(g, r, d, diag, wn));
+            const unsigned long long e = ek[d];
             mx[d] = e > mx[d] ? e : mx[d];
             mn[d] = e < mn[d] ? e : mn[d];
         }
@@ -547,7 +560,7 @@ __device__ __forceinline__ int tile_of(const int32_t *__restrict__ tbeg, int nti
 // split) and the tile of every row
 __global__ void k_slice_keys(const int32_t *__restrict__ rows, int64_t M, const int32_t *__restrict__ tbeg,
                              const int32_t *__restrict__ tslot, int ntiles, const unsigned long long *__restrict__ ext,
-                             unsigned long long *keys, int32_t *row_tile, GView g, double diag, double wn)
+                             unsigned long long *keys, int32_t *row_tile, const unsigned long long *__restrict__ keys6)
 {
     int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= M) return;
@@ -563,7 +576,7 @@ __global__ void k_slice_keys(const int32_t *__restrict__ rows, int64_t M, const 
         double e = dec_key(ext[slot * 12 + d]) - dec_key(ext[slot * 12 + 6 + d]);
         if (e > bext) { bext = e; best = d; }
     }
-    keys[k] = enc_key(slice_key(g, r, best, diag, wn));
+    keys[k] = keys6[6 * (int64_t)r + best];
 }
 
 __global__ void k_tile_keys(const int32_t *__restrict__ rows_sorted, const int32_t *__restrict__ row_tile, int64_t M,
@@ -712,6 +725,7 @@ cudaError_t run_slicing(lmc_ctx *c)
     int32_t *row_tile = c->d.sl_i32, *f = c->d.sl_i32 + M, *pre = c->d.sl_i32 + 2 * M, *tmp_rows = c->d.sl_i32 + 3 * M;
     uint32_t *tkey = reinterpret_cast<uint32_t *>(c->d.keys), *tkey_alt = reinterpret_cast<uint32_t *>(c->d.keys) + M;
     k_iota<<<nb, 256, 0, st>>>(rows, M);
+    k_keys6<<<(unsigned)((6 * M + 255) / 256), 256, 0, st>>>(g, M, diag, wn, c->d.keys6);
     for (const auto &L : c->levels) {
         // rows [L.lo, L.lo + L.n) of this level (all rows, or this rank's subtree): every position
         // array is offset by lo; row_tile / left-flags are indexed by the G-buffer row itself
@@ -723,8 +737,8 @@ cudaError_t run_slicing(lmc_ctx *c)
         const int32_t *tend = c->d.lvl_end + L.tile_off;
         const int32_t *tslot = c->d.lvl_slot + L.tile_off;
         k_ext_init<<<(L.nslots * 12 + 255) / 256, 256, 0, st>>>(c->d.ext, L.nslots);
-        k_slice_extent<<<L.work_n, 256, 0, st>>>(rws, c->d.lvl_work + 3 * L.work_off, c->d.ext, g, diag, wn);
-        k_slice_keys<<<nbl, 256, 0, st>>>(rws, n, tbeg, tslot, L.tile_n, c->d.ext, c->d.keys_alt + lo, row_tile, g, diag, wn);
+        k_slice_extent<<<L.work_n, 256, 0, st>>>(rws, c->d.lvl_work + 3 * L.work_off, c->d.ext, c->d.keys6);
+        k_slice_keys<<<nbl, 256, 0, st>>>(rws, n, tbeg, tslot, L.tile_n, c->d.ext, c->d.keys_alt + lo, row_tile, c->d.keys6);
         size_t bytes = c->d.cub_tmp_bytes;
         unsigned long long *kin = c->d.keys_alt + lo, *kout = c->d.keys_sorted + lo;
         cudaError_t e;

@@ -94,7 +94,7 @@ void free_all(lmc_ctx *c)
                     d.newcells, d.newpos, d.U, d.V, d.Lam, d.Pi, d.Xold, d.S, d.flags, d.iters, d.resid,
                     d.direct_rgb, d.counters, d.img, d.rows_rgb, d.vpl_soa, d.r_perm, d.r_len, d.c_perm, d.c_len,
                     d.r_goff, d.c_goff, d.c_nsolo, d.adm_order, d.r_ent, d.c_ent, d.norm, d.r_grp, d.c_grp,
-                    d.r_slot, d.c_slot, d.ngrp, d.ctot, d.slot_st, d.ord_tmp, d.ord_cub, d.rank_pix, d.all4, d.prev_cut, d.prev_n, d.prev_flags, d.prev_rows, d.warm_ok, d.bvh, d.tri4};
+                    d.r_slot, d.c_slot, d.ngrp, d.ctot, d.slot_st, d.ord_tmp, d.ord_cub, d.rank_pix, d.all4, d.prev_cut, d.prev_n, d.prev_flags, d.prev_rows, d.warm_ok, d.bvh, d.tri4, d.keys6};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (c->h_stage) cudaFreeHost(c->h_stage);
@@ -662,10 +662,15 @@ static lmc_status create_impl(lmc_ctx *c, const lmc_gbuffer *g, const lmc_vpls *
         // two >= ceil(len / T) segments (< 2 len / T + 2), groups of 32 segments of <= T entries
         // padded to multiples of 8 k-steps
         // q <= 8: lane-per-segment kernel (complete2.cu; 1.6-2.6x faster than the lane-group kernel
-        // on the C5 sweep); q = 16: the lane-group kernel (complete.cu) unless LMC_ADM2=1 (equal at
-        // C2/C3, slower when the residuals S spill from shared memory, C4 and 20% rates: DESIGN.md §6)
+        // on the C5 sweep).  q = 16: lane-per-segment while a slice's expected samples rate * m * |g|
+        // stay <= 64k (its residuals S then mostly fit in shared memory: 1-4% faster at C2, C3 and
+        // 5% rates), else the lane-group kernel of complete.cu (C4 and 20% rates: S spills to
+        // global memory and the lane-per-segment kernel is 7-10% slower).
+        // LMC_ADM2=1 / 0 forces the choice at q = 16, LMC_ADM_V1=1 forces complete.cu at every q.
         const char *ev = getenv("LMC_ADM_V1"), *e2 = getenv("LMC_ADM2");
-        c->use_adm2 = cfg.solver == LMC_SOLVER_ADM && (cfg.rank_q <= 8 || (cfg.rank_q == 16 && e2 && e2[0] == '1')) &&
+        const double per_slice = cfg.rate * ((double)c->M / std::max(c->S, 1)) * (double)G;
+        const bool q16_adm2 = e2 && e2[0] ? e2[0] == '1' : per_slice <= 65536.0;
+        c->use_adm2 = cfg.solver == LMC_SOLVER_ADM && (cfg.rank_q <= 8 || (cfg.rank_q == 16 && q16_adm2)) &&
                       !(ev && ev[0] == '1');
         if (c->use_adm2) {
             const int64_t T = std::min(c->adm2_Tr, c->adm2_Tc), Tmax = std::max(c->adm2_Tr, c->adm2_Tc);
@@ -688,6 +693,7 @@ static lmc_status create_impl(lmc_ctx *c, const lmc_gbuffer *g, const lmc_vpls *
     CK(dalloc(&d.keys, M), "alloc slicing");
     CK(dalloc(&d.keys_alt, M), "alloc slicing");
     CK(dalloc(&d.keys_sorted, M), "alloc slicing");
+    CK(dalloc(&d.keys6, 6 * M), "alloc slicing");
     CK(dalloc(&d.sl_i32, 4 * M), "alloc slicing");
     CK(slicing_tmp_bytes(std::max<int64_t>(M, 1), c->max_tiles, &d.cub_tmp_bytes), "cub sizing");
     CK(cudaMalloc(&d.cub_tmp, std::max<size_t>(d.cub_tmp_bytes, 16)), "alloc cub");

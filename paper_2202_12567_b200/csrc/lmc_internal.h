@@ -72,6 +72,7 @@ struct Dev {
     // slicing
     int32_t *rows, *rows_alt;          // M
     unsigned long long *keys, *keys_alt, *keys_sorted; // M each (keys also holds 2M uint32 tile keys)
+    unsigned long long *keys6;         // 6 M: encoded keys of the 6 dimensions per G-buffer row
     int32_t *sl_i32;                   // 4M: row_tile, flags, prefix, rows scratch
     int32_t *lvl_begin, *lvl_end;      // concatenated level tilings
     int32_t *lvl_slot;                 // per tile: extent slot of a splitting tile, -1 otherwise

@@ -184,6 +184,7 @@ def test_mals_survey_lambda():
 # ------------------------------------------------------------------------------ both ADM kernels
 
 @pytest.mark.parametrize("name,q,env", [("t_interior", 16, {"LMC_ADM2": "1"}), ("c1", 16, {"LMC_ADM2": "1"}),
+                                        ("t_interior", 16, {"LMC_ADM2": "0"}), ("c1", 16, {"LMC_ADM2": "0"}),
                                         ("t_interior", 8, {"LMC_ADM_V1": "1"}), ("t_interior", 4, {"LMC_ADM_V1": "1"}),
                                         ("t_cornell", 8, {}), ("t_cornell", 4, {})])
 def test_adm_kernels_all_ranks(name, q, env):
