@@ -19,6 +19,22 @@ COMMON = ["-O3", "-std=c++17", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC,-ffp-con
 UNITS = [("exact.cu", ["-fmad=false"]), ("complete.cu", []), ("complete2.cu", []), ("mals.cu", []), ("lighttree.cu", ["-fmad=false"]), ("lmc_api.cu", [])]
 
 
+def _nccl_link():
+    """Link the NCCL that PyTorch ships (and rpath it): libtorch_cuda and liblmc then share one
+    libnccl.so.2 whichever is loaded first (the system NCCL is older than torch's and lacks symbols
+    libtorch_cuda needs, so loading it first would break `import torch`)."""
+    try:
+        import importlib.util
+        spec = importlib.util.find_spec("nvidia")
+        for base in (spec.submodule_search_locations or []) if spec else []:
+            d = os.path.join(base, "nccl", "lib")
+            if os.path.exists(os.path.join(d, "libnccl.so.2")):
+                return ["-L" + d, "-l:libnccl.so.2", "-Xlinker", "-rpath", "-Xlinker", d]
+    except (ImportError, ValueError):
+        pass
+    return ["-lnccl"]
+
+
 def _stale(obj, deps):
     return not os.path.exists(obj) or os.path.getmtime(obj) < max(os.path.getmtime(d) for d in deps)
 
@@ -44,7 +60,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
                 f.write(r.stderr)
     if force or _stale(LIB, objs):
         tmp = LIB + f".tmp{os.getpid()}"
-        cmd = [NVCC, "-shared", *ARCH, "-o", tmp, *objs, "-lnccl"]
+        cmd = [NVCC, "-shared", *ARCH, "-o", tmp, *objs, *_nccl_link()]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)

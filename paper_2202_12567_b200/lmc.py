@@ -10,6 +10,7 @@ import ctypes as C
 import os
 
 import numpy as np
+import torch  # noqa: F401  -- before liblmc.so: one libnccl.so.2 (torch's) serves both
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 # LMC_LIB: alternative build of the same library (diagnostic builds); default in-tree

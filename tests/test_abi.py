@@ -49,3 +49,15 @@ def test_oracle_struct_layouts_match():
     L.orc_sizeof_result.restype = ctypes.c_int64
     assert ctypes.sizeof(oracle._Inputs) == L.orc_sizeof_inputs()
     assert ctypes.sizeof(oracle._Result) == L.orc_sizeof_result()
+
+
+def test_library_loaded_before_torch_keeps_torch_importable():
+    """liblmc.so links the NCCL that PyTorch ships: loading it first (as a C caller or the driver's
+    build() would) must not put an older libnccl.so.2 in the process ahead of libtorch_cuda"""
+    import subprocess
+    import sys
+    import paper_2202_12567_b200.build as b
+    path = b.build()
+    code = f"import ctypes; ctypes.CDLL({path!r}); import torch; print('ok')"
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
