@@ -342,8 +342,12 @@ def main():
         if solver == 0 else fl
     traffic, limiter = None, None
     try:   # DRAM bytes per launch of the dominant kernel from the committed ncu --set full capture
-        tj = json.load(open(os.path.join(ROOT, "profiles", "r01_traffic.json")))
-        ent = tj.get(f"{args.config}/{args.solver}/q{x.cfg.rank_q}")
+        key = f"{args.config}/{args.solver}/q{x.cfg.rank_q}"
+        ent = None
+        for fn in ("r02_traffic.json", "r01_traffic.json"):   # the latest capture of this workload
+            fp = os.path.join(ROOT, "profiles", fn)
+            if ent is None and os.path.exists(fp):
+                ent = json.load(open(fp)).get(key)
         traffic = ent["bytes"] if ent else None
         limiter = ent.get("limiter") if ent else None
     except Exception:
