@@ -81,6 +81,22 @@ __device__ double dblock_reduce(double v, double *red)
 
 // one ridge system per group of Q lanes: accumulate sum v v^T and sum m v over the system's
 // samples (operand rows of F, row-major Q doubles), then solve in place; returns x_l on lane l.
+// 1 / x for the (positive, normal) pivots: the hardware approximation refined by two Newton steps
+// (error well below 1 ulp of the fp64 parity bars) instead of the IEEE division's longer sequence
+__device__ __forceinline__ double rcp_pivot(double x)
+{
+#ifdef MALS_IEEE_RCP
+    return 1.0 / x;
+#else
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    double e = fma(-x, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-x, r, 1.0);
+    return fma(r, e, r);
+#endif
+}
+
 template <int Q>
 __device__ __forceinline__ double solve_group(double (&a)[Q], double b, int l, int lane0)
 {
@@ -90,7 +106,7 @@ __device__ __forceinline__ double solve_group(double (&a)[Q], double b, int l, i
 #pragma unroll
         for (int c = k; c < Q; ++c) p[c] = __shfl_sync(0xffffffffu, a[c], lane0 + k);
         const double pb = __shfl_sync(0xffffffffu, b, lane0 + k);
-        const double ip = 1.0 / p[k];
+        const double ip = rcp_pivot(p[k]);
         if (l == k) {
 #pragma unroll
             for (int c = k; c < Q; ++c) a[c] = p[c] * ip;
