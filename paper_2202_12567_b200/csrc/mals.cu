@@ -141,18 +141,28 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b)
 // handed to the 4-sample steps by shuffles.  F^T F is symmetric: the tensor cores form the blocks
 // (0,0), (0,1), (1,1) and (1,0) is written as the transpose of (0,1); F^T m is a per-lane fp64
 // FMA sum over the lane's samples, reduced over the 4 lanes of a component at the end.
+// the first 32-entry batch of a system's (index, value) list: lane k holds entry p0 + k (the zero
+// row nf and value 0 past the end)
+__device__ __forceinline__ void first_batch(const MArgs &A, int64_t ob, int half, int p0, int p1, int nf, int &bcol,
+                                            double &bval)
+{
+    const int lane = threadIdx.x & 31;
+    const uint16_t *idx = half == 0 ? A.col + ob : A.csc_row + ob;
+    const double *val = half == 0 ? A.val + ob : A.valc + ob;
+    bcol = nf;
+    bval = 0.0;
+    if (p0 + lane < p1) { bcol = idx[p0 + lane]; bval = val[p0 + lane]; }
+}
+
 __device__ __forceinline__ void accumulate_tc(const double *F, int nf, const MArgs &A, int64_t ob, int half, int p0,
-                                              int p1, double inv_sigma, double *scr)
+                                              int p1, double inv_sigma, double *scr, int bcol, double bval)
 {
     const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
     double c00[2] = {0.0, 0.0}, c01[2] = {0.0, 0.0}, c11[2] = {0.0, 0.0};
     double b0 = 0.0, b1 = 0.0;
     const uint16_t *idx = half == 0 ? A.col + ob : A.csc_row + ob;
     const double *val = half == 0 ? A.val + ob : A.valc + ob;
-    // lane k holds entry pb + k of the current batch (zero row nf and value 0 past the end)
-    int bcol = nf;
-    double bval = 0.0;
-    if (p0 + lane < p1) { bcol = idx[p0 + lane]; bval = val[p0 + lane]; }
+    // (bcol, bval): the first batch, loaded by the caller ahead of time (first_batch)
     for (int pb = p0; pb < p1; pb += 32) {
         int ncol = nf;
         double nval = 0.0;
@@ -248,12 +258,32 @@ __global__ void __launch_bounds__(MCfg<Q>::NT, 1) k_mals(MArgs A)
                 // two systems per warp: tensor-core accumulation one after the other into the
                 // warp's scratch, then one 16-lane Gauss-Jordan solve per system side by side
                 double *scr = F + (size_t)(A.fmax + 1) * Q + (size_t)warp * 2 * 16 * 17;
+                // the list bounds and first batches of both systems of the next pair are loaded
+                // before this pair's accumulation / solve, so their global latency is hidden
+                int q0n[2], q1n[2], bc[2];
+                double bv[2];
+#pragma unroll
+                for (int h2 = 0; h2 < 2; ++h2) {
+                    const int sy = warp * 2 + h2;
+                    q0n[h2] = sy < nsys ? ptr[sy] : 0;
+                    q1n[h2] = sy < nsys ? ptr[sy + 1] : 0;
+                    first_batch(A, ob, half, q0n[h2], q1n[h2], nf, bc[h2], bv[h2]);
+                }
                 for (int sys0 = warp * 2; sys0 < nsys; sys0 += nwarps * 2) {
-                    for (int h2 = 0; h2 < 2; ++h2) {
-                        const int sy = sys0 + h2;
-                        const int q0 = sy < nsys ? ptr[sy] : 0, q1 = sy < nsys ? ptr[sy + 1] : 0;
-                        accumulate_tc(F, nf, A, ob, half, q0, q1, 1.0 / sigma, scr + h2 * 16 * 17);
+                    int q0[2], q1[2], bcc[2];
+                    double bvc[2];
+#pragma unroll
+                    for (int h2 = 0; h2 < 2; ++h2) { q0[h2] = q0n[h2]; q1[h2] = q1n[h2]; bcc[h2] = bc[h2]; bvc[h2] = bv[h2]; }
+#pragma unroll
+                    for (int h2 = 0; h2 < 2; ++h2) {   // prefetch the next pair
+                        const int sy = sys0 + nwarps * 2 + h2;
+                        q0n[h2] = sy < nsys ? ptr[sy] : 0;
+                        q1n[h2] = sy < nsys ? ptr[sy + 1] : 0;
+                        first_batch(A, ob, half, q0n[h2], q1n[h2], nf, bc[h2], bv[h2]);
                     }
+#pragma unroll
+                    for (int h2 = 0; h2 < 2; ++h2)
+                        accumulate_tc(F, nf, A, ob, half, q0[h2], q1[h2], 1.0 / sigma, scr + h2 * 16 * 17, bcc[h2], bvc[h2]);
                     __syncwarp();
                     const int sys = sys0 + gi;
                     double a[Q];
