@@ -565,7 +565,6 @@ static lmc_status create_impl(lmc_ctx *c, const lmc_gbuffer *g, const lmc_vpls *
     if (!(cfg.alpha > 0.0 && cfg.beta > 0.0)) return fail(c, LMC_EINVAL, "alpha, beta must be > 0");
     if (!(cfg.rank_q == 4 || cfg.rank_q == 8 || cfg.rank_q == 16 || cfg.rank_q == 32))
         return fail(c, LMC_EINVAL, "rank_q must be one of 4, 8, 16, 32");
-    if (cfg.solver == LMC_SOLVER_MALS && cfg.rank_q > 16) return fail(c, LMC_EINVAL, "MALS supports rank_q <= 16");
     if (cfg.solver == LMC_SOLVER_MALS && !(cfg.lambda > 0.0)) return fail(c, LMC_EINVAL, "MALS needs lambda > 0");
     if (cfg.solver != LMC_SOLVER_ADM && cfg.solver != LMC_SOLVER_MALS) return fail(c, LMC_EINVAL, "unknown solver");
     if (cfg.p1_nmax < 1 || cfg.p1_nmax > MAX_NMAX || cfg.p1_nmin < 1) return fail(c, LMC_EINVAL, "p1_nmax must be in [1, 32], p1_nmin >= 1");

@@ -37,10 +37,14 @@ struct MArgs {
 };
 
 constexpr int MT = 256;
-// threads per CTA: q = 16 runs the tensor-core accumulation (few registers) with 16 warps
+// threads per CTA: q = 16 runs the tensor-core accumulation (few registers) with 16 warps.
+// q = 32: one 32-lane system per warp; the operand rows (256 bytes each) would not fit in shared
+// memory next to each other at |g| = 1024, so they are read from the fp64 factor in global memory
+// (L2-resident per slice: 1025 x 256 bytes)
 template <int Q>
 struct MCfg {
     static constexpr int NT = Q == 16 ? 512 : MT;
+    static constexpr bool FG = Q == 32;   // operand gathered from global memory
 };
 // operand layout in shared memory: at q = 16 the two 64-byte halves of odd rows are swapped, so the
 // four rows a tensor-core fragment load touches fall into both bank halves
@@ -251,8 +255,11 @@ __global__ void __launch_bounds__(MCfg<Q>::NT, 1) k_mals(MArgs A)
             const int32_t *ptr = half == 0 ? rp : cp;
             const double *src = half == 0 ? Yg : Xg;     // operand gathered per sample
             double *O = half == 0 ? Xg : Yg;             // unknowns solved for
-            for (int e = tid; e < nf * Q; e += MCfg<Q>::NT) F[fidx<Q>(e / Q, e % Q)] = src[e];
-            for (int e = tid; e < Q; e += MCfg<Q>::NT) F[nf * Q + e] = 0.0;   // zero row for padding samples
+            if constexpr (!MCfg<Q>::FG) {
+                for (int e = tid; e < nf * Q; e += MCfg<Q>::NT) F[fidx<Q>(e / Q, e % Q)] = src[e];
+                for (int e = tid; e < Q; e += MCfg<Q>::NT) F[nf * Q + e] = 0.0;   // zero row for padding samples
+            }
+            const double *Fh = MCfg<Q>::FG ? src : F;
             __syncthreads();
             if constexpr (Q == 16) {
                 // two systems per warp: tensor-core accumulation one after the other into the
@@ -319,7 +326,7 @@ __global__ void __launch_bounds__(MCfg<Q>::NT, 1) k_mals(MArgs A)
                         v = A.valc[ob + p];
                     }
                     const double mh = v / sigma;
-                    const double *f = F + (size_t)other * Q;
+                    const double *f = Fh + (size_t)other * Q;
                     const double fl = f[l];
 #pragma unroll
                     for (int c = 0; c < Q; c += 2) {
@@ -339,21 +346,22 @@ __global__ void __launch_bounds__(MCfg<Q>::NT, 1) k_mals(MArgs A)
             }
         }
     }
-    // after the last column half F holds X: residual on Omega (y from global), outputs (X, sigma Y)
+    // after the last column half F holds X (q = 32: X in global memory): residual on Omega (y from
+    // global), outputs (X, sigma Y)
     double ss = 0.0;
     for (int i = tid; i < m; i += MCfg<Q>::NT) {
         for (int p = rp[i]; p < rp[i + 1]; ++p) {
             const double *y = Yg + (size_t)A.col[ob + p] * Q;
             double d = 0.0;
 #pragma unroll
-            for (int c = 0; c < Q; ++c) d = fma(F[fidx<Q>(i, c)], y[c], d);
+            for (int c = 0; c < Q; ++c) d = fma(MCfg<Q>::FG ? Xg[(size_t)i * Q + c] : F[fidx<Q>(i, c)], y[c], d);
             const double e = A.val[ob + p] / sigma - d;
             ss = fma(e, e, ss);
         }
     }
     ss = dblock_reduce<false>(ss, red);
     const double res = sqrt(ss / nrmM2);
-    for (int e = tid; e < m * Q; e += MCfg<Q>::NT) Ug[e] = (float)F[fidx<Q>(e / Q, e % Q)];
+    for (int e = tid; e < m * Q; e += MCfg<Q>::NT) Ug[e] = (float)(MCfg<Q>::FG ? Xg[e] : F[fidx<Q>(e / Q, e % Q)]);
     for (int e = tid; e < n * Q; e += MCfg<Q>::NT) Vg[e] = (float)(sigma * Yg[e]);
     if (tid == 0) {
         const bool bad = !(res == res) || isinf(res);
@@ -367,6 +375,7 @@ size_t mals_smem_bytes(int q, int mmax, int G)
 {
     // operand (max(m, n) + 1 zero row) x q fp64, plus at q = 16 a 2 x 16 x 17 scratch per warp
     const size_t scr = q == 16 ? (size_t)(MCfg<16>::NT / 32) * 2 * 16 * 17 * sizeof(double) : 0;
+    if (q == 32) return 16;   // operand in global memory (MCfg<32>::FG)
     return ((size_t)std::max(mmax, G) + 1) * q * sizeof(double) + scr;
 }
 
@@ -415,6 +424,7 @@ cudaError_t run_mals(lmc_ctx *c)
     case 4: return launch_mals<4>(c, A);
     case 8: return launch_mals<8>(c, A);
     case 16: return launch_mals<16>(c, A);
+    case 32: return launch_mals<32>(c, A);
     default: return cudaErrorInvalidValue;
     }
 }

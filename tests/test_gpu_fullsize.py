@@ -63,3 +63,8 @@ def test_variants_full_size():
 def test_count_target_full_size():
     """SURVEY f2 count-target coarsening at C2 size (cut of 450 nodes per slice)"""
     _check(*_frame(scenegen.preset("c2", coarsen_target=450)))
+
+
+def test_mals_rank32_full_size():
+    """masked ALS at the configs[4] corner q = 32, 5% (1024-node cut at 512-row slices)"""
+    _check(*_frame(scenegen.preset("c5_q32_r5", solver=1)))

@@ -183,9 +183,11 @@ def test_direct_slices_when_rank_exceeds_columns():
         check_slice(x, fr, img, r)
 
 
-@pytest.mark.parametrize("name", ["t_interior", "c1"])
-def test_mals_parity(name):
-    x, fr, img = frame(name, solver=1)
+@pytest.mark.parametrize("name,q", [("t_interior", 8), ("c1", 8), ("t_interior", 4), ("t_interior", 16),
+                                    ("t_interior", 32)])
+def test_mals_parity(name, q):
+    """masked ALS at every rank (q = 32: the operand gathered from global memory)"""
+    x, fr, img = frame(name, solver=1, rank_q=q)
     off, _ = fr.slices()
     for r in oracle_slices(x, pick(off.size - 1, 6)):
         check_slice(x, fr, img, r)
