@@ -223,6 +223,15 @@ lmc_status lmc_nccl_unique_id(uint8_t out[128]);
 /* The ranks' shares: slice_first[r] / row_first[r] = first slice / first slice-ordered row of rank r
  * (world + 1 entries each, last = S / M).  Host buffers; either may be NULL. */
 lmc_status lmc_get_partition(lmc_ctx *ctx, int32_t *slice_first, int64_t *row_first);
+/* The triangle BVH lmc_create builds for lmc_scene.tri (host only, no GPU): nodes[8 k ..]
+ * = (lo3, first, hi3, count) with first / count int32 bit patterns (count 0: internal node whose
+ * children are nodes first and first + 1; else a leaf of count <= 4 triangles starting at
+ * triangle `first` of the reordered list), tris[12 k ..] = (v0, v1, v2, 0, 0, 0) in leaf order, order[k]
+ * = the input index of reordered triangle k.  Capacities: nodes 8 (2 n_tri - 1) floats, tris 12 n_tri
+ * floats, order n_tri; *n_nodes = nodes written.  Any output may be NULL.  LMC_EINVAL on bad sizes
+ * or non-finite vertices. */
+lmc_status lmc_plan_bvh(const float *tri, int32_t n_tri, float *nodes, int32_t *n_nodes, float *tris, int32_t *order);
+
 /* The same shares without a context or a GPU (host planning only, e.g. for tests): for `rows`
  * G-buffer rows and slice_target, world + 1 entries each and the frame's slice count. */
 lmc_status lmc_plan_partition(int64_t rows, int32_t slice_target, int32_t world, int32_t *slice_first,

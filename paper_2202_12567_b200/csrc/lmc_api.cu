@@ -465,7 +465,8 @@ void ev_rec(lmc_ctx *c, int k)
 // bounds, ties by triangle index (deterministic), at most 4 triangles per leaf; children of a
 // node are adjacent (first, first + 1).  Node bounds are the exact float32 min / max of the
 // vertices.  Only acceleration: the decision per triangle is the exact fp64 test in exact.cu.
-static void build_tri_bvh(const float *tri, int32_t n, std::vector<float4> &nodes, std::vector<float4> &tris)
+static void build_tri_bvh(const float *tri, int32_t n, std::vector<float4> &nodes, std::vector<float4> &tris,
+                          std::vector<int32_t> *order_out = nullptr)
 {
     std::vector<int32_t> idx(n);
     for (int32_t k = 0; k < n; ++k) idx[k] = k;
@@ -519,6 +520,7 @@ static void build_tri_bvh(const float *tri, int32_t n, std::vector<float4> &node
         stack.push_back({child + 1, mid, j.hi});
         stack.push_back({child, j.lo, mid});
     }
+    if (order_out) *order_out = idx;
     tris.resize(3 * (size_t)n);
     for (int32_t i = 0; i < n; ++i) {
         const float *t = tri + 9 * (size_t)idx[i];
@@ -1287,6 +1289,21 @@ lmc_status lmc_nccl_unique_id(uint8_t out[128])
     ncclUniqueId id;
     if (ncclGetUniqueId(&id) != ncclSuccess) return LMC_ENCCL;
     memcpy(out, id.internal, 128);
+    return LMC_OK;
+}
+
+lmc_status lmc_plan_bvh(const float *tri, int32_t n_tri, float *nodes, int32_t *n_nodes, float *tris, int32_t *order)
+{
+    if (n_tri < 1 || n_tri > (1 << 26) || !tri) return LMC_EINVAL;
+    for (int64_t k = 0; k < 9ll * n_tri; ++k)
+        if (!std::isfinite(tri[k])) return LMC_EINVAL;
+    std::vector<float4> nd, tr;
+    std::vector<int32_t> ord;
+    build_tri_bvh(tri, n_tri, nd, tr, &ord);
+    if (nodes) memcpy(nodes, nd.data(), nd.size() * sizeof(float4));
+    if (n_nodes) *n_nodes = (int32_t)(nd.size() / 2);
+    if (tris) memcpy(tris, tr.data(), tr.size() * sizeof(float4));
+    if (order) memcpy(order, ord.data(), ord.size() * sizeof(int32_t));
     return LMC_OK;
 }
 

@@ -74,7 +74,7 @@ EXPORTS = ["lmc_create", "lmc_upload_inputs", "lmc_build_slices", "lmc_sample_pa
            "lmc_destroy", "lmc_last_error", "lmc_status_str", "lmc_get_slices", "lmc_get_pass1", "lmc_get_coarsen",
            "lmc_get_cut", "lmc_get_samples", "lmc_get_factors", "lmc_get_stats", "lmc_set_timing",
            "lmc_eval_entries", "lmc_nccl_unique_id", "lmc_get_partition", "lmc_plan_partition", "lmc_sizeof_struct",
-           "lmc_build_light_tree"]
+           "lmc_build_light_tree", "lmc_plan_bvh"]
 
 
 def _load():
@@ -98,6 +98,7 @@ def _load():
     L.lmc_sizeof_struct.argtypes = [C.c_int32]
     L.lmc_sizeof_struct.restype = C.c_int64
     L.lmc_plan_partition.argtypes = [C.c_int64, C.c_int32, C.c_int32, _P, _P, _P]
+    L.lmc_plan_bvh.argtypes = [_P, C.c_int32, _P, _P, _P, _P]
     L.lmc_destroy.argtypes = [_P]
     L.lmc_destroy.restype = None
     L.lmc_last_error.argtypes = [_P]
@@ -371,6 +372,21 @@ def plan_partition(rows: int, slice_target: int, world: int):
     if st != LMC_OK:
         raise LmcError(f"lmc_plan_partition: {lib.lmc_status_str(st).decode()}")
     return s, r, int(n[0])
+
+
+def plan_bvh(tri):
+    """the triangle BVH lmc_create builds (host only, no GPU): (nodes (N, 8) float32 with int32
+    first / count in columns 3 / 7, reordered triangles (n, 12), order (n,))"""
+    tri = np.ascontiguousarray(tri, np.float32).reshape(-1, 9)
+    n = tri.shape[0]
+    nodes = np.zeros((max(2 * n - 1, 1), 8), np.float32)
+    tris = np.zeros((n, 12), np.float32)
+    order = np.zeros(n, np.int32)
+    nn = np.zeros(1, np.int32)
+    st = lib.lmc_plan_bvh(_ptr(tri), n, _ptr(nodes), _ptr(nn), _ptr(tris), _ptr(order))
+    if st != LMC_OK:
+        raise LmcError(f"lmc_plan_bvh: {lib.lmc_status_str(st).decode()}")
+    return nodes[:int(nn[0])], tris, order
 
 
 def build_light_tree(vpls, cut_max: int, device="cuda"):
