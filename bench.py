@@ -375,8 +375,15 @@ def main():
                                 + ("; mesh occluders excluded from the count (BVH work not counted: a lower bound)"
                                    if x.prims.get("tri") is not None and x.prims["tri"].shape[0] else "")}
     e2e = None
-    if not args.no_e2e and world == 1:
-        e2e = measure_e2e(x, args, solver, dev)
+    if not args.no_e2e and (world == 1 or lib_gather):
+        e2e_id = None
+        if world > 1:   # a second context, so its own NCCL communicator (id from rank 0)
+            idt = torch.zeros(128, dtype=torch.uint8, device=dev)
+            if rank == 0:
+                idt.copy_(torch.frombuffer(bytearray(lmc.nccl_unique_id()), dtype=torch.uint8))
+            dist.broadcast(idt, 0)
+            e2e_id = bytes(idt.cpu().tolist())
+        e2e = measure_e2e(x, args, solver, dev, rank, world, e2e_id)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cores = omp_threads()
@@ -420,15 +427,20 @@ def main():
         dist.destroy_process_group()
 
 
-def measure_e2e(x, args, solver, dev):
+def measure_e2e(x, args, solver, dev, rank=0, world=1, nccl_id=None):
     """Same metric through the C-ABI with HOST buffers: per step, H2D of the frame's inputs
-    (G-buffer + VPLs from pinned memory), the seven calls, D2H of the image."""
+    (G-buffer + VPLs from pinned memory), the seven calls, D2H of the image.  At N > 1 every rank
+    uploads the frame's inputs and renders its slices, rank 0 gathers the image over NCCL inside
+    lmc_resolve_image and writes it to host memory; the step time is the max over ranks (host
+    clock, barrier-aligned) and the byte counts are the totals over ranks."""
     import torch
+    import torch.distributed as dist
     from paper_2202_12567_b200 import lmc
-    fr = lmc.Frame(x, memory=lmc.MEM_HOST, stream=torch.cuda.current_stream(dev))
+    fr = lmc.Frame(x, memory=lmc.MEM_HOST, stream=torch.cuda.current_stream(dev), rank=rank, world=world,
+                   nccl_id=nccl_id)
     npix = x.height * x.width
-    host_img = torch.zeros(npix * 3, dtype=torch.float32).pin_memory()
-    h2d = x.m * (14 * 4) + x.vpls["px"].size * 6 * 4
+    host_img = torch.zeros(npix * 3, dtype=torch.float32).pin_memory() if rank == 0 else None
+    h2d = (x.m * (14 * 4) + x.vpls["px"].size * 6 * 4) * world
     d2h = npix * 3 * 4
 
     def step():
@@ -438,12 +450,14 @@ def measure_e2e(x, args, solver, dev):
         fr.coarsen_cut()
         fr.sample_pass2()
         fr.complete()
-        fr.resolve_image(host_img.numpy(), lmc.MEM_HOST)
+        fr.resolve_image(host_img.numpy() if host_img is not None else None, lmc.MEM_HOST)
 
     for _ in range(max(1, args.warmup)):
         step()
     ts = []
     for _ in range(args.steps):
+        if world > 1:
+            dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         step()
@@ -451,7 +465,16 @@ def measure_e2e(x, args, solver, dev):
         ts.append(time.perf_counter() - t0)
     st = fr.stats()
     fr.close()
-    return {"value": st["sum_completed"] / statistics.mean(ts), "unit": UNIT, "ms_per_step": statistics.mean(ts) * 1e3,
+    sec = statistics.mean(ts)
+    done = float(st["sum_completed"])
+    if world > 1:
+        t = torch.tensor([sec, done], device=dev, dtype=torch.float64)
+        tmax = t[:1].clone()
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        tsum = t[1:].clone()
+        dist.all_reduce(tsum)
+        sec, done = float(tmax.item()), float(tsum.item())
+    return {"value": done / sec, "unit": UNIT, "ms_per_step": sec * 1e3,
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
 
 
