@@ -1276,7 +1276,7 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2(P2Args A)
     // shared memory carve-up
     uint32_t *bm = (uint32_t *)smem;                                    // m*W
     int32_t *colcnt = (int32_t *)(bm + (size_t)A.mmax * 32);            // G
-    unsigned char *phase = (unsigned char *)(colcnt + A.G);
+    unsigned char *phase = smem + ((((size_t)A.mmax * 32 + A.G) * 4 + 15) & ~(size_t)15);   // 16-byte aligned (odd G)
     // phase A
     unsigned long long *cdf = (unsigned long long *)phase;              // G (also holds g as double)
     uint32_t *hkey = (uint32_t *)(cdf + A.G);                           // P2_HSLOTS
@@ -1753,7 +1753,7 @@ static size_t pass2_smem(int mmax, int G)
 {
     size_t phaseA = (size_t)G * 8 + (size_t)P2_HSLOTS * 4 * 2 + (size_t)mmax * 20;   // + row importance
     size_t phaseB = ((((size_t)mmax * 33 + 7) & ~(size_t)7) * 2) + ((size_t)mmax + 1) * 4;
-    size_t base = (size_t)mmax * 32 * 4 + (size_t)G * 4;
+    size_t base = (((size_t)mmax * 32 + G) * 4 + 15) & ~(size_t)15;
     return base + (phaseA > phaseB ? phaseA : phaseB) + 64;
 }
 
