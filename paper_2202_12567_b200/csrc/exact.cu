@@ -812,6 +812,30 @@ __device__ int warp_floyd(int m, int n, uint32_t a, int s, uint64_t seed, int la
     return out;
 }
 
+// Floyd sampling of n distinct rows of [0, m) (any n <= m <= 1024) into the bitmap fb (zeroed by
+// the caller): step k (j = m - n + k) draws t = randint(j + 1) with the same Philox counter as
+// warp_floyd and inserts t, or j when t is already in the set.  Rounds of 32 steps: lane k draws
+// t_k, then the round's inserts are applied in step order with the bitmap as the set.
+__device__ void warp_floyd_bm(int m, int n, uint32_t a, int s, uint64_t seed, int lane, uint32_t *fb)
+{
+    for (int k0 = 0; k0 < n; k0 += 32) {
+        const int k = k0 + lane, j = m - n + k;
+        int t = 0;
+        if (k < n) {
+            uint4 u = philox4(a, (uint32_t)j, (uint32_t)s, TAG_P1, seed);
+            t = (int)randint_u(u.x, (uint32_t)(j + 1));
+        }
+        const int kn = min(32, n - k0);
+        for (int q = 0; q < kn; ++q) {
+            if (lane == q) {
+                const int e = ((fb[t >> 5] >> (t & 31)) & 1u) ? j : t;
+                fb[e >> 5] |= 1u << (e & 31);
+            }
+            __syncwarp();
+        }
+    }
+}
+
 // bounding box (lo3, hi3) of each slice's points: exact fp32 min / max (order-free)
 __global__ void __launch_bounds__(256) k_slice_bbox(const int32_t *__restrict__ slice_off, int32_t s0, int32_t lbase,
                                                     const float4 *__restrict__ prow, float *sbox)
@@ -941,6 +965,7 @@ __global__ void __launch_bounds__(CO_THREADS, CO_MINB) k_coarsen(
     uint8_t *sh_flag = (uint8_t *)(sh_bm + CO_WARPS * 32);
     __shared__ int sh_pool;
     __shared__ int sh_scan[CO_THREADS];
+    __shared__ uint32_t sh_fbm[CO_WARPS][32];   // per-warp Floyd set of a mixed pair with n > 32
 
     const int ls = blockIdx.x, s = s0 + ls;
     const int m = slice_off[s + 1] - slice_off[s];
@@ -1011,8 +1036,16 @@ __global__ void __launch_bounds__(CO_THREADS, CO_MINB) k_coarsen(
             } else {
                 const int o = ml ? r : l;
                 int n = up.nunc[o] < m ? up.nunc[o] : m;
-                int i = warp_floyd(m, n, (uint32_t)up.node[f], s, seed, lane);
-                if (lane < n) atomicOr(&bm[i >> 5], 1u << (i & 31));
+                if (n <= 32) {
+                    int i = warp_floyd(m, n, (uint32_t)up.node[f], s, seed, lane);
+                    if (lane < n) atomicOr(&bm[i >> 5], 1u << (i & 31));
+                } else {   // n(I_o) > 32: an original node brighter than every base pair (P:104 sets no cap)
+                    uint32_t *fb = sh_fbm[w];
+                    fb[lane] = 0u;
+                    __syncwarp();
+                    warp_floyd_bm(m, n, (uint32_t)up.node[f], s, seed, lane, fb);
+                    atomicOr(&bm[lane], fb[lane]);
+                }
             }
             __syncwarp();
             uint32_t word = bm[lane];
