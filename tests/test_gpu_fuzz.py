@@ -36,3 +36,26 @@ def test_random_configs(kind, k):
     for r in o.run_slices(list(range(off.size - 1)), stage=4):
         check_slice(x, fr, img, r)
     fr.close()
+
+
+@pytest.mark.parametrize("k", range(16))
+def test_random_light_trees(k):
+    """lmc_build_light_tree on random VPL sets (sizes from 1 to 40k, coordinate ties, zero and
+    equal intensities, cut sizes beyond the leaf count) equals the oracle node for node (R38)"""
+    rng = np.random.default_rng(330 + k)
+    nv = int(rng.choice([1, 2, 3, 7, 100, 1023, 1024, 1025, 5000, 40000]))
+    v = {a: rng.uniform(-2, 3, nv).astype(np.float32) for a in ("px", "py", "pz")}
+    v.update({a: rng.uniform(-1, 1, nv).astype(np.float32) for a in ("nx", "ny", "nz")})
+    v.update({a: rng.exponential(1.0, nv).astype(np.float32) for a in ("ir", "ig", "ib")})
+    if k % 4 == 1:   # coordinate ties on every axis
+        for a in ("px", "py", "pz"):
+            v[a] = np.round(v[a] * 2) / 2
+    if k % 4 == 2:   # zero and equal intensities
+        for a in ("ir", "ig", "ib"):
+            v[a][::3] = 0.0
+            v[a][1::3] = 1.0
+    cut_max = int(rng.choice([1, 2, 16, 256, 1024, 100000]))
+    got = lmc.build_light_tree(v, cut_max)
+    ref = oracle.build_light_tree(v, cut_max)
+    for key in ("left", "right", "rep", "ir", "ig", "ib", "global_cut"):
+        assert np.array_equal(got[key], ref[key]), (key, nv, cut_max)
