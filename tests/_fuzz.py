@@ -52,6 +52,23 @@ def config_small(k):
         seed=int(rng.integers(1, 2**62)), fixture_seed=int(rng.integers(1, 1000)))
 
 
+def config_tiny(k):
+    """degenerate sizes: 1-3 node cuts, 1-8 row slices, images of a few pixels"""
+    rng = np.random.default_rng(9_000_000 + k)
+    kind = ["cornell", "interior", "mesh"][k % 3]
+    nv = int(rng.integers(1, 50))
+    cut = int(rng.integers(1, min(nv, 3) + 1))
+    solver = int(rng.random() < 0.3)
+    base = scenegen.PRESETS["t_mesh" if kind == "mesh" else "t_cornell" if kind == "cornell" else "t_interior"]
+    return dataclasses.replace(
+        base, name=f"fzT{k}", width=int(rng.integers(1, 9)), height=int(rng.integers(1, 9)), n_vpls=nv,
+        cut_max=cut, slice_target=int(rng.integers(1, 9)), rank_q=int(rng.choice([4, 8, 16, 32])),
+        rate=float(rng.uniform(0.01, 1.0)), tau=TAU[kind] * float(rng.choice([0.0, 1.0, 100.0])), solver=solver,
+        max_iter=int(rng.integers(1, 20)), p1_nmax=int(rng.choice([1, 2, 32])), p1_nmin=1,
+        coarsen_target=1 if rng.random() < 0.3 else 0, mesh_level=1 if kind == "mesh" else 0,
+        seed=int(rng.integers(1, 2**62)), fixture_seed=int(rng.integers(1, 1000)))
+
+
 # configurations that exposed bugs (kept as regression cases): an odd cut size misaligned the u64
 # CDF in k_pass2's shared memory; a mixed pair whose original child is brighter than every base
 # pair needs a Floyd draw of more than 32 rows (P:104)

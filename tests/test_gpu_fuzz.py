@@ -1,6 +1,6 @@
 """Randomised GPU parity: seeded random configurations (tests/_fuzz.py: scene kind incl. triangle
 meshes, image size, VPL count, cut size, slice target, rank, rate, tau, solver, iteration count,
-tolerance, pass-1 counts, the f2-f3 variants, seeds; 48 small and 12 with large slices and cuts); plus the configurations that exposed bugs) — every slice through every stage against the
+tolerance, pass-1 counts, the f2-f3 variants, seeds; 48 small, 12 with large slices and cuts, 12 of a few pixels and 1-3 node cuts); plus the configurations that exposed bugs) — every slice through every stage against the
 oracle with the same bars as tests/test_gpu_parity.check_slice (bit-exact cuts / Omega, completion <= 1e-4, pixels
 <= 1e-3)."""
 import numpy as np
@@ -15,14 +15,15 @@ torch = pytest.importorskip("torch")
 if not torch.cuda.is_available():
     pytest.skip("no GPU", allow_module_level=True)
 from paper_2202_12567_b200 import lmc  # noqa: E402
-from tests._fuzz import REGRESSIONS, config_large, config_small  # noqa: E402
+from tests._fuzz import REGRESSIONS, config_large, config_small, config_tiny  # noqa: E402
 from tests.test_gpu_parity import check_slice  # noqa: E402
 
 
 @pytest.mark.parametrize("kind,k", [("small", k) for k in range(48)] + [("large", k) for k in range(12)] +
-                         [("regression", k) for k in range(len(REGRESSIONS))])
+                         [("tiny", k) for k in range(12)] + [("regression", k) for k in range(len(REGRESSIONS))])
 def test_random_configs(kind, k):
-    cfg = {"small": config_small, "large": config_large, "regression": REGRESSIONS.__getitem__}[kind](k)
+    cfg = {"small": config_small, "large": config_large, "tiny": config_tiny,
+           "regression": REGRESSIONS.__getitem__}[kind](k)
     x = scenegen.make_inputs(cfg)
     fr = lmc.Frame(x)
     img = torch.zeros(x.height * x.width * 3, device="cuda")

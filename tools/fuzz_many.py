@@ -12,14 +12,14 @@ import torch  # noqa: E402
 import oracle  # noqa: E402
 import scenegen  # noqa: E402
 from paper_2202_12567_b200 import lmc  # noqa: E402
-from tests._fuzz import config_large, config_small  # noqa: E402
+from tests._fuzz import config_large, config_small, config_tiny  # noqa: E402
 from tests.test_gpu_parity import check_slice  # noqa: E402
 
 MODE = os.environ.get("FUZZ_MODE", "small")
 
 
 def config(k):
-    return config_large(k) if MODE == "large" else config_small(k)
+    return {"large": config_large, "tiny": config_tiny}.get(MODE, config_small)(k)
 
 
 def run(k):
