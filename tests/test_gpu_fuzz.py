@@ -60,3 +60,41 @@ def test_random_light_trees(k):
     ref = oracle.build_light_tree(v, cut_max)
     for key in ("left", "right", "rep", "ir", "ig", "ib", "global_cut"):
         assert np.array_equal(got[key], ref[key]), (key, nv, cut_max)
+
+
+@pytest.mark.parametrize("k", range(10))
+def test_random_warm_start_sequences(k):
+    """SURVEY f4 on random small configurations: three frames, the albedo of a random share of the
+    pixels changed between frames, ADM warm-started where rows and cut are unchanged (R42); every
+    frame against the oracle's same sequence"""
+    import dataclasses
+    rng = np.random.default_rng(4400 + k)
+    cfg = dataclasses.replace(config_small(k), solver=0, warm_start=1, warm_iters=int(rng.choice([0, 5, 20])),
+                              tol=0.0)
+    xs = [scenegen.make_inputs(cfg)]
+    for _ in range(2):
+        g = dict(xs[-1].gbuf)
+        sel = rng.random(g["px"].size) < rng.uniform(0.0, 0.5)
+        f = np.float32(rng.uniform(0.2, 1.5))
+        for key in ("rho_r", "rho_g", "rho_b"):
+            g[key] = np.where(sel, g[key] * f, g[key]).astype(np.float32)
+        xs.append(dataclasses.replace(xs[-1], gbuf=g))
+    fr = lmc.Frame(xs[0])
+    prev = None
+    for i, x in enumerate(xs):
+        if i:
+            fr.upload_inputs(x)
+        img = torch.zeros(x.height * x.width * 3, device="cuda")
+        fr.run(img)
+        torch.cuda.synchronize()
+        img = img.view(-1, 3).cpu().numpy().astype(np.float64)
+        o = oracle.Oracle(x)
+        if prev is not None:
+            o.set_warm(prev)
+        off, _ = fr.slices()
+        res = o.run_slices(list(range(off.size - 1)), stage=4)
+        assert fr.stats()["n_warm"] == sum(r["warm"] for r in res)
+        for r in res:
+            check_slice(x, fr, img, r)
+        prev = res
+    fr.close()
