@@ -1,6 +1,6 @@
-"""The slice-sharded multi-rank frame on the GPU: world-size 2 (a depth-1 subtree
-per rank: the ranks slice only the top level of the whole G-buffer, then their own subtree) and 3
-(slice index ranges), every rank on GPU 0 with the gloo transport (one GPU is available to the
+"""The slice-sharded multi-rank frame on the GPU: world sizes 2 and 4 (a depth-1 / -2
+subtree per rank: the ranks slice only the top levels of the whole G-buffer, then their own
+subtree) and 3 (slice index ranges), on the interior, Cornell and mesh scenes, every rank on GPU 0 with the gloo transport (one GPU is available to the
 tests; the production path gathers with NCCL inside lmc_resolve_image, one rank per GPU).  Each
 rank runs the CUDA path on its share (lmc_get_partition), packs its rows (lmc_resolve_rows), the
 tiles are gathered to rank 0 and scattered (lmc_scatter_rows): the image must equal the
@@ -66,10 +66,10 @@ def _worker(rank, world, port, name, q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_sharded_frame_equals_single_rank(world):
+@pytest.mark.parametrize("name,world", [("t_interior", 2), ("t_interior", 3), ("t_interior", 4), ("c1", 4),
+                                        ("t_mesh", 2)])
+def test_sharded_frame_equals_single_rank(name, world):
     from paper_2202_12567_b200 import lmc
-    name = "t_interior"
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
