@@ -1272,8 +1272,6 @@ struct P2Args {
     uint16_t *csc_row;
     int32_t *csc_src;
     int32_t *nnz, *target_n, *n_new;
-    uint32_t *newcells;
-    int32_t *newpos;
     unsigned long long *counters;
     int row_importance;            // rows drawn by f(i) = max - min of their carried entries
 };
@@ -1495,7 +1493,7 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2(P2Args A)
     // accepted set is the first N - |carried| distinct unobserved cells in draw order.  While the
     // budget left is at least a whole fast batch (P2_FAST draws per thread), no draw of the batch can
     // be cut off, so every new cell of the batch is accepted and duplicates resolve by atomicOr on
-    // the bitmap in any order (same set; newcells order is not used).  The last batches take the
+    // the bitmap in any order (same set).  The last batches take the
     // exact path: first occurrence per cell by smallest draw index, cut off at the budget.
     for (int64_t t0 = 0; t0 < cap;) {
         const int count = sh_count;
@@ -1505,7 +1503,7 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2(P2Args A)
             for (int u = 0; u < P2_FAST; ++u) {
                 const int64_t t = t0 + (int64_t)u * P2_THREADS + tid;
                 bool isnew = false;
-                int cell = 0, cc = 0;
+                int cc = 0;
                 if (t < cap && n > 0) {
                     uint4 uu = philox4((uint32_t)t, 0u, (uint32_t)s, TAG_P2, A.seed);
                     unsigned long long x = ((unsigned long long)uu.x * Wsum) >> 32;
@@ -1517,18 +1515,12 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2(P2Args A)
                     cc = lo;
                     const int i = A.row_importance ? row_pick(rcdf, m, ((unsigned long long)uu.y * Wr) >> 32)
                                                    : (int)randint_u(uu.y, (uint32_t)m);
-                    cell = (i << 11) | cc;
                     const uint32_t bit = 1u << (cc & 31);
                     isnew = !(atomicOr(&bm[i * W + (cc >> 5)], bit) & bit);
                 }
                 const unsigned bal = __ballot_sync(FULL_MASK, isnew);
-                int base = 0;
-                if (lane == 0 && bal) base = atomicAdd(&sh_bacc, __popc(bal));
-                base = __shfl_sync(FULL_MASK, base, 0);
-                if (isnew) {
-                    atomicAdd(&colcnt[cc], 1);
-                    A.newcells[ob + (count - sh_obs) + base + __popc(bal & ((1u << lane) - 1u))] = (uint32_t)cell;
-                }
+                if (lane == 0 && bal) atomicAdd(&sh_bacc, __popc(bal));
+                if (isnew) atomicAdd(&colcnt[cc], 1);
             }
             __syncthreads();
             if (tid == 0) { sh_count = count + sh_bacc; sh_bacc = 0; }
@@ -1576,7 +1568,6 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2(P2Args A)
         if (accept) {
             atomicOr(&bm[(cell >> 11) * W + (cc >> 5)], 1u << (cc & 31));
             atomicAdd(&colcnt[cc], 1);
-            A.newcells[ob + (count - sh_obs) + pre] = (uint32_t)cell;
             if (pre == remaining - 1) sh_draws = (int)(t + 1);
         }
         __syncthreads();
@@ -1599,7 +1590,6 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2(P2Args A)
             int c = cell & 2047;
             atomicOr(&bm[(cell >> 11) * W + (c >> 5)], 1u << (c & 31));
             colcnt[c] = 1;
-            A.newcells[ob + nd + pre] = (uint32_t)cell;
         }
         __syncthreads();
         if (tid == 0) {
@@ -1645,6 +1635,7 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2(P2Args A)
             while (word) {
                 const int bit = __ffs(word) - 1;
                 word &= word - 1;
+                A.carried[ob + pos] = 0;   // the carried pass below sets the carried entries' flags
                 A.col[ob + pos++] = (uint16_t)(lane * 32 + bit);
             }
         }
@@ -1658,26 +1649,23 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2(P2Args A)
     if (tid == 0) gcp[n] = ctot;
     sh_cpre[tid] = cpre;
     __syncthreads();
-    // a warp per 32-column strip: 32x32 bit blocks of the row-major bitmap are transposed with
-    // ballots, lane b then walks the rows of column 32 wi + b in ascending order
-    for (int wi = w; wi < W; wi += 32) {
-        const int c = wi * 32 + lane;
-        int k = c < n ? sh_cpre[c] : 0;
+    // a warp per column: the lanes test bit c of 32 rows at a time, and the set rows are written in
+    // ascending order by consecutive lanes (coalesced stores of csc_row / csc_src)
+    for (int c = w; c < n; c += P2_THREADS / 32) {
+        const int wi = c >> 5;
+        const uint32_t bit = 1u << (c & 31);
+        int k = sh_cpre[c];
         for (int r0 = 0; r0 < m; r0 += 32) {
-            const uint32_t word = r0 + lane < m ? bm[(r0 + lane) * W + wi] : 0u;
-            uint32_t colw = 0u;   // rows r0..r0+31 of column c
-#pragma unroll
-            for (int b = 0; b < 32; ++b) {
-                const uint32_t bal = __ballot_sync(FULL_MASK, (word >> b) & 1u);
-                if (lane == b) colw = bal;
+            const int i = r0 + lane;
+            const uint32_t word = i < m ? bm[i * W + wi] : 0u;
+            const bool set = (word & bit) != 0u;
+            const unsigned bal = __ballot_sync(FULL_MASK, set);
+            if (set) {
+                const int kk = k + __popc(bal & ((1u << lane) - 1u));
+                A.csc_row[ob + kk] = (uint16_t)i;
+                A.csc_src[ob + kk] = rp[i] + P[i * (W + 1) + wi] + __popc(word & (bit - 1u));
             }
-            while (colw) {
-                const int i = r0 + __ffs(colw) - 1;
-                colw &= colw - 1u;
-                A.csc_row[ob + k] = (uint16_t)i;
-                A.csc_src[ob + k] = csr_pos(bm, P, rp, W, i, c);
-                ++k;
-            }
+            k += __popc(bal);
         }
     }
     // carried values at their CSR positions (flat list over all columns, as above)
@@ -1706,14 +1694,7 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2(P2Args A)
             A.carried[ob + pos] = 1;
         }
     }
-    // new entries: CSR positions (values are evaluated by k_eval_new)
-    for (int k = tid; k < nnew; k += P2_THREADS) {
-        uint32_t cell = A.newcells[ob + k];
-        int i = (int)(cell >> 11), c = (int)(cell & 2047u);
-        int pos = csr_pos(bm, P, rp, W, i, c);
-        A.newpos[ob + k] = pos;
-        A.carried[ob + pos] = 0;
-    }
+    // new entries: their values are evaluated by k_eval_new in CSC order (carried flag 0)
     if (tid == 0) {
         A.nnz[ls] = nnz;
         A.target_n[ls] = (int32_t)N;
@@ -1824,8 +1805,6 @@ cudaError_t run_pass2(lmc_ctx *c)
     A.nnz = c->d.nnz;
     A.target_n = c->d.target_n;
     A.n_new = c->d.n_new;
-    A.newcells = c->d.newcells;
-    A.newpos = c->d.newpos;
     A.counters = c->d.counters;
     A.row_importance = c->cfg.row_importance;
     size_t sm = pass2_smem(c->mmax, c->G);

@@ -99,7 +99,7 @@ void free_all(lmc_ctx *c)
                     d.p1_rows, d.p1_Ta, d.p1_Tb, d.p1_cnt, d.pool_rows, d.pool_Ta, d.pool_Tb, d.pool_used, d.cs_flags,
                     d.cs_eps, d.cs_cost, d.cs_zoff, d.cs_zlen, d.cut_n, d.cut_cols, d.src_off, d.src_len, d.src_side,
                     d.rowptr, d.col, d.val, d.val64, d.Xd, d.Yd, d.val64c, d.carried, d.colptr, d.csc_row, d.csc_src, d.nnz, d.target_n, d.n_new,
-                    d.newcells, d.newpos, d.U, d.V, d.Lam, d.Pi, d.Xold, d.S, d.flags, d.iters, d.resid,
+                    d.newpos, d.U, d.V, d.Lam, d.Pi, d.Xold, d.S, d.flags, d.iters, d.resid,
                     d.direct_rgb, d.counters, d.img, d.rows_rgb, d.vpl_soa, d.r_perm, d.r_len, d.c_perm, d.c_len,
                     d.r_goff, d.c_goff, d.c_nsolo, d.adm_order, d.r_ent, d.c_ent, d.norm, d.r_grp, d.c_grp,
                     d.r_slot, d.c_slot, d.ngrp, d.ctot, d.slot_st, d.ord_tmp, d.ord_cub, d.rank_pix, d.all4, d.prev_cut, d.prev_n, d.prev_flags, d.prev_rows, d.warm_ok, d.bvh, d.tri4, d.keys6};
@@ -742,7 +742,6 @@ static lmc_status create_impl(lmc_ctx *c, const lmc_gbuffer *g, const lmc_vpls *
     CK(dalloc(&d.nnz, SL), "alloc pass2");
     CK(dalloc(&d.target_n, SL), "alloc pass2");
     CK(dalloc(&d.n_new, SL), "alloc pass2");
-    CK(dalloc(&d.newcells, SL * c->ncap), "alloc pass2");
     CK(dalloc(&d.newpos, SL * c->ncap), "alloc pass2");
     // + q: the lane-group ADM kernel reads (and discards) the zero sentinel row m / column n
     CK(dalloc(&d.U, ML * c->q + c->q), "alloc factors");

@@ -109,8 +109,7 @@ struct Dev {
     uint16_t *csc_row;                 // [SL][ncap]
     int32_t *csc_src;                  // [SL][ncap]
     int32_t *nnz, *target_n, *n_new;   // [SL]
-    uint32_t *newcells;                // [SL][ncap] (cell = i << 11 | c)
-    int32_t *newpos;                   // [SL][ncap] CSR position of new cell
+    int32_t *newpos;                   // [SL][ncap] scratch: the completion layouts' CSR index -> S position map
     // completion
     // sliced-ELL layout of Omega for the completion (k_layout)
     uint16_t *r_perm, *r_len;          // [SL][mmax] rows by (length desc, id)
