@@ -1287,14 +1287,23 @@ __device__ __forceinline__ int row_pick(const unsigned long long *rcdf, int m, u
     return lo;
 }
 
-__device__ __forceinline__ int csr_pos(const uint32_t *bm, const uint16_t *P, const int32_t *rp, int W, int i, int c)
+__device__ __forceinline__ int csr_pos(const uint32_t *bm, int Wb, const uint16_t *P, const int32_t *rp, int W, int i, int c)
 {
     const int wi = c >> 5;
-    return rp[i] + P[i * (W + 1) + wi] + __popc(bm[i * W + wi] & ((1u << (c & 31)) - 1u));
+    return rp[i] + P[i * (W + 1) + wi] + __popc(bm[i * Wb + wi] & ((1u << (c & 31)) - 1u));
 }
 
+// P2_PROF (diagnostic build): block-cycles per phase of k_pass2, printed by run_pass2
+#ifdef P2_PROF
+#define P2T(k) do { __syncthreads(); if (threadIdx.x == 0) { long long t_ = clock64(); if (k > 0) atomicAdd(&A.counters[8 + (k) - 1], (unsigned long long)(t_ - p2t0)); p2t0 = t_; } } while (0)
+#else
+#define P2T(k) do { } while (0)
+#endif
 __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2(P2Args A)
 {
+#ifdef P2_PROF
+    long long p2t0 = 0;
+#endif
     extern __shared__ __align__(16) unsigned char smem[];
     typedef cub::BlockScan<int32_t, P2_THREADS> ScanI;
     typedef cub::BlockScan<unsigned long long, P2_THREADS> ScanU;
@@ -1303,11 +1312,12 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2(P2Args A)
     const int n = A.cut_n[ls];
     const int64_t lrow0 = A.slice_off[s] - A.lbase;
     const int W = (n + 31) >> 5;
+    const int Wb = W | 1;   // bitmap row stride in words: odd, so a warp reading one word of 32 rows is conflict-free
     const int64_t cb = (int64_t)ls * A.G, pb = (int64_t)ls * A.pool_cap, ob = (int64_t)ls * A.ncap;
     // shared memory carve-up
-    uint32_t *bm = (uint32_t *)smem;                                    // m*W
-    int32_t *colcnt = (int32_t *)(bm + (size_t)A.mmax * 32);            // G
-    unsigned char *phase = smem + ((((size_t)A.mmax * 32 + A.G) * 4 + 15) & ~(size_t)15);   // 16-byte aligned (odd G)
+    uint32_t *bm = (uint32_t *)smem;                                    // m * Wb
+    int32_t *colcnt = (int32_t *)(bm + (size_t)A.mmax * 33);            // G
+    unsigned char *phase = smem + ((((size_t)A.mmax * 33 + A.G) * 4 + 15) & ~(size_t)15);   // 16-byte aligned (odd G)
     // phase A
     unsigned long long *cdf = (unsigned long long *)phase;              // G (also holds g as double)
     uint32_t *hkey = (uint32_t *)(cdf + A.G);                           // P2_HSLOTS
@@ -1327,11 +1337,12 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2(P2Args A)
     __shared__ int sh_count, sh_obs, sh_nnew, sh_draws, sh_bacc;
     __shared__ int sh_cpre[P2_THREADS];   // per-column prefix offsets (carried entries, CSC)
 
-    for (int k = tid; k < m * W; k += P2_THREADS) bm[k] = 0u;
+    for (int k = tid; k < m * Wb; k += P2_THREADS) bm[k] = 0u;
     for (int c = tid; c < n; c += P2_THREADS) colcnt[c] = 0;
     if (A.row_importance)
         for (int i = tid; i < m; i += P2_THREADS) { rcdf[i] = 0ull; rlo[i] = 0x7FF0000000000000ull; rcnt[i] = 0; }
     __syncthreads();
+    P2T(0);
     // carried observations (R13) and light importance g(c) = max C_c - min C_c.
     // The carried entries of all columns form one flat list (prefix of the per-column counts), so
     // all threads work on them at once; values are >= +0, so their bit patterns order like the
@@ -1367,7 +1378,7 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2(P2Args A)
             const unsigned long long vb = (unsigned long long)__double_as_longlong(v);
             atomicMax(&chi[c], vb);
             atomicMin(&clo[c], vb);
-            atomicOr(&bm[i * W + (c >> 5)], 1u << (c & 31));
+            atomicOr(&bm[i * Wb + (c >> 5)], 1u << (c & 31));
             if (A.row_importance) {
                 atomicMax(&rcdf[i], vb);
                 atomicMin(&rlo[i], vb);
@@ -1382,6 +1393,7 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2(P2Args A)
         }
     }
     __syncthreads();
+    P2T(1);
     // G = max g; integer weights (R14)
     double gmax = 0.0;
     for (int c = tid; c < n; c += P2_THREADS) gmax = fmax(gmax, gcol[c]);
@@ -1484,6 +1496,7 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2(P2Args A)
         __syncthreads();
         Wr = m > 0 ? rcdf[m - 1] : 0ull;
     }
+    P2T(2);
     const int64_t N = (int64_t)ceil(((double)((int64_t)m * (int64_t)n)) * A.rate);
     const int64_t cap = 64 * N;
     if (tid == 0) { sh_count = sh_obs; sh_nnew = 0; sh_draws = 0; sh_bacc = 0; }
@@ -1516,7 +1529,7 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2(P2Args A)
                     const int i = A.row_importance ? row_pick(rcdf, m, ((unsigned long long)uu.y * Wr) >> 32)
                                                    : (int)randint_u(uu.y, (uint32_t)m);
                     const uint32_t bit = 1u << (cc & 31);
-                    isnew = !(atomicOr(&bm[i * W + (cc >> 5)], bit) & bit);
+                    isnew = !(atomicOr(&bm[i * Wb + (cc >> 5)], bit) & bit);
                 }
                 const unsigned bal = __ballot_sync(FULL_MASK, isnew);
                 if (lane == 0 && bal) atomicAdd(&sh_bacc, __popc(bal));
@@ -1543,7 +1556,7 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2(P2Args A)
             cc = lo;
             int i = A.row_importance ? row_pick(rcdf, m, ((unsigned long long)u.y * Wr) >> 32) : (int)randint_u(u.y, (uint32_t)m);
             cell = (i << 11) | cc;   // i < 1024, cc < 2048
-            if (!(bm[i * W + (cc >> 5)] & (1u << (cc & 31)))) key = (uint32_t)cell;
+            if (!(bm[i * Wb + (cc >> 5)] & (1u << (cc & 31)))) key = (uint32_t)cell;
         }
         // first occurrence of each new cell within the batch: a shared hash table keeps the
         // smallest draw index per cell (linear probing, 2 x P2_THREADS slots)
@@ -1566,7 +1579,7 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2(P2Args A)
         const int64_t remaining = N - count;
         const bool accept = acc && pre < remaining;
         if (accept) {
-            atomicOr(&bm[(cell >> 11) * W + (cc >> 5)], 1u << (cc & 31));
+            atomicOr(&bm[(cell >> 11) * Wb + (cc >> 5)], 1u << (cc & 31));
             atomicAdd(&colcnt[cc], 1);
             if (pre == remaining - 1) sh_draws = (int)(t + 1);
         }
@@ -1574,6 +1587,7 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2(P2Args A)
         if (tid == 0) sh_count = count + (int)(tot < remaining ? tot : remaining);
         __syncthreads();
     }
+    P2T(3);
     // one forced entry per still-empty column (R17)
     int nd = sh_count - sh_obs;
     {
@@ -1588,7 +1602,7 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2(P2Args A)
         ScanI(scani_tmp).ExclusiveSum(need, pre, tot);
         if (need) {
             int c = cell & 2047;
-            atomicOr(&bm[(cell >> 11) * W + (c >> 5)], 1u << (c & 31));
+            atomicOr(&bm[(cell >> 11) * Wb + (c >> 5)], 1u << (c & 31));
             colcnt[c] = 1;
         }
         __syncthreads();
@@ -1600,11 +1614,12 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2(P2Args A)
     }
     const int nnew = sh_nnew;
     const int nnz = sh_obs + nnew;
+    P2T(4);
     // phase B: CSR row pointers from per-row word prefix counts.  A warp per row: lane wi takes
     // bitmap word wi (W <= 32), the word prefix is a warp scan, so the row's column indices are
     // then written by all lanes at once in ascending order (consecutive lanes, consecutive ranges).
     for (int i = w; i < m; i += P2_THREADS / 32) {
-        const uint32_t word = lane < W ? bm[i * W + lane] : 0u;
+        const uint32_t word = lane < W ? bm[i * Wb + lane] : 0u;
         const int cnt = __popc(word);
         int incl = cnt;
 #pragma unroll
@@ -1630,7 +1645,7 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2(P2Args A)
     for (int i = tid; i <= m; i += P2_THREADS) grp[i] = rp[i];
     for (int i = w; i < m; i += P2_THREADS / 32) {   // column indices, ascending within the row
         if (lane < W) {
-            uint32_t word = bm[i * W + lane];
+            uint32_t word = bm[i * Wb + lane];
             int pos = rp[i] + P[i * (W + 1) + lane];
             while (word) {
                 const int bit = __ffs(word) - 1;
@@ -1640,6 +1655,7 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2(P2Args A)
             }
         }
     }
+    P2T(5);
     // CSC: column pointers, rows ascending within a column, CSR index of each entry
     int cpre, ctot;
     int cc0 = tid < n ? colcnt[tid] : 0;
@@ -1655,19 +1671,28 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2(P2Args A)
         const int wi = c >> 5;
         const uint32_t bit = 1u << (c & 31);
         int k = sh_cpre[c];
-        for (int r0 = 0; r0 < m; r0 += 32) {
-            const int i = r0 + lane;
-            const uint32_t word = i < m ? bm[i * W + wi] : 0u;
-            const bool set = (word & bit) != 0u;
-            const unsigned bal = __ballot_sync(FULL_MASK, set);
-            if (set) {
-                const int kk = k + __popc(bal & ((1u << lane) - 1u));
-                A.csc_row[ob + kk] = (uint16_t)i;
-                A.csc_src[ob + kk] = rp[i] + P[i * (W + 1) + wi] + __popc(word & (bit - 1u));
+        for (int r0 = 0; r0 < m; r0 += 128) {   // 4 blocks of 32 rows: their loads in flight together
+            uint32_t wd[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int i = r0 + 32 * u + lane;
+                wd[u] = i < m ? bm[i * Wb + wi] : 0u;
             }
-            k += __popc(bal);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int i = r0 + 32 * u + lane;
+                const bool set = (wd[u] & bit) != 0u;
+                const unsigned bal = __ballot_sync(FULL_MASK, set);
+                if (set) {
+                    const int kk = k + __popc(bal & ((1u << lane) - 1u));
+                    A.csc_row[ob + kk] = (uint16_t)i;
+                    A.csc_src[ob + kk] = rp[i] + P[i * (W + 1) + wi] + __popc(wd[u] & (bit - 1u));
+                }
+                k += __popc(bal);
+            }
         }
     }
+    P2T(6);
     // carried values at their CSR positions (flat list over all columns, as above)
     {
         const int sl_t = tid < n ? A.src_len[cb + tid] : 0;
@@ -1688,13 +1713,15 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2(P2Args A)
             const double *Tv = sd ? A.pool_Tb : A.pool_Ta;
             const int i = A.pool_rows[pb + so + k];
             const double v = (lum_rho_d(A.prow, lrow0 + i) * lI) * Tv[pb + so + k];
-            const int pos = csr_pos(bm, P, rp, W, i, c);
+            const int pos = csr_pos(bm, Wb, P, rp, W, i, c);
             A.val[ob + pos] = (float)v;
             if (A.val64) A.val64[ob + pos] = v;
             A.carried[ob + pos] = 1;
         }
     }
+    P2T(7);
     // new entries: their values are evaluated by k_eval_new in CSC order (carried flag 0)
+    P2T(8);
     if (tid == 0) {
         A.nnz[ls] = nnz;
         A.target_n[ls] = (int32_t)N;
@@ -1767,7 +1794,7 @@ static size_t pass2_smem(int mmax, int G)
 {
     size_t phaseA = (size_t)G * 8 + (size_t)P2_HSLOTS * 4 * 2 + (size_t)mmax * 20;   // + row importance
     size_t phaseB = ((((size_t)mmax * 33 + 7) & ~(size_t)7) * 2) + ((size_t)mmax + 1) * 4;
-    size_t base = (((size_t)mmax * 32 + G) * 4 + 15) & ~(size_t)15;
+    size_t base = (((size_t)mmax * 33 + G) * 4 + 15) & ~(size_t)15;
     return base + (phaseA > phaseB ? phaseA : phaseB) + 64;
 }
 
@@ -1817,6 +1844,19 @@ cudaError_t run_pass2(lmc_ctx *c)
         return e;
     }
     k_pass2<<<c->SL, P2_THREADS, sm, c->stream>>>(A);
+#ifdef P2_PROF
+    {
+        cudaStreamSynchronize(c->stream);
+        unsigned long long h[8];
+        cudaMemcpy(h, c->d.counters + 8, sizeof h, cudaMemcpyDeviceToHost);
+        double tot = 0;
+        for (int k = 0; k < 8; ++k) tot += (double)h[k];
+        fprintf(stderr, "k_pass2 phase shares: carried %.3f weights %.3f draws %.3f forced %.3f csr %.3f csc %.3f "
+                "carried-values %.3f tail %.3f\n", h[0] / tot, h[1] / tot, h[2] / tot, h[3] / tot, h[4] / tot, h[5] / tot,
+                h[6] / tot, h[7] / tot);
+        cudaMemsetAsync(c->d.counters + 8, 0, sizeof h, c->stream);
+    }
+#endif
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     dim3 grid(64 / EV_WARPS, c->SL);   // 64 warps per slice
