@@ -1336,6 +1336,7 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2(P2Args A)
     __shared__ int sh_ired[32];
     __shared__ int sh_count, sh_obs, sh_nnew, sh_draws, sh_bacc;
     __shared__ int sh_cpre[P2_THREADS];   // per-column prefix offsets (carried entries, CSC)
+    __shared__ int sh_guide[257];         // CDF guide table of the draws
 
     for (int k = tid; k < m * Wb; k += P2_THREADS) bm[k] = 0u;
     for (int c = tid; c < n; c += P2_THREADS) colcnt[c] = 0;
@@ -1446,6 +1447,24 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2(P2Args A)
     if (tid < n) cdf[tid] = incl;
     __syncthreads();
     const unsigned long long Wsum = n > 0 ? cdf[n - 1] : 0ull;
+    // guide table of the CDF inversion: for the draws whose u has top byte j, x = (u W) >> 32 lies
+    // in [(j W) >> 8, ((j + 1) W) >> 8], so the column is in [guide[j], guide[j + 1]] with guide[j] =
+    // the smallest c with CDF_c > (j W) >> 8 (guide[256] = n - 1): the same smallest c with CDF_c > x
+    // (R29) after a search over a few columns instead of all n
+    if (tid <= 256 && n > 0) {
+        int c = n - 1;
+        if (tid < 256) {
+            const unsigned long long xl = ((unsigned long long)tid * Wsum) >> 8;
+            int lo = 0, hi = n - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (cdf[mid] > xl) hi = mid; else lo = mid + 1;
+            }
+            c = lo;
+        }
+        sh_guide[tid] = c;
+    }
+    __syncthreads();
     // row weights by the rule of the column weights (R14) on f(i) = max - min of row i's carried
     // entries, and the row CDF (DESIGN R36); m <= 1024 = one row per thread
     unsigned long long Wr = 0ull;
@@ -1520,7 +1539,7 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2(P2Args A)
                 if (t < cap && n > 0) {
                     uint4 uu = philox4((uint32_t)t, 0u, (uint32_t)s, TAG_P2, A.seed);
                     unsigned long long x = ((unsigned long long)uu.x * Wsum) >> 32;
-                    int lo = 0, hi = n - 1;
+                    int lo = sh_guide[uu.x >> 24], hi = sh_guide[(uu.x >> 24) + 1];
                     while (lo < hi) {
                         int mid = (lo + hi) >> 1;
                         if (cdf[mid] > x) hi = mid; else lo = mid + 1;
@@ -1548,7 +1567,7 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2(P2Args A)
         if (t < cap && n > 0) {
             uint4 u = philox4((uint32_t)t, 0u, (uint32_t)s, TAG_P2, A.seed);
             unsigned long long x = ((unsigned long long)u.x * Wsum) >> 32;
-            int lo = 0, hi = n - 1;
+            int lo = sh_guide[u.x >> 24], hi = sh_guide[(u.x >> 24) + 1];
             while (lo < hi) {
                 int mid = (lo + hi) >> 1;
                 if (cdf[mid] > x) hi = mid; else lo = mid + 1;
