@@ -262,31 +262,57 @@ __device__ __forceinline__ void stage_scene(SceneConst *dst, int slot)
 }
 
 // Candidate occluders of every segment from a point of a slice (box bx = lo3, hi3) to the VPL
-// position y: the primitives whose bounds meet the box of the slice and y, widened by the
-// screening margin.  Each such segment lies in that box and an exact hit lies on the primitive,
-// so a primitive left out cannot hit.  Warp-collective (lane k tests primitive k of each kind).
+// position y: a primitive is a candidate when (1) its bounds meet the box of the slice and y, and
+// (2) its bounding sphere (S, r) comes within R + r of the segment [C, y], (C, R) the sphere around
+// the slice's box — both widened by the screening margin.  Each segment [x, y] of the slice lies
+// in that box and within distance R of [C, y] (|x - C| <= R), and an exact hit lies on the
+// primitive, so a primitive left out cannot hit.  Warp-collective (lane k tests primitive k of
+// each kind); fp32 with the margin far above its rounding.
 struct Cand {
     uint32_t s, b, r;
 };
+__device__ __forceinline__ bool near_seg(float S0, float S1, float S2, float rad, float C0, float C1, float C2, float w0,
+                                         float w1, float w2, float ww, float reach)
+{
+    // distance from S to the segment C + t w, t in [0, 1], against reach + rad
+    const float v0 = S0 - C0, v1 = S1 - C1, v2 = S2 - C2;
+    const float t = ww > 0.f ? fminf(fmaxf((v0 * w0 + v1 * w1 + v2 * w2) / ww, 0.f), 1.f) : 0.f;
+    const float d0 = v0 - t * w0, d1 = v1 - t * w1, d2 = v2 - t * w2;
+    const float lim = reach + rad;
+    return d0 * d0 + d1 * d1 + d2 * d2 <= lim * lim;
+}
 __device__ __forceinline__ Cand col_candidates(const SceneConst *sc, const float *bx, float y0, float y1, float y2)
 {
     const int lane = threadIdx.x & 31;
     const float mg = sc->margin;
     const float L0 = fminf(bx[0], y0) - mg, L1 = fminf(bx[1], y1) - mg, L2 = fminf(bx[2], y2) - mg;
     const float H0 = fmaxf(bx[3], y0) + mg, H1 = fmaxf(bx[4], y1) + mg, H2 = fmaxf(bx[5], y2) + mg;
+    // sphere around the slice's box, and the segment from its centre to the VPL
+    const float C0 = 0.5f * (bx[0] + bx[3]), C1 = 0.5f * (bx[1] + bx[4]), C2 = 0.5f * (bx[2] + bx[5]);
+    const float e0 = bx[3] - bx[0], e1 = bx[4] - bx[1], e2 = bx[5] - bx[2];
+    const float reach = 0.5f * sqrtf(e0 * e0 + e1 * e1 + e2 * e2) + 2.f * mg;
+    const float w0 = y0 - C0, w1 = y1 - C1, w2 = y2 - C2;
+    const float ww = w0 * w0 + w1 * w1 + w2 * w2;
     bool ps = false, pb = false, pr = false;
     if (lane < sc->nsph) {
         const float *q = sc->sph + 4 * lane;
         const float r = q[3];
-        ps = q[0] - r <= H0 && q[0] + r >= L0 && q[1] - r <= H1 && q[1] + r >= L1 && q[2] - r <= H2 && q[2] + r >= L2;
+        ps = q[0] - r <= H0 && q[0] + r >= L0 && q[1] - r <= H1 && q[1] + r >= L1 && q[2] - r <= H2 && q[2] + r >= L2 &&
+             near_seg(q[0], q[1], q[2], r, C0, C1, C2, w0, w1, w2, ww, reach);
     }
     if (lane < sc->nbox) {
         const float *q = sc->box + 6 * lane;
-        pb = q[0] <= H0 && q[3] >= L0 && q[1] <= H1 && q[4] >= L1 && q[2] <= H2 && q[5] >= L2;
+        const float f0 = q[3] - q[0], f1 = q[4] - q[1], f2 = q[5] - q[2];
+        pb = q[0] <= H0 && q[3] >= L0 && q[1] <= H1 && q[4] >= L1 && q[2] <= H2 && q[5] >= L2 &&
+             near_seg(0.5f * (q[0] + q[3]), 0.5f * (q[1] + q[4]), 0.5f * (q[2] + q[5]),
+                      0.5f * sqrtf(f0 * f0 + f1 * f1 + f2 * f2), C0, C1, C2, w0, w1, w2, ww, reach);
     }
     if (lane < sc->nrect) {
         const float *q = sc->rbox + 6 * lane;
-        pr = q[0] <= H0 && q[3] >= L0 && q[1] <= H1 && q[4] >= L1 && q[2] <= H2 && q[5] >= L2;
+        const float f0 = q[3] - q[0], f1 = q[4] - q[1], f2 = q[5] - q[2];
+        pr = q[0] <= H0 && q[3] >= L0 && q[1] <= H1 && q[4] >= L1 && q[2] <= H2 && q[5] >= L2 &&
+             near_seg(0.5f * (q[0] + q[3]), 0.5f * (q[1] + q[4]), 0.5f * (q[2] + q[5]),
+                      0.5f * sqrtf(f0 * f0 + f1 * f1 + f2 * f2), C0, C1, C2, w0, w1, w2, ww, reach);
     }
     Cand c;
     c.s = __ballot_sync(FULL_MASK, ps);
