@@ -98,3 +98,28 @@ def test_random_warm_start_sequences(k):
             check_slice(x, fr, img, r)
         prev = res
     fr.close()
+
+
+@pytest.mark.parametrize("k", range(6))
+def test_random_configs_host_buffers(k):
+    """the host-buffer path (inputs and image in host memory, as bench.py's e2e uses it) gives the
+    device path's image bit for bit; pixels outside the G-buffer keep their host values"""
+    cfg = config_small(100 + k)
+    x = scenegen.make_inputs(cfg)
+    fr = lmc.Frame(x)
+    img = torch.zeros(x.height * x.width * 3, device="cuda")
+    fr.run(img)
+    torch.cuda.synchronize()
+    ref = img.cpu().numpy()
+    fr.close()
+    frh = lmc.Frame(x, memory=lmc.MEM_HOST)
+    host = np.full(x.height * x.width * 3, 7.0, np.float32)
+    for _ in range(2):   # a re-upload of the same inputs renders the same frame
+        frh.upload_inputs()
+        frh.run(host, lmc.MEM_HOST)
+    frh.close()
+    covered = np.zeros(x.height * x.width, bool)
+    covered[x.gbuf["pixel"]] = True
+    cov3 = np.repeat(covered, 3)
+    assert np.array_equal(host[cov3], ref[cov3])
+    assert np.all(host[~cov3] == 7.0)
