@@ -123,3 +123,24 @@ def test_random_configs_host_buffers(k):
     cov3 = np.repeat(covered, 3)
     assert np.array_equal(host[cov3], ref[cov3])
     assert np.all(host[~cov3] == 7.0)
+
+
+@pytest.mark.parametrize("k", range(6))
+def test_random_configs_deterministic(k):
+    """two contexts on the same inputs give bit-identical images and factors (no float atomics,
+    fixed reduction orders), on random configurations incl. MALS and the variants"""
+    cfg = config_small(200 + k)
+    x = scenegen.make_inputs(cfg)
+    outs = []
+    for _ in range(2):
+        fr = lmc.Frame(x)
+        img = torch.zeros(x.height * x.width * 3, device="cuda")
+        fr.run(img)
+        torch.cuda.synchronize()
+        off, _ = fr.slices()
+        fac = [fr.factors(s) for s in range(off.size - 1)]
+        outs.append((img.cpu().numpy(), fac))
+        fr.close()
+    assert np.array_equal(outs[0][0], outs[1][0])
+    for a, b in zip(outs[0][1], outs[1][1]):
+        assert np.array_equal(a["U"], b["U"]) and np.array_equal(a["V"], b["V"]) and a["iters"] == b["iters"]
