@@ -676,6 +676,9 @@ __global__ void __launch_bounds__(Cfg<Q>::NT, 1) k_adm(CArgs A)
     const char *rent = reinterpret_cast<const char *>(A.r_ent + sb);
     const char *cent = reinterpret_cast<const char *>(A.c_ent + sb);
     float *S = A.S + sb;
+    // rank-level element index of this slice's layout base (SL * scap < 2^32, checked at create):
+    // the hot loops form their global addresses from 32-bit indices and the kernel-parameter bases
+    const uint32_t sb32 = (uint32_t)sb;
     float *X = sm;                                  // (mmax + 1) x Q, row m_s is the zero sentinel
     float *Y = X + (size_t)(A.mmax + 1) * Q;        // (nmax + 1) x Q (column j contiguous), row n_s zero
     float *Bm = Y + (size_t)(A.nmax + 1) * Q;       // (Y Y^T + aI)^{-1}
@@ -742,18 +745,20 @@ __global__ void __launch_bounds__(Cfg<Q>::NT, 1) k_adm(CArgs A)
             const bool valid = rank < m;
             const int row = valid ? rperm[rank] : m;          // m: the zero sentinel row
             const int nch = (rgoff[g + 1] - rgoff[g]) / (CKR * R);
-            const char *eg = rent + (size_t)rgoff[g] * 8;
+            const uint32_t eg32 = sb32 + (uint32_t)rgoff[g] + 2u * (uint32_t)lane;   // this lane's 16 bytes of a chunk
             const float4 x4 = *reinterpret_cast<const float4 *>(X + row * Q + 4 * sub);
             float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+            // gathers address byte offsets from the lane's own float4 slot: column * 4Q + this base
+            const char *ysub = reinterpret_cast<const char *>(Y + 4 * sub);
 #pragma unroll
             for (int p = 0; p < ROW_NS - 1; ++p) {
-                if (p < nch) cp_async16(slot0 + p * 512 + lane * 16, eg + p * 512 + lane * 16);
+                if (p < nch) cp_async16(slot0 + p * 512 + lane * 16, A.r_ent + (eg32 + 64u * p));
                 cp_commit();
             }
             int cs = 0;   // ring stage of chunk c
             for (int c = 0; c < nch; ++c) {
                 const int pf = c + ROW_NS - 1;
-                if (pf < nch) cp_async16(slot0 + (cs == 0 ? ROW_NS - 1 : cs - 1) * 512 + lane * 16, eg + pf * 512 + lane * 16);
+                if (pf < nch) cp_async16(slot0 + (cs == 0 ? ROW_NS - 1 : cs - 1) * 512 + lane * 16, A.r_ent + (eg32 + 64u * pf));
                 cp_commit();
                 cp_wait<ROW_NS - 1>();
                 __syncwarp();
@@ -768,11 +773,11 @@ __global__ void __launch_bounds__(Cfg<Q>::NT, 1) k_adm(CArgs A)
                         // padding entries gather the zero row n of Y: they add exactly 0 and park a
                         // zero residual in the dummy slot, so no masking is needed
                         const unsigned long long w = h == 0 ? wp.x : wp.y;
-                        const float4 y4 = *reinterpret_cast<const float4 *>(Y + (int)((uint32_t)w & 2047u) * Q + 4 * sub);
+                        const float4 y4 = *reinterpret_cast<const float4 *>(ysub + ((uint32_t)w & 2047u) * (4u * Q));
                         const float d = group_sum<Q>(f4dot(x4, y4));
                         const float sv = fmaf(-fd, d, __uint_as_float((uint32_t)(w >> 32)));
                         acc = f4fma(sv, y4, acc);
-                        st_pred(S + (((uint32_t)w) >> 11), sv, sub == 0);
+                        st_pred(A.S + (sb32 + (((uint32_t)w) >> 11)), sv, sub == 0);
                     }
                 }
                 __syncwarp();
@@ -830,15 +835,16 @@ __global__ void __launch_bounds__(Cfg<Q>::NT, 1) k_adm(CArgs A)
             const int colj = valid ? cperm[rank] : n;         // n: the zero sentinel column
             const int cb = cgoff[g];
             const int nch = (cgoff[g + 1] - cb) / (CKC * R);
-            const char *sg = reinterpret_cast<const char *>(S + cb);
-            const char *rg = cent + (size_t)cb * 2;
+            const uint32_t sg32 = sb32 + (uint32_t)cb + 4u * (uint32_t)lane;   // this lane's 16 bytes of S
+            const uint32_t rg32 = sb32 + (uint32_t)cb + 8u * (uint32_t)lane;   // and of rows
             const float4 y4 = *reinterpret_cast<const float4 *>(Y + colj * Q + 4 * sub);
             float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+            const char *xsub = reinterpret_cast<const char *>(X + 4 * sub);
 #pragma unroll
             for (int p = 0; p < COL_NS - 1; ++p) {
                 if (p < nch) {
-                    if (lane < SB / 16) cp_async16(slot0 + p * CST + lane * 16, sg + p * SB + lane * 16);
-                    if (lane < RB / 16) cp_async16(slot0 + p * CST + SB + lane * 16, rg + p * RB + lane * 16);
+                    if (lane < SB / 16) cp_async16(slot0 + p * CST + lane * 16, A.S + (sg32 + (uint32_t)(COL_CHUNK * p)));
+                    if (lane < RB / 16) cp_async16(slot0 + p * CST + SB + lane * 16, A.c_ent + (rg32 + (uint32_t)(COL_CHUNK * p)));
                 }
                 cp_commit();
             }
@@ -847,8 +853,8 @@ __global__ void __launch_bounds__(Cfg<Q>::NT, 1) k_adm(CArgs A)
                 const int pf = c + COL_NS - 1;
                 if (pf < nch) {
                     char *nx = slot0 + (cs == 0 ? COL_NS - 1 : cs - 1) * CST;
-                    if (lane < SB / 16) cp_async16(nx + lane * 16, sg + pf * SB + lane * 16);
-                    if (lane < RB / 16) cp_async16(nx + SB + lane * 16, rg + pf * RB + lane * 16);
+                    if (lane < SB / 16) cp_async16(nx + lane * 16, A.S + (sg32 + (uint32_t)(COL_CHUNK * pf)));
+                    if (lane < RB / 16) cp_async16(nx + SB + lane * 16, A.c_ent + (rg32 + (uint32_t)(COL_CHUNK * pf)));
                 }
                 cp_commit();
                 cp_wait<COL_NS - 1>();
@@ -875,8 +881,8 @@ __global__ void __launch_bounds__(Cfg<Q>::NT, 1) k_adm(CArgs A)
                         for (int h = 0; h < VS; ++h) {
                             // padding: zero row m of X and a zero S slot
                             const int k = k4 + h;
-                            const int row = (int)((rw[k >> 1] >> (16 * (k & 1))) & 0xffffu);
-                            const float4 xv = *reinterpret_cast<const float4 *>(X + row * Q + 4 * sub);
+                            const uint32_t row = (k & 1) ? (rw[k >> 1] >> 16) : (rw[k >> 1] & 0xffffu);
+                            const float4 xv = *reinterpret_cast<const float4 *>(xsub + row * (4u * Q));
                             acc = f4fma(f4get(s4, h), xv, acc);
                         }
                     }

@@ -798,6 +798,8 @@ static lmc_status create_impl(lmc_ctx *c, const lmc_gbuffer *g, const lmc_vpls *
     CK(cudaMemsetAsync(d.img, 0, 3 * sizeof(float) * (size_t)std::max<int64_t>((int64_t)c->W * c->H, 1), c->stream), "memset");
     size_t need = cfg.solver == LMC_SOLVER_MALS ? mals_smem_bytes(c->q, c->mmax, (int)G) : adm_smem_bytes(c->q, c->mmax, (int)G);
     if (c->scap >= (1ll << 21)) return fail(c, LMC_EINVAL, "per-slice sample capacity %lld exceeds 2^21", (long long)c->scap);
+    if ((double)SL * (double)c->scap >= 4294967296.0)   // the ADM kernels index the layout with 32-bit element offsets
+        return fail(c, LMC_EINVAL, "%lld slices x %lld samples of layout capacity exceed 2^32", (long long)SL, (long long)c->scap);
 
     int maxsm = 0, dev = 0;
     CK(cudaGetDevice(&dev), "device");
