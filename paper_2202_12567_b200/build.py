@@ -16,7 +16,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC,-ffp-contract=off",
           "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-Xptxas", "-v"]
-UNITS = [("exact.cu", ["-fmad=false"]), ("complete.cu", []), ("complete2.cu", []), ("mals.cu", []), ("lighttree.cu", ["-fmad=false"]), ("lmc_api.cu", [])]
+UNITS = [("exact.cu", ["-fmad=false"]), ("complete.cu", []), ("complete2.cu", []), ("mals.cu", []), ("lighttree.cu", ["-fmad=false"]), ("slice.cu", ["-fmad=false"]), ("lmc_api.cu", [])]
 
 
 def _nccl_link():

@@ -1290,16 +1290,24 @@ cudaError_t run_rank_pixels(lmc_ctx *c, int32_t *out)
 }
 
 // G-buffer pixel indices must lie in [0, width * height) (lmc.h: LMC_EINVAL otherwise)
-__global__ void k_check_pixels(int64_t M, const int32_t *__restrict__ pixel, int64_t npix, unsigned long long *flag)
+// bit 0: a pixel index outside [0, npix); bit 1: a non-finite position / normal (the slicing keys
+// are exact 32-bit encodings of finite floats, slice.cu)
+__global__ void k_check_pixels(int64_t M, const int32_t *__restrict__ pixel, int64_t npix, const float *__restrict__ px,
+                               const float *__restrict__ py, const float *__restrict__ pz, const float *__restrict__ nx,
+                               const float *__restrict__ ny, const float *__restrict__ nz, unsigned long long *flag)
 {
     int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k < M && (pixel[k] < 0 || pixel[k] >= npix)) atomicOr(flag, 1ull);
+    if (k >= M) return;
+    if (pixel[k] < 0 || pixel[k] >= npix) atomicOr(flag, 1ull);
+    if (!(isfinite(px[k]) && isfinite(py[k]) && isfinite(pz[k]) && isfinite(nx[k]) && isfinite(ny[k]) && isfinite(nz[k])))
+        atomicOr(flag, 2ull);
 }
 cudaError_t run_check_pixels(lmc_ctx *c, unsigned long long *flag)
 {
     cudaError_t e = cudaMemsetAsync(flag, 0, sizeof(unsigned long long), c->stream);
     if (e != cudaSuccess || c->M == 0) return e;
-    k_check_pixels<<<(unsigned)((c->M + 255) / 256), 256, 0, c->stream>>>(c->M, c->d.pixel, (int64_t)c->W * c->H, flag);
+    k_check_pixels<<<(unsigned)((c->M + 255) / 256), 256, 0, c->stream>>>(c->M, c->d.pixel, (int64_t)c->W * c->H, c->d.g[0], c->d.g[1],
+                                                                 c->d.g[2], c->d.g[3], c->d.g[4], c->d.g[5], flag);
     return cudaGetLastError();
 }
 

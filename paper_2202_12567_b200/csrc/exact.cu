@@ -481,172 +481,11 @@ __device__ __forceinline__ double lum_rho_d(const float4 *__restrict__ prow, int
 }
 
 // ------------------------------------------------------------------------------------------
-// Slicing (R26)
+// Row packing in slice order (slicing itself: slice.cu)
 // ------------------------------------------------------------------------------------------
-__device__ __forceinline__ unsigned long long enc_key(double k)
-{
-    k = __dadd_rn(k, 0.0);   // canonical +0 (the reference compares -0 == +0)
-    unsigned long long u = (unsigned long long)__double_as_longlong(k);
-    return (u & 0x8000000000000000ull) ? ~u : (u | 0x8000000000000000ull);
-}
-__device__ __forceinline__ double dec_key(unsigned long long u)
-{
-    u = (u & 0x8000000000000000ull) ? (u & 0x7fffffffffffffffull) : ~u;
-    return __longlong_as_double((long long)u);
-}
-
 struct GView {
     const float *px, *py, *pz, *nx, *ny, *nz;
 };
-
-__device__ __forceinline__ double slice_key(const GView &g, int32_t r, int d, double diag, double wn)
-{
-    switch (d) {
-    case 0: return (double)g.px[r] / diag;
-    case 1: return (double)g.py[r] / diag;
-    case 2: return (double)g.pz[r] / diag;
-    case 3: return wn * (double)g.nx[r];
-    case 4: return wn * (double)g.ny[r];
-    default: return wn * (double)g.nz[r];
-    }
-}
-
-// encoded keys of all 6 dimensions of every G-buffer row, once per frame (row-major, 48 bytes per
-// row): the per-level extent and key kernels then gather one record per row
-__global__ void k_keys6(GView g, int64_t M, double diag, double wn, unsigned long long *keys6)
-{
-    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= 6 * M) return;
-    const int32_t r = (int32_t)(k / 6);
-    keys6[k] = enc_key(slice_key(g, r, (int)(k - 6 * (int64_t)r), diag, wn));
-}
-
-__global__ void k_ext_init(unsigned long long *ext, int n)
-{
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n * 12) ext[i] = (i % 12) < 6 ? 0ull : ~0ull;   // [0,6) max slots, [6,12) min slots
-}
-
-// one CTA per work item (slot, start, len): extents of the 6 key dimensions of a chunk
-__global__ void __launch_bounds__(256) k_slice_extent(const int32_t *__restrict__ rows, const int32_t *__restrict__ work,
-                                                      unsigned long long *ext, const unsigned long long *__restrict__ keys6)
-{
-    int slot = work[3 * blockIdx.x], start = work[3 * blockIdx.x + 1], len = work[3 * blockIdx.x + 2];
-    unsigned long long mx[6], mn[6];
-#pragma unroll
-    for (int d = 0; d < 6; ++d) { mx[d] = 0ull; mn[d] = ~0ull; }
-    for (int k = threadIdx.x; k < len; k += blockDim.x) {
-        const int64_t r = rows[start + k];
-        const ulonglong2 *kr = reinterpret_cast<const ulonglong2 *>(keys6 + 6 * r);
-        const ulonglong2 e01 = kr[0], e23 = kr[1], e45 = kr[2];
-        const unsigned long long ek[6] = {e01.x, e01.y, e23.x, e23.y, e45.x, e45.y};
-#pragma unroll
-        for (int d = 0; d < 6; ++d) {
-            const unsigned long long e = ek[d];
-            mx[d] = e > mx[d] ? e : mx[d];
-            mn[d] = e < mn[d] ? e : mn[d];
-        }
-    }
-    __shared__ unsigned long long red[8][12];
-    int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-#pragma unroll
-    for (int d = 0; d < 6; ++d) {
-        for (int o = 16; o > 0; o >>= 1) {
-            unsigned long long a = __shfl_xor_sync(FULL_MASK, mx[d], o);
-            unsigned long long b = __shfl_xor_sync(FULL_MASK, mn[d], o);
-            mx[d] = a > mx[d] ? a : mx[d];
-            mn[d] = b < mn[d] ? b : mn[d];
-        }
-        if (lane == 0) { red[w][d] = mx[d]; red[w][6 + d] = mn[d]; }
-    }
-    __syncthreads();
-    if (threadIdx.x < 12) {
-        int d = threadIdx.x;
-        unsigned long long v = red[0][d];
-        for (int k = 1; k < (int)(blockDim.x >> 5); ++k) {
-            unsigned long long o = red[k][d];
-            v = d < 6 ? (o > v ? o : v) : (o < v ? o : v);
-        }
-        if (d < 6) atomicMax(&ext[slot * 12 + d], v);
-        else atomicMin(&ext[slot * 12 + d], v);
-    }
-}
-
-__device__ __forceinline__ int tile_of(const int32_t *__restrict__ tbeg, int ntiles, int64_t k)
-{
-    int lo = 0, hi = ntiles - 1;   // last tile with begin <= k
-    while (lo < hi) {
-        int mid = (lo + hi + 1) >> 1;
-        if (tbeg[mid] <= k) lo = mid; else hi = mid - 1;
-    }
-    return lo;
-}
-
-// sort key of every element (encoded key of its tile's split dimension, 0 for tiles that do not
-// split) and the tile of every row
-__global__ void k_slice_keys(const int32_t *__restrict__ rows, int64_t M, const int32_t *__restrict__ tbeg,
-                             const int32_t *__restrict__ tslot, int ntiles, const unsigned long long *__restrict__ ext,
-                             unsigned long long *keys, int32_t *row_tile, const unsigned long long *__restrict__ keys6)
-{
-    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= M) return;
-    const int t = tile_of(tbeg, ntiles, k);
-    const int r = rows[k];
-    row_tile[r] = t;
-    const int slot = tslot[t];
-    if (slot < 0) { keys[k] = 0ull; return; }
-    int best = 0;
-    double bext = -1.0;
-#pragma unroll
-    for (int d = 0; d < 6; ++d) {
-        double e = dec_key(ext[slot * 12 + d]) - dec_key(ext[slot * 12 + 6 + d]);
-        if (e > bext) { bext = e; best = d; }
-    }
-    keys[k] = keys6[6 * (int64_t)r + best];
-}
-
-__global__ void k_tile_keys(const int32_t *__restrict__ rows_sorted, const int32_t *__restrict__ row_tile, int64_t M,
-                            uint32_t *tkey)
-{
-    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k < M) tkey[k] = (uint32_t)row_tile[rows_sorted[k]];
-}
-
-// rows now in (tile, key, row) order: the lower ceil(n/2) of a splitting tile go left (R26)
-__global__ void k_split_flags(const int32_t *__restrict__ rows_sorted, int64_t M, const int32_t *__restrict__ tbeg,
-                              const int32_t *__restrict__ tend, const int32_t *__restrict__ tslot, int ntiles,
-                              int32_t *left_by_row)
-{
-    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= M) return;
-    const int t = tile_of(tbeg, ntiles, k);
-    const int len = tend[t] - tbeg[t];
-    const int nl = tslot[t] < 0 ? len : (len + 1) / 2;
-    left_by_row[rows_sorted[k]] = (k - tbeg[t]) < nl ? 1 : 0;
-}
-
-__global__ void k_gather_flags(const int32_t *__restrict__ rows, const int32_t *__restrict__ left_by_row, int64_t M,
-                               int32_t *f)
-{
-    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k < M) f[k] = left_by_row[rows[k]];
-}
-
-// stable partition of every tile (in its ascending-row input order) into left / right child
-__global__ void k_split_scatter(const int32_t *__restrict__ rows, const int32_t *__restrict__ f,
-                                const int32_t *__restrict__ pre, int64_t M, const int32_t *__restrict__ tbeg,
-                                const int32_t *__restrict__ tend, const int32_t *__restrict__ tslot, int ntiles,
-                                int32_t *rows_out)
-{
-    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= M) return;
-    const int t = tile_of(tbeg, ntiles, k);
-    const int b = tbeg[t], len = tend[t] - b;
-    const int nl = tslot[t] < 0 ? len : (len + 1) / 2;
-    const int before_left = pre[k] - pre[b];
-    const int pos = f[k] ? b + before_left : b + nl + ((int)(k - b) - before_left);
-    rows_out[pos] = rows[k];
-}
 
 __global__ void k_pack_rows(const int32_t *__restrict__ rows, int64_t row0, int64_t ML, GView g,
                             const float *__restrict__ vx, const float *__restrict__ vy, const float *__restrict__ vz,
@@ -701,99 +540,12 @@ cudaError_t run_pack_vpls(lmc_ctx *c)
 
 
 
-cudaError_t slicing_tmp_bytes(int64_t M, int32_t max_tiles, size_t *bytes)
-{
-    size_t a = 0, b = 0, d = 0, sg = 0;
-    cudaError_t e = cub::DeviceRadixSort::SortPairs<unsigned long long, int32_t>(
-        nullptr, a, (const unsigned long long *)nullptr, (unsigned long long *)nullptr, (const int32_t *)nullptr,
-        (int32_t *)nullptr, (int)M, 0, 64, 0);
-    if (e != cudaSuccess) return e;
-    e = cub::DeviceRadixSort::SortPairs<uint32_t, int32_t>(nullptr, b, (const uint32_t *)nullptr, (uint32_t *)nullptr,
-                                                            (const int32_t *)nullptr, (int32_t *)nullptr, (int)M, 0, 32, 0);
-    if (e != cudaSuccess) return e;
-    e = cub::DeviceScan::ExclusiveSum(nullptr, d, (const int32_t *)nullptr, (int32_t *)nullptr, (int)M, 0);
-    if (e != cudaSuccess) return e;
-    e = cub::DeviceSegmentedSort::StableSortPairs<unsigned long long, int32_t>(
-        nullptr, sg, (const unsigned long long *)nullptr, (unsigned long long *)nullptr, (const int32_t *)nullptr,
-        (int32_t *)nullptr, (int)M, std::max(max_tiles, 1), (const int32_t *)nullptr, (const int32_t *)nullptr, 0);
-    *bytes = std::max(std::max(a, b), std::max(d, sg));
-    return e;
-}
-
 static GView gview(lmc_ctx *c)
 {
     GView g;
     g.px = c->d.g[0]; g.py = c->d.g[1]; g.pz = c->d.g[2];
     g.nx = c->d.g[3]; g.ny = c->d.g[4]; g.nz = c->d.g[5];
     return g;
-}
-
-__global__ void k_iota(int32_t *a, int64_t n)
-{
-    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k < n) a[k] = (int32_t)k;
-}
-
-#ifndef SLICE_SEG_MIN
-#define SLICE_SEG_MIN 128   // levels with at least this many tiles use the segmented sort (measured: 16 -> 7.2 ms, 2 -> 31 ms, 128 -> 4.7 ms, never -> 5.1 ms of slicing at C4)
-#endif
-// per level: extents -> split keys -> radix sort by key (stable, rows ascending within ties) ->
-// stable radix sort by tile -> lower-median flags -> stable partition of the ascending-row tiles.
-cudaError_t run_slicing(lmc_ctx *c)
-{
-    cudaStream_t st = c->stream;
-    const int64_t M = c->M;
-    GView g = gview(c);
-    const double diag = c->diag, wn = c->cfg.normal_weight;
-    if (M == 0) return cudaSuccess;
-    const unsigned nb = (unsigned)((M + 255) / 256);
-    int32_t *rows = c->d.rows, *alt = c->d.rows_alt;
-    int32_t *row_tile = c->d.sl_i32, *f = c->d.sl_i32 + M, *pre = c->d.sl_i32 + 2 * M, *tmp_rows = c->d.sl_i32 + 3 * M;
-    uint32_t *tkey = reinterpret_cast<uint32_t *>(c->d.keys), *tkey_alt = reinterpret_cast<uint32_t *>(c->d.keys) + M;
-    k_iota<<<nb, 256, 0, st>>>(rows, M);
-    k_keys6<<<(unsigned)((6 * M + 255) / 256), 256, 0, st>>>(g, M, diag, wn, c->d.keys6);
-    for (const auto &L : c->levels) {
-        // rows [L.lo, L.lo + L.n) of this level (all rows, or this rank's subtree): every position
-        // array is offset by lo; row_tile / left-flags are indexed by the G-buffer row itself
-        const int64_t lo = L.lo, n = L.n;
-        const unsigned nbl = (unsigned)((n + 255) / 256);
-        int32_t *rws = rows + lo, *alt_l = alt + lo, *f_l = f + lo, *pre_l = pre + lo, *tmp_l = tmp_rows + lo;
-        uint32_t *tkey_l = tkey + lo, *tkey_alt_l = tkey_alt + lo;
-        const int32_t *tbeg = c->d.lvl_begin + L.tile_off;
-        const int32_t *tend = c->d.lvl_end + L.tile_off;
-        const int32_t *tslot = c->d.lvl_slot + L.tile_off;
-        k_ext_init<<<(L.nslots * 12 + 255) / 256, 256, 0, st>>>(c->d.ext, L.nslots);
-        k_slice_extent<<<L.work_n, 256, 0, st>>>(rws, c->d.lvl_work + 3 * L.work_off, c->d.ext, c->d.keys6);
-        k_slice_keys<<<nbl, 256, 0, st>>>(rws, n, tbeg, tslot, L.tile_n, c->d.ext, c->d.keys_alt + lo, row_tile, c->d.keys6);
-        size_t bytes = c->d.cub_tmp_bytes;
-        unsigned long long *kin = c->d.keys_alt + lo, *kout = c->d.keys_sorted + lo;
-        cudaError_t e;
-        if (L.tile_n >= SLICE_SEG_MIN) {
-            // tiles are contiguous ranges of `rows` (ascending rows inside): one stable segmented
-            // sort by key per tile gives the same (tile, key, row) order as the two global sorts
-            e = cub::DeviceSegmentedSort::StableSortPairs(c->d.cub_tmp, bytes, kin, kout, rws, tmp_l, (int)n,
-                                                          L.tile_n, tbeg, tend, st);
-            if (e != cudaSuccess) return e;
-        } else {
-            e = cub::DeviceRadixSort::SortPairs(c->d.cub_tmp, bytes, kin, kout, rws, alt_l, (int)n, 0, 64, st);
-            if (e != cudaSuccess) return e;
-            k_tile_keys<<<nbl, 256, 0, st>>>(alt_l, row_tile, n, tkey_l);
-            int tbits = 1;
-            while ((1 << tbits) < L.tile_n) ++tbits;
-            bytes = c->d.cub_tmp_bytes;
-            e = cub::DeviceRadixSort::SortPairs(c->d.cub_tmp, bytes, tkey_l, tkey_alt_l, alt_l, tmp_l, (int)n, 0, tbits, st);
-            if (e != cudaSuccess) return e;
-        }
-        k_split_flags<<<nbl, 256, 0, st>>>(tmp_l, n, tbeg, tend, tslot, L.tile_n, alt /* left_by_row */);
-        k_gather_flags<<<nbl, 256, 0, st>>>(rws, alt, n, f_l);
-        bytes = c->d.cub_tmp_bytes;
-        e = cub::DeviceScan::ExclusiveSum(c->d.cub_tmp, bytes, f_l, pre_l, (int)n, st);
-        if (e != cudaSuccess) return e;
-        k_split_scatter<<<nbl, 256, 0, st>>>(rws, f_l, pre_l, n, tbeg, tend, tslot, L.tile_n, tmp_l);
-        e = cudaMemcpyAsync(rws, tmp_l, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, st);
-        if (e != cudaSuccess) return e;
-    }
-    return cudaGetLastError();
 }
 
 cudaError_t run_pack_rows(lmc_ctx *c)

@@ -94,15 +94,15 @@ void free_all(lmc_ctx *c)
     }
     Dev &d = c->d;
     void *ptrs[] = {d.pixel, d.g[0], d.g[1], d.g[2], d.g[3], d.g[4], d.g[5], d.g[6], d.g[7], d.g[8], d.g[9], d.g[10],
-                    d.g[11], d.g[12], d.expo, d.vpl, d.ut_i32, d.ut_lum, d.ut_I, d.rows, d.rows_alt, d.keys,
-                    d.keys_alt, d.keys_sorted, d.sl_i32, d.lvl_begin, d.lvl_end, d.lvl_slot, d.lvl_work, d.ext, d.slice_off, d.cub_tmp, d.prow, d.sbox,
+                    d.g[11], d.g[12], d.expo, d.vpl, d.ut_i32, d.ut_lum, d.ut_I, d.rows, d.rows_alt, d.sk,
+                    d.sl_ext, d.sl_hist, d.sl_cnt, d.sl_state, d.lvl_begin, d.lvl_end, d.lvl_slot, d.lvl_work, d.slice_off, d.prow, d.sbox,
                     d.p1_rows, d.p1_Ta, d.p1_Tb, d.p1_cnt, d.pool_rows, d.pool_Ta, d.pool_Tb, d.pool_used, d.cs_flags,
                     d.cs_eps, d.cs_cost, d.cs_zoff, d.cs_zlen, d.cut_n, d.cut_cols, d.src_off, d.src_len, d.src_side,
                     d.rowptr, d.col, d.val, d.val64, d.Xd, d.Yd, d.val64c, d.carried, d.colptr, d.csc_row, d.csc_src, d.nnz, d.target_n, d.n_new,
                     d.newpos, d.U, d.V, d.Lam, d.Pi, d.Xold, d.S, d.flags, d.iters, d.resid,
                     d.direct_rgb, d.counters, d.img, d.rows_rgb, d.vpl_soa, d.r_perm, d.r_len, d.c_perm, d.c_len,
                     d.r_goff, d.c_goff, d.c_nsolo, d.adm_order, d.r_ent, d.c_ent, d.norm, d.r_grp, d.c_grp,
-                    d.r_slot, d.c_slot, d.ngrp, d.ctot, d.slot_st, d.ord_tmp, d.ord_cub, d.rank_pix, d.all4, d.prev_cut, d.prev_n, d.prev_flags, d.prev_rows, d.warm_ok, d.bvh, d.tri4, d.keys6};
+                    d.r_slot, d.c_slot, d.ngrp, d.ctot, d.slot_st, d.ord_tmp, d.ord_cub, d.rank_pix, d.all4, d.prev_cut, d.prev_n, d.prev_flags, d.prev_rows, d.warm_ok, d.bvh, d.tri4};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (c->h_stage) cudaFreeHost(c->h_stage);
@@ -377,7 +377,7 @@ lmc_status build_levels(lmc_ctx *c)
             if ((n.depth == d || (n.leaf && n.depth < d)) && n.start >= lo && n.start < hi) out.push_back(n);
         std::sort(out.begin(), out.end(), [](const Node &a, const Node &b) { return a.start < b.start; });
     };
-    int max_tiles = 1;
+    int max_tiles = 1, max_slots = 1, max_work = 1;
     std::vector<Node> cur;
     for (int d = 0; d < maxd; ++d) {
         const bool sub = k >= 0 && d >= k;
@@ -389,26 +389,36 @@ lmc_status build_levels(lmc_ctx *c)
         L.tile_off = (int32_t)beg.size();
         L.tile_n = (int32_t)cur.size();
         int ns = 0;
-        L.work_off = (int32_t)(work.size() / 3);
-        for (auto &n : cur) {
+        int32_t maxlen = 0;
+        for (auto &n : cur) maxlen = std::max(maxlen, n.len);
+        L.fused = maxlen <= 8192;
+        const size_t w0 = work.size();
+        L.work_off = (int32_t)(work.size() / 4);
+        for (int ti = 0; ti < (int)cur.size(); ++ti) {
+            const Node &n = cur[ti];
             beg.push_back(n.start - (int32_t)lo);
             end.push_back(n.start + n.len - (int32_t)lo);
-            if (n.depth == d && !n.leaf) {
-                slot.push_back(ns);
+            const bool split = n.depth == d && !n.leaf;
+            slot.push_back(split ? ns++ : -1);
+            if (!L.fused) {   // chunks of <= 4096 rows of every tile (leaves: copied through)
+                const int32_t first = (int32_t)((work.size() - w0) / 4);
                 for (int32_t o = 0; o < n.len; o += 4096) {
-                    work.push_back(ns);
+                    work.push_back(ti);
                     work.push_back(n.start - (int32_t)lo + o);
                     work.push_back(std::min<int32_t>(4096, n.len - o));
+                    work.push_back(first);
                 }
-                ++ns;
-            } else {
-                slot.push_back(-1);
             }
         }
-        L.work_n = (int32_t)(work.size() / 3) - L.work_off;
+        L.work_n = (int32_t)(work.size() / 4) - L.work_off;
         L.nslots = ns;
         max_tiles = std::max(max_tiles, (int)cur.size());
-        if (L.n > 0 && ns > 0) c->levels.push_back(L);
+        if (L.n > 0 && ns > 0) {
+            c->levels.push_back(L);
+            if (!L.fused) { max_slots = std::max(max_slots, ns); max_work = std::max(max_work, (int)L.work_n); }
+        } else {
+            work.resize(w0);
+        }
     }
     c->max_tiles = max_tiles;
     Dev &d = c->d;
@@ -416,7 +426,10 @@ lmc_status build_levels(lmc_ctx *c)
     CK(dalloc(&d.lvl_end, end.size()), "alloc slicing");
     CK(dalloc(&d.lvl_slot, slot.size()), "alloc slicing");
     CK(dalloc(&d.lvl_work, work.size()), "alloc slicing");
-    CK(dalloc(&d.ext, (size_t)max_tiles * 12), "alloc slicing");
+    CK(dalloc(&d.sl_ext, (size_t)max_slots * 12), "alloc slicing");
+    CK(dalloc(&d.sl_hist, (size_t)max_slots * 1024), "alloc slicing");
+    CK(dalloc(&d.sl_state, (size_t)max_slots * 4), "alloc slicing");
+    CK(dalloc(&d.sl_cnt, (size_t)max_work * 2), "alloc slicing");
     if (!beg.empty()) {
         CK(cudaMemcpy(d.lvl_begin, beg.data(), beg.size() * 4, cudaMemcpyHostToDevice), "upload slicing");
         CK(cudaMemcpy(d.lvl_end, end.data(), end.size() * 4, cudaMemcpyHostToDevice), "upload slicing");
@@ -590,7 +603,9 @@ static lmc_status create_impl(lmc_ctx *c, const lmc_gbuffer *g, const lmc_vpls *
         sc->n_rect > MAX_PRIMS)
         return fail(c, LMC_EINVAL, "at most %d occluders of each kind", MAX_PRIMS);
     if ((sc->n_sph && !sc->sph) || (sc->n_box && !sc->box) || (sc->n_rect && !sc->rect)) return fail(c, LMC_EINVAL, "null occluder array");
-    if (!(sc->diag > 0.0)) return fail(c, LMC_EINVAL, "scene diagonal must be > 0");
+    if (!(sc->diag >= 1e-30 && sc->diag <= 1e30)) return fail(c, LMC_EINVAL, "scene diagonal must be in [1e-30, 1e30]");
+    if (!(cfg.normal_weight == 0.0 || (cfg.normal_weight >= 1e-30 && cfg.normal_weight <= 1e30)))
+        return fail(c, LMC_EINVAL, "normal_weight must be 0 or in [1e-30, 1e30]");
     if (sc->n_tri < 0 || sc->n_tri > (1 << 26) || (sc->n_tri && !sc->tri)) return fail(c, LMC_EINVAL, "bad triangle array");
     c->M = g->count;
     c->W = g->width;
@@ -699,13 +714,7 @@ static lmc_status create_impl(lmc_ctx *c, const lmc_gbuffer *g, const lmc_vpls *
     CK(dalloc(&d.vpl_soa, 6 * (size_t)c->NV), "alloc vpls");
     CK(dalloc(&d.rows, M), "alloc slicing");
     CK(dalloc(&d.rows_alt, M), "alloc slicing");
-    CK(dalloc(&d.keys, M), "alloc slicing");
-    CK(dalloc(&d.keys_alt, M), "alloc slicing");
-    CK(dalloc(&d.keys_sorted, M), "alloc slicing");
-    CK(dalloc(&d.keys6, 6 * M), "alloc slicing");
-    CK(dalloc(&d.sl_i32, 4 * M), "alloc slicing");
-    CK(slicing_tmp_bytes(std::max<int64_t>(M, 1), c->max_tiles, &d.cub_tmp_bytes), "cub sizing");
-    CK(cudaMalloc(&d.cub_tmp, std::max<size_t>(d.cub_tmp_bytes, 16)), "alloc cub");
+    CK(dalloc(&d.sk, 12 * M), "alloc slicing");
     CK(dalloc(&d.prow, 4 * (size_t)ML), "alloc rows");
     const int64_t nB = c->up.nB, U = c->up.U;
     CK(dalloc(&d.p1_rows, SL * nB * c->nmax), "alloc pass1");
@@ -875,7 +884,8 @@ lmc_status lmc_upload_inputs(lmc_ctx *c, const lmc_gbuffer *g, const lmc_vpls *v
     unsigned long long bad = 0;
     CK(cudaMemcpyAsync(&bad, d.counters + 8, sizeof bad, cudaMemcpyDeviceToHost, st), "check pixels");
     CK(cudaStreamSynchronize(st), "sync");
-    if (bad) return fail(c, LMC_EINVAL, "a G-buffer pixel index is outside [0, width * height)");
+    if (bad & 1ull) return fail(c, LMC_EINVAL, "a G-buffer pixel index is outside [0, width * height)");
+    if (bad & 2ull) return fail(c, LMC_EINVAL, "a G-buffer position or normal is not finite");
     c->state = 0;
     return LMC_OK;
 }
@@ -896,7 +906,7 @@ lmc_status lmc_build_slices(lmc_ctx *c)
     CK(cudaMemsetAsync(c->d.counters, 0, 8 * sizeof(unsigned long long), c->stream), "memset counters");
     CK(run_slicing(c), "slicing");
     CK(run_pack_rows(c), "pack rows");
-    c->launches += (c->M > 0 ? 2 : 0) + 11 * (int64_t)c->levels.size();   // CUB sorts / scan: 1 each
+    c->launches += slicing_launches(c) + (c->M > 0 ? 1 : 0);   // + the row packing
     ev_rec(c, 1);
     c->state = 1;
     return LMC_OK;

@@ -70,17 +70,16 @@ struct Dev {
     double *ut_lum;
     float *ut_I;
     // slicing
-    int32_t *rows, *rows_alt;          // M
-    unsigned long long *keys, *keys_alt, *keys_sorted; // M each (keys also holds 2M uint32 tile keys)
-    unsigned long long *keys6;         // 6 M: encoded keys of the 6 dimensions per G-buffer row
-    int32_t *sl_i32;                   // 4M: row_tile, flags, prefix, rows scratch
+    int32_t *rows, *rows_alt;          // M each: slicing order, ping-pong
+    uint32_t *sk;                      // 2 x 6 M: order-preserving 32-bit keys of the 6 dimensions (SoA, ping-pong)
     int32_t *lvl_begin, *lvl_end;      // concatenated level tilings
-    int32_t *lvl_slot;                 // per tile: extent slot of a splitting tile, -1 otherwise
-    int32_t *lvl_work;                 // concatenated extent work items (seg, start, len) triples
-    unsigned long long *ext;           // max-segments * 12
+    int32_t *lvl_slot;                 // per tile: slot of a splitting tile, -1 otherwise
+    int32_t *lvl_work;                 // chunked levels: work items (tile, start, len, first item of the tile)
+    uint32_t *sl_ext;                  // [slots][12] encoded per-dimension maxima / minima
+    uint32_t *sl_hist;                 // [slots][4][256] radix-select histograms
+    uint32_t *sl_cnt;                  // [2 x work items] rows below / equal to the threshold per chunk
+    uint32_t *sl_state;                // [slots][4] threshold key, rows of it going left, dimension, ceil(n/2)
     int32_t *slice_off;                // S+1
-    void *cub_tmp;
-    size_t cub_tmp_bytes;
     float4 *prow;                      // 4 per local row (slice order)
     float *sbox;                       // [SL][6] bounding box (lo3, hi3) of each slice's points (fp32, exact)
     // pass 1: [SL][nB][nmax]
@@ -171,7 +170,8 @@ struct lmc_ctx {
     int32_t adm2_Tr = 64, adm2_Tc = 64;   // segment length caps (rows, columns)
     bool use_adm2 = false;         // complete2.cu kernels (q <= 16) instead of complete.cu
     // slicing level structure
-    struct Level { int64_t lo, n; int32_t tile_off, tile_n, work_off, work_n, nslots; };   // rows [lo, lo + n); tiles relative to lo
+    // rows [lo, lo + n); tiles relative to lo; fused: every tile <= 8192 rows (one CTA per tile)
+    struct Level { int64_t lo, n; int32_t tile_off, tile_n, work_off, work_n, nslots; bool fused; };
     int32_t sub_k = -1;            // P = 2^k ranks: slicing levels >= k run in this rank's subtree only
     std::vector<int32_t> h_part_slice;   // [world + 1] first slice of every rank
     std::vector<int64_t> h_part_row;     // [world + 1] first row of every rank
@@ -208,7 +208,7 @@ cudaError_t run_pass2(lmc_ctx *c);
 cudaError_t run_direct(lmc_ctx *c);
 cudaError_t run_eval_entries(lmc_ctx *c, int64_t n, const int32_t *d_rows, const int32_t *d_vpls, double *d_out,
                              float4 *d_tmp_rows);
-cudaError_t slicing_tmp_bytes(int64_t M, int32_t max_tiles, size_t *bytes);
+int64_t slicing_launches(const lmc_ctx *c);
 cudaError_t run_pack_vpls(lmc_ctx *c);
 int acquire_scene_slot();
 void release_scene_slot(int slot);
