@@ -391,7 +391,7 @@ lmc_status build_levels(lmc_ctx *c)
         int ns = 0;
         int32_t maxlen = 0;
         for (auto &n : cur) maxlen = std::max(maxlen, n.len);
-        L.fused = maxlen <= 8192;
+        L.fused = maxlen <= 8192 || (int)cur.size() >= 64;   // slice.cu: one CTA per tile
         const size_t w0 = work.size();
         L.work_off = (int32_t)(work.size() / 4);
         for (int ti = 0; ti < (int)cur.size(); ++ti) {

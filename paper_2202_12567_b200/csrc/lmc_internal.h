@@ -170,7 +170,7 @@ struct lmc_ctx {
     int32_t adm2_Tr = 64, adm2_Tc = 64;   // segment length caps (rows, columns)
     bool use_adm2 = false;         // complete2.cu kernels (q <= 16) instead of complete.cu
     // slicing level structure
-    // rows [lo, lo + n); tiles relative to lo; fused: every tile <= 8192 rows (one CTA per tile)
+    // rows [lo, lo + n); tiles relative to lo; fused: one CTA per tile (slice.cu)
     struct Level { int64_t lo, n; int32_t tile_off, tile_n, work_off, work_n, nslots; bool fused; };
     int32_t sub_k = -1;            // P = 2^k ranks: slicing levels >= k run in this rank's subtree only
     std::vector<int32_t> h_part_slice;   // [world + 1] first slice of every rank

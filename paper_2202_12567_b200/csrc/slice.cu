@@ -14,9 +14,9 @@
 // four 8-bit MSB-first histogram passes.  Extents are computed in fp64 from the float extremes
 // exactly as the fp64 keys would give them.
 //
-// Levels whose tiles all have <= 8192 rows run one CTA per tile (everything in registers and
-// shared memory, one launch per level); larger tiles run as chunks of <= 4096 rows over
-// extent / 4 histogram passes / count / scatter launches with per-tile histograms in HBM.
+// Levels with many tiles (or only tiles of <= 8192 rows) run one CTA per tile, one launch per
+// level; the top levels (few, large tiles) run as chunks of <= 4096 rows over extent /
+// 4 histogram passes / count / scatter launches with per-tile histograms in HBM.
 #include <cstdint>
 #include <cstdio>
 
@@ -41,6 +41,12 @@ __device__ __forceinline__ float dec32(uint32_t u)
 struct SliceKeys {   // 6 SoA key arrays of one ping-pong buffer, each M long
     uint32_t *k[6];
 };
+
+__device__ __forceinline__ const uint32_t *key_dim(const SliceKeys &K, int d)
+{
+    // select without indexing the parameter array (no local-memory copy)
+    return d == 0 ? K.k[0] : d == 1 ? K.k[1] : d == 2 ? K.k[2] : d == 3 ? K.k[3] : d == 4 ? K.k[4] : K.k[5];
+}
 
 // fp64 key of dimension d of the float decoded from an extreme, +0 canonical (as the fp64 keys)
 __device__ __forceinline__ double key64(uint32_t e, int d, double diag, double wn)
@@ -99,7 +105,7 @@ __device__ __forceinline__ void pick_bucket(uint32_t h, uint32_t k, uint32_t *sh
     __syncthreads();
 }
 
-// ---- chunked path (tiles > 8192 rows) --------------------------------------------------------
+// ---- chunked path (the top levels) --------------------------------------------------------
 // work item w: (tile, start, len, first work item of the tile), positions relative to the level
 struct LvArgs {
     const int32_t *tbeg, *tend, *tslot, *work;
@@ -190,7 +196,7 @@ __global__ void __launch_bounds__(256) k_sl_hist(LvArgs A, int pass)
     __shared__ uint32_t h[256];
     h[threadIdx.x] = 0u;
     __syncthreads();
-    const uint32_t *kd = A.kin.k[dim] + A.lo + start;
+    const uint32_t *kd = key_dim(A.kin, dim) + A.lo + start;
     const int sh = 24 - 8 * pass;
     for (int i = threadIdx.x; i < len; i += blockDim.x) {
         const uint32_t e = kd[i];
@@ -214,7 +220,7 @@ __global__ void __launch_bounds__(256) k_sl_count(LvArgs A)
         uint32_t *st = A.state + 4 * slot;
         st[0] = kstar; st[1] = need; st[2] = (uint32_t)dim; st[3] = (uint32_t)((n + 1) / 2);
     }
-    const uint32_t *kd = A.kin.k[dim] + A.lo + start;
+    const uint32_t *kd = key_dim(A.kin, dim) + A.lo + start;
     uint32_t c = 0;
     for (int i = threadIdx.x; i < len; i += blockDim.x) {
         const uint32_t e = kd[i];
@@ -250,6 +256,25 @@ __device__ __forceinline__ uint32_t block_excl_256(uint32_t v, uint32_t *sh_w)
     return base + x - v;
 }
 
+// Staged output of a run of nr rows (source positions src .. src + nr): row i goes to local slot
+// sl[i]; slots [0, nleft) are the left child's positions L0 .., the rest the right child's R0 ..
+// (both contiguous).  Each array is scattered into shared memory and written out coalesced.
+__device__ __forceinline__ void staged_copy(const int32_t *rows_in, int32_t *rows_out, const SliceKeys &kin,
+                                            const SliceKeys &kout, int64_t src, int nr, const uint16_t *sl,
+                                            uint32_t *stage, int nleft, int64_t L0, int64_t R0)
+{
+    const int t = threadIdx.x, NT = blockDim.x;
+#pragma unroll
+    for (int a = 0; a < 7; ++a) {   // unrolled: the key arrays are picked at compile time
+        const uint32_t *in = a == 0 ? reinterpret_cast<const uint32_t *>(rows_in) : kin.k[a - 1];
+        uint32_t *out = a == 0 ? reinterpret_cast<uint32_t *>(rows_out) : kout.k[a - 1];
+        for (int i = t; i < nr; i += NT) stage[sl[i]] = in[src + i];
+        __syncthreads();
+        for (int q = t; q < nr; q += NT) out[q < nleft ? L0 + q : R0 + (q - nleft)] = stage[q];
+        __syncthreads();
+    }
+}
+
 constexpr int SC_EPT = 16;   // rows per thread of a 4096-row chunk
 __global__ void __launch_bounds__(256) k_sl_scatter(LvArgs A)
 {
@@ -281,7 +306,7 @@ __global__ void __launch_bounds__(256) k_sl_scatter(LvArgs A)
     __syncthreads();
     // blocked: thread t owns rows [t * EPT, t * EPT + EPT) of the chunk
     const int i0 = threadIdx.x * SC_EPT;
-    const uint32_t *kd = A.kin.k[dim] + b;
+    const uint32_t *kd = key_dim(A.kin, dim) + b;
     uint32_t fl[SC_EPT], tsum = 0;
 #pragma unroll
     for (int j = 0; j < SC_EPT; ++j) {
@@ -295,27 +320,40 @@ __global__ void __launch_bounds__(256) k_sl_scatter(LvArgs A)
         tsum += f;
     }
     uint32_t pre = block_excl_256(tsum, sh_w);   // packed in-chunk prefix (< 2^16 per half)
+    __shared__ uint32_t sh_tot;
+    if (threadIdx.x == blockDim.x - 1) sh_tot = pre + tsum;
+    __syncthreads();
+    const uint32_t tot = sh_tot;
     const int tb = A.tbeg[tile];
     const int64_t tbase = A.lo + tb;
-    const int ic0 = start - tb;   // chunk offset in the tile
+    const int ic0 = start - tb;                    // chunk offset in the tile
+    const uint32_t lbf = offl + min(offe, need);   // left rows of the tile before this chunk
+    const int nleft = (int)(offl + (tot >> 16) + min(offe + (tot & 0xffffu), need) - lbf);
+    __shared__ uint16_t sl[4096];
+    __shared__ uint32_t stage[4096];
 #pragma unroll
     for (int j = 0; j < SC_EPT; ++j) {
         const int i = i0 + j;
         if (i < len) {
             const uint32_t less = offl + (pre >> 16), eq = offe + (pre & 0xffffu);
-            const uint32_t lb = less + min(eq, need);
+            const uint32_t lb = less + min(eq, need) - lbf;   // left rows of this chunk before i
             const bool left = fl[j] == 0x10000u || (fl[j] == 1u && eq < need);
-            const int64_t pos = left ? tbase + lb : tbase + nl + ((uint32_t)(ic0 + i) - lb);
-            A.rows_out[pos] = A.rows_in[b + i];
-#pragma unroll
-            for (int d = 0; d < 6; ++d) A.kout.k[d][pos] = A.kin.k[d][b + i];
+            sl[i] = (uint16_t)(left ? lb : (uint32_t)nleft + ((uint32_t)i - lb));
         }
         pre += fl[j];
     }
+    __syncthreads();
+    staged_copy(A.rows_in, A.rows_out, A.kin, A.kout, b, len, sl, stage, nleft, tbase + lbf,
+                tbase + nl + ((uint32_t)ic0 - lbf));
 }
 
-// ---- fused path: one CTA (1024 threads) per tile of <= 8192 rows -----------------------------
-constexpr int FT = 1024, FEPT = 8;
+// ---- fused path: one CTA (1024 threads) per tile -------------------------------------------
+// Tiles of <= 8192 rows keep their keys in registers over the four passes; larger tiles stream
+// rounds of 8192 rows from L2 per pass.  Positions: rounds of 8192 with running totals.
+constexpr int FT = 1024, FEPT = 8, FROUND = FT * FEPT;
+constexpr int FT_SMEM = FROUND * 6;   // bytes: staging words + slots
+
+
 __global__ void __launch_bounds__(FT, 1) k_sl_tile(const int32_t *__restrict__ tbeg, const int32_t *__restrict__ tend,
                                                   const int32_t *__restrict__ tslot, int64_t lo, const int32_t *rows_in,
                                                   int32_t *rows_out, SliceKeys kin, SliceKeys kout, double diag, double wn)
@@ -335,6 +373,9 @@ __global__ void __launch_bounds__(FT, 1) k_sl_tile(const int32_t *__restrict__ t
     __shared__ uint32_t red[32][12];
     __shared__ uint32_t h[256], sh_w[32], sh_out[2];
     __shared__ int sh_dim;
+    extern __shared__ __align__(16) uint32_t sl_dyn[];   // FROUND staging words + FROUND u16 slots
+    uint32_t *stage = sl_dyn;
+    uint16_t *sl = reinterpret_cast<uint16_t *>(sl_dyn + FROUND);
     // extents over the tile (strided loads, coalesced)
     uint32_t mx[6], mn[6];
 #pragma unroll
@@ -363,18 +404,28 @@ __global__ void __launch_bounds__(FT, 1) k_sl_tile(const int32_t *__restrict__ t
     __syncthreads();
     if (t == 0) sh_dim = best_dim(&red[0][0], &red[0][6], diag, wn);
     __syncthreads();
-    const int dim = sh_dim;
-    // this thread's rows, blocked: [t * FEPT, t * FEPT + FEPT)
+    const uint32_t *kdim = key_dim(kin, sh_dim) + b;
+    const bool resident = n <= FROUND;
+    // rows of round r owned by this thread, blocked: [r * FROUND + t * FEPT, ... + FEPT)
     const int i0 = t * FEPT;
     uint32_t kd[FEPT];
+    if (resident) {
 #pragma unroll
-    for (int j = 0; j < FEPT; ++j) kd[j] = i0 + j < n ? kin.k[dim][b + i0 + j] : 0xffffffffu;
+        for (int j = 0; j < FEPT; ++j) kd[j] = i0 + j < n ? kdim[i0 + j] : 0u;
+    }
     uint32_t prefix = 0u, mask = 0u, k = (uint32_t)((n + 1) / 2);
     for (int p = 0; p < 4; ++p) {
         const int sh = 24 - 8 * p;
+        if (resident) {
 #pragma unroll
-        for (int j = 0; j < FEPT; ++j)
-            if (i0 + j < n && ((kd[j] ^ prefix) & mask) == 0u) atomicAdd(&h[(kd[j] >> sh) & 0xffu], 1u);
+            for (int j = 0; j < FEPT; ++j)
+                if (i0 + j < n && ((kd[j] ^ prefix) & mask) == 0u) atomicAdd(&h[(kd[j] >> sh) & 0xffu], 1u);
+        } else {
+            for (int i = t; i < n; i += FT) {   // strided: coalesced L2 reads
+                const uint32_t e = kdim[i];
+                if (((e ^ prefix) & mask) == 0u) atomicAdd(&h[(e >> sh) & 0xffu], 1u);
+            }
+        }
         __syncthreads();
         if (t < 256) {
             const uint32_t hv = h[t];
@@ -399,45 +450,59 @@ __global__ void __launch_bounds__(FT, 1) k_sl_tile(const int32_t *__restrict__ t
         __syncthreads();
     }
     const uint32_t kstar = prefix, need = k, nl = (uint32_t)((n + 1) / 2);
-    uint32_t fl[FEPT], tsum = 0;
+    uint32_t offl = 0, offe = 0;   // rows below / equal to k* in the earlier rounds
+    for (int r0 = 0; r0 < n; r0 += FROUND) {
+        if (!resident) {
 #pragma unroll
-    for (int j = 0; j < FEPT; ++j) {
-        fl[j] = i0 + j < n ? (kd[j] < kstar ? 0x10000u : (kd[j] == kstar ? 1u : 0u)) : 0u;
-        tsum += fl[j];
-    }
-    // exclusive block scan of tsum (1024 threads)
-    uint32_t x = tsum;
+            for (int j = 0; j < FEPT; ++j) kd[j] = r0 + i0 + j < n ? kdim[r0 + i0 + j] : 0u;
+        }
+        uint32_t fl[FEPT], tsum = 0;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t nn = __shfl_up_sync(SFULL, x, o);
-        if (lane >= o) x += nn;
-    }
-    if (lane == 31) sh_w[w] = x;
-    __syncthreads();
-    if (w == 0) {
-        uint32_t s = sh_w[lane], y = s;
+        for (int j = 0; j < FEPT; ++j) {
+            fl[j] = r0 + i0 + j < n ? (kd[j] < kstar ? 0x10000u : (kd[j] == kstar ? 1u : 0u)) : 0u;
+            tsum += fl[j];
+        }
+        // exclusive block scan of tsum (1024 threads; a round has < 2^16 rows per half)
+        uint32_t x = tsum;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t nn = __shfl_up_sync(SFULL, y, o);
-            if (lane >= o) y += nn;
+            const uint32_t nn = __shfl_up_sync(SFULL, x, o);
+            if (lane >= o) x += nn;
         }
-        sh_w[lane] = y - s;
-    }
-    __syncthreads();
-    uint32_t pre = sh_w[w] + x - tsum;
+        if (lane == 31) sh_w[w] = x;
+        __syncthreads();
+        if (w == 0) {
+            const uint32_t s = sh_w[lane];
+            uint32_t y = s;
 #pragma unroll
-    for (int j = 0; j < FEPT; ++j) {
-        const int i = i0 + j;
-        if (i < n) {
-            const uint32_t less = pre >> 16, eq = pre & 0xffffu;
-            const uint32_t lb = less + min(eq, need);
-            const bool left = fl[j] == 0x10000u || (fl[j] == 1u && eq < need);
-            const int64_t pos = left ? b + lb : b + nl + ((uint32_t)i - lb);
-            rows_out[pos] = rows_in[b + i];
-#pragma unroll
-            for (int d = 0; d < 6; ++d) kout.k[d][pos] = kin.k[d][b + i];
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t nn = __shfl_up_sync(SFULL, y, o);
+                if (lane >= o) y += nn;
+            }
+            sh_w[lane] = y - s;
+            if (lane == 31) { sh_out[0] = y >> 16; sh_out[1] = y & 0xffffu; }   // round totals
         }
-        pre += fl[j];
+        __syncthreads();
+        uint32_t pre = sh_w[w] + x - tsum;
+        const int nr = min(FROUND, n - r0);
+        const uint32_t rl = sh_out[0], re = sh_out[1];   // round totals
+        const uint32_t lbf = offl + min(offe, need);      // left rows before the round
+        const int nleft = (int)(offl + rl + min(offe + re, need) - lbf);
+#pragma unroll
+        for (int j = 0; j < FEPT; ++j) {
+            const int i = i0 + j;   // round-relative
+            if (r0 + i < n) {
+                const uint32_t less = offl + (pre >> 16), eq = offe + (pre & 0xffffu);
+                const uint32_t lb = less + min(eq, need) - lbf;
+                const bool left = fl[j] == 0x10000u || (fl[j] == 1u && eq < need);
+                sl[i] = (uint16_t)(left ? lb : (uint32_t)nleft + ((uint32_t)i - lb));
+            }
+            pre += fl[j];
+        }
+        __syncthreads();
+        staged_copy(rows_in, rows_out, kin, kout, b + r0, nr, sl, stage, nleft, b + lbf, b + nl + ((uint32_t)r0 - lbf));
+        offl += rl;
+        offe += re;
     }
 }
 
@@ -463,7 +528,13 @@ cudaError_t run_slicing(lmc_ctx *c)
     for (const auto &L : c->levels) {
         const int32_t *tbeg = d.lvl_begin + L.tile_off, *tend = d.lvl_end + L.tile_off, *tslot = d.lvl_slot + L.tile_off;
         if (L.fused) {
-            k_sl_tile<<<L.tile_n, FT, 0, st>>>(tbeg, tend, tslot, L.lo, rbuf[cur], rbuf[cur ^ 1], kbuf[cur], kbuf[cur ^ 1],
+            static bool attr = false;
+            if (!attr) {
+                cudaError_t e = cudaFuncSetAttribute(k_sl_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, FT_SMEM);
+                if (e != cudaSuccess) return e;
+                attr = true;
+            }
+            k_sl_tile<<<L.tile_n, FT, FT_SMEM, st>>>(tbeg, tend, tslot, L.lo, rbuf[cur], rbuf[cur ^ 1], kbuf[cur], kbuf[cur ^ 1],
                                                diag, wn);
         } else {
             LvArgs A;
