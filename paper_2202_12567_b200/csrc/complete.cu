@@ -189,13 +189,34 @@ __global__ void __launch_bounds__(LT, 1) k_layout(LArgs A)
         // every entry's position has a closed form, so the member's entries are placed in parallel
         const int lane = tid & 31, warp = tid >> 5;
         const unsigned lt_mask = (1u << lane) - 1u;
-        for (int mr = warp; mr < nsolo + (ng - nsolo) * R; mr += LT / 32) {
+        const int nmem = nsolo + (ng - nsolo) * R;
+        // the next member's list start is loaded one member ahead; the residues of a member's first
+        // LCH x 32 entries are loaded together (independent loads) and kept for the placement sweep
+        constexpr int LCH = 4;
+        int mp0_next = warp < cnt ? ptr[sh_who[warp]] : 0;
+        for (int mr = warp; mr < nmem; mr += LT / 32) {
             const int mown = mr < cnt ? sh_len[mr] : 0;
-            const int mp0 = mr < cnt ? ptr[sh_who[mr]] : 0;
+            const int mp0 = mp0_next;
+            {
+                const int mn = mr + LT / 32;
+                mp0_next = mn < cnt ? ptr[sh_who[mn]] : 0;
+            }
             int cntr[P];
 #pragma unroll
             for (int b2 = 0; b2 < P; ++b2) cntr[b2] = 0;
-            for (int k0 = 0; k0 < mown; k0 += 32) {
+            int rc[LCH];
+#pragma unroll
+            for (int c4 = 0; c4 < LCH; ++c4) {
+                const int k = 32 * c4 + lane;
+                rc[c4] = k < mown ? (int)gidx[mp0 + k] % P : -1;
+            }
+#pragma unroll
+            for (int c4 = 0; c4 < LCH; ++c4)
+                if (32 * c4 < mown) {
+#pragma unroll
+                    for (int b2 = 0; b2 < P; ++b2) cntr[b2] += __popc(__ballot_sync(FULLM, rc[c4] == b2));
+                }
+            for (int k0 = 32 * LCH; k0 < mown; k0 += 32) {
                 const int k = k0 + lane;
                 const int res = k < mown ? (int)gidx[mp0 + k] % P : -1;
 #pragma unroll
@@ -244,7 +265,14 @@ __global__ void __launch_bounds__(LT, 1) k_layout(LArgs A)
                 const int k = k0 + lane;
                 const bool in = k < mown;
                 const int pos = mp0 + k;
-                const int res = in ? (int)gidx[pos] % P : -1;
+                int res = -1;
+                if (k0 < 32 * LCH) {
+#pragma unroll
+                    for (int c4 = 0; c4 < LCH; ++c4)
+                        if (k0 == 32 * c4) res = rc[c4];
+                } else {
+                    res = in ? (int)gidx[pos] % P : -1;
+                }
                 int j = 0, sres = 0, fres = 0;
 #pragma unroll
                 for (int b2 = 0; b2 < P; ++b2) {
