@@ -658,10 +658,10 @@ __global__ void __launch_bounds__(256, P1_MINB) k_pass1(int slot, Upper up, cons
                                                const float *__restrict__ sbox, unsigned long long *counters)
 {
     __shared__ __align__(16) SceneConst sc;
-    stage_scene(&sc, slot);
+    stage_scene(&sc, slot);   // once per CTA: the CTAs stride over the (slice, pair) warps
     const int lane = threadIdx.x & 31;
-    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (gw >= (int64_t)SL * up.nB) return;
+    const int64_t nw = (int64_t)SL * up.nB, wstride = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; gw < nw; gw += wstride) {
     const int ls = (int)(gw / up.nB), b = (int)(gw % up.nB);
     const int s = s0 + ls;
     const int m = slice_off[s + 1] - slice_off[s];
@@ -694,6 +694,7 @@ __global__ void __launch_bounds__(256, P1_MINB) k_pass1(int slot, Upper up, cons
         p1_cnt[gw] = n;
         atomicAdd(&counters[0], (unsigned long long)(2 * n));
     }
+    }
 }
 
 cudaError_t run_pass1(lmc_ctx *c)
@@ -702,7 +703,8 @@ cudaError_t run_pass1(lmc_ctx *c)
     k_slice_bbox<<<c->SL, 256, 0, c->stream>>>(c->d.slice_off, c->s0, c->h_slice_off[c->s0], c->d.prow, c->d.sbox);
     if (c->up.nB == 0) return cudaGetLastError();
     int64_t warps = (int64_t)c->SL * c->up.nB;
-    unsigned blocks = (unsigned)((warps * 32 + 255) / 256);
+    // persistent: P1_MINB resident CTAs per SM stride over the warps (the scene is staged once per CTA)
+    unsigned blocks = (unsigned)std::min<int64_t>((warps * 32 + 255) / 256, (int64_t)c->nsm * P1_MINB);
     k_pass1<<<blocks, 256, 0, c->stream>>>(c->scene_slot, c->up, c->d.slice_off, c->s0, c->SL, c->h_slice_off[c->s0], c->d.prow,
                                            c->d.vpl, c->cfg.seed, c->nmax, c->d.p1_rows, c->d.p1_Ta, c->d.p1_Tb,
                                            c->d.p1_cnt, c->d.sbox, c->d.counters);
@@ -877,9 +879,20 @@ __global__ void __launch_bounds__(CO_THREADS, CO_MINB) k_coarsen(
         __syncwarp();
     };
     if (count_target <= 0) {
-        // threshold rule: candidates height by height (a node's outcome depends on its subtree only)
+        // threshold rule: candidates height by height (a node's outcome depends on its subtree only);
+        // the warps take the nodes of a height from a shared counter (merged candidates cost far
+        // more than base pairs), counters alternate between heights so one barrier per height stays
+        __shared__ int sh_next[2];
+        if (threadIdx.x == 0 && up.H >= 1) sh_next[1] = up.hoff[1];
+        __syncthreads();
         for (int h = 1; h <= up.H; ++h) {
-            for (int idx = up.hoff[h] + w; idx < up.hoff[h + 1]; idx += CO_WARPS) {
+            if (threadIdx.x == 0 && h < up.H) sh_next[(h + 1) & 1] = up.hoff[h + 1];
+            const int hend = up.hoff[h + 1];
+            for (;;) {
+                int idx = 0;
+                if (lane == 0) idx = atomicAdd(&sh_next[h & 1], 1);
+                idx = __shfl_sync(FULL_MASK, idx, 0);
+                if (idx >= hend) break;
                 const int f = up.hlist[idx];
                 const int l = up.left[f], r = up.right[f];
                 if (!((sh_flag[l] & F_INCUT) && (sh_flag[r] & F_INCUT))) continue;   // not a candidate
