@@ -83,7 +83,8 @@ typedef struct {
  * analytic scene").  HOST pointers, float32: sph[4*k] = (cx,cy,cz,r); box[6*k] = (lo3, hi3);
  * rect[12*k] = (p0, e1, e2, nrm = e1 x e2).  At most 32 of each.  clamp_dist = d_c of the
  * d^2 clamp (DESIGN R2); shadow_eps = segment shrink at both ends (R3); diag = scene
- * diagonal D used by the slicing keys (R26). */
+ * diagonal D used by the slicing keys (R26), in [1e-30, 1e30] (R43: the slicing orders 32-bit
+ * encodings of the coordinates, exact in that range; LMC_EINVAL outside). */
 typedef struct {
     int32_t n_sph, n_box, n_rect;
     const float *sph, *box, *rect;
@@ -99,7 +100,7 @@ typedef struct {
 
 typedef struct {
     int32_t slice_target;   /* max rows per slice ("about 800 pixels"), <= 1024 */
-    double normal_weight;   /* w_n of the 6D slicing key (R26) */
+    double normal_weight;   /* w_n of the 6D slicing key (R26): 0 or in [1e-30, 1e30] (R43), else LMC_EINVAL */
     uint64_t seed;          /* Philox key for every random draw (R7) */
     int32_t p1_nmax, p1_nmin; /* pass-1 rows per pair: min(m, max(nmin, ceil(nmax lum I_f / l_max))) (R6) */
     double coarsen_tau;     /* coarsening bound: merge iff cost(L_f) < tau (R11) */
@@ -163,7 +164,9 @@ lmc_status lmc_create(const lmc_gbuffer *g, const lmc_vpls *v, const lmc_light_t
 
 /* Re-upload the per-frame inputs (G-buffer, VPLs) of an existing context: same counts and
  * memory kind as at lmc_create; the light tree and global cut are those given at creation.
- * Synchronises cfg->stream.  Resets the stage state to "created". */
+ * Synchronises cfg->stream.  Resets the stage state to "created".  LMC_EINVAL when a pixel index
+ * lies outside [0, width * height) or a G-buffer position / normal is not finite (R43); the same
+ * checks run inside lmc_create. */
 lmc_status lmc_upload_inputs(lmc_ctx *ctx, const lmc_gbuffer *g, const lmc_vpls *v, const lmc_light_tree *t);
 
 /* Matrix slicing: recursive binary split of the rows as 6D points
