@@ -125,6 +125,54 @@ __device__ __forceinline__ double solve_group(double (&a)[Q], double b, int l, i
     return b;
 }
 
+// The in-register Cholesky alternative (MALS_CHOL=1 builds; measured against Gauss-Jordan, DESIGN
+// §6): right-looking A = L L^T with the forward substitution fused (b becomes y = L^-1 b); at step
+// k lane i receives l_jk of every j > k, and lane k keeps them (column k of L) for the back
+// substitution x = L^-T y, which then needs one broadcast per step.
+template <int Q>
+__device__ __forceinline__ double solve_chol(double (&a)[Q], double b, int l, int lane0)
+{
+    double c[Q];   // lane l: c[j] = l_jl (j > l), column l of L
+    double rown = 0.0;   // 1 / l_ll
+#pragma unroll
+    for (int j = 0; j < Q; ++j) c[j] = 0.0;
+#pragma unroll Q
+    for (int k = 0; k < Q; ++k) {
+        const double akk = __shfl_sync(0xffffffffu, a[k], lane0 + k);
+        const double r = rcp_pivot(sqrt(akk));    // 1 / l_kk
+        const double lik = a[k] * r;               // l_ik (lane k: l_kk)
+        const double yk = __shfl_sync(0xffffffffu, b * r, lane0 + k);
+        if (l == k) { rown = r; b = yk; }
+        else if (l > k) b = fma(-lik, yk, b);
+#pragma unroll
+        for (int j = 0; j < Q; ++j) {
+            if (j > k) {   // compile-time after unrolling
+                const double ljk = __shfl_sync(0xffffffffu, lik, lane0 + j);
+                c[j] = l == k ? ljk : c[j];
+                a[j] = fma(-lik, ljk, a[j]);
+            }
+        }
+    }
+    double x = 0.0;
+#pragma unroll
+    for (int jj = 0; jj < Q; ++jj) {
+        const int j = Q - 1 - jj;
+        const double xj = __shfl_sync(0xffffffffu, b * rown, lane0 + j);
+        x = l == j ? xj : x;
+        b = l < j ? fma(-c[j], xj, b) : b;
+    }
+    return x;
+}
+#ifndef MALS_CHOL
+#define MALS_CHOL 0
+#endif
+template <int Q>
+__device__ __forceinline__ double solve_sys(double (&a)[Q], double b, int l, int lane0)
+{
+    if constexpr (MALS_CHOL) return solve_chol<Q>(a, b, l, lane0);
+    return solve_group<Q>(a, b, l, lane0);
+}
+
 // ---- q = 16: normal equations on the fp64 tensor cores ------------------------------------
 // mma.sync m8n8k4 f64 (g = lane/4, t = lane%4): A (8x4) a0 = A[g][t]; B (4x8) b0 = B[t][g];
 // C (8x8) c0, c1 = C[g][2t], C[g][2t+1].  For a system with samples k (gathered operand rows
@@ -302,7 +350,7 @@ __global__ void __launch_bounds__(MCfg<Q>::NT, 1) k_mals(MArgs A)
 #pragma unroll
                     for (int c = 0; c < Q; ++c)
                         if (c == l) a[c] += lam;
-                    const double x = solve_group<Q>(a, b, l, lane0);
+                    const double x = solve_sys<Q>(a, b, l, lane0);
                     if (sys < nsys) O[(size_t)sys * Q + l] = x;
                 }
                 __syncthreads();
@@ -339,7 +387,7 @@ __global__ void __launch_bounds__(MCfg<Q>::NT, 1) k_mals(MArgs A)
 #pragma unroll
                 for (int c = 0; c < Q; ++c)
                     if (c == l) a[c] += lam;   // static register index (no local-memory spill)
-                const double x = solve_group<Q>(a, b, l, lane0);
+                const double x = solve_sys<Q>(a, b, l, lane0);
                 if (valid) O[(size_t)sys * Q + l] = x;
             }
             __syncthreads();
