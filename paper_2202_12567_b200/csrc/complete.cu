@@ -107,8 +107,11 @@ __host__ __device__ __forceinline__ int vperm(int rel, int R, int KA, int V)
 // scheduled so that at step k member t takes, when it can, an entry whose gathered index has
 // residue (t + k) mod P: the P gathers of a phase then fall into different bank sets.  Member
 // r of a group has t = (r / D) mod P (D = 1: a lane group owns a row).
+#ifndef LAYOUT_MINB
+#define LAYOUT_MINB 1
+#endif
 template <int PP>
-__global__ void __launch_bounds__(LT, 1) k_layout(LArgs A)
+__global__ void __launch_bounds__(LT, LAYOUT_MINB) k_layout(LArgs A)
 {
     typedef cub::BlockRadixSort<uint32_t, LT, 1> Sort;
     typedef cub::BlockScan<int32_t, LT> Scan;
@@ -701,9 +704,6 @@ __global__ void __launch_bounds__(Cfg<Q>::NT, 1) k_adm(CArgs A)
     const uint16_t *rperm = A.r_perm + (int64_t)ls * A.mmax;
     const uint16_t *cperm = A.c_perm + (int64_t)ls * A.G;
     const int32_t *rgoff = A.r_goff + (int64_t)ls * (A.mmax + 1), *cgoff = A.c_goff + (int64_t)ls * (A.G + 1);
-    const char *rent = reinterpret_cast<const char *>(A.r_ent + sb);
-    const char *cent = reinterpret_cast<const char *>(A.c_ent + sb);
-    float *S = A.S + sb;
     // rank-level element index of this slice's layout base (SL * scap < 2^32, checked at create):
     // the hot loops form their global addresses from 32-bit indices and the kernel-parameter bases
     const uint32_t sb32 = (uint32_t)sb;
