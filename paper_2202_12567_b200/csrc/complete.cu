@@ -596,6 +596,30 @@ __device__ __forceinline__ void cp_async16(void *smem, const void *gmem)
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+// 1-D bulk copies (TMA engine, no tensor map) completing on a per-stage mbarrier: one elected lane
+// issues a whole ring stage, the warp waits on the barrier's phase
+__device__ __forceinline__ void mbar_init(unsigned long long *bar, int count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, unsigned long long *bar)
+{
+    asm volatile("fence.proxy.async.shared::cta;\n"
+                 "mbarrier.arrive.expect_tx.shared::cta.b64 _, [%2], %3;\n"
+                 "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %3, [%2];\n"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *bar, uint32_t parity)
+{
+    asm volatile("{\n .reg .pred p;\n WAIT_%=:\n"
+                 " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+                 " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)), "r"(parity)
+                 : "memory");
+}
+#ifndef ADM_TMA_ROW
+#define ADM_TMA_ROW 0
+#endif
 // predicated global store without a branch
 __device__ __forceinline__ void st_pred(float *addr, float v, bool p)
 {
@@ -692,6 +716,9 @@ __global__ void __launch_bounds__(Cfg<Q>::NT, 1) k_adm(CArgs A)
     __shared__ int sh_ctr[2];
     __shared__ unsigned long long sh_prof[8];
     __shared__ long long sh_exit[32];
+#if ADM_TMA_ROW
+    __shared__ unsigned long long sh_bar[32 * ROW_NS];   // per warp: one mbarrier per row-ring stage
+#endif
     const int ls = A.order ? A.order[blockIdx.x] : (int)blockIdx.x, s = A.s0 + ls, tid = threadIdx.x, NT = blockDim.x;
     long long pt0 = PROF ? clock64() : 0;
     unsigned long long pacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -715,6 +742,13 @@ __global__ void __launch_bounds__(Cfg<Q>::NT, 1) k_adm(CArgs A)
     char *ring = reinterpret_cast<char *>(Cm + Q * Q);   // nwarps x 2 x RING_SLOT, also Gram partials
     float *part = reinterpret_cast<float *>(ring);
     char *slot0 = ring + (size_t)warp * 2 * RING_SLOT;
+#if ADM_TMA_ROW
+    unsigned long long *wbar = sh_bar + warp * ROW_NS;
+    uint32_t wph = 0;   // phase parity of each of the warp's stage barriers
+    if (lane < ROW_NS) mbar_init(wbar + lane, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    __syncwarp();
+#endif
     float *Ug = A.U + lrow0 * Q, *Lg = A.Lam + lrow0 * Q, *Xo = A.Xold + lrow0 * Q;
     float *Vg = A.V + vb, *Pg = A.Pi + vb;
     if (m <= Q || n <= Q) {   // R25: rank not below the slice dimensions -> direct rendering
@@ -778,17 +812,35 @@ __global__ void __launch_bounds__(Cfg<Q>::NT, 1) k_adm(CArgs A)
             float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
             // gathers address byte offsets from the lane's own float4 slot: column * 4Q + this base
             const char *ysub = reinterpret_cast<const char *>(Y + 4 * sub);
+#if ADM_TMA_ROW
+            const unsigned long long *egb = A.r_ent + (sb32 + (uint32_t)rgoff[g]);   // the group's entries
+            if (lane == 0) {
+#pragma unroll
+                for (int p = 0; p < ROW_NS - 1; ++p)
+                    if (p < nch) bulk_g2s(slot0 + p * 512, egb + 64 * p, 512u, wbar + p);
+            }
+#else
 #pragma unroll
             for (int p = 0; p < ROW_NS - 1; ++p) {
                 if (p < nch) cp_async16(slot0 + p * 512 + lane * 16, A.r_ent + (eg32 + 64u * p));
                 cp_commit();
             }
+#endif
             int cs = 0;   // ring stage of chunk c
             for (int c = 0; c < nch; ++c) {
                 const int pf = c + ROW_NS - 1;
+#if ADM_TMA_ROW
+                if (lane == 0 && pf < nch) {
+                    const int ps = cs == 0 ? ROW_NS - 1 : cs - 1;
+                    bulk_g2s(slot0 + ps * 512, egb + 64 * pf, 512u, wbar + ps);
+                }
+                mbar_wait(wbar + cs, (wph >> cs) & 1u);
+                wph ^= 1u << cs;
+#else
                 if (pf < nch) cp_async16(slot0 + (cs == 0 ? ROW_NS - 1 : cs - 1) * 512 + lane * 16, A.r_ent + (eg32 + 64u * pf));
                 cp_commit();
                 cp_wait<ROW_NS - 1>();
+#endif
                 __syncwarp();
                 const unsigned long long *wb = reinterpret_cast<const unsigned long long *>(slot0 + cs * 512) + VROW * grp;
                 cs = cs + 1 == ROW_NS ? 0 : cs + 1;
