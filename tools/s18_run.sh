@@ -1,0 +1,6 @@
+set -x
+timeout 1800 python -m pytest tests -m gpu -q > gpurun_out/s18_gputests.log 2>&1; tail -3 gpurun_out/s18_gputests.log
+timeout 300 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/s18_smoke.log 2>&1; tail -1 gpurun_out/s18_smoke.log
+timeout 600 python bench.py > gpurun_out/s18_bench_c4.json 2>/dev/null; python -c "import json; d=json.loads(open('gpurun_out/s18_bench_c4.json').read().strip().splitlines()[-1]); print(d['ms_per_step'], d['value'], d['e2e']['value'], d['roofline']['frac'], d['clocks'])"
+timeout 900 python bench.py --solver mals --no-cpu-baseline > gpurun_out/s18_bench_c4_mals.json 2>/dev/null
+timeout 600 python bench.py --config c2 --solver mals --no-cpu-baseline > gpurun_out/s18_bench_c2_mals.json 2>/dev/null
