@@ -33,22 +33,24 @@ UNIT = "entries/s"
 FP32_PEAK_DERIVED = 148 * 128 * 2 * 1.965e9 / 1e12   # 74.4: 148 SMs x 128 FP32 lanes x FMA x max clock
 
 
-def fp32_peak():
-    """Measured FP32 FMA peak (tools/peaks.cu on a B200 of this pool, profiles/r01_peaks.json), else derived."""
+def _microbench(key):
     try:
-        pk = json.load(open(os.path.join(ROOT, "profiles", "r01_peaks.json")))
-        return float(pk["fp32_fma_tflops"]), "measured: tools/peaks.cu FP32 FMA microbenchmark (profiles/r01_peaks.json)"
+        return float(json.load(open(os.path.join(ROOT, "profiles", "r01_peaks.json")))[key])
     except Exception:
-        return FP32_PEAK_DERIVED, "derived: 148 SMs x 128 FP32 FMA lanes x 2 x 1.965 GHz"
+        return None
+
+
+def fp32_peak():
+    """FP32 roofline peak derived from the unit counts and the max clock (the task's rule for an
+    ALU-bound path: MEASURED_PEAKS.json holds no FP32 figure); the FMA microbenchmark of this pool
+    (tools/peaks.cu, profiles/r01_peaks.json: 71.0 TF/s, 95% of it) is reported beside it."""
+    return FP32_PEAK_DERIVED, "derived: 148 SMs x 128 FP32 FMA lanes x 2 x 1.965 GHz", _microbench("fp32_fma_tflops")
 
 
 def fp64_peak():
-    """Measured FP64 FMA peak (tools/peaks.cu, profiles/r01_peaks.json): the denominator of the fp64 MALS kernel."""
-    try:
-        pk = json.load(open(os.path.join(ROOT, "profiles", "r01_peaks.json")))
-        return float(pk["fp64_fma_tflops"]), "measured: tools/peaks.cu FP64 FMA microbenchmark (profiles/r01_peaks.json)"
-    except Exception:
-        return FP32_PEAK_DERIVED / 2, "derived: half the FP32 rate (148 SMs x 64 FP64 FMA lanes x 2 x 1.965 GHz)"
+    """FP64 roofline peak derived the same way (half the FP32 rate: 64 FP64 FMA lanes per SM); the
+    microbenchmark (34.2 TF/s, 92%) beside it."""
+    return FP32_PEAK_DERIVED / 2, "derived: 148 SMs x 64 FP64 FMA lanes x 2 x 1.965 GHz", _microbench("fp64_fma_tflops")
 
 
 def parse():
@@ -337,7 +339,7 @@ def main():
     fl = (adm_flops if solver == 0 else mals_flops)(q, st["sum_samples"], st["rows"], st["sum_cols"],
                                                      st["slice_end"] - st["slice_begin"], K)
     achieved = fl / (ms_c * 1e-3) / 1e12
-    peak, peak_src = fp32_peak() if solver == 0 else fp64_peak()
+    peak, peak_src, peak_mb = fp32_peak() if solver == 0 else fp64_peak()
     fl_survey = adm_flops_survey(q, st["sum_samples"], st["rows"], st["sum_cols"], st["slice_end"] - st["slice_begin"], K) \
         if solver == 0 else fl
     traffic, limiter = None, None
@@ -362,7 +364,7 @@ def main():
         ev2 = float(st["evals_pass2"])
         efl = f1 * ev1 + f2 * ev2
         ems = statistics.mean(stage["pass1"]) + statistics.mean(stage["coarsen"]) + statistics.mean(eval2_ms)
-        p64, p64_src = fp64_peak()
+        p64, p64_src, p64_mb = fp64_peak()
         ach = efl / (ems * 1e-3) / 1e12
         roof_entry = {"bound": "alu", "kernel": "k_pass1 + k_coarsen + k_eval_new (+ k_slice_bbox)",
                       "achieved": ach, "peak": p64, "unit": "TFLOP/s", "frac": ach / p64, "traffic": None,
@@ -370,6 +372,7 @@ def main():
                                                "(-fmad=false) path cap the fraction at 0.5",
                       "flops_per_entry": {"pass1+coarsen": f1, "pass2": f2},
                       "entries": {"pass1+coarsen": ev1, "pass2": ev2}, "flops_per_frame": efl, "kernel_ms": ems,
+                      "frac_of_microbench_peak": (ach / p64_mb) if p64_mb else None,
                       "sample": f"oracle operation count over {n1} pass-1/coarsening pairs and {n2} pass-2 "
                                 f"entries of {nsl_s} slices of this frame"
                                 + ("; mesh occluders excluded from the count (BVH work not counted: a lower bound)"
@@ -412,7 +415,8 @@ def main():
                      "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                      "traffic": traffic, "peak_source": peak_src, "flops_per_launch": fl,
                      "flops_per_launch_survey_count": fl_survey, "frac_survey_count": fl_survey / (ms_c * 1e-3) / 1e12 / peak,
-                     "kernel_ms": ms_c, "limiter": limiter},
+                     "kernel_ms": ms_c, "limiter": limiter,
+                     "frac_of_microbench_peak": (achieved / peak_mb) if peak_mb else None},
         "roofline_entry": roof_entry,
         "clocks": cl,
         "gpu_launches": launches,

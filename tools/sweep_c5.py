@@ -62,7 +62,7 @@ def main():
     x = scenegen.make_inputs(scenegen.preset("c3"))
     stream = torch.cuda.current_stream(dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
-    peak, _ = bench.fp32_peak()
+    peak = bench.fp32_peak()[0]
     out = []
     for q in (4, 8, 16, 32):
         for rate in (0.05, 0.10, 0.20):
