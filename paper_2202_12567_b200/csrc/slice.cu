@@ -528,12 +528,9 @@ cudaError_t run_slicing(lmc_ctx *c)
     for (const auto &L : c->levels) {
         const int32_t *tbeg = d.lvl_begin + L.tile_off, *tend = d.lvl_end + L.tile_off, *tslot = d.lvl_slot + L.tile_off;
         if (L.fused) {
-            static bool attr = false;
-            if (!attr) {
-                cudaError_t e = cudaFuncSetAttribute(k_sl_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, FT_SMEM);
-                if (e != cudaSuccess) return e;
-                attr = true;
-            }
+            // per device (a process may drive several GPUs): set on every call, a cheap host call
+            cudaError_t e = cudaFuncSetAttribute(k_sl_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, FT_SMEM);
+            if (e != cudaSuccess) return e;
             k_sl_tile<<<L.tile_n, FT, FT_SMEM, st>>>(tbeg, tend, tslot, L.lo, rbuf[cur], rbuf[cur ^ 1], kbuf[cur], kbuf[cur ^ 1],
                                                diag, wn);
         } else {
