@@ -102,3 +102,14 @@ def test_diag_out_of_range_rejected(diag):
 def test_normal_weight_out_of_range_rejected(wn):
     with pytest.raises(lmc.LmcError):
         lmc.Frame(scenegen.make_inputs(scenegen.preset("t_cornell", normal_weight=wn)))
+
+
+@pytest.mark.parametrize("m,target", [(262144, 1000), (200001, 777), (6001, 5), (70000, 33), (8193, 1024),
+                                      (65537, 1024), (4097, 9)])
+def test_slices_unbalanced_trees(m, target):
+    """row counts and targets whose slicing trees have leaves at several depths (leaf tiles carried
+    through the later levels: the copy path of both slicing kernels), tiles just above and below the
+    4096-row chunk and 8192-row round sizes, and levels switching between the chunked and one-CTA paths"""
+    x = scenegen.make_inputs(scenegen.preset("c2", slice_target=target))
+    g = {k: np.ascontiguousarray(v[:m]) for k, v in x.gbuf.items()}
+    check(dataclasses.replace(x, gbuf=g))
