@@ -262,7 +262,10 @@ def main():
             idt.copy_(torch.frombuffer(bytearray(lmc.nccl_unique_id()), dtype=torch.uint8))
         dist.broadcast(idt, 0)
         nccl_id = bytes(idt.cpu().tolist())
-    fr = lmc.Frame(x, rank=rank, world=world, stream=stream, nccl_id=nccl_id)
+    # world > 1: interleaved slices (rank r takes slices r, r + P, ...): the ranks' loads balance
+    # (subtree shares differ by up to 1.8x in completion work at P = 8)
+    part = int(os.environ.get("BENCH_PARTITION", "1"))
+    fr = lmc.Frame(x, rank=rank, world=world, stream=stream, nccl_id=nccl_id, partition=part)
     fr.set_timing(True)
     npix = x.height * x.width
     img = torch.zeros(npix * 3, device=dev)
@@ -441,7 +444,7 @@ def measure_e2e(x, args, solver, dev, rank=0, world=1, nccl_id=None):
     import torch.distributed as dist
     from paper_2202_12567_b200 import lmc
     fr = lmc.Frame(x, memory=lmc.MEM_HOST, stream=torch.cuda.current_stream(dev), rank=rank, world=world,
-                   nccl_id=nccl_id)
+                   nccl_id=nccl_id, partition=int(os.environ.get("BENCH_PARTITION", "1")))
     npix = x.height * x.width
     host_img = torch.zeros(npix * 3, dtype=torch.float32).pin_memory() if rank == 0 else None
     h2d = (x.m * (14 * 4) + x.vpls["px"].size * 6 * 4) * world

@@ -133,6 +133,12 @@ typedef struct {
      * pair of sibling cut nodes (ties: smallest node id) until the cut has coarsen_target nodes
      * (coarsen_tau unused); 0 = the threshold rule */
     int32_t coarsen_target;
+    /* world > 1, how the slices are shared: 0 = slicing subtrees for P = 2^k ranks
+     * (each rank slices the top k levels of the whole G-buffer, then its own subtree), contiguous
+     * slice ranges otherwise; 1 = interleaved: every rank slices the whole G-buffer and takes
+     * slices r, r + P, r + 2P, ... (neighbouring slices cost alike, so the ranks' loads balance;
+     * random draws stay keyed by the global slice id, so the image is the same either way) */
+    int32_t partition;
 } lmc_config;
 
 typedef struct {

@@ -349,6 +349,7 @@ __global__ void __launch_bounds__(LT, LAYOUT_MINB) k_layout(LArgs A)
 struct CArgs {
     const int32_t *slice_off;
     int32_t s0, lbase, G, mmax, nmax;
+    int32_t rs0, rss;   // global slice id of local slice ls: rs0 + ls * rss (the draws' key)
     int64_t scap;
     int K;
     float alpha, beta, gamma, tol;
@@ -770,14 +771,14 @@ __global__ void __launch_bounds__(Cfg<Q>::NT, 1) k_adm(CArgs A)
     const int Keff = warm && A.warm_iters > 0 ? A.warm_iters : A.K;
     for (int e = tid; e < m * Q; e += NT) {
         const int i = e / Q, l = e % Q;
-        const float x = warm ? Ug[e] : c0 * unif_f(philox4((uint32_t)i, (uint32_t)l, (uint32_t)s, TAG_X0, A.seed).x);
+        const float x = warm ? Ug[e] : c0 * unif_f(philox4((uint32_t)i, (uint32_t)l, (uint32_t)(A.rs0 + ls * A.rss), TAG_X0, A.seed).x);
         X[e] = x;
         Ug[e] = x;
         Lg[e] = 0.f;
     }
     for (int e = tid; e < n * Q; e += NT) {
         const int j = e / Q, l = e % Q;
-        const float y = warm ? Vg[e] * nm.y : c0 * unif_f(philox4((uint32_t)l, (uint32_t)j, (uint32_t)s, TAG_Y0, A.seed).x);
+        const float y = warm ? Vg[e] * nm.y : c0 * unif_f(philox4((uint32_t)l, (uint32_t)j, (uint32_t)(A.rs0 + ls * A.rss), TAG_Y0, A.seed).x);
         Y[e] = y;
         Vg[e] = y;
         Pg[e] = 0.f;
@@ -1047,7 +1048,7 @@ cudaError_t run_layout(lmc_ctx *c)
 {
     if (c->SL == 0) return cudaSuccess;
     LArgs A;
-    A.slice_off = c->d.slice_off;
+    A.slice_off = c->soff_k;
     A.cut_n = c->d.cut_n;
     A.rowptr = c->d.rowptr;
     A.colptr = c->d.colptr;
@@ -1056,7 +1057,7 @@ cudaError_t run_layout(lmc_ctx *c)
     A.col = c->d.col;
     A.csc_row = c->d.csc_row;
     A.val = c->d.val;
-    A.s0 = c->s0;
+    A.s0 = c->s0k;
     A.G = c->G;
     A.mmax = c->mmax;
     A.R = layout_R(c->q);
@@ -1103,9 +1104,11 @@ cudaError_t run_adm(lmc_ctx *c, int nmax)
 {
     if (c->SL == 0) return cudaSuccess;
     CArgs A;
-    A.slice_off = c->d.slice_off;
-    A.s0 = c->s0;
-    A.lbase = c->h_slice_off[c->s0];
+    A.slice_off = c->soff_k;
+    A.s0 = c->s0k;
+    A.lbase = c->lbase_k;
+    A.rs0 = c->rs0;
+    A.rss = c->rss;
     A.G = c->G;
     A.mmax = c->mmax;
     A.nmax = nmax;
@@ -1286,17 +1289,17 @@ cudaError_t run_resolve(lmc_ctx *c, float *image, float *rows_rgb, float4 *tile4
 {
     if (c->SL == 0) return cudaSuccess;
     RArgs A;
-    A.slice_off = c->d.slice_off;
-    A.rows = c->d.rows;
+    A.slice_off = c->soff_k;
+    A.rows = c->rows_k;
     A.pixel = c->d.pixel;
     A.cut_n = c->d.cut_n;
     A.cut_cols = c->d.cut_cols;
     A.flags = c->d.flags;
-    A.s0 = c->s0;
-    A.lbase = c->h_slice_off[c->s0];
+    A.s0 = c->s0k;
+    A.lbase = c->lbase_k;
     A.G = c->G;
     A.q = c->q;
-    A.row0 = c->row0;
+    A.row0 = c->row0_k;
     A.npix = (int64_t)c->W * c->H;
     A.U = c->d.U;
     A.V = c->d.V;
@@ -1365,7 +1368,7 @@ __global__ void k_rank_pixels(int64_t ML, int64_t row0, const int32_t *__restric
 cudaError_t run_rank_pixels(lmc_ctx *c, int32_t *out)
 {
     if (c->ML == 0) return cudaSuccess;
-    k_rank_pixels<<<(unsigned)((c->ML + 255) / 256), 256, 0, c->stream>>>(c->ML, c->row0, c->d.rows, c->d.pixel, out);
+    k_rank_pixels<<<(unsigned)((c->ML + 255) / 256), 256, 0, c->stream>>>(c->ML, c->row0_k, c->rows_k, c->d.pixel, out);
     return cudaGetLastError();
 }
 
@@ -1482,7 +1485,7 @@ __global__ void k_warm_save(int SL, int G, int64_t ML, int64_t row0, const int32
 cudaError_t run_warm_check(lmc_ctx *c)
 {
     if (c->SL == 0) return cudaSuccess;
-    k_warm_check<<<c->SL, 256, 0, c->stream>>>(c->d.slice_off, c->s0, c->h_slice_off[c->s0], c->row0, c->d.rows, c->d.cut_n,
+    k_warm_check<<<c->SL, 256, 0, c->stream>>>(c->soff_k, c->s0k, c->lbase_k, c->row0_k, c->rows_k, c->d.cut_n,
                                                c->d.cut_cols, c->d.prev_rows, c->d.prev_n, c->d.prev_cut, c->d.prev_flags,
                                                c->G, c->have_prev ? 1 : 0, c->d.warm_ok);
     return cudaGetLastError();
@@ -1492,7 +1495,7 @@ cudaError_t run_warm_save(lmc_ctx *c)
 {
     if (c->SL == 0) return cudaSuccess;
     const int64_t n = std::max<int64_t>(std::max<int64_t>(c->ML, (int64_t)c->SL * c->G), c->SL);
-    k_warm_save<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(c->SL, c->G, c->ML, c->row0, c->d.rows, c->d.cut_n,
+    k_warm_save<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(c->SL, c->G, c->ML, c->row0_k, c->rows_k, c->d.cut_n,
                                                                    c->d.cut_cols, c->d.flags, c->d.prev_rows, c->d.prev_n,
                                                                    c->d.prev_cut, c->d.prev_flags);
     c->have_prev = true;

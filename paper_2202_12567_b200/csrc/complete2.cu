@@ -293,6 +293,7 @@ __global__ void __launch_bounds__(LT2, 1) k_layout2(L2Args A)
 struct C2Args {
     const int32_t *slice_off;
     int32_t s0, lbase, G, mmax;
+    int32_t rs0, rss;   // global slice id of local slice ls: rs0 + ls * rss (the draws' key)
     int64_t scap, gcap;
     int K;
     float alpha, beta, gamma, tol;
@@ -705,13 +706,13 @@ __global__ void __launch_bounds__(K2<Q>::NT, 1) k_adm2(C2Args A)
     for (int e = tid; e < (m + 2) * 16; e += NT) {
         const int i = e >> 4, ph = e & 15, l = ph % Q;   // physical float ph of slot i holds element l
         const float x = i >= m ? 0.f : warm ? Ug[i * Q + l]
-                                            : c0 * unif_f(philox4((uint32_t)i, (uint32_t)l, (uint32_t)s, TAG_X0, A.seed).x);
+                                            : c0 * unif_f(philox4((uint32_t)i, (uint32_t)l, (uint32_t)(A.rs0 + ls * A.rss), TAG_X0, A.seed).x);
         reinterpret_cast<float *>(Xb + i * RB)[ph] = x;
     }
     for (int e = tid; e < (n + 2) * 16; e += NT) {
         const int j = e >> 4, ph = e & 15, l = ph % Q;
         const float y = j >= n ? 0.f : warm ? Vg[j * Q + l] * nm.y
-                                            : c0 * unif_f(philox4((uint32_t)l, (uint32_t)j, (uint32_t)s, TAG_Y0, A.seed).x);
+                                            : c0 * unif_f(philox4((uint32_t)l, (uint32_t)j, (uint32_t)(A.rs0 + ls * A.rss), TAG_Y0, A.seed).x);
         reinterpret_cast<float *>(Yb + j * RB)[ph] = y;
     }
     (void)CP;
@@ -978,7 +979,7 @@ cudaError_t run_layout2(lmc_ctx *c)
 {
     if (c->SL == 0) return cudaSuccess;
     L2Args A;
-    A.slice_off = c->d.slice_off;
+    A.slice_off = c->soff_k;
     A.cut_n = c->d.cut_n;
     A.rowptr = c->d.rowptr;
     A.colptr = c->d.colptr;
@@ -987,7 +988,7 @@ cudaError_t run_layout2(lmc_ctx *c)
     A.col = c->d.col;
     A.csc_row = c->d.csc_row;
     A.val = c->d.val;
-    A.s0 = c->s0;
+    A.s0 = c->s0k;
     A.G = c->G;
     A.mmax = c->mmax;
     A.q = c->q;
@@ -1040,9 +1041,11 @@ cudaError_t run_adm2(lmc_ctx *c)
 {
     if (c->SL == 0) return cudaSuccess;
     C2Args A;
-    A.slice_off = c->d.slice_off;
-    A.s0 = c->s0;
-    A.lbase = c->h_slice_off[c->s0];
+    A.slice_off = c->soff_k;
+    A.s0 = c->s0k;
+    A.lbase = c->lbase_k;
+    A.rs0 = c->rs0;
+    A.rss = c->rss;
     A.G = c->G;
     A.mmax = c->mmax;
     A.scap = c->scap;

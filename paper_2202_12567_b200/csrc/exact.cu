@@ -553,7 +553,7 @@ cudaError_t run_pack_rows(lmc_ctx *c)
     if (c->ML == 0) return cudaSuccess;
     GView g = gview(c);
     k_pack_rows<<<(unsigned)((c->ML + 255) / 256), 256, 0, c->stream>>>(
-        c->d.rows, c->row0, c->ML, g, c->d.g[6], c->d.g[7], c->d.g[8], c->d.g[9], c->d.g[10], c->d.g[11], c->d.g[12],
+        c->rows_k, c->row0_k, c->ML, g, c->d.g[6], c->d.g[7], c->d.g[8], c->d.g[9], c->d.g[10], c->d.g[11], c->d.g[12],
         c->d.expo, c->d.prow);
     return cudaGetLastError();
 }
@@ -671,7 +671,7 @@ __global__ void __launch_bounds__(256, P1_MINB) k_pass1(int slot, Upper up, cons
     const int a = (up.rep[l] == up.rep[f]) ? l : r;
     const int bb = (a == l) ? r : l;
     int n = up.nunc[f] < m ? up.nunc[f] : m;
-    int row = warp_floyd(m, n, (uint32_t)up.node[f], s, seed, lane);
+    int row = warp_floyd(m, n, (uint32_t)up.node[f], up.rs0 + ls * up.rss, seed, lane);
     const int va = up.rep[a], vb = up.rep[bb];
     const float4 Pa = vpl[2 * (int64_t)va], Pb = vpl[2 * (int64_t)vb];
     const Cand ca = col_candidates(&sc, sbox + 6 * ls, Pa.x, Pa.y, Pa.z);
@@ -700,12 +700,12 @@ __global__ void __launch_bounds__(256, P1_MINB) k_pass1(int slot, Upper up, cons
 cudaError_t run_pass1(lmc_ctx *c)
 {
     if (c->SL == 0) return cudaSuccess;
-    k_slice_bbox<<<c->SL, 256, 0, c->stream>>>(c->d.slice_off, c->s0, c->h_slice_off[c->s0], c->d.prow, c->d.sbox);
+    k_slice_bbox<<<c->SL, 256, 0, c->stream>>>(c->soff_k, c->s0k, c->lbase_k, c->d.prow, c->d.sbox);
     if (c->up.nB == 0) return cudaGetLastError();
     int64_t warps = (int64_t)c->SL * c->up.nB;
     // persistent: P1_MINB resident CTAs per SM stride over the warps (the scene is staged once per CTA)
     unsigned blocks = (unsigned)std::min<int64_t>((warps * 32 + 255) / 256, (int64_t)c->nsm * P1_MINB);
-    k_pass1<<<blocks, 256, 0, c->stream>>>(c->scene_slot, c->up, c->d.slice_off, c->s0, c->SL, c->h_slice_off[c->s0], c->d.prow,
+    k_pass1<<<blocks, 256, 0, c->stream>>>(c->scene_slot, c->up, c->soff_k, c->s0k, c->SL, c->lbase_k, c->d.prow,
                                            c->d.vpl, c->cfg.seed, c->nmax, c->d.p1_rows, c->d.p1_Ta, c->d.p1_Tb,
                                            c->d.p1_cnt, c->d.sbox, c->d.counters);
     return cudaGetLastError();
@@ -817,13 +817,13 @@ __global__ void __launch_bounds__(CO_THREADS, CO_MINB) k_coarsen(
                 const int o = ml ? r : l;
                 int n = up.nunc[o] < m ? up.nunc[o] : m;
                 if (n <= 32) {
-                    int i = warp_floyd(m, n, (uint32_t)up.node[f], s, seed, lane);
+                    int i = warp_floyd(m, n, (uint32_t)up.node[f], up.rs0 + ls * up.rss, seed, lane);
                     if (lane < n) atomicOr(&bm[i >> 5], 1u << (i & 31));
                 } else {   // n(I_o) > 32: an original node brighter than every base pair (P:104 sets no cap)
                     uint32_t *fb = sh_fbm[w];
                     fb[lane] = 0u;
                     __syncwarp();
-                    warp_floyd_bm(m, n, (uint32_t)up.node[f], s, seed, lane, fb);
+                    warp_floyd_bm(m, n, (uint32_t)up.node[f], up.rs0 + ls * up.rss, seed, lane, fb);
                     atomicOr(&bm[lane], fb[lane]);
                 }
             }
@@ -1021,7 +1021,7 @@ cudaError_t run_coarsen(lmc_ctx *c)
     cudaError_t e = cudaFuncSetAttribute(k_coarsen, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
     k_coarsen<<<c->SL, CO_THREADS, sm, c->stream>>>(
-        c->scene_slot, c->up, c->d.slice_off, c->s0, c->h_slice_off[c->s0], c->d.prow, c->d.vpl, c->cfg.seed, c->nmax,
+        c->scene_slot, c->up, c->soff_k, c->s0k, c->lbase_k, c->d.prow, c->d.vpl, c->cfg.seed, c->nmax,
         c->cfg.coarsen_tau, c->d.p1_rows, c->d.p1_Ta, c->d.p1_Tb, c->d.p1_cnt, c->d.pool_rows, c->d.pool_Ta,
         c->d.pool_Tb, c->d.pool_used, c->pool_cap, c->d.cs_flags, c->d.cs_eps, c->d.cs_cost, c->d.cs_zoff,
         c->d.cs_zlen, c->d.cut_n, c->d.cut_cols, c->d.src_off, c->d.src_len, c->d.src_side, c->G, c->d.counters,
@@ -1099,6 +1099,7 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2(P2Args A)
     typedef cub::BlockScan<int32_t, P2_THREADS> ScanI;
     typedef cub::BlockScan<unsigned long long, P2_THREADS> ScanU;
     const int ls = blockIdx.x, s = A.s0 + ls, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const uint32_t srng = (uint32_t)(A.up.rs0 + ls * A.up.rss);   // global slice id: the draws' key
     const int m = A.slice_off[s + 1] - A.slice_off[s];
     const int n = A.cut_n[ls];
     const int64_t lrow0 = A.slice_off[s] - A.lbase;
@@ -1328,7 +1329,7 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2(P2Args A)
                 bool isnew = false;
                 int cc = 0;
                 if (t < cap && n > 0) {
-                    uint4 uu = philox4((uint32_t)t, 0u, (uint32_t)s, TAG_P2, A.seed);
+                    uint4 uu = philox4((uint32_t)t, 0u, srng, TAG_P2, A.seed);
                     unsigned long long x = ((unsigned long long)uu.x * Wsum) >> 32;
                     int lo = sh_guide[uu.x >> 24], hi = sh_guide[(uu.x >> 24) + 1];
                     while (lo < hi) {
@@ -1356,7 +1357,7 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2(P2Args A)
         uint32_t key = P2_INVALID;
         int cell = 0, cc = 0;
         if (t < cap && n > 0) {
-            uint4 u = philox4((uint32_t)t, 0u, (uint32_t)s, TAG_P2, A.seed);
+            uint4 u = philox4((uint32_t)t, 0u, srng, TAG_P2, A.seed);
             unsigned long long x = ((unsigned long long)u.x * Wsum) >> 32;
             int lo = sh_guide[u.x >> 24], hi = sh_guide[(u.x >> 24) + 1];
             while (lo < hi) {
@@ -1403,7 +1404,7 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_pass2(P2Args A)
     {
         int need = 0, cell = 0;
         if (tid < n && colcnt[tid] == 0) {
-            uint4 u = philox4((uint32_t)tid, 0u, (uint32_t)s, TAG_FORCE, A.seed);
+            uint4 u = philox4((uint32_t)tid, 0u, srng, TAG_FORCE, A.seed);
             int i = (int)randint_u(u.x, (uint32_t)m);
             cell = (i << 11) | tid;
             need = 1;
@@ -1613,9 +1614,9 @@ cudaError_t run_pass2(lmc_ctx *c)
     if (c->SL == 0) return cudaSuccess;
     P2Args A;
     A.up = c->up;
-    A.slice_off = c->d.slice_off;
-    A.s0 = c->s0;
-    A.lbase = c->h_slice_off[c->s0];
+    A.slice_off = c->soff_k;
+    A.s0 = c->s0k;
+    A.lbase = c->lbase_k;
     A.G = c->G;
     A.prow = c->d.prow;
     A.seed = c->cfg.seed;
@@ -1671,7 +1672,7 @@ cudaError_t run_pass2(lmc_ctx *c)
     if (e != cudaSuccess) return e;
     dim3 grid(64 / EV_WARPS, c->SL);   // 64 warps per slice
     if (c->timing && c->ev_ok) cudaEventRecord(c->ev[10], c->stream);   // pass-2 entry kernel alone (stats.ms_eval2)
-    k_eval_new<<<grid, EV_WARPS * 32, 0, c->stream>>>(c->scene_slot, c->up, c->d.slice_off, c->s0, A.lbase, c->G, c->d.prow,
+    k_eval_new<<<grid, EV_WARPS * 32, 0, c->stream>>>(c->scene_slot, c->up, c->soff_k, c->s0k, A.lbase, c->G, c->d.prow,
                                                       c->d.vpl, c->d.cut_n, c->d.cut_cols, c->d.colptr, c->d.csc_row,
                                                       c->d.csc_src, c->d.carried, c->d.n_new, c->d.sbox, c->d.val, c->d.val64,
                                                       c->ncap, c->d.counters);
@@ -1721,7 +1722,7 @@ __global__ void __launch_bounds__(256) k_direct(int slot, Upper up, const int32_
 cudaError_t run_direct(lmc_ctx *c)
 {
     if (c->SL == 0) return cudaSuccess;
-    k_direct<<<c->SL, 256, 0, c->stream>>>(c->scene_slot, c->up, c->d.slice_off, c->s0, c->h_slice_off[c->s0], c->G, c->d.prow,
+    k_direct<<<c->SL, 256, 0, c->stream>>>(c->scene_slot, c->up, c->soff_k, c->s0k, c->lbase_k, c->G, c->d.prow,
                                             c->d.vpl, c->d.cut_n, c->d.cut_cols, c->d.flags, c->d.direct_rgb);
     return cudaGetLastError();
 }

@@ -102,7 +102,7 @@ void free_all(lmc_ctx *c)
                     d.newpos, d.U, d.V, d.Lam, d.Pi, d.Xold, d.S, d.flags, d.iters, d.resid,
                     d.direct_rgb, d.counters, d.img, d.rows_rgb, d.vpl_soa, d.r_perm, d.r_len, d.c_perm, d.c_len,
                     d.r_goff, d.c_goff, d.c_nsolo, d.adm_order, d.r_ent, d.c_ent, d.norm, d.r_grp, d.c_grp,
-                    d.r_slot, d.c_slot, d.ngrp, d.ctot, d.slot_st, d.ord_tmp, d.ord_cub, d.rank_pix, d.all4, d.prev_cut, d.prev_n, d.prev_flags, d.prev_rows, d.warm_ok, d.bvh, d.tri4};
+                    d.r_slot, d.c_slot, d.ngrp, d.ctot, d.slot_st, d.ord_tmp, d.ord_cub, d.rank_pix, d.all4, d.prev_cut, d.prev_n, d.prev_flags, d.prev_rows, d.warm_ok, d.bvh, d.tri4, d.soff_loc, d.rows_loc};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (c->h_stage) cudaFreeHost(c->h_stage);
@@ -365,7 +365,24 @@ lmc_status build_levels(lmc_ctx *c)
     c->h_slice_off = leaf_offsets(all);
     c->S = (int32_t)c->h_slice_off.size() - 1;
     // ---- the ranks' shares, see plan_partition
-    int k = plan_partition(all, c->h_slice_off, c->M, c->cfg.world, c->h_part_slice, c->h_part_row);
+    int k;
+    if (c->cfg.world > 1 && c->cfg.partition == 1) {
+        // interleaved shares: rank r takes slices r, r + P, ...; every rank slices the whole frame.
+        // part_slice / part_row: cumulative slice / row counts per rank (the gather's tile offsets)
+        const int P = c->cfg.world;
+        k = -1;
+        c->h_part_slice.assign(P + 1, 0);
+        c->h_part_row.assign(P + 1, 0);
+        for (int r = 0; r < P; ++r) {
+            int32_t ns = 0;
+            int64_t nr = 0;
+            for (int s = r; s < c->S; s += P) { ++ns; nr += c->h_slice_off[s + 1] - c->h_slice_off[s]; }
+            c->h_part_slice[r + 1] = c->h_part_slice[r] + ns;
+            c->h_part_row[r + 1] = c->h_part_row[r] + nr;
+        }
+    } else {
+        k = plan_partition(all, c->h_slice_off, c->M, c->cfg.world, c->h_part_slice, c->h_part_row);
+    }
     c->sub_k = k;
     const int64_t sub_a = c->h_part_row[c->cfg.rank], sub_b = c->h_part_row[c->cfg.rank + 1];
     // tilings per depth: nodes at depth d + leaves at depth < d; from depth k on only this rank's
@@ -659,8 +676,31 @@ static lmc_status create_impl(lmc_ctx *c, const lmc_gbuffer *g, const lmc_vpls *
     c->s0 = c->h_part_slice[cfg.rank];
     c->s1 = c->h_part_slice[cfg.rank + 1];
     c->SL = c->s1 - c->s0;
-    c->row0 = c->h_slice_off[c->s0];
-    c->ML = c->h_slice_off[c->s1] - c->row0;
+    c->interleaved = cfg.world > 1 && cfg.partition == 1;
+    c->h_lrow.assign(c->SL + 1, 0);
+    if (c->interleaved) {
+        // this rank's slices r, r + P, ... gathered into local arrays each frame (slice.cu)
+        c->row0 = c->h_part_row[cfg.rank];
+        c->ML = c->h_part_row[cfg.rank + 1] - c->row0;
+        for (int ls = 0; ls < c->SL; ++ls) {
+            const int s = cfg.rank + ls * cfg.world;
+            c->h_lrow[ls + 1] = c->h_lrow[ls] + (c->h_slice_off[s + 1] - c->h_slice_off[s]);
+        }
+        c->s0k = 0;
+        c->lbase_k = 0;
+        c->row0_k = 0;
+        c->rs0 = cfg.rank;
+        c->rss = cfg.world;
+    } else {
+        c->row0 = c->h_slice_off[c->s0];
+        c->ML = c->h_slice_off[c->s1] - c->row0;
+        for (int ls = 0; ls <= c->SL; ++ls) c->h_lrow[ls] = c->h_slice_off[c->s0 + ls] - (int32_t)c->row0;
+        c->s0k = c->s0;
+        c->lbase_k = c->h_slice_off[c->s0];
+        c->row0_k = c->row0;
+        c->rs0 = c->s0;
+        c->rss = 1;
+    }
     c->mmax = 1;
     for (int s = 0; s < c->S; ++s) c->mmax = std::max(c->mmax, c->h_slice_off[s + 1] - c->h_slice_off[s]);
     // light tree on the host for the upper-tree construction
@@ -674,6 +714,8 @@ static lmc_status create_impl(lmc_ctx *c, const lmc_gbuffer *g, const lmc_vpls *
     CK(hcopy_in(ht.cut, t->global_cut, (size_t)c->G, cfg.input_memory, c->stream), "read tree");
     st = build_upper(c, ht);
     if (st != LMC_OK) return st;
+    c->up.rs0 = c->rs0;   // random draws keyed by the global slice id
+    c->up.rss = c->rss;
     const int64_t G = c->G, SL = c->SL, ML = c->ML, M = c->M;
     {
         int64_t nt = (int64_t)std::ceil((double)(c->mmax * G) * cfg.rate);
@@ -714,6 +756,16 @@ static lmc_status create_impl(lmc_ctx *c, const lmc_gbuffer *g, const lmc_vpls *
     CK(dalloc(&d.vpl_soa, 6 * (size_t)c->NV), "alloc vpls");
     CK(dalloc(&d.rows, M), "alloc slicing");
     CK(dalloc(&d.rows_alt, M), "alloc slicing");
+    if (c->interleaved) {   // this rank's slice offsets and rows, gathered after the slicing of each frame
+        CK(dalloc(&d.soff_loc, SL + 1), "alloc slicing");
+        CK(dalloc(&d.rows_loc, std::max<int64_t>(ML, 1)), "alloc slicing");
+        CK(cudaMemcpy(d.soff_loc, c->h_lrow.data(), (SL + 1) * sizeof(int32_t), cudaMemcpyHostToDevice), "upload slicing");
+        c->soff_k = d.soff_loc;
+        c->rows_k = d.rows_loc;
+    } else {
+        c->soff_k = d.slice_off;
+        c->rows_k = d.rows;
+    }
     CK(dalloc(&d.sk, 12 * M), "alloc slicing");
     CK(dalloc(&d.prow, 4 * (size_t)ML), "alloc rows");
     const int64_t nB = c->up.nB, U = c->up.U;
@@ -905,8 +957,9 @@ lmc_status lmc_build_slices(lmc_ctx *c)
     ev_rec(c, 0);
     CK(cudaMemsetAsync(c->d.counters, 0, 8 * sizeof(unsigned long long), c->stream), "memset counters");
     CK(run_slicing(c), "slicing");
+    if (c->interleaved) CK(run_rank_rows(c), "slicing");
     CK(run_pack_rows(c), "pack rows");
-    c->launches += slicing_launches(c) + (c->M > 0 ? 1 : 0);   // + the row packing
+    c->launches += slicing_launches(c) + (c->M > 0 ? 1 : 0) + (c->interleaved && c->ML > 0 ? 1 : 0);   // + row packing (+ rank rows)
     ev_rec(c, 1);
     c->state = 1;
     return LMC_OK;
@@ -1140,6 +1193,12 @@ static lmc_status sync_check(lmc_ctx *c, int need)
 
 static lmc_status local_slice(lmc_ctx *c, int32_t slice, int *ls)
 {
+    if (c->interleaved) {
+        if (slice < 0 || slice >= c->S || slice % c->cfg.world != c->cfg.rank)
+            return fail(c, LMC_EINVAL, "slice %d is not on this rank (%d of %d, interleaved)", slice, c->cfg.rank, c->cfg.world);
+        *ls = slice / c->cfg.world;
+        return LMC_OK;
+    }
     if (slice < c->s0 || slice >= c->s1) return fail(c, LMC_EINVAL, "slice %d is not on this rank [%d, %d)", slice, c->s0, c->s1);
     *ls = slice - c->s0;
     return LMC_OK;
@@ -1270,7 +1329,7 @@ lmc_status lmc_get_factors(lmc_ctx *c, int32_t slice, float *U, float *V, int32_
     CK(d2h(flags, c->d.flags + ls, 1), "get factors");
     CK(d2h(iters, c->d.iters + ls, 1), "get factors");
     CK(d2h(resid, c->d.resid + ls, 1), "get factors");
-    const int64_t lrow0 = c->h_slice_off[slice] - c->row0;
+    const int64_t lrow0 = c->h_lrow[ls];
     CK(d2h(U, c->d.U + lrow0 * c->q, (size_t)mm * c->q), "get factors");
     if (V) {   // device layout: column j contiguous (n x q); returned q x n row-major
         std::vector<float> vt((size_t)nn * c->q);
@@ -1368,7 +1427,7 @@ lmc_status lmc_get_stats(lmc_ctx *c, lmc_stats *st)
         std::vector<int32_t> cn(c->SL);
         CK(d2h(cn.data(), c->d.cut_n, (size_t)c->SL), "stats");
         for (int ls = 0; ls < c->SL; ++ls) {
-            int64_t m = c->h_slice_off[c->s0 + ls + 1] - c->h_slice_off[c->s0 + ls];
+            int64_t m = c->h_lrow[ls + 1] - c->h_lrow[ls];
             st->sum_cols += cn[ls];
             st->sum_completed += m * cn[ls];
         }

@@ -55,6 +55,7 @@ struct Upper {
     const int32_t *base_of;   // local id -> base index or -1
     const double *lum;        // lum(I_f), fp64 from the float32 intensities
     const float *I;           // 3 per node
+    int32_t rs0, rss;         // global id of this rank's local slice ls: rs0 + ls * rss (random-draw key)
 };
 
 // Per-frame device state (all allocated in lmc_create)
@@ -80,6 +81,7 @@ struct Dev {
     uint32_t *sl_cnt;                  // [2 x work items] rows below / equal to the threshold per chunk
     uint32_t *sl_state;                // [slots][4] threshold key, rows of it going left, dimension, ceil(n/2)
     int32_t *slice_off;                // S+1
+    int32_t *soff_loc, *rows_loc;      // interleaved partition: this rank's slice offsets (SL+1) and rows (ML)
     float4 *prow;                      // 4 per local row (slice order)
     float *sbox;                       // [SL][6] bounding box (lo3, hi3) of each slice's points (fp32, exact)
     // pass 1: [SL][nB][nmax]
@@ -163,6 +165,15 @@ struct lmc_ctx {
     std::vector<int32_t> h_slice_off;
     int32_t s0 = 0, s1 = 0, SL = 0;
     int64_t row0 = 0, ML = 0;
+    // what the stage kernels index: the whole frame's slice offsets / rows from s0, row0
+    // (contiguous shares), or this rank's gathered copy from 0 (interleaved); random draws use the
+    // global slice id rs0 + ls * rss
+    bool interleaved = false;
+    const int32_t *soff_k = nullptr;
+    int32_t *rows_k = nullptr;
+    int32_t s0k = 0, lbase_k = 0, rs0 = 0, rss = 1;
+    int64_t row0_k = 0;
+    std::vector<int32_t> h_lrow;       // local row offset of each of this rank's slices (SL + 1), both modes
     int32_t mmax = 0;
     int32_t q = 0, nmax = 0;
     int64_t pool_cap = 0, ncap = 0, scap = 0;
@@ -209,6 +220,7 @@ cudaError_t run_direct(lmc_ctx *c);
 cudaError_t run_eval_entries(lmc_ctx *c, int64_t n, const int32_t *d_rows, const int32_t *d_vpls, double *d_out,
                              float4 *d_tmp_rows);
 int64_t slicing_launches(const lmc_ctx *c);
+cudaError_t run_rank_rows(lmc_ctx *c);   // interleaved partition: this rank's rows into rows_loc
 cudaError_t run_pack_vpls(lmc_ctx *c);
 int acquire_scene_slot();
 void release_scene_slot(int slot);

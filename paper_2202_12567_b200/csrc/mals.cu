@@ -21,6 +21,7 @@ namespace lmc {
 struct MArgs {
     const int32_t *slice_off;
     int32_t s0, lbase, G, mmax;
+    int32_t rs0, rss;   // global slice id of local slice ls: rs0 + ls * rss (the draws' key)
     int64_t ncap;
     int K;
     double lambda;
@@ -298,9 +299,9 @@ __global__ void __launch_bounds__(MCfg<Q>::NT, 1) k_mals(MArgs A)
     const double nrmM2 = dblock_reduce<false>(sq, red);
     const double c0 = 2.0 * sqrt((sum / (double)nnz) / (double)Q);
     for (int e = tid; e < m * Q; e += MCfg<Q>::NT)
-        Xg[e] = c0 * (double)unif_f(philox4((uint32_t)(e / Q), (uint32_t)(e % Q), (uint32_t)s, TAG_X0, A.seed).x);
+        Xg[e] = c0 * (double)unif_f(philox4((uint32_t)(e / Q), (uint32_t)(e % Q), (uint32_t)(A.rs0 + ls * A.rss), TAG_X0, A.seed).x);
     for (int e = tid; e < n * Q; e += MCfg<Q>::NT)
-        Yg[e] = c0 * (double)unif_f(philox4((uint32_t)(e % Q), (uint32_t)(e / Q), (uint32_t)s, TAG_Y0, A.seed).x);
+        Yg[e] = c0 * (double)unif_f(philox4((uint32_t)(e % Q), (uint32_t)(e / Q), (uint32_t)(A.rs0 + ls * A.rss), TAG_Y0, A.seed).x);
     __syncthreads();
     const double lam = A.lambda;
     for (int it = 0; it < A.K; ++it) {
@@ -447,9 +448,11 @@ cudaError_t run_mals(lmc_ctx *c)
 {
     if (c->SL == 0) return cudaSuccess;
     MArgs A;
-    A.slice_off = c->d.slice_off;
-    A.s0 = c->s0;
-    A.lbase = c->h_slice_off[c->s0];
+    A.slice_off = c->soff_k;
+    A.s0 = c->s0k;
+    A.lbase = c->lbase_k;
+    A.rs0 = c->rs0;
+    A.rss = c->rss;
     A.G = c->G;
     A.mmax = c->mmax;
     A.ncap = c->ncap;

@@ -560,6 +560,31 @@ cudaError_t run_slicing(lmc_ctx *c)
     return cudaGetLastError();
 }
 
+// interleaved partition: rank r's slices r, r + P, ... copied row by row into its local
+// array (local slice offsets soff_loc, planned on the host); one thread per local row
+__global__ void k_rank_rows(int64_t ML, int SL, int rank, int P, const int32_t *__restrict__ soff_loc,
+                            const int32_t *__restrict__ slice_off, const int32_t *__restrict__ rows, int32_t *rows_loc)
+{
+    const int64_t li = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (li >= ML) return;
+    int lo = 0, hi = SL - 1;   // last local slice with offset <= li
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (soff_loc[mid] <= li) lo = mid; else hi = mid - 1;
+    }
+    const int s = rank + lo * P;
+    rows_loc[li] = rows[slice_off[s] + (li - soff_loc[lo])];
+}
+
+cudaError_t run_rank_rows(lmc_ctx *c)
+{
+    if (c->ML == 0 || c->SL == 0) return cudaSuccess;
+    k_rank_rows<<<(unsigned)((c->ML + 255) / 256), 256, 0, c->stream>>>(c->ML, c->SL, c->cfg.rank, c->cfg.world,
+                                                                        c->d.soff_loc, c->d.slice_off, c->d.rows,
+                                                                        c->d.rows_loc);
+    return cudaGetLastError();
+}
+
 // launches of run_slicing (the launch counter of lmc_stats)
 int64_t slicing_launches(const lmc_ctx *c)
 {

@@ -54,7 +54,7 @@ class Config(C.Structure):
                 ("rank", C.c_int32), ("world", C.c_int32), ("input_memory", C.c_int32), ("stream", _P),
                 ("nccl_id", C.c_uint8 * 128), ("row_importance", C.c_int32), ("cost_mode", C.c_int32),
                 ("resolve_mode", C.c_int32), ("warm_start", C.c_int32), ("warm_iters", C.c_int32),
-                ("coarsen_target", C.c_int32)]
+                ("coarsen_target", C.c_int32), ("partition", C.c_int32)]
 
 
 class Stats(C.Structure):
@@ -193,6 +193,7 @@ class Frame:
         self.cfg.warm_start = int(prm.get("warm_start", 0))
         self.cfg.warm_iters = int(prm.get("warm_iters", 0))
         self.cfg.coarsen_target = int(prm.get("coarsen_target", 0))
+        self.cfg.partition = int(prm.get("partition", 0))   # world > 1: 0 subtrees / ranges, 1 interleaved
         h = _P()
         st = lib.lmc_create(C.byref(self.gb), C.byref(self.vp), C.byref(self.tr), C.byref(self.sc),
                             C.byref(self.cfg), C.byref(h))

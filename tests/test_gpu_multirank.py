@@ -31,7 +31,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, name, q):
+def _worker(rank, world, port, name, q, partition=0):
     import torch.distributed as dist
 
     from paper_2202_12567_b200 import dist as pdist
@@ -41,7 +41,7 @@ def _worker(rank, world, port, name, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     torch.cuda.set_device(0)
     x = scenegen.make_inputs(name)
-    fr = lmc.Frame(x, rank=rank, world=world)
+    fr = lmc.Frame(x, rank=rank, world=world, partition=partition)
     fr.build_slices()
     sf, rf = fr.partition()
     counts = pdist.row_counts(rf)
@@ -55,7 +55,10 @@ def _worker(rank, world, port, name, q):
     tile = torch.zeros(counts[rank] * 4, device="cuda")
     fr.resolve_rows(tile)
     allrows = pdist.gather_rows(tile, counts)
-    q.put(("rows", rank, int(rf[rank]), int(rf[rank + 1]), rows[rf[rank]:rf[rank + 1]].copy()))
+    if partition == 1:   # interleaved: every rank slices the whole frame
+        q.put(("rows", rank, 0, rows.size, rows.copy()))
+    else:
+        q.put(("rows", rank, int(rf[rank]), int(rf[rank + 1]), rows[rf[rank]:rf[rank + 1]].copy()))
     if rank == 0:
         img = torch.zeros(x.height * x.width * 3, device="cuda")
         fr.scatter_rows(allrows, img)
@@ -66,14 +69,17 @@ def _worker(rank, world, port, name, q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("name,world", [("t_interior", 2), ("t_interior", 3), ("t_interior", 4), ("c1", 4),
-                                        ("t_mesh", 2)])
-def test_sharded_frame_equals_single_rank(name, world):
+@pytest.mark.parametrize("name,world,partition", [("t_interior", 2, 0), ("t_interior", 3, 0), ("t_interior", 4, 0),
+                                                  ("c1", 4, 0), ("t_mesh", 2, 0), ("t_interior", 2, 1),
+                                                  ("t_interior", 3, 1), ("c1", 4, 1), ("t_cornell", 5, 1)])
+def test_sharded_frame_equals_single_rank(name, world, partition):
+    """partition 0: slicing subtrees (P = 2^k) or slice ranges; 1: interleaved slices (the draws
+    keyed by the global slice id, so the image is bit-identical either way)"""
     from paper_2202_12567_b200 import lmc
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, name, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, name, q, partition)) for r in range(world)]
     for p in procs:
         p.start()
     items = [q.get(timeout=600) for _ in range(world + 1)]
