@@ -113,7 +113,9 @@ typedef struct {
     double lambda;          /* MALS ridge */
     int32_t rank, world;    /* this process' share of the slices (lmc_get_partition): for world = 2^k the
                                rank-th subtree of depth k of the slicing (levels >= k are sliced by
-                               that rank only), otherwise slices [S*rank/world, S*(rank+1)/world) */
+                               that rank only), otherwise slices [S*rank/world, S*(rank+1)/world);
+                               with partition = 1 (below) slices rank, rank + world, ...  Per-slice getters
+                               take the global slice id */
     int32_t input_memory;   /* lmc_memory of the gbuffer / vpls / tree arrays */
     void *stream;           /* cudaStream_t */
     uint8_t nccl_id[128];   /* world > 1: the ncclUniqueId from lmc_nccl_unique_id() on rank 0, broadcast

@@ -2,7 +2,9 @@
 
 Slices are independent after slicing.  With P = 2^k ranks, rank r owns the
 r-th depth-k subtree of the slicing (every rank slices the top k levels of the whole G-buffer,
-then only inside its subtree); other P split the slice index range.  The library reports the
+then only inside its subtree); other P split the slice index range; with lmc_config.partition = 1
+(the bench's default at N > 1) rank r takes slices r, r + P, ... of a full slicing, which balances
+the ranks' completion work.  The library reports the
 shares (Frame.partition()).  The production image assembly is inside the library: the ranks pass
 an NCCL id (lmc_nccl_unique_id on rank 0, broadcast with torch.distributed) and
 lmc_resolve_image gathers every rank's packed rows to rank 0 over NVLink (one NCCL group of
