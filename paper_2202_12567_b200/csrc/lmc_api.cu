@@ -1008,9 +1008,9 @@ lmc_status lmc_sample_pass2(lmc_ctx *c)
 static cudaError_t completion_order(lmc_ctx *c)
 {
     const char *te = getenv("LMC_ADM_TAIL");
-    const int ntail = (te ? atoi(te) : 1) * c->nsm;
+    const int ntail = std::min<int>((te ? atoi(te) : 1) * c->nsm, c->SL);   // SL: all slices, largest first
     c->adm_ordered = false;
-    if (!(ntail > 0 && c->SL > ntail)) return cudaSuccess;
+    if (!(ntail > 0 && (c->SL > ntail || (te && ntail == c->SL)))) return cudaSuccess;
     cudaError_t e = run_launch_order(c, ntail);
     if (e != cudaSuccess) return e;
     c->adm_ordered = true;
